@@ -1,0 +1,486 @@
+#!/usr/bin/env python
+"""Benchmark: FFAST sparse transforms/sec on BASELINE config 5 (the scaling config).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1; one rank per GPU)
+
+Workload (BASELINE.json configs[4]): 8192 independent exactly-sparse signals,
+complex64, N = 127*128*129 = 2,097,024, K = 256 unit-magnitude random-phase
+tones, cycle plan 127/128/129 with delays 0,1,2 (explicit plan, SURVEY
+Appendix A), sharded by signal across ranks (strong scaling: the 8192 total is
+fixed) and the recovered [signals, K] slots all-gathered over NCCL.  One step =
+one FFAST pass (|x|^2 stream for the exact thresholds, gather + 127/128/129-point
+DFTs, GPU-resident peeling, top-K truncation, result gather) over the whole
+resident batch.  Inputs are 137 GB >> 126 MB L2, so no L2 flush is needed.
+
+Inputs follow generate_test_case's model (signals.py:81-117) with the bench's
+per-signal seeds (bench.py:123-127): truth drawn on the host with numpy's
+PCG64, the clean signal synthesised on the device (n * ifft, cast to c64).
+
+--impl reference times the CPU restatement of the reference path (oracle/, a
+numpy port pinned against the reference's outputs) on all host cores, on the
+same workload, one bounded sample of signals per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+import zlib
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_SIG = 2097024
+K = 256
+FACTORS = [127, 128, 129]
+TOTAL_SIGNALS = 8192
+METRIC = "sparse transforms/sec (signals/s) at N,K; achieved HBM sector GB/s fraction"
+UNIT = "signals/s"
+SIGNAL_BYTES = N_SIG * 8  # complex64
+# 32-byte sectors the gather touches per signal (unique per kernel), SURVEY §8d
+GATHER_SECTOR_BYTES = None
+
+
+def case_seed(n, k, snr, seed_base, trial):
+    tag = "exact" if snr == "exact" else f"{float(snr):.9g}"
+    return zlib.crc32(f"{n}|{k}|{tag}|{seed_base}|{trial}".encode()) ^ (seed_base << 1)
+
+
+def gather_sector_bytes(n=N_SIG, factors=FACTORS, shifts=(0, 1, 2), esz=8):
+    secs = set()
+    for b in factors:
+        j = np.arange(b, dtype=np.int64) * (n // b)
+        for t in shifts:
+            secs.update(((j - t) % n * esz // 32).tolist())
+    return 32 * len(secs)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- inputs
+
+
+def synth_signals(x, first_trial: int, dev, chunk: int = 32):
+    """Fill x[i] with trial first_trial+i of config 5 (n*ifft of the sparse truth, c64)."""
+    import torch
+
+    from paper_2011_05749_b200.signals import draw_truth
+
+    count = x.shape[0]
+    spec = torch.zeros((chunk, N_SIG), dtype=torch.complex128, device=dev)
+    truths = []
+    for c0 in range(0, count, chunk):
+        c1 = min(count, c0 + chunk)
+        spec.zero_()
+        for i in range(c0, c1):
+            rng = np.random.default_rng(case_seed(N_SIG, K, "exact", 0, first_trial + i))
+            pos, coef = draw_truth(N_SIG, K, rng)
+            truths.append((pos, coef))
+            spec[i - c0, torch.from_numpy(pos).to(dev)] = torch.from_numpy(coef).to(dev)
+        x[c0:c1] = (torch.fft.ifft(spec[: c1 - c0], dim=1) * N_SIG).to(torch.complex64)
+    del spec
+    return truths
+
+
+# ----------------------------------------------------------------------------- our arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_05749_b200 import _device, _lib
+    from paper_2011_05749_b200.batch import ffast_batch, ffast_workspace_bytes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    total = args.signals
+    per = total // world
+    first = rank * per
+    lib = _lib.load()
+
+    x = torch.empty((per, N_SIG), dtype=torch.complex64, device=dev)
+    truths = synth_signals(x, first, dev)
+    torch.cuda.synchronize()
+
+    fb, nc = _lib.host_i64(FACTORS)
+    code = _lib.AFFT_C64
+    nodes = sum(FACTORS)
+    nparts = int(lib.afft_sumsq_parts(N_SIG, code))
+    ws = torch.empty(ffast_workspace_bytes(N_SIG, code, per, FACTORS), dtype=torch.uint8,
+                     device=dev)
+    partials = torch.empty((per, nparts), dtype=torch.float64, device=dev)
+    eps = torch.empty(per, dtype=torch.float64, device=dev)
+    nodebuf = torch.empty((per, nodes, 3), dtype=torch.complex128, device=dev)
+    state = torch.empty((per, nodes), dtype=torch.int8, device=dev)
+    rpos = torch.empty((per, nodes), dtype=torch.int64, device=dev)
+    rval = torch.empty((per, nodes), dtype=torch.complex128, device=dev)
+    rcount = torch.empty(per, dtype=torch.int32, device=dev)
+    rounds = torch.empty(per, dtype=torch.int32, device=dev)
+    unres = torch.empty(per, dtype=torch.int32, device=dev)
+    opos = torch.empty((per, K), dtype=torch.int64, device=dev)
+    oval = torch.empty((per, K), dtype=torch.complex128, device=dev)
+    ocount = torch.empty(per, dtype=torch.int32, device=dev)
+    if world > 1:
+        gpos = torch.empty((total, K), dtype=torch.int64, device=dev)
+        gval = torch.empty((total, K), dtype=torch.complex128, device=dev)
+        gcnt = torch.empty(total, dtype=torch.int32, device=dev)
+    sb, ns = _lib.host_i64([0, 1, 2])
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    ev_norm = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    ev_peel = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+
+    def step(i=None):
+        """One FFAST pass over the resident batch: the five launches afft_ffast makes,
+        issued individually so the dominant kernel can be bracketed by events."""
+        if i is not None:
+            ev_norm[i][0].record(stream)
+        _lib.check(lib.afft_sumsq(x.data_ptr(), code, N_SIG, per, N_SIG, partials.data_ptr(),
+                                  sp), "sumsq")
+        if i is not None:
+            ev_norm[i][1].record(stream)
+        _lib.check(lib.afft_exact_thresholds(partials.data_ptr(), nparts, N_SIG, per,
+                                             eps.data_ptr(), sp), "thresholds")
+        _lib.check(lib.afft_build_graph(x.data_ptr(), code, N_SIG, per, N_SIG, fb, nc, sb, ns,
+                                        nodebuf.data_ptr(), sp), "build_graph")
+        state.zero_()
+        rcount.zero_()
+        if i is not None:
+            ev_peel[i][0].record(stream)
+        _lib.check(lib.afft_peel_exact(N_SIG, per, fb, nc, nodebuf.data_ptr(), state.data_ptr(),
+                                       None, None, eps.data_ptr(), eps.data_ptr(), K + 4,
+                                       rpos.data_ptr(), rval.data_ptr(), nodes,
+                                       rcount.data_ptr(), rounds.data_ptr(), unres.data_ptr(),
+                                       sp), "peel")
+        if i is not None:
+            ev_peel[i][1].record(stream)
+        _lib.check(lib.afft_truncate(rpos.data_ptr(), rval.data_ptr(), rcount.data_ptr(), nodes,
+                                     per, K, opos.data_ptr(), oval.data_ptr(),
+                                     ocount.data_ptr(), sp), "truncate")
+        if world > 1:
+            dist.all_gather_into_tensor(gpos, opos)
+            dist.all_gather_into_tensor(gval, oval)
+            dist.all_gather_into_tensor(gcnt, ocount)
+
+    launches_per_step = 5  # sumsq, thresholds, gather_dft, peel_exact, truncate
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness of the measured pass: every recovered tone is a true tone
+    cnt = ocount.cpu().numpy()
+    pos = opos.cpu().numpy()
+    exact = sum(int(cnt[i]) == K and set(pos[i, :K].tolist()) == set(truths[i][0].tolist())
+                for i in range(per))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    norm_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_norm)
+    peel_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_peel)
+    t = torch.tensor([ms, norm_ms, peel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, norm_ms, peel_ms = (float(v) for v in t.tolist())
+    ms_per_step = ms / args.steps
+
+    # whole-call check: afft_ffast (the C-ABI entry a user binds) gives the same step time
+    res = ffast_batch(x, K, FACTORS, workspace=ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        ffast_batch(x, K, FACTORS, workspace=ws, out=res)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ffast_call_ms = e0.elapsed_time(e1) / 3
+
+    e2e = run_e2e(args, dev, x, world) if rank == 0 else None
+    cpu = cpu_baseline_sample(x[: args.cpu_signals]) if (rank == 0 and world == 1) else None
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        norm_bytes = per * SIGNAL_BYTES
+        achieved = norm_bytes / (norm_ms * 1e-3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_sumsq_traffic.json")
+        if os.path.exists(prof):
+            with open(prof) as fh:
+                d = json.load(fh)
+            traffic = float(d["dram_bytes_per_signal"]) * per
+        gsec = gather_sector_bytes()
+        value = total / (ms_per_step * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c64 in, f64 compute", "data": "synthetic (generate_test_case model, seeded)",
+            "config": {
+                "workload": "config5_ffast_n2097024_k256_127x128x129_c64",
+                "n": N_SIG, "k": K, "factors": FACTORS, "shifts": [0, 1, 2],
+                "signals_total": total, "signals_per_rank": per,
+                "l2": "inputs 137 GB >> 126 MB L2 (no flush needed)",
+                "parallelism": f"signal-sharded x{world}, NCCL all-gather of result slots",
+                "exact_recovered_fraction": exact / per,
+                "norm_kernel_ms": norm_ms, "peel_kernel_ms": peel_ms,
+                "afft_ffast_call_ms": ffast_call_ms,
+                "step_hbm_gbs": (norm_bytes + per * gsec) / (ms_per_step * 1e-3) / 1e9,
+            },
+            "roofline": {
+                "kernel": "sumsq_kernel (|x|^2 stream of exact_thresholds)",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": norm_bytes, "traffic": traffic,
+                "gather_sector_bytes_per_signal": gsec,
+            },
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, dev, x, world):
+    """Same metric through the public API with HOST (pinned) buffers: H2D of every
+    step's signals + the decode + D2H of the result slots, all timed."""
+    import torch
+
+    from paper_2011_05749_b200.batch import ffast_batch
+
+    m = min(args.e2e_signals, x.shape[0])
+    host = torch.empty((m, N_SIG), dtype=torch.complex64, pin_memory=True)
+    host.copy_(x[:m])
+    dbuf = torch.empty((m, N_SIG), dtype=torch.complex64, device=dev)
+    res = ffast_batch(dbuf.copy_(host, non_blocking=True), K, FACTORS)
+    hpos = torch.empty((m, K), dtype=torch.int64, pin_memory=True)
+    hval = torch.empty((m, K), dtype=torch.complex128, pin_memory=True)
+    hcnt = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dbuf.copy_(host, non_blocking=True)
+        ffast_batch(dbuf, K, FACTORS, out=res)
+        hpos.copy_(res.pos, non_blocking=True)
+        hval.copy_(res.val, non_blocking=True)
+        hcnt.copy_(res.count, non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    steps = max(2, min(args.steps, 5))
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        step()
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    return {"value": m / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": m * SIGNAL_BYTES,
+            "d2h_bytes_per_step": m * K * (8 + 16) + m * 4, "signals_per_step": m,
+            "ms_per_step": ms, "api": "paper_2011_05749_b200.ffast_batch (afft_ffast) on pinned host"}
+
+
+def cpu_baseline_sample(xs):
+    """The oracle port timed on one host core over a bounded sample of the same signals."""
+    from oracle import ffast as oracle_ffast
+
+    arr = xs.cpu().numpy()
+    t0 = time.perf_counter()
+    done = 0
+    for row in arr:
+        oracle_ffast.ffast(row.astype(np.complex128), K, FACTORS)
+        done += 1
+        if time.perf_counter() - t0 > 20.0:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{done} config-5 signals (same device-synthesised inputs), oracle/ffast.py, "
+                      "1 thread, upcast c64->c128 as the reference does"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+
+def _ref_worker(args_tuple):
+    wid, per_step, steps, warmup, barrier, q = args_tuple
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import ffast as oracle_ffast
+    from paper_2011_05749_b200.signals import generate_test_case
+
+    xs = []
+    for j in range(per_step):
+        seed = case_seed(N_SIG, K, "exact", 0, wid * per_step + j)
+        xs.append(generate_test_case(N_SIG, K, "exact", seed).signal.astype(np.complex64)
+                  .astype(np.complex128))
+    for _ in range(warmup):
+        oracle_ffast.ffast(xs[0], K, FACTORS)
+    times = []
+    for _ in range(steps):
+        barrier.wait()
+        t0 = time.perf_counter()
+        for x in xs:
+            oracle_ffast.ffast(x, K, FACTORS)
+        times.append((t0, time.perf_counter()))
+    q.put(times)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    per_step = 1
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(cores)
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ref_worker,
+                         args=((w, per_step, args.steps, args.warmup, barrier, q),))
+             for w in range(cores)]
+    for p in procs:
+        p.start()
+    results = [q.get() for _ in procs]
+    for p in procs:
+        p.join()
+    step_ms = []
+    for s in range(args.steps):
+        t0 = min(r[s][0] for r in results)
+        t1 = max(r[s][1] for r in results)
+        step_ms.append((t1 - t0) * 1e3)
+    ms = statistics.mean(step_ms)
+    value = cores * per_step / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128 (reference upcasts c64)",
+        "data": "synthetic (generate_test_case, seeded)", "impl": "reference",
+        "config": {"workload": "config5_ffast_n2097024_k256_127x128x129_c64", "n": N_SIG, "k": K,
+                   "factors": FACTORS, "signals_per_step": cores * per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{cores * per_step} signals per step (one per core), "
+                                   "oracle/ffast.py numpy port of the reference FFAST path, "
+                                   "signal generation excluded as bench.py:172-176 does"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--signals", type=int, default=TOTAL_SIGNALS)
+    ap.add_argument("--e2e-signals", type=int, default=256)
+    ap.add_argument("--cpu-signals", type=int, default=128)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * aliasfft_b200.h — C ABI of the B200-native aliasing-filter sparse-FFT hot path.
+ *
+ * The reference (`aliasfft` 0.1.0, pure Python on numpy) has no FFI: its operator
+ * API is the Python function surface re-exported by
+ * /root/reference/pkg/src/aliasfft/__init__.py:9-79.  Each entry point below is the
+ * device-side body of one of those functions (cited per function), with plain
+ * pointers and sizes so any host language can bind it (see INTEGRATION.md for the
+ * ctypes binding the Python mirror uses).
+ *
+ * Conventions
+ *  - Every pointer named x/out/nodes/... is DEVICE memory unless marked (host).
+ *    Small plan arrays (factors, shifts) are HOST arrays copied into kernel
+ *    parameters; the library never reads device memory on the host.
+ *  - Complex values are interleaved (re, im).  Signals may be complex64
+ *    (AFFT_C64, float2) or complex128 (AFFT_C128, double2); all arithmetic after
+ *    the gather is IEEE float64 with no FMA contraction, as numpy computes.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls only enqueue work; nothing synchronises except afft_sync_device_flag.
+ *  - Return codes: 0 OK, <0 error (AFFT_E*); afft_last_error() gives the
+ *    thread-local message.  No exception crosses the ABI.
+ *  - Batched layout: `batch` signals, signal s starting at x + s*ld elements.
+ *  - Node layout (peeling graph, /root/reference/pkg/src/aliasfft/peeling.py:169-178):
+ *    node g = (sum of factors before cycle c) + bucket index i, measurements
+ *    contiguous per node: nodes[s][g][r], r over the shift list.
+ */
+#ifndef ALIASFFT_B200_H
+#define ALIASFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum afft_dtype { AFFT_C64 = 0, AFFT_C128 = 1 };
+
+enum afft_status {
+  AFFT_OK = 0,
+  AFFT_EINVAL = -1,       /* maps to ValueError */
+  AFFT_EUNSUPPORTED = -2, /* maps to UnsupportedSizeError / ValueError */
+  AFFT_ECUDA = -3,        /* CUDA launch/runtime failure */
+  AFFT_ENOMEM = -4        /* workspace too small */
+};
+
+/* NodeState (peeling.py:29-34) as stored in the int8 state arrays. */
+enum afft_node_state {
+  AFFT_UNKNOWN = 0,
+  AFFT_ZERO_TON = 1,
+  AFFT_SINGLE_TON = 2,
+  AFFT_MULTI_TON = 3,
+  AFFT_RESOLVED = 4
+};
+
+#define AFFT_MAX_CYCLES 16
+#define AFFT_MAX_SHIFTS 512
+#define AFFT_MAX_SMEM_DFT 4096 /* largest bucket count handled by the one-CTA DFT */
+
+const char* afft_last_error(void);
+int afft_version(void);
+
+/*
+ * bucketize / bucketize_set (bucketize.py:83-106):
+ *   out[s][t][i] = (1/b) * sum_j x_s[(j*(n/b) - shifts[t]) mod n] * exp(-2*pi*i*j*i/b)
+ * Output strides (in complex elements) let one call write either the
+ * FilteredSpectrum layout [s][t][i] or the node layout [s][i][t].
+ */
+int afft_bucketize(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                   int64_t b, const int64_t* shifts /* host */, int32_t nshift,
+                   double* out, int64_t out_signal_stride, int64_t out_shift_stride,
+                   int64_t out_bin_stride, void* stream);
+
+/*
+ * build_graph (peeling.py:169-178): all cycles and shifts in one launch, node layout
+ * nodes[s][g][r] with g = cycle offset + bucket, r over shifts (stride nshift).
+ */
+int afft_build_graph(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                     const int64_t* factors /* host */, int32_t ncycles,
+                     const int64_t* shifts /* host */, int32_t nshift, double* nodes,
+                     void* stream);
+
+/*
+ * Per-signal sum of |x|^2 in float64, written as fixed-order partials
+ * partials[s][p], p < afft_sumsq_parts(n, dtype).  The 2-norm used by
+ * exact_thresholds (peeling.py:316-318) is sqrt(sum_p partials[s][p]).
+ */
+int32_t afft_sumsq_parts(int64_t n, int dtype);
+int afft_sumsq(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+               double* partials, void* stream);
+
+/* exact_thresholds (peeling.py:316-318) from the partials: eps[s] = 1e-6*||x_s||/sqrt(n). */
+int afft_exact_thresholds(const double* partials, int32_t nparts, int64_t n, int64_t batch,
+                          double* eps, void* stream);
+
+/*
+ * peel_decode, exact mode (peeling.py:270-313 with classify_exact 193-215 and
+ * subtract 181-190).  One CTA per signal; synchronous rounds with first-found
+ * dedupe in (cycle, bucket) order, subtraction in found order, ZERO_TON frozen.
+ *   residual  [batch][nodes][3]  in/out (complex128)
+ *   state     [batch][nodes]     in/out (afft_node_state)
+ *   node_f0   [batch][nodes]     out (last decoded position, -1 if none)
+ *   node_val  [batch][nodes]     out (complex128, last decoded value)
+ *   eps_zero / eps_ratio [batch] per-signal thresholds
+ *   rec_pos/rec_val [batch][rec_cap] in/out: recovered spectrum in insertion
+ *     order; rec_count[s] on entry is the number already recovered.
+ *   rounds/unresolved [batch] out.
+ * node_f0/node_val may be NULL.
+ */
+int afft_peel_exact(int64_t n, int64_t batch, const int64_t* factors /* host */,
+                    int32_t ncycles, double* residual, int8_t* state, int64_t* node_f0,
+                    double* node_val, const double* eps_zero, const double* eps_ratio,
+                    int32_t max_rounds, int64_t* rec_pos, double* rec_val, int32_t rec_cap,
+                    int32_t* rec_count, int32_t* rounds, int32_t* unresolved, void* stream);
+
+/*
+ * classify_exact (peeling.py:193-215) for `count` independent nodes of one cycle
+ * size b: residual [count][3] complex128, index [count] bucket indices.  Writes
+ * state, and f0/val where the node is a SINGLE_TON (f0/val are in/out so a
+ * node's last decode survives, like BucketNode.f0/.value).
+ */
+int afft_classify_exact(const double* residual, const int64_t* index, int64_t count, int64_t b,
+                        int64_t n, double eps_zero, double eps_ratio, int8_t* state,
+                        int64_t* f0, double* val, void* stream);
+
+/*
+ * subtract (peeling.py:186-190): residual[i][r] -= value[i] * exp(-2j*pi*((shifts[r]*f[i]) mod n)/n)
+ * for `count` nodes with `nshift` measurements each (residue check is the caller's).
+ */
+int afft_subtract(double* residual, const int64_t* shifts /* host */, int32_t nshift,
+                  const int64_t* f, const double* value, int64_t count, int64_t n,
+                  void* stream);
+
+/*
+ * truncate_spectrum (oneshot.py:260-263): keep the k largest |v|, ties to the
+ * smaller position; output sorted by that key.  out_count[s] = min(k, count[s]).
+ */
+int afft_truncate(const int64_t* pos, const double* val, const int32_t* count, int32_t cap,
+                  int64_t batch, int32_t k, int64_t* out_pos, double* out_val,
+                  int32_t* out_count, void* stream);
+
+/*
+ * ffast (peeling.py:321-332) over a batch with an explicit cycle plan and the
+ * exact shift set (0,1,2): fused norm → thresholds → build_graph → peel → truncate.
+ * Workspace: afft_ffast_workspace_size bytes of device memory.
+ *   out_pos/out_val [batch][k] (truncated, sorted by (-|v|, f)), out_count [batch]
+ *   all_pos/all_val [batch][sum factors] pre-truncation spectrum (may be NULL)
+ *   all_count, rounds, unresolved [batch] (may be NULL)
+ * max_rounds <= 0 means k + 4 (peeling.py:330).
+ */
+size_t afft_ffast_workspace_size(int64_t n, int dtype, int64_t batch,
+                                 const int64_t* factors /* host */, int32_t ncycles);
+int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+               const int64_t* factors /* host */, int32_t ncycles, int32_t k,
+               int32_t max_rounds, int64_t* out_pos, double* out_val, int32_t* out_count,
+               int64_t* all_pos, double* all_val, int32_t* all_count, int32_t* rounds,
+               int32_t* unresolved, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALIASFFT_B200_H */

@@ -1,0 +1,106 @@
+"""ctypes binding of the C ABI in include/aliasfft_b200.h.
+
+The shared library is built in-tree (``paper_2011_05749_b200/libaliasfft_b200.so``)
+by ``__graft_entry__.build()`` / ``make -C paper_2011_05749_b200/csrc``.  There is
+no CPU fallback: every hot-path call goes through this library on a CUDA
+device, and a missing library or device raises instead of degrading.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libaliasfft_b200.so")
+
+AFFT_C64 = 0
+AFFT_C128 = 1
+
+AFFT_OK = 0
+AFFT_EINVAL = -1
+AFFT_EUNSUPPORTED = -2
+AFFT_ECUDA = -3
+AFFT_ENOMEM = -4
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+_SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes); the list every test checks against the header.
+SIGNATURES = {
+    "afft_last_error": (ctypes.c_char_p, []),
+    "afft_version": (_INT, []),
+    "afft_bucketize": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _P, _I32, _P, _I64, _I64, _I64, _P]),
+    "afft_build_graph": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _I32, _P, _I32, _P, _P]),
+    "afft_sumsq_parts": (_I32, [_I64, _INT]),
+    "afft_sumsq": (_INT, [_P, _INT, _I64, _I64, _I64, _P, _P]),
+    "afft_exact_thresholds": (_INT, [_P, _I32, _I64, _I64, _P, _P]),
+    "afft_peel_exact": (
+        _INT,
+        [_I64, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P],
+    ),
+    "afft_classify_exact": (_INT, [_P, _P, _I64, _I64, _I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]),
+    "afft_subtract": (_INT, [_P, _P, _I32, _P, _P, _I64, _I64, _P]),
+    "afft_truncate": (_INT, [_P, _P, _P, _I32, _I64, _I32, _P, _P, _P, _P]),
+    "afft_ffast_workspace_size": (_SZ, [_I64, _INT, _I64, _P, _I32]),
+    "afft_ffast": (
+        _INT,
+        [_P, _INT, _I64, _I64, _I64, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+    ),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LibraryNotBuilt(ImportError):
+    """The CUDA library is missing: build it with __graft_entry__.build()."""
+
+
+def load():
+    """Load (once) and return the ctypes handle; raises if the .so is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise LibraryNotBuilt(
+                    f"{LIB_PATH} not found; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    """Map a C status to the reference's exception classes."""
+    if status == AFFT_OK:
+        return
+    msg = load().afft_last_error().decode(errors="replace")
+    text = f"{what}: {msg}"
+    if status == AFFT_EINVAL:
+        raise ValueError(text)
+    if status == AFFT_EUNSUPPORTED:
+        from .peeling import UnsupportedSizeError
+
+        raise UnsupportedSizeError(text)
+    if status == AFFT_ENOMEM:
+        raise MemoryError(text)
+    raise RuntimeError(text)
+
+
+def host_i64(values) -> tuple[ctypes.Array, int]:
+    """A host int64 array for the small plan arguments (factors, shifts)."""
+    arr = np.ascontiguousarray(np.asarray(list(values), dtype=np.int64))
+    buf = (ctypes.c_int64 * max(1, arr.size))(*arr.tolist())
+    return buf, int(arr.size)

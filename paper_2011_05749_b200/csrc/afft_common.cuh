@@ -1,0 +1,100 @@
+// Shared device helpers: numpy-faithful complex128 arithmetic, error plumbing.
+//
+// Every floating-point helper here mirrors the operation numpy performs on the
+// reference path, in the same order, and the library is compiled with
+// --fmad=false so no multiply-add is contracted.  That keeps decision values
+// (threshold comparisons, rounding of decoded bins) within an ulp or two of the
+// reference instead of drifting with the compiler's choice of FMAs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/aliasfft_b200.h"
+
+namespace afft {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+#define AFFT_CHECK_LAUNCH(what)                                   \
+  do {                                                            \
+    cudaError_t _e = cudaGetLastError();                          \
+    if (_e != cudaSuccess) return ::afft::cuda_status(_e, what);  \
+  } while (0)
+
+// ---------------------------------------------------------------- complex128
+struct cd {
+  double re, im;
+};
+
+__device__ __forceinline__ cd mk(double r, double i) { return cd{r, i}; }
+__device__ __forceinline__ cd cadd(cd a, cd b) { return cd{a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return cd{a.re - b.re, a.im - b.im}; }
+// numpy complex multiply: (ac - bd) + (ad + bc)i, no FMA.
+__device__ __forceinline__ cd cmul(cd a, cd b) {
+  return cd{__dsub_rn(__dmul_rn(a.re, b.re), __dmul_rn(a.im, b.im)),
+            __dadd_rn(__dmul_rn(a.re, b.im), __dmul_rn(a.im, b.re))};
+}
+__device__ __forceinline__ cd cscale(cd a, double s) {
+  return cd{__dmul_rn(a.re, s), __dmul_rn(a.im, s)};
+}
+// numpy complex divide (Smith's algorithm, numpy/_core/src/umath/loops.c.src
+// CDOUBLE_divide): the form numpy uses for every complex128 '/'.
+__device__ __forceinline__ cd cdiv(cd a, cd b) {
+  double br = fabs(b.re), bi = fabs(b.im);
+  if (br >= bi) {
+    if (br == 0.0 && bi == 0.0) return cd{a.re / br, a.im / br};
+    double rat = b.im / b.re;
+    double scl = 1.0 / __dadd_rn(b.re, __dmul_rn(b.im, rat));
+    return cd{__dmul_rn(__dadd_rn(a.re, __dmul_rn(a.im, rat)), scl),
+              __dmul_rn(__dsub_rn(a.im, __dmul_rn(a.re, rat)), scl)};
+  } else {
+    double rat = b.re / b.im;
+    double scl = 1.0 / __dadd_rn(b.im, __dmul_rn(b.re, rat));
+    return cd{__dmul_rn(__dadd_rn(__dmul_rn(a.re, rat), a.im), scl),
+              __dmul_rn(__dsub_rn(__dmul_rn(a.im, rat), a.re), scl)};
+  }
+}
+__device__ __forceinline__ double cabs_(cd a) { return hypot(a.re, a.im); }
+
+// exp(-2j*pi*prod/n) exactly as numpy evaluates it on the reference path
+// (peeling.py:182-183, oneshot.py:146-147): theta = (-2*pi*prod) * (1/n)
+// (complex/int division is multiplication by the reciprocal in numpy), then
+// (cos theta, sin theta).  prod must already be reduced into [0, n).
+__device__ __forceinline__ cd unit_root(int64_t prod, int64_t n) {
+  double theta = __dmul_rn(__dmul_rn(-6.283185307179586, (double)prod), 1.0 / (double)n);
+  double s, c;
+  sincos(theta, &s, &c);
+  return cd{c, s};
+}
+
+// (a*b) mod n for 0 <= a,b < n < 2^31.5 (no overflow in int64).
+__device__ __forceinline__ int64_t mulmod(int64_t a, int64_t b, int64_t n) {
+  return (a * b) % n;
+}
+__device__ __forceinline__ int64_t pymod(int64_t a, int64_t n) {
+  int64_t r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+// Load one sample as complex128 from a c64 or c128 signal.
+__device__ __forceinline__ cd load_sample(const void* x, int dtype, int64_t off) {
+  if (dtype == AFFT_C64) {
+    float2 v = __ldg(reinterpret_cast<const float2*>(x) + off);
+    return cd{(double)v.x, (double)v.y};
+  }
+  double2 v = __ldg(reinterpret_cast<const double2*>(x) + off);
+  return cd{v.x, v.y};
+}
+
+inline int64_t host_pymod(int64_t a, int64_t n) {
+  int64_t r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+}  // namespace afft

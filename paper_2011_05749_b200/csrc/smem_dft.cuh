@@ -1,0 +1,175 @@
+// Batched mixed-radix forward DFT held entirely in shared memory (K2 in SURVEY §2).
+//
+// Replaces the size-b `np.fft.fft` of bucketize.py:99.  Stockham autosort
+// formulation: stage s with radix R reads butterfly j's inputs at stride n/R,
+// applies the twiddles w_{Ns*R}^{(j mod Ns)*r}, does a size-R DFT and writes
+// the outputs at stride Ns into the other buffer, so the result comes out in
+// natural order without a bit-reversal pass.  Radix 4 and 2 use add-only
+// butterflies; 3..8 use register-resident direct DFTs; larger primes (the 127,
+// 73, 43, 17 ... of co-prime cycle sizes) use an in-place scaled direct DFT.
+// All twiddles come from one table tw[k] = exp(-2*pi*i*k/n) built with
+// sincospi, exact at the quarter points, so every factor is accurate to ~1 ulp.
+#pragma once
+
+#include "afft_common.cuh"
+
+namespace afft {
+
+constexpr int kMaxStages = 40;
+
+struct DftPlan {
+  int32_t n;
+  int32_t nstages;
+  int16_t radix[kMaxStages];
+};
+
+// Host: factor n into radices (4s first, then 2, then odd primes ascending).
+inline bool make_dft_plan(int64_t n, DftPlan* p) {
+  if (n < 1 || n > (1 << 30)) return false;
+  p->n = (int32_t)n;
+  p->nstages = 0;
+  int64_t m = n;
+  while (m % 4 == 0) {
+    if (p->nstages >= kMaxStages) return false;
+    p->radix[p->nstages++] = 4;
+    m /= 4;
+  }
+  if (m % 2 == 0) {
+    p->radix[p->nstages++] = 2;
+    m /= 2;
+  }
+  for (int64_t q = 3; q * q <= m; q += 2) {
+    while (m % q == 0) {
+      if (p->nstages >= kMaxStages || q > 32767) return false;
+      p->radix[p->nstages++] = (int16_t)q;
+      m /= q;
+    }
+  }
+  if (m > 1) {
+    if (p->nstages >= kMaxStages || m > 32767) return false;
+    p->radix[p->nstages++] = (int16_t)m;
+  }
+  return true;
+}
+
+// Fill tw[0..n) cooperatively.
+__device__ __forceinline__ void build_twiddles(cd* tw, int n, int tid, int nthreads) {
+  for (int k = tid; k < n; k += nthreads) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)n, &s, &c);
+    tw[k] = cd{c, s};
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void bfly_small(const cd* __restrict__ src, cd* __restrict__ dst,
+                                           const cd* __restrict__ tw, int n, int nb, int Ns,
+                                           int j) {
+  const int jm = j % Ns;
+  const int tstep = n / (Ns * R);
+  cd v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    cd a = src[j + r * nb];
+    v[r] = (r == 0 || jm == 0) ? a : cmul(a, tw[jm * r * tstep]);
+  }
+  const int idxD = (j / Ns) * Ns * R + jm;
+  if constexpr (R == 2) {
+    dst[idxD] = cadd(v[0], v[1]);
+    dst[idxD + Ns] = csub(v[0], v[1]);
+  } else if constexpr (R == 4) {
+    cd a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+    cd c = cadd(v[1], v[3]), d = csub(v[1], v[3]);
+    dst[idxD] = cadd(a, c);
+    dst[idxD + 2 * Ns] = csub(a, c);
+    dst[idxD + Ns] = cd{b.re + d.im, b.im - d.re};      // b - i*d
+    dst[idxD + 3 * Ns] = cd{b.re - d.im, b.im + d.re};  // b + i*d
+  } else {
+    const int wstep = n / R;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      cd acc = v[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], tw[((r * q) % R) * wstep]));
+      dst[idxD + q * Ns] = acc;
+    }
+  }
+}
+
+// Large prime radix: two passes (scale inputs in place, then direct sums).
+// Each input element belongs to exactly one butterfly, so in-place scaling is
+// race-free within a stage.
+__device__ __forceinline__ void scale_generic(cd* src, const cd* tw, int n, int R, int nb, int Ns,
+                                              int j) {
+  const int jm = j % Ns;
+  if (jm == 0) return;
+  const int tstep = n / (Ns * R);
+  for (int r = 1; r < R; ++r) src[j + r * nb] = cmul(src[j + r * nb], tw[jm * r * tstep]);
+}
+__device__ __forceinline__ void out_generic(const cd* src, cd* dst, const cd* tw, int n, int R,
+                                            int nb, int Ns, int j, int q) {
+  const int jm = j % Ns;
+  const int wstep = n / R;
+  cd acc = src[j];
+  int e = 0;  // (r*q) mod R, updated incrementally
+  for (int r = 1; r < R; ++r) {
+    e += q;
+    if (e >= R) e -= R;
+    acc = cadd(acc, cmul(src[j + r * nb], tw[e * wstep]));
+  }
+  dst[(j / Ns) * Ns * R + jm + q * Ns] = acc;
+}
+
+// Forward DFT of `count` contiguous length-n sequences in smem buffer `a`,
+// ping-ponging with `b`.  Returns the buffer that holds the result.  Must be
+// called by all threads of the block (contains __syncthreads).
+__device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const cd* tw, int tid,
+                        int nthreads) {
+  const int n = p.n;
+  int Ns = 1;
+  for (int s = 0; s < p.nstages; ++s) {
+    const int R = p.radix[s];
+    const int nb = n / R;
+    const int total = count * nb;
+    switch (R) {
+      case 2:
+      case 3:
+      case 4:
+      case 5:
+      case 7:
+        for (int w = tid; w < total; w += nthreads) {
+          const int seq = w / nb, j = w - seq * nb;
+          const cd* src = a + (size_t)seq * n;
+          cd* dst = b + (size_t)seq * n;
+          if (R == 2) bfly_small<2>(src, dst, tw, n, nb, Ns, j);
+          else if (R == 3) bfly_small<3>(src, dst, tw, n, nb, Ns, j);
+          else if (R == 4) bfly_small<4>(src, dst, tw, n, nb, Ns, j);
+          else if (R == 5) bfly_small<5>(src, dst, tw, n, nb, Ns, j);
+          else bfly_small<7>(src, dst, tw, n, nb, Ns, j);
+        }
+        break;
+      default: {
+        for (int w = tid; w < total; w += nthreads) {
+          const int seq = w / nb, j = w - seq * nb;
+          scale_generic(a + (size_t)seq * n, tw, n, R, nb, Ns, j);
+        }
+        __syncthreads();
+        const int outs = total * R;
+        for (int w = tid; w < outs; w += nthreads) {
+          const int q = w % R;
+          const int bw = w / R;
+          const int seq = bw / nb, j = bw - seq * nb;
+          out_generic(a + (size_t)seq * n, b + (size_t)seq * n, tw, n, R, nb, Ns, j, q);
+        }
+      }
+    }
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+    Ns *= R;
+  }
+  return a;
+}
+
+}  // namespace afft

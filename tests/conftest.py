@@ -1,0 +1,78 @@
+"""Test configuration: the `gpu` marker, golden fixtures, seeded inputs.
+
+`-m "not gpu"` tests run on any host (oracle vs goldens, host logic, ABI
+exports); `-m gpu` tests call the CUDA library and are skipped, not failed, when
+no CUDA device is visible.
+"""
+
+import json
+import os
+import sys
+import zlib
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device")
+    try:
+        from hypothesis import settings
+
+        settings.register_profile("deterministic", derandomize=True, deadline=None)
+        settings.load_profile("deterministic")
+    except ImportError:  # pragma: no cover
+        pass
+
+
+def pytest_collection_modifyitems(config, items):
+    import torch
+
+    if torch.cuda.is_available():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device visible")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
+def load_golden(name: str) -> dict:
+    with open(os.path.join(GOLDEN_DIR, name)) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def golden_ffast():
+    return load_golden("golden_ffast.json")
+
+
+def cx(pair) -> complex:
+    return complex(pair[0], pair[1])
+
+
+def case_seed(n, k, snr, seed_base, trial):
+    """The reference bench seed convention (bench.py:123-127)."""
+    tag = "exact" if snr == "exact" else f"{float(snr):.9g}"
+    return zlib.crc32(f"{n}|{k}|{tag}|{seed_base}|{trial}".encode()) ^ (seed_base << 1)
+
+
+def golden_signal(gen: dict) -> np.ndarray:
+    """Regenerate a golden case's input with the package's (pinned) input model."""
+    from paper_2011_05749_b200.signals import generate_test_case
+
+    x = generate_test_case(gen["n"], gen["k"], gen["snr"], gen["seed"],
+                           positions=gen.get("positions")).signal
+    if gen.get("c64"):
+        x = x.astype(np.complex64)
+    return x
+
+
+@pytest.fixture
+def rng():
+    return np.random.default_rng(12345)

@@ -1,0 +1,105 @@
+"""GPU bucketization (gather + small DFT) against the reference goldens and the oracle.
+
+Mirrors the reference's tests/test_bucketize.py: exhaustive alias sums at small
+n, single-tone residues, linearity, ledger accounting — plus config-shaped
+stages (b = 49..51, 127..129, 1024 with the sFFT-DT structured shifts).
+Tolerance: 1e-12 relative to the largest bucket magnitude (complex128
+arithmetic; the DFT differs from pocketfft only in rounding).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import cx, golden_signal
+from oracle import ffast as of
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(got, want, rel=1e-12):
+    scale = max(1.0, float(np.max(np.abs(want))))
+    return float(np.max(np.abs(np.asarray(got) - np.asarray(want)))) <= rel * scale
+
+
+def test_goldens(golden_ffast):
+    from paper_2011_05749_b200 import bucketize
+
+    for case in golden_ffast["bucketize"]:
+        if "x" in case:
+            x = np.array([cx(v) for v in case["x"]])
+        else:
+            x = golden_signal(case["gen"])  # complex64 stays complex64 on the device
+        got = bucketize(x, case["b"], case["tau"]).values
+        want = np.array([cx(v) for v in case["values"]])
+        assert _close(got, want), (case["b"], case["tau"])
+
+
+def test_alias_sum_exhaustive_small(rng):
+    from paper_2011_05749_b200 import bucketize_set, dense_dft
+
+    for n in (8, 12, 20, 30, 49, 60):
+        x = rng.normal(size=n) + 1j * rng.normal(size=n)
+        dense = dense_dft(x)
+        for b in [d for d in range(1, n + 1) if n % d == 0]:
+            taus = list(range(-2, n + 2))
+            got = bucketize_set(x, b, taus)
+            for tau, sp in zip(taus, got):
+                # alias sum: y[i] = sum_j X[j*b + i] * w^(tau*(j*b+i))
+                f = np.arange(n)
+                contrib = dense * np.exp(-2j * np.pi * ((tau * f) % n) / n)
+                want = np.array([contrib[i::b].sum() for i in range(b)])
+                assert np.allclose(sp.values, want, atol=1e-9)
+
+
+@pytest.mark.parametrize("n,b", [(124950, 49), (124950, 50), (124950, 51), (2097024, 127),
+                                 (2097024, 128), (2097024, 129), (1 << 22, 1024),
+                                 (1 << 24, 4096), (511 * 512 * 8, 511), (3 * 17 * 19 * 73, 73 * 17)])
+def test_config_sizes_vs_oracle(n, b):
+    from paper_2011_05749_b200.bucketize import bucketize_device
+
+    rng = np.random.default_rng(n + b)
+    x = (rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.complex128)
+    shifts = [0, 1, 2, -4, 7, n - 1, 12345]
+    got = bucketize_device(torch.from_numpy(x).cuda(), b, shifts).cpu().numpy()
+    want = of.bucket_values(x, b, shifts)
+    assert _close(got, want, 1e-12)
+
+
+def test_complex64_input_upcasts_exactly():
+    from paper_2011_05749_b200.bucketize import bucketize_device
+
+    rng = np.random.default_rng(5)
+    x = (rng.normal(size=129 * 64) + 1j * rng.normal(size=129 * 64)).astype(np.complex64)
+    got = bucketize_device(torch.from_numpy(x).cuda(), 129, [0, 1, 2]).cpu().numpy()
+    want = of.bucket_values(x.astype(np.complex128), 129, [0, 1, 2])
+    assert _close(got, want, 1e-12)
+
+
+def test_single_tone_residue_and_linearity(rng):
+    from paper_2011_05749_b200 import SparseSpectrum, bucketize, inverse_dft
+
+    n = 24
+    for f in (0, 5, 17):
+        x = inverse_dft(SparseSpectrum(n, {f: 1.0}))
+        for b in (4, 6, 8):
+            for tau in (0, 1, 7, -3):
+                out = bucketize(x, b, tau).values
+                assert abs(out[f % b] - np.exp(-2j * np.pi * ((tau * f) % n) / n)) < 1e-9
+                assert np.max(np.abs(np.delete(out, f % b))) < 1e-9
+    x = rng.normal(size=20) + 1j * rng.normal(size=20)
+    y = rng.normal(size=20) + 1j * rng.normal(size=20)
+    a, c = 2.0 - 1j, -0.5 + 3j
+    comb = bucketize(a * x + c * y, 5, 3).values
+    sep = a * bucketize(x, 5, 3).values + c * bucketize(y, 5, 3).values
+    assert np.linalg.norm(comb - sep) <= 1e-9 * max(1.0, np.linalg.norm(sep))
+
+
+def test_errors_and_ledger():
+    from paper_2011_05749_b200 import SampleLedger, bucketize, bucketize_set
+
+    with pytest.raises(ValueError):
+        bucketize(np.zeros(10), 4, 0)
+    ledger = SampleLedger(24)
+    bucketize_set(np.zeros(24), 6, [0, 1, 2, 3, 10], ledger)
+    assert ledger.count == 30 and ledger.unique_count <= 24
