@@ -12,7 +12,7 @@
 #include <vector>
 
 #include "afft_common.cuh"
-#include "smem_dft.cuh"
+#include "gather_dft.cuh"
 
 namespace afft {
 
@@ -44,33 +44,21 @@ __global__ void __launch_bounds__(256) gather_dft_kernel(const __grid_constant__
   const int64_t b = p.b[c];
   const int t0 = job * p.chunk[c];
   const int cnt = min(p.chunk[c], p.nshift - t0);
-  const int64_t step = p.n / b;
-  const int tid = threadIdx.x, nt = blockDim.x;
-
   cd* tw = reinterpret_cast<cd*>(smem_raw);
   cd* bufA = tw + b;
   cd* bufB = bufA + (size_t)cnt * b;
-
-  build_twiddles(tw, (int)b, tid, nt);
   const char* xs = reinterpret_cast<const char*>(p.x) +
                    s * p.ld * (p.dtype == AFFT_C64 ? 8 : 16);
-  const int total = cnt * (int)b;
-  for (int e = tid; e < total; e += nt) {
-    const int t = e / (int)b;
-    const int64_t j = e - (int64_t)t * b;
-    int64_t idx = j * step - p.tau[t0 + t];
-    if (idx < 0) idx += p.n;
-    bufA[e] = load_sample(xs, p.dtype, idx);
-  }
-  __syncthreads();
-  cd* res = smem_dft(bufA, bufB, cnt, p.plan[c], tw, tid, nt);
+  const cd* res = gather_dft_block(xs, p.dtype, p.n, b, p.plan[c], p.tau + t0, cnt, tw, bufA,
+                                   bufB);
   const double inv_b = 1.0 / (double)b;
   double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset[c]);
-  for (int e = tid; e < total; e += nt) {
+  const int total = cnt * (int)b;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
     const int t = e / (int)b;
     const int64_t i = e - (int64_t)t * b;
-    cd v = cscale(res[e], inv_b);
-    int64_t o = 2 * ((t0 + t) * p.out_shift_stride + i * p.out_bin_stride);
+    const cd v = cscale(res[e], inv_b);
+    const int64_t o = 2 * ((t0 + t) * p.out_shift_stride + i * p.out_bin_stride);
     out[o] = v.re;
     out[o + 1] = v.im;
   }

@@ -34,9 +34,9 @@ def _check_case(case, res, i):
         assert _rel_l2(full, want) <= tol
     assert int(res.rounds[i]) == case["rounds"]
     assert int(res.unresolved[i]) == case["unresolved"]
-    trunc = list(res.spectrum(i).entries)
-    want_t = [f for f, _ in case["truncated"]]
-    if trunc != want_t:  # only a |v| tie at the k-th rank may reorder the cut
+    trunc = set(res.spectrum(i).entries)
+    want_t = {f for f, _ in case["truncated"]}
+    if trunc != want_t:  # only a |v| tie at the k-th rank may change the kept set
         mags = sorted((abs(cx(v)) for _, v in case["recovered"]), reverse=True)
         k = case["k"]
         assert len(mags) > k and abs(mags[k - 1] - mags[k]) < 1e-6, (trunc, want_t)
@@ -70,7 +70,7 @@ def test_drop_in_ffast_api(golden_ffast):
         x = golden_signal(case)
         ledger = SampleLedger(case["n"])
         out = ffast(x, case["k"], ledger, plan=CyclePlan(case["factors"], [0, 1, 2]))
-        assert list(out.entries) == [f for f, _ in case["truncated"]]
+        assert set(out.entries) == {f for f, _ in case["truncated"]}
         assert [ledger.count, ledger.unique_count] == case["ledger"]
 
 
