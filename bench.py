@@ -219,8 +219,9 @@ def run_ours(args):
     pos = res.pos.cpu().numpy()
     exact = sum(int(cnt[i]) == K and set(pos[i, :K].tolist()) == set(truths[i][0].tolist())
                 for i in range(per))
-    sound = all(set(pos[i, :int(cnt[i])].tolist()) <= set(truths[i][0].tolist())
-                for i in range(per))
+    kept = sum(int(c) for c in cnt)
+    true_kept = sum(len(set(pos[i, :int(cnt[i])].tolist()) & set(truths[i][0].tolist()))
+                    for i in range(per))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -268,7 +269,7 @@ def run_ours(args):
                 "signals_total": total, "signals_per_rank": per,
                 "l2": "inputs 137 GB >> 126 MB L2 (no flush needed)",
                 "parallelism": f"signal-sharded x{world}, NCCL all-gather of result slots",
-                "exact_recovered_fraction": exact / per, "recovered_subset_of_truth": sound,
+                "exact_recovered_fraction": exact / per, "true_tone_fraction": true_kept / max(1, kept),
                 "kernel_ms": kern_ms,
             },
             "roofline": {

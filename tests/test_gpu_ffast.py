@@ -152,10 +152,12 @@ def test_edge_cases():
             assert abs(v - dense[f]) < 1e-6
 
 
-def test_config5_full_batch_properties():
-    """Config 5 shape at a full-size batch, checked by size-independent properties:
-    every recovered tone is a true tone with |v - truth| < 1e-4, and the oracle
-    agrees bit-exactly on a subsample of the batch."""
+def test_config5_full_batch_vs_oracle():
+    """Config 5 shape (N=2,097,024, K=256, 127/128/129, complex64) on a 256-signal batch:
+    the pre-truncation support of EVERY signal equals the oracle's bit for bit, in
+    insertion order (the reference itself emits occasional spurious singletons, so
+    "recovered is a subset of truth" is not a valid property), and >= 99% of all
+    recovered tones are true tones within 1e-4."""
     from paper_2011_05749_b200 import ffast_batch
     from paper_2011_05749_b200.signals import draw_truth
 
@@ -170,13 +172,14 @@ def test_config5_full_batch_properties():
     x = (torch.fft.ifft(spec, dim=1) * n).to(torch.complex64)
     del spec
     res = ffast_batch(x, k, factors)
-    exact = 0
+    xh = x.cpu().numpy()
+    good = total = 0
     for i in range(batch):
         got = res.full_spectrum(i).entries
-        assert set(got) <= set(truths[i])
-        assert all(abs(v - truths[i][f]) < 1e-4 for f, v in got.items())
-        exact += len(got) == k
-    assert exact >= 0.8 * batch
-    for i in range(0, batch, 64):
-        _, o = of.ffast(x[i].cpu().numpy().astype(np.complex128), k, factors)
-        assert list(o["recovered"]) == list(res.full_spectrum(i).entries)
+        _, o = of.ffast(xh[i].astype(np.complex128), k, factors)
+        assert list(o["recovered"]) == list(got), i
+        assert int(res.rounds[i]) == o["rounds"] and int(res.unresolved[i]) == o["unresolved"]
+        for f, v in got.items():
+            total += 1
+            good += f in truths[i] and abs(v - truths[i][f]) < 1e-4
+    assert good >= 0.99 * total
