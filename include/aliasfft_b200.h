@@ -16,7 +16,7 @@
  *    (AFFT_C64, float2) or complex128 (AFFT_C128, double2); all arithmetic after
  *    the gather is IEEE float64 with no FMA contraction, as numpy computes.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
- *    Calls only enqueue work; nothing synchronises except afft_sync_device_flag.
+ *    Calls only enqueue work, except those documented as synchronising.
  *  - Return codes: 0 OK, <0 error (AFFT_E*); afft_last_error() gives the
  *    thread-local message.  No exception crosses the ABI.
  *  - Batched layout: `batch` signals, signal s starting at x + s*ld elements.
@@ -155,6 +155,60 @@ int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                int32_t max_rounds, int64_t* out_pos, double* out_val, int32_t* out_count,
                int64_t* all_pos, double* all_val, int32_t* all_count, int32_t* rounds,
                int32_t* unresolved, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ R-FFAST (noisy) */
+
+/* Node energies ||vec_e||^2 over `nshift` measurements each (peeling.py:354-357). */
+int afft_node_energies(const double* vec, int32_t nshift, int64_t count, double* energy,
+                       void* stream);
+
+/*
+ * robust_thresholds (peeling.py:335-351) per signal over `count` energies:
+ * sigma = sqrt(median(E[mask]) / r), floor = 1e-8 * sqrt(max E),
+ * t0 = max(1.5 sigma sqrt(r), floor), t1 = max(2.5 sigma sqrt(r), floor).
+ * mask [batch][count] selects the median's reference set (NULL = all; an empty
+ * set falls back to all, dsfft.py:164-166).
+ */
+int afft_robust_thresholds(const double* energy, const uint8_t* mask, int64_t count,
+                           int64_t batch, int32_t r, double* t0, double* t1, void* stream);
+
+/* Workspace bytes for afft_peel_noisy / (with batch = node count) the per-node search. */
+size_t afft_noisy_workspace_size(int64_t n, int64_t batch, const int64_t* factors /* host */,
+                                 int32_t ncycles, int32_t c, int32_t m);
+
+/*
+ * singleton_search_noisy (peeling.py:222-250) for `count` nodes of one cycle size b:
+ * residual [count][c*m], index [count]; shifts (host) = SearchPlan.shifts, weights
+ * (host) = kay_weights(m).  Outputs f0, val (complex128), resnorm per node.
+ * Workspace: afft_noisy_workspace_size(n, count, &b, 1, c, m).  Synchronises.
+ */
+int afft_singleton_search_noisy(const double* residual, const int64_t* index, int64_t count,
+                                int64_t b, int64_t n, const int64_t* shifts, int32_t nshift,
+                                int32_t c, int32_t m, const double* weights, int64_t* f0,
+                                double* val, double* resnorm, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* classify_noisy (peeling.py:253-267) for `count` nodes: search + the t0/t1 gates. */
+int afft_classify_noisy(const double* residual, const int64_t* index, int64_t count, int64_t b,
+                        int64_t n, const int64_t* shifts, int32_t nshift, int32_t c, int32_t m,
+                        const double* weights, double t0, double t1, int8_t* state,
+                        int64_t* f0, double* val, double* resnorm, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/*
+ * peel_decode, noisy mode (peeling.py:270-313 with classify_noisy 253-267) over a
+ * batch of graphs in node layout residual[s][g][c*m]: rounds of
+ * prep -> exhaustive search -> fit -> harvest/subtract on the device; the host
+ * only reads one counter per round to stop.  t0/t1 [batch] per-signal gates.
+ * State/f0/val/rec_* as in afft_peel_exact.  Synchronises.
+ */
+int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors /* host */, int32_t ncycles,
+                    const int64_t* shifts /* host */, int32_t nshift, int32_t c, int32_t m,
+                    const double* weights /* host */, double* residual, int8_t* state,
+                    int64_t* node_f0, double* node_val, const double* t0, const double* t1,
+                    int32_t max_rounds, int64_t* rec_pos, double* rec_val, int32_t rec_cap,
+                    int32_t* rec_count, int32_t* rounds, int32_t* unresolved, void* workspace,
+                    size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,7 @@ _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 _INT = ctypes.c_int
 _SZ = ctypes.c_size_t
+_D = ctypes.c_double
 
 # name -> (restype, argtypes); the list every test checks against the header.
 SIGNATURES = {
@@ -52,6 +53,17 @@ SIGNATURES = {
         _INT,
         [_P, _INT, _I64, _I64, _I64, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
     ),
+    "afft_node_energies": (_INT, [_P, _I32, _I64, _P, _P]),
+    "afft_robust_thresholds": (_INT, [_P, _P, _I64, _I64, _I32, _P, _P, _P]),
+    "afft_noisy_workspace_size": (_SZ, [_I64, _I64, _P, _I32, _I32, _I32]),
+    "afft_singleton_search_noisy": (
+        _INT, [_P, _P, _I64, _I64, _I64, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "afft_classify_noisy": (
+        _INT, [_P, _P, _I64, _I64, _I64, _P, _I32, _I32, _I32, _P, _D, _D, _P, _P, _P, _P, _P,
+               _SZ, _P]),
+    "afft_peel_noisy": (
+        _INT, [_I64, _I64, _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P,
+               _P, _I32, _P, _P, _P, _P, _SZ, _P]),
 }
 
 _lock = threading.Lock()
@@ -97,6 +109,11 @@ def check(status: int, what: str) -> None:
     if status == AFFT_ENOMEM:
         raise MemoryError(text)
     raise RuntimeError(text)
+
+
+def host_f64(values) -> ctypes.Array:
+    vals = [float(v) for v in values]
+    return (ctypes.c_double * max(1, len(vals)))(*vals)
 
 
 def host_i64(values) -> tuple[ctypes.Array, int]:

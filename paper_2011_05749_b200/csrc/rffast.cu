@@ -1,0 +1,847 @@
+// K3 (noisy) + K4 (noisy) + K7 (median): R-FFAST on the GPU.
+//
+//   robust_thresholds  (peeling.py:335-358)  per-signal median of node energies
+//                      by an in-smem bitonic sort, T0/T1 gates;
+//   singleton_search_noisy (peeling.py:222-250)  the exhaustive candidate scan:
+//                      for every residue-class candidate cand = i + b*t and every
+//                      stride 2^j, wrap(est_j - target_j(cand))^2 summed in j
+//                      order, first argmin; then the 1-column least-squares fit;
+//   peel_decode(mode="noisy") (peeling.py:270-313 with classify_noisy 253-267)
+//                      as rounds of kernels over device-resident state: prep
+//                      (zero-ton gate, phase estimates, compacted active list)
+//                      → search → finalize → harvest/subtract, one host sync per
+//                      round for the loop exit.
+//
+// Bit-faithfulness of the scan: target is
+// ((-2*pi) * r) / n with r = (2^j * cand) mod n carried exactly by doubling
+// mod n; _wrap(p) = ((p + pi) mod 2pi) - pi with numpy's floor-mod sign rule,
+// evaluated exactly (x - q*2pi is exact by Sterbenz for q in {1, 2}); no FMA
+// contraction (--fmad=false); scores summed in j order; ties keep the first
+// candidate.  Only atan2 differs from glibc, by <= 2 ulp in the estimates.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "afft_common.cuh"
+#include "peel_core.cuh"
+
+namespace afft {
+
+constexpr int kMaxStrides = 40;
+constexpr int kMaxRounds = 16;  // rounds per stride (m)
+constexpr int kSearchThreads = 256;
+constexpr int kCandPerThread = 16;
+constexpr int kChunk = kSearchThreads * kCandPerThread;
+constexpr double kPi = 3.141592653589793;
+constexpr double kTwoPi = 6.283185307179586;
+
+struct NoisyPlan {
+  int64_t n;
+  int ncycles;
+  int nodes;
+  int R;  // = c * m
+  int c, m;
+  int hmask;
+  int64_t b[AFFT_MAX_CYCLES];
+  int32_t base[AFFT_MAX_CYCLES + 1];
+  double w[kMaxRounds];          // Kay weights (m - 1 entries)
+  int64_t tau[AFFT_MAX_SHIFTS];  // shifts reduced mod n
+};
+
+// numpy: np.remainder(p + pi, 2pi) - pi
+__device__ __forceinline__ double wrap_phase(double p) {
+  const double x = __dadd_rn(p, kPi);
+  double r;
+  if (x >= 0.0 && x < kTwoPi) {
+    r = x;
+  } else if (x >= kTwoPi && x < 2.0 * kTwoPi) {
+    r = __dsub_rn(x, kTwoPi);  // exact (Sterbenz)
+  } else if (x >= 2.0 * kTwoPi && x < 3.0 * kTwoPi) {
+    r = __dsub_rn(x, 2.0 * kTwoPi);  // exact (Sterbenz), 2*2pi exact
+  } else if (x < 0.0 && x >= -kTwoPi) {
+    r = __dadd_rn(x, kTwoPi);  // fmod(x) = x (<0): numpy adds the divisor
+  } else {
+    r = fmod(x, kTwoPi);
+    if (r != 0.0 && r < 0.0) r = __dadd_rn(r, kTwoPi);
+  }
+  if (r == 0.0) r = 0.0;  // copysign(0, +2pi)
+  return __dsub_rn(r, kPi);
+}
+
+// Phase estimate of stride j (peeling.py:241-244): Kay-weighted mean of the
+// re-centred consecutive phase differences of y[j*m .. j*m+m-1].
+__device__ __forceinline__ double stride_estimate(const cd* y, int m, const double* w) {
+  double d[kMaxRounds];
+  for (int t = 0; t + 1 < m; ++t) {
+    const cd a = y[t + 1], b = y[t];
+    // a * conj(b), numpy complex multiply on (b.re, -b.im)
+    const double re = __dsub_rn(__dmul_rn(a.re, b.re), __dmul_rn(a.im, -b.im));
+    const double im = __dadd_rn(__dmul_rn(a.re, -b.im), __dmul_rn(a.im, b.re));
+    d[t] = atan2(im, re);
+  }
+  const double d0 = d[0];
+  double est = 0.0;
+  for (int t = 0; t + 1 < m; ++t) {
+    const double dt = __dadd_rn(d0, wrap_phase(__dsub_rn(d[t], d0)));
+    est = __dadd_rn(est, __dmul_rn(w[t], dt));
+  }
+  return est;
+}
+
+__device__ __forceinline__ int noisy_cycle(const NoisyPlan& P, int g) {
+  int c = 0;
+  while (g >= P.base[c + 1]) ++c;
+  return c;
+}
+
+// -------------------------------------------------------------- candidate scan
+
+// One CTA scores kChunk consecutive candidates t of one active node.
+// Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
+__global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
+    int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
+    const double* __restrict__ est, int chunks, double* __restrict__ part_score,
+    int32_t* __restrict__ part_t) {
+  __shared__ double s_est[kMaxStrides];
+  __shared__ double w_score[kSearchThreads / 32];
+  __shared__ int32_t w_t[kSearchThreads / 32];
+  const int a = blockIdx.y;
+  const int chunk = blockIdx.x;
+  const int64_t b = act_b[a];
+  const int64_t L = n / b;
+  const int64_t t0 = (int64_t)chunk * kChunk;
+  if (threadIdx.x < c) s_est[threadIdx.x] = est[(int64_t)a * c + threadIdx.x];
+  __syncthreads();
+  const int64_t idx = act_index[a];
+  const double dn = (double)n;
+  double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  int32_t bt = INT32_MAX;
+  if (t0 < L) {
+    const int64_t t1 = min(L, t0 + (int64_t)kChunk);
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads) {
+      int64_t r = idx + b * t;  // cand = (index + b*t) mod n, already < n
+      double sc = 0.0;
+      for (int j = 0; j < c; ++j) {
+        const double tgt = __ddiv_rn(__dmul_rn(-kTwoPi, (double)r), dn);
+        const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
+        sc = __dadd_rn(sc, __dmul_rn(wv, wv));
+        r <<= 1;
+        if (r >= n) r -= n;
+      }
+      if (sc < best) {
+        best = sc;
+        bt = (int32_t)t;
+      }
+    }
+  }
+  // block argmin, ties -> smaller t
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ob < best || (ob == best && ot < bt)) {
+      best = ob;
+      bt = ot;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    w_score[threadIdx.x >> 5] = best;
+    w_t[threadIdx.x >> 5] = bt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b0 = w_score[0];
+    int32_t t0w = w_t[0];
+    for (int w = 1; w < kSearchThreads / 32; ++w) {
+      if (w_score[w] < b0 || (w_score[w] == b0 && w_t[w] < t0w)) {
+        b0 = w_score[w];
+        t0w = w_t[w];
+      }
+    }
+    part_score[(int64_t)a * chunks + chunk] = b0;
+    part_t[(int64_t)a * chunks + chunk] = t0w;
+  }
+}
+
+// Phase estimates of the active nodes (one thread per (node, stride)).
+__global__ void noisy_est_kernel(int A, int c, int m, const int64_t* __restrict__ act_row,
+                                 const double* __restrict__ residual, int R,
+                                 const __grid_constant__ NoisyPlan P, double* __restrict__ est) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)A * c) return;
+  const int64_t a = e / c;
+  const int j = (int)(e - a * c);
+  const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * R + (int64_t)j * m;
+  est[e] = stride_estimate(y, m, P.w);
+}
+
+// Reduce the chunk partials, then the least-squares fit (peeling.py:247-250):
+// x = a^H y / a^H a with a_r = exp(-2j*pi*((tau_r*f0) mod n)/n), resnorm = ||a x - y||.
+// One warp per active node.
+__global__ void noisy_finalize_kernel(int A, int chunks, const double* __restrict__ part_score,
+                                      const int32_t* __restrict__ part_t,
+                                      const int64_t* __restrict__ act_row,
+                                      const int64_t* __restrict__ act_index,
+                                      const int64_t* __restrict__ act_b,
+                                      const double* __restrict__ residual,
+                                      const __grid_constant__ NoisyPlan P,
+                                      int64_t* __restrict__ out_f0, double* __restrict__ out_val,
+                                      double* __restrict__ out_res) {
+  const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (a >= A) return;
+  double best = __longlong_as_double(0x7ff0000000000000LL);
+  int32_t bt = INT32_MAX;
+  for (int ch = lane; ch < chunks; ch += 32) {
+    const double sc = part_score[(int64_t)a * chunks + ch];
+    const int32_t t = part_t[(int64_t)a * chunks + ch];
+    if (sc < best || (sc == best && t < bt)) {
+      best = sc;
+      bt = t;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ob < best || (ob == best && ot < bt)) {
+      best = ob;
+      bt = ot;
+    }
+  }
+  if (bt == INT32_MAX) bt = 0;  // all-NaN scores: numpy argmin would return the first NaN
+  const int64_t n = P.n;
+  const int64_t f0 = (act_index[a] + act_b[a] * (int64_t)bt) % n;
+  const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * P.R;
+  // a^H y and a^H a
+  double nre = 0.0, nim = 0.0, den = 0.0;
+  for (int r = lane; r < P.R; r += 32) {
+    const cd at = unit_root(mulmod(P.tau[r], f0, n), n);
+    const cd yv = y[r];
+    nre += at.re * yv.re + at.im * yv.im;
+    nim += at.re * yv.im - at.im * yv.re;
+    den += at.re * at.re + at.im * at.im;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nre += __shfl_xor_sync(0xffffffffu, nre, o);
+    nim += __shfl_xor_sync(0xffffffffu, nim, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  const cd x = cd{nre / den, nim / den};
+  double rs = 0.0;
+  for (int r = lane; r < P.R; r += 32) {
+    const cd at = unit_root(mulmod(P.tau[r], f0, n), n);
+    const cd d = csub(cmul(at, x), y[r]);
+    rs += d.re * d.re + d.im * d.im;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+  if (lane == 0) {
+    out_f0[a] = f0;
+    reinterpret_cast<cd*>(out_val)[a] = x;
+    out_res[a] = sqrt(rs);
+  }
+}
+
+// -------------------------------------------------------------- decoder rounds
+
+__device__ __forceinline__ double node_norm(const cd* y, int R) {
+  double sre = 0.0, sim = 0.0;
+  for (int r = 0; r < R; ++r) sre = __dadd_rn(sre, __dmul_rn(y[r].re, y[r].re));
+  for (int r = 0; r < R; ++r) sim = __dadd_rn(sim, __dmul_rn(y[r].im, y[r].im));
+  return sqrt(__dadd_rn(sre, sim));
+}
+
+// classify_noisy's zero-ton gate (peeling.py:257-259) for every live, changed
+// node of every unfinished signal; survivors join the active list.
+__global__ void noisy_prep_kernel(int64_t batch, const __grid_constant__ NoisyPlan P,
+                                  const double* __restrict__ residual, int8_t* __restrict__ state,
+                                  int8_t* __restrict__ dirty, const int32_t* __restrict__ done,
+                                  const double* __restrict__ t0, int32_t* __restrict__ counter,
+                                  int64_t* __restrict__ act_row, int64_t* __restrict__ act_index,
+                                  int64_t* __restrict__ act_b) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= batch * P.nodes) return;
+  const int64_t s = e / P.nodes;
+  const int g = (int)(e - s * P.nodes);
+  if (done[s]) return;
+  const int8_t st = state[e];
+  if (st == AFFT_RESOLVED || st == AFFT_ZERO_TON || !dirty[e]) return;
+  const cd* y = reinterpret_cast<const cd*>(residual) + e * P.R;
+  if (node_norm(y, P.R) <= t0[s]) {
+    state[e] = AFFT_ZERO_TON;
+    dirty[e] = 0;
+    return;
+  }
+  const int slot = atomicAdd(counter, 1);
+  const int c = noisy_cycle(P, g);
+  act_row[slot] = e;
+  act_index[slot] = g - P.base[c];
+  act_b[slot] = P.b[c];
+}
+
+// SINGLE_TON iff resnorm <= T1 (peeling.py:260-267).
+__global__ void noisy_apply_kernel(int A, const __grid_constant__ NoisyPlan P,
+                                   const int64_t* __restrict__ act_row,
+                                   const int64_t* __restrict__ f0s, const double* __restrict__ vals,
+                                   const double* __restrict__ res, const double* __restrict__ t1,
+                                   int8_t* __restrict__ state, int8_t* __restrict__ dirty,
+                                   int64_t* __restrict__ node_f0, double* __restrict__ node_val) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const int64_t e = act_row[a];
+  const int64_t s = e / P.nodes;
+  dirty[e] = 0;
+  if (res[a] <= t1[s]) {
+    state[e] = AFFT_SINGLE_TON;
+    node_f0[e] = f0s[a];
+    reinterpret_cast<cd*>(node_val)[e] = reinterpret_cast<const cd*>(vals)[a];
+  } else {
+    state[e] = AFFT_MULTI_TON;
+  }
+}
+
+// Harvest (first-found) + subtract for one signal per CTA (peeling.py:296-308).
+__global__ void __launch_bounds__(512) noisy_harvest_kernel(
+    const __grid_constant__ NoisyPlan P, double* __restrict__ residual, int8_t* __restrict__ state,
+    int8_t* __restrict__ dirty, const int64_t* __restrict__ node_f0,
+    const double* __restrict__ node_val, int32_t* __restrict__ done, int64_t* __restrict__ rec_pos,
+    double* __restrict__ rec_val, int rec_cap, int32_t* __restrict__ rec_count,
+    int32_t* __restrict__ rounds, int32_t* __restrict__ total_found) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tmp[32];
+  __shared__ int carry;
+  const int64_t s = blockIdx.x;
+  if (done[s]) return;
+  const int N = P.nodes;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  unsigned long long* hash = reinterpret_cast<unsigned long long*>(smem_raw);
+  int* flag = reinterpret_cast<int*>(hash + P.hmask + 1);
+  int32_t* found_g = flag + N;
+  int32_t* found_res = found_g + N;          // [nf][ncycles]
+  int8_t* hv = reinterpret_cast<int8_t*>(found_res + (size_t)N * P.ncycles);
+  const int64_t so = s * N;
+  int64_t* rpos = rec_pos + s * (int64_t)rec_cap;
+  cd* rval = reinterpret_cast<cd*>(rec_val) + s * (int64_t)rec_cap;
+  const int rc = rec_count[s];
+  for (int h = tid; h <= P.hmask; h += nt) hash[h] = kEmpty;
+  for (int g = tid; g < N; g += nt) hv[g] = 0;
+  __syncthreads();
+  for (int i = tid; i < rc; i += nt) hash_insert(hash, P.hmask, rpos[i]);
+  if (tid == 0) rounds[s] += 1;
+  __syncthreads();
+  for (int g = tid; g < N; g += nt) {
+    int take = 0;
+    if (state[so + g] == AFFT_SINGLE_TON) {
+      const int64_t f = node_f0[so + g];
+      if (!hash_contains(hash, P.hmask, f)) {
+        take = 1;
+        const int c = noisy_cycle(P, g);
+        for (int c2 = 0; c2 < c; ++c2) {
+          const int g2 = P.base[c2] + (int)(f % P.b[c2]);
+          if (state[so + g2] == AFFT_SINGLE_TON && node_f0[so + g2] == f) {
+            take = 0;
+            break;
+          }
+        }
+      }
+    }
+    flag[g] = take;
+    if (take) hv[g] = 1;
+  }
+  __syncthreads();
+  const int nf = block_exclusive_scan(flag, N, warp_tmp, &carry);
+  if (nf == 0) {
+    if (tid == 0) done[s] = 1;
+    return;
+  }
+  for (int g = tid; g < N; g += nt) {
+    if (hv[g]) {
+      found_g[flag[g]] = g;
+      hv[g] = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nf; i += nt) state[so + found_g[i]] = AFFT_RESOLVED;
+  for (int e = tid; e < nf * P.ncycles; e += nt) {
+    const int i = e / P.ncycles, c = e - i * P.ncycles;
+    const int32_t r = (int32_t)(node_f0[so + found_g[i]] % P.b[c]);
+    found_res[e] = r;
+    hv[P.base[c] + r] = 1;
+  }
+  __syncthreads();
+  // subtract: one warp per hit node, lanes over the R measurements, found order
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int g = wid; g < N; g += nw) {
+    if (!hv[g]) continue;
+    const int c = noisy_cycle(P, g);
+    const int idx = g - P.base[c];
+    cd* y = reinterpret_cast<cd*>(residual) + (so + g) * P.R;
+    for (int r = lane; r < P.R; r += 32) {
+      cd acc = y[r];
+      for (int i = 0; i < nf; ++i) {
+        if (found_res[i * P.ncycles + c] != idx) continue;
+        const int64_t f = node_f0[so + found_g[i]];
+        const cd v = reinterpret_cast<const cd*>(node_val)[so + found_g[i]];
+        acc = csub(acc, cmul(v, unit_root(mulmod(P.tau[r], f, P.n), P.n)));
+      }
+      y[r] = acc;
+    }
+    if (lane == 0) dirty[so + g] = 1;
+  }
+  for (int i = tid; i < nf; i += nt) {
+    rpos[rc + i] = node_f0[so + found_g[i]];
+    rval[rc + i] = reinterpret_cast<const cd*>(node_val)[so + found_g[i]];
+  }
+  if (tid == 0) {
+    rec_count[s] = rc + nf;
+    atomicAdd(total_found, nf);
+  }
+}
+
+__global__ void count_multi_kernel(int64_t batch, int N, const int8_t* __restrict__ state,
+                                   int32_t* __restrict__ unresolved) {
+  const int64_t s = blockIdx.x;
+  int cnt = 0;
+  for (int g = threadIdx.x; g < N; g += blockDim.x) cnt += state[s * N + g] == AFFT_MULTI_TON;
+  __shared__ int red;
+  if (threadIdx.x == 0) red = 0;
+  __syncthreads();
+  atomicAdd(&red, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) unresolved[s] = red;
+}
+
+// -------------------------------------------------------------- thresholds
+
+// energies[e] = ||vec_e||^2 (peeling.py:355-357: float(norm(vec) ** 2))
+__global__ void node_energy_kernel(int64_t count, int R, const double* __restrict__ vec,
+                                   double* __restrict__ energy) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  const double nv = node_norm(reinterpret_cast<const cd*>(vec) + e * R, R);
+  energy[e] = __dmul_rn(nv, nv);
+}
+
+// robust_thresholds (peeling.py:335-351) per signal: median of the masked
+// energies (all when mask is null), floor from the max of all energies.
+__global__ void robust_thresholds_kernel(int count, int pow2, const double* __restrict__ energy,
+                                         const uint8_t* __restrict__ mask, int r,
+                                         double* __restrict__ t0, double* __restrict__ t1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* v = reinterpret_cast<double*>(smem_raw);
+  __shared__ int m_count;
+  __shared__ double m_max;
+  const int64_t s = blockIdx.x;
+  const double* E = energy + s * (int64_t)count;
+  const uint8_t* M = mask ? mask + s * (int64_t)count : nullptr;
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    double mx = 0.0;  // scale.max(initial=0.0)
+    for (int i = 0; i < count; ++i) {
+      mx = fmax(mx, E[i]);
+      if (!M || M[i]) v[cnt++] = E[i];
+    }
+    if (M && cnt == 0) {  // empty reference set: fall back to all energies
+      for (int i = 0; i < count; ++i) v[i] = E[i];
+      cnt = count;
+    }
+    m_count = cnt;
+    m_max = mx;
+  }
+  __syncthreads();
+  const int cnt = m_count;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int i = cnt + threadIdx.x; i < pow2; i += blockDim.x) v[i] = inf;
+  __syncthreads();
+  // bitonic sort ascending
+  for (int k = 2; k <= pow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const double a = v[i], b = v[ixj];
+          if ((a > b) == up) {
+            v[i] = b;
+            v[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    double med;
+    if (cnt == 0) med = __longlong_as_double(0x7ff8000000000000LL);
+    else if (cnt & 1) med = v[cnt / 2];
+    else med = (v[cnt / 2 - 1] + v[cnt / 2]) / 2.0;  // np.mean of the two middles
+    const double sigma = sqrt(fmax(med, 0.0) / (double)r);
+    const double floor_ = 1e-8 * sqrt(m_max);
+    const double base = sigma * sqrt((double)r);
+    t0[s] = fmax(1.5 * base, floor_);
+    t1[s] = fmax(2.5 * base, floor_);
+  }
+}
+
+// -------------------------------------------------------------- host side
+
+static int make_noisy_plan(NoisyPlan* P, int64_t n, const int64_t* factors, int ncycles,
+                           const int64_t* shifts, int R, int c, int m, const double* weights,
+                           int rec_cap) {
+  memset(P, 0, sizeof(*P));
+  if (n < 1 || n > 2000000000LL) {
+    set_error("signal size %lld outside the supported 1..2e9", (long long)n);
+    return AFFT_EUNSUPPORTED;
+  }
+  if (c < 1 || c > kMaxStrides || m < 2 || m > kMaxRounds || R != c * m || R > AFFT_MAX_SHIFTS) {
+    set_error("search plan c=%d m=%d R=%d unsupported", c, m, R);
+    return AFFT_EUNSUPPORTED;
+  }
+  if (ncycles < 1 || ncycles > AFFT_MAX_CYCLES) {
+    set_error("number of cycles %d outside 1..%d", ncycles, AFFT_MAX_CYCLES);
+    return AFFT_EUNSUPPORTED;
+  }
+  P->n = n;
+  P->ncycles = ncycles;
+  P->R = R;
+  P->c = c;
+  P->m = m;
+  int64_t total = 0;
+  for (int k = 0; k < ncycles; ++k) {
+    if (factors[k] < 1 || n % factors[k]) {
+      set_error("bucket count %lld does not divide signal size %lld", (long long)factors[k],
+                (long long)n);
+      return AFFT_EINVAL;
+    }
+    P->b[k] = factors[k];
+    P->base[k] = (int32_t)total;
+    total += factors[k];
+  }
+  if (total > (1 << 20)) {
+    set_error("graph with %lld nodes is too large", (long long)total);
+    return AFFT_EUNSUPPORTED;
+  }
+  for (int k = ncycles; k <= AFFT_MAX_CYCLES; ++k) P->base[k] = INT32_MAX;
+  P->base[ncycles] = (int32_t)total;
+  P->nodes = (int)total;
+  for (int t = 0; t < m - 1; ++t) P->w[t] = weights[t];
+  for (int r = 0; r < R; ++r) P->tau[r] = host_pymod(shifts[r], n);
+  int hcap = 16;
+  while (hcap < 2 * std::max(rec_cap, 1)) hcap <<= 1;
+  P->hmask = hcap - 1;
+  return AFFT_OK;
+}
+
+static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct NoisyWs {
+  size_t est, act_row, act_index, act_b, part_s, part_t, f0, val, res, dirty, done, counters,
+      total;
+  int chunks;
+};
+
+static NoisyWs noisy_ws(const NoisyPlan& P, int64_t rows) {
+  NoisyWs w;
+  int64_t bmin = P.b[0];
+  for (int k = 1; k < P.ncycles; ++k) bmin = std::min(bmin, P.b[k]);
+  const int64_t Lmax = P.n / bmin;
+  w.chunks = (int)((Lmax + kChunk - 1) / kChunk);
+  size_t o = 0;
+  w.est = o;       o = al256(o + (size_t)rows * P.c * 8);
+  w.act_row = o;   o = al256(o + (size_t)rows * 8);
+  w.act_index = o; o = al256(o + (size_t)rows * 8);
+  w.act_b = o;     o = al256(o + (size_t)rows * 8);
+  w.part_s = o;    o = al256(o + (size_t)rows * w.chunks * 8);
+  w.part_t = o;    o = al256(o + (size_t)rows * w.chunks * 4);
+  w.f0 = o;        o = al256(o + (size_t)rows * 8);
+  w.val = o;       o = al256(o + (size_t)rows * 16);
+  w.res = o;       o = al256(o + (size_t)rows * 8);
+  w.dirty = o;     o = al256(o + (size_t)rows);
+  w.done = o;      o = al256(o + (size_t)rows * 4);
+  w.counters = o;  o = al256(o + 64);
+  w.total = o;
+  return w;
+}
+
+// est → scan → reduce + LS fit for A active rows already listed in the workspace.
+static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
+                      const double* residual, cudaStream_t st) {
+  if (A == 0) return AFFT_OK;
+  const int64_t* act_row = reinterpret_cast<const int64_t*>(ws + w.act_row);
+  const int64_t* act_index = reinterpret_cast<const int64_t*>(ws + w.act_index);
+  const int64_t* act_b = reinterpret_cast<const int64_t*>(ws + w.act_b);
+  double* est = reinterpret_cast<double*>(ws + w.est);
+  const int64_t ne = (int64_t)A * P.c;
+  noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(A, P.c, P.m, act_row, residual,
+                                                                P.R, P, est);
+  AFFT_CHECK_LAUNCH("noisy_est_kernel");
+  for (int a0 = 0; a0 < A; a0 += 65535) {
+    const int cnt = std::min(65535, A - a0);
+    dim3 grid((unsigned)w.chunks, (unsigned)cnt);
+    noisy_search_kernel<<<grid, kSearchThreads, 0, st>>>(
+        P.n, P.c, act_index + a0, act_b + a0, est + (int64_t)a0 * P.c, w.chunks,
+        reinterpret_cast<double*>(ws + w.part_s) + (int64_t)a0 * w.chunks,
+        reinterpret_cast<int32_t*>(ws + w.part_t) + (int64_t)a0 * w.chunks);
+  }
+  AFFT_CHECK_LAUNCH("noisy_search_kernel");
+  noisy_finalize_kernel<<<(unsigned)((A * 32 + 255) / 256), 256, 0, st>>>(
+      A, w.chunks, reinterpret_cast<const double*>(ws + w.part_s),
+      reinterpret_cast<const int32_t*>(ws + w.part_t), act_row, act_index, act_b, residual, P,
+      reinterpret_cast<int64_t*>(ws + w.f0), reinterpret_cast<double*>(ws + w.val),
+      reinterpret_cast<double*>(ws + w.res));
+  AFFT_CHECK_LAUNCH("noisy_finalize_kernel");
+  return AFFT_OK;
+}
+
+static int32_t* pinned_counter() {
+  static thread_local int32_t* h = nullptr;
+  if (!h) {
+    if (cudaMallocHost(&h, 64) != cudaSuccess) h = nullptr;
+  }
+  return h;
+}
+
+}  // namespace afft
+
+using namespace afft;
+
+extern "C" size_t afft_noisy_workspace_size(int64_t n, int64_t batch, const int64_t* factors,
+                                            int32_t ncycles, int32_t c, int32_t m) {
+  NoisyPlan* P = new NoisyPlan();
+  std::vector<int64_t> zeros((size_t)std::max(1, c * m), 0);
+  double wts[kMaxRounds] = {0};
+  int64_t nodes = 0;
+  for (int k = 0; k < ncycles && factors; ++k) nodes += factors[k];
+  size_t out = 0;
+  if (!make_noisy_plan(P, n, factors, ncycles, zeros.data(), c * m, c, m, wts, (int)nodes))
+    out = noisy_ws(*P, batch * P->nodes).total;
+  delete P;
+  return out;
+}
+
+extern "C" int afft_node_energies(const double* vec, int32_t nshift, int64_t count,
+                                  double* energy, void* stream) {
+  if (count == 0) return AFFT_OK;
+  if (!vec || !energy || nshift < 1 || count < 0) {
+    set_error("afft_node_energies: bad arguments");
+    return AFFT_EINVAL;
+  }
+  node_energy_kernel<<<(unsigned)((count + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      count, nshift, vec, energy);
+  AFFT_CHECK_LAUNCH("node_energy_kernel");
+  return AFFT_OK;
+}
+
+extern "C" int afft_robust_thresholds(const double* energy, const uint8_t* mask, int64_t count,
+                                      int64_t batch, int32_t r, double* t0, double* t1,
+                                      void* stream) {
+  if (batch == 0) return AFFT_OK;
+  if (!energy || !t0 || !t1 || count < 1 || r < 1) {
+    set_error("afft_robust_thresholds: bad arguments");
+    return AFFT_EINVAL;
+  }
+  int pow2 = 1;
+  while (pow2 < count) pow2 <<= 1;
+  const size_t smem = (size_t)pow2 * 8;
+  if (smem > 200 * 1024) {
+    set_error("robust_thresholds: %lld energies per signal exceed the in-smem median",
+              (long long)count);
+    return AFFT_EUNSUPPORTED;
+  }
+  cudaError_t e = cudaFuncSetAttribute(robust_thresholds_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(robust_thresholds)");
+  robust_thresholds_kernel<<<(unsigned)batch, 256, smem, (cudaStream_t)stream>>>(
+      (int)count, pow2, energy, mask, r, t0, t1);
+  AFFT_CHECK_LAUNCH("robust_thresholds_kernel");
+  return AFFT_OK;
+}
+
+extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t* index,
+                                           int64_t count, int64_t b, int64_t n,
+                                           const int64_t* shifts, int32_t nshift, int32_t c,
+                                           int32_t m, const double* weights, int64_t* f0,
+                                           double* val, double* resnorm, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  if (count == 0) return AFFT_OK;
+  if (!residual || !index || !f0 || !val || !resnorm || !shifts || !weights || b < 1 ||
+      n % b) {
+    set_error("afft_singleton_search_noisy: bad arguments");
+    return AFFT_EINVAL;
+  }
+  NoisyPlan* P = new NoisyPlan();
+  int rc = make_noisy_plan(P, n, &b, 1, shifts, nshift, c, m, weights, 1);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  const NoisyWs w = noisy_ws(*P, count);
+  if (!workspace || workspace_bytes < w.total) {
+    delete P;
+    set_error("afft_singleton_search_noisy: workspace of %zu bytes needed", w.total);
+    return AFFT_ENOMEM;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = reinterpret_cast<char*>(workspace);
+  // active list = the given nodes, rows 0..count-1 of `residual`
+  std::vector<int64_t> rows((size_t)count), bs((size_t)count, b);
+  for (int64_t i = 0; i < count; ++i) rows[i] = i;
+  cudaMemcpyAsync(ws + w.act_row, rows.data(), count * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(ws + w.act_index, index, count * 8, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(ws + w.act_b, bs.data(), count * 8, cudaMemcpyHostToDevice, st);
+  rc = run_search(*P, w, ws, (int)count, residual, st);
+  if (!rc) {
+    cudaMemcpyAsync(f0, ws + w.f0, count * 8, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(val, ws + w.val, count * 16, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(resnorm, ws + w.res, count * 8, cudaMemcpyDeviceToDevice, st);
+    cudaError_t e = cudaStreamSynchronize(st);  // host vectors above must outlive the copies
+    if (e != cudaSuccess) rc = cuda_status(e, "singleton_search_noisy");
+  }
+  delete P;
+  return rc;
+}
+
+extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors, int32_t ncycles,
+                               const int64_t* shifts, int32_t nshift, int32_t c, int32_t m,
+                               const double* weights, double* residual, int8_t* state,
+                               int64_t* node_f0, double* node_val, const double* t0,
+                               const double* t1, int32_t max_rounds, int64_t* rec_pos,
+                               double* rec_val, int32_t rec_cap, int32_t* rec_count,
+                               int32_t* rounds, int32_t* unresolved, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (batch == 0) return AFFT_OK;
+  if (!residual || !state || !node_f0 || !node_val || !t0 || !t1 || !rec_pos || !rec_val ||
+      !rec_count || !rounds || !unresolved || !weights || !shifts || max_rounds < 0) {
+    set_error("afft_peel_noisy: bad arguments");
+    return AFFT_EINVAL;
+  }
+  NoisyPlan* P = new NoisyPlan();
+  int rc = make_noisy_plan(P, n, factors, ncycles, shifts, nshift, c, m, weights, rec_cap);
+  if (rc) {
+    delete P;
+    return rc;
+  }
+  const int N = P->nodes;
+  const NoisyWs w = noisy_ws(*P, batch * N);
+  if (!workspace || workspace_bytes < w.total) {
+    delete P;
+    set_error("afft_peel_noisy: workspace of %zu bytes needed, %zu given", w.total,
+              workspace_bytes);
+    return AFFT_ENOMEM;
+  }
+  if ((int64_t)batch * N > INT32_MAX) {
+    delete P;
+    set_error("afft_peel_noisy: batch * nodes exceeds 2^31");
+    return AFFT_EUNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = reinterpret_cast<char*>(workspace);
+  int8_t* dirty = reinterpret_cast<int8_t*>(ws + w.dirty);
+  int32_t* done = reinterpret_cast<int32_t*>(ws + w.done);
+  int32_t* counters = reinterpret_cast<int32_t*>(ws + w.counters);
+  int32_t* host = pinned_counter();
+  if (!host) {
+    delete P;
+    set_error("afft_peel_noisy: cannot allocate a pinned host counter");
+    return AFFT_ENOMEM;
+  }
+  cudaError_t e = cudaMemsetAsync(dirty, 1, (size_t)batch * N, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(done, 0, (size_t)batch * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(rounds, 0, (size_t)batch * 4, st);
+  if (e != cudaSuccess) {
+    delete P;
+    return cuda_status(e, "afft_peel_noisy init");
+  }
+  int hcap = P->hmask + 1;
+  const size_t hsmem = (size_t)hcap * 8 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64;
+  if (hsmem > 200 * 1024) {
+    delete P;
+    set_error("afft_peel_noisy: graph of %d nodes exceeds the harvest kernel's smem", N);
+    return AFFT_EUNSUPPORTED;
+  }
+  e = cudaFuncSetAttribute(noisy_harvest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)hsmem);
+  if (e != cudaSuccess) {
+    delete P;
+    return cuda_status(e, "cudaFuncSetAttribute(noisy_harvest)");
+  }
+  const int64_t total = batch * N;
+  for (int it = 0; it < max_rounds; ++it) {
+    cudaMemsetAsync(counters, 0, 8, st);
+    noisy_prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        batch, *P, residual, state, dirty, done, t0, counters,
+        reinterpret_cast<int64_t*>(ws + w.act_row), reinterpret_cast<int64_t*>(ws + w.act_index),
+        reinterpret_cast<int64_t*>(ws + w.act_b));
+    AFFT_CHECK_LAUNCH("noisy_prep_kernel");
+    cudaMemcpyAsync(host, counters, 4, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      delete P;
+      return cuda_status(e, "afft_peel_noisy round sync");
+    }
+    const int A = host[0];
+    if ((rc = run_search(*P, w, ws, A, residual, st))) {
+      delete P;
+      return rc;
+    }
+    if (A > 0) {
+      noisy_apply_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(
+          A, *P, reinterpret_cast<const int64_t*>(ws + w.act_row),
+          reinterpret_cast<const int64_t*>(ws + w.f0), reinterpret_cast<const double*>(ws + w.val),
+          reinterpret_cast<const double*>(ws + w.res), t1, state, dirty, node_f0, node_val);
+      AFFT_CHECK_LAUNCH("noisy_apply_kernel");
+    }
+    noisy_harvest_kernel<<<(unsigned)batch, 512, hsmem, st>>>(
+        *P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap,
+        rec_count, rounds, counters + 1);
+    AFFT_CHECK_LAUNCH("noisy_harvest_kernel");
+    cudaMemcpyAsync(host + 1, counters + 1, 4, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      delete P;
+      return cuda_status(e, "afft_peel_noisy round sync");
+    }
+    if (host[1] == 0) break;  // every signal found nothing: all loops have exited
+  }
+  count_multi_kernel<<<(unsigned)batch, 256, 0, st>>>(batch, N, state, unresolved);
+  AFFT_CHECK_LAUNCH("count_multi_kernel");
+  delete P;
+  return AFFT_OK;
+}
+
+namespace afft {
+// classify_noisy's decision for nodes searched unconditionally (per-node API):
+// ZERO_TON if ||residual|| <= t0, else SINGLE_TON iff resnorm <= t1.
+__global__ void noisy_decide_kernel(int64_t count, int R, const double* __restrict__ residual,
+                                    double t0, double t1, const double* __restrict__ res,
+                                    int8_t* __restrict__ state) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  if (node_norm(reinterpret_cast<const cd*>(residual) + i * R, R) <= t0)
+    state[i] = AFFT_ZERO_TON;
+  else
+    state[i] = res[i] <= t1 ? AFFT_SINGLE_TON : AFFT_MULTI_TON;
+}
+}  // namespace afft
+
+extern "C" int afft_classify_noisy(const double* residual, const int64_t* index, int64_t count,
+                                   int64_t b, int64_t n, const int64_t* shifts, int32_t nshift,
+                                   int32_t c, int32_t m, const double* weights, double t0,
+                                   double t1, int8_t* state, int64_t* f0, double* val,
+                                   double* resnorm, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  if (count == 0) return AFFT_OK;
+  if (!state) {
+    set_error("afft_classify_noisy: bad arguments");
+    return AFFT_EINVAL;
+  }
+  int rc = afft_singleton_search_noisy(residual, index, count, b, n, shifts, nshift, c, m,
+                                       weights, f0, val, resnorm, workspace, workspace_bytes,
+                                       stream);
+  if (rc) return rc;
+  noisy_decide_kernel<<<(unsigned)((count + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      count, nshift, residual, t0, t1, resnorm, state);
+  AFFT_CHECK_LAUNCH("noisy_decide_kernel");
+  return AFFT_OK;
+}

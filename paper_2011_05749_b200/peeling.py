@@ -330,8 +330,6 @@ def peel_decode(graph: PeelingGraph, mode: str = "exact", eps_zero: float = 0.0,
     if max_rounds is None:
         max_rounds = len(graph.recovered) + 8
     if mode != "exact":
-        from .rffast import peel_decode_noisy
-
         return peel_decode_noisy(graph, search_plan, max_rounds)
     live = any(
         node.state not in (NodeState.RESOLVED, NodeState.ZERO_TON)
@@ -398,3 +396,13 @@ def ffast(x, k: int, ledger: SampleLedger | None = None, max_rounds: int | None 
     if not k:
         return SparseSpectrum(n, {})
     return out.spectrum(0)
+
+
+from .rffast import (  # noqa: E402  (R-FFAST device paths, re-exported like the reference)
+    classify_noisy,
+    noisy_thresholds,
+    peel_decode_noisy,
+    r_ffast,
+    robust_thresholds,
+    singleton_search_noisy,
+)

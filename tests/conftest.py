@@ -76,3 +76,16 @@ def golden_signal(gen: dict) -> np.ndarray:
 @pytest.fixture
 def rng():
     return np.random.default_rng(12345)
+
+
+@pytest.fixture(scope="session")
+def golden_rffast():
+    return load_golden("golden_rffast.json")
+
+
+def search_plan_of(case):
+    """SearchPlan of a golden R-FFAST run (anchors as captured from the reference)."""
+    from paper_2011_05749_b200.peeling import SearchPlan, kay_weights
+
+    return SearchPlan(c=case["c"], m=case["m"], anchors=list(case["anchors"]),
+                      weights=kay_weights(case["m"]))
