@@ -210,6 +210,62 @@ int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors /* host */,
                     int32_t* rec_count, int32_t* rounds, int32_t* unresolved, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------ sFFT-DT1/2/3 */
+/*
+ * Measurement rows (oneshot.py:86-106): rows[s][bucket][3*a_m + p] = bucket values at the
+ * structured shifts -a_m..2a_m-1 then the p random shifts rand_shifts[s][0..p) (device,
+ * raw values as drawn by rng.choice(n, p, replace=False) with each signal's seed).
+ */
+int afft_bucketize_table(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                         int64_t b, const int64_t* shift_table, int32_t nshift, double* out,
+                         int64_t out_signal_stride, int64_t out_shift_stride,
+                         int64_t out_bin_stride, void* stream);
+int afft_dt_collect(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld, int64_t b,
+                    int32_t a_m, int32_t p, const int64_t* rand_shifts, double* rows,
+                    void* stream);
+
+/*
+ * detect_sparsity (oneshot.py:116-140) over nrows rows per signal (R measurements each):
+ * sigmas [batch][nrows][a_m] (out), counts [batch][nrows] (out).
+ */
+int afft_dt_detect(const double* rows, int64_t batch, int64_t nrows, int32_t R, int32_t a_m,
+                   int32_t k, int32_t* counts, double* sigmas, void* stream);
+
+/* locate (oneshot.py:161-200) per row: out_pos [count][4], out_n [count] (-1 = None). */
+int afft_dt_locate(const double* rows, int64_t count, int32_t R, int32_t a_m, const int32_t* a,
+                   const int64_t* bucket, int32_t variant /* 1 dt1, 2 dt2, 3 dt3 */, int64_t b,
+                   int64_t n, int64_t* out_pos, int32_t* out_n, void* stream);
+
+/* estimate_values (oneshot.py:203-257) per row from candidates [count][4] (ncand each). */
+int afft_dt_estimate(const double* rows, const int64_t* rand_shifts, int64_t count, int32_t a_m,
+                     int32_t p, const int64_t* cands, const int32_t* ncand, int64_t b, int64_t n,
+                     int64_t* out_pos, double* out_val, int32_t* out_n, void* stream);
+
+/*
+ * The per-bucket loop of sfft_dt (oneshot.py:279-288) for every row with counts > 0:
+ * locate + estimate, entries to out_pos/out_val [batch][nrows][a_m], out_cnt [batch][nrows].
+ * bucket_ids [batch][nrows] maps rows to bucket indices (NULL = row index); a_cap > 0
+ * caps a (dsfft.py:219).
+ */
+int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int64_t batch, int64_t nrows,
+                  int32_t a_m, int32_t p, const int32_t* counts, const int64_t* bucket_ids,
+                  int32_t variant, int32_t a_cap, int64_t b, int64_t n, int64_t* out_pos,
+                  double* out_val, int32_t* out_cnt, void* stream);
+
+/* Entries in row order -> all_* [batch][nrows*a_m] and the top-k truncation out_* [batch][k]. */
+int afft_dt_truncate(const int64_t* pos, const double* val, const int32_t* cnt, int64_t batch,
+                     int64_t nrows, int32_t a_m, int32_t k, int64_t* all_pos, double* all_val,
+                     int32_t* all_count, int64_t* out_pos, double* out_val, int32_t* out_count,
+                     void* stream);
+
+/* sfft_dt (oneshot.py:266-289) over a batch: collect, detect, solve, truncate. */
+size_t afft_sfft_dt_workspace_size(int64_t n, int64_t batch, int64_t b, int32_t a_m, int32_t p);
+int afft_sfft_dt(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld, int64_t b,
+                 int32_t a_m, int32_t p, int32_t variant, int32_t k, const int64_t* rand_shifts,
+                 int64_t* out_pos, double* out_val, int32_t* out_count, int64_t* all_pos,
+                 double* all_val, int32_t* all_count, int32_t* counts_out, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,18 @@ SIGNATURES = {
     "afft_peel_noisy": (
         _INT, [_I64, _I64, _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P,
                _P, _I32, _P, _P, _P, _P, _SZ, _P]),
+    "afft_bucketize_table": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _P, _I32, _P, _I64, _I64,
+                                    _I64, _P]),
+    "afft_dt_collect": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _I32, _I32, _P, _P, _P]),
+    "afft_dt_detect": (_INT, [_P, _I64, _I64, _I32, _I32, _I32, _P, _P, _P]),
+    "afft_dt_locate": (_INT, [_P, _I64, _I32, _I32, _P, _P, _I32, _I64, _I64, _P, _P, _P]),
+    "afft_dt_estimate": (_INT, [_P, _P, _I64, _I32, _I32, _P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "afft_dt_solve": (_INT, [_P, _P, _I64, _I64, _I32, _I32, _P, _P, _I32, _I32, _I64, _I64, _P,
+                             _P, _P, _P]),
+    "afft_dt_truncate": (_INT, [_P, _P, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "afft_sfft_dt_workspace_size": (_SZ, [_I64, _I64, _I64, _I32, _I32]),
+    "afft_sfft_dt": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P,
+                            _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
 _lock = threading.Lock()

@@ -29,6 +29,7 @@ struct GatherDftParams {
   DftPlan plan[AFFT_MAX_CYCLES];
   double* out;
   int64_t out_signal_stride, out_shift_stride, out_bin_stride;  // complex elements
+  const int64_t* shift_table;    // optional device [batch][nshift] raw per-signal shifts
   int64_t tau[AFFT_MAX_SHIFTS];  // shifts reduced into [0, n)
 };
 
@@ -44,13 +45,20 @@ __global__ void __launch_bounds__(256) gather_dft_kernel(const __grid_constant__
   const int64_t b = p.b[c];
   const int t0 = job * p.chunk[c];
   const int cnt = min(p.chunk[c], p.nshift - t0);
+  __shared__ int64_t s_tau[AFFT_MAX_SHIFTS];
   cd* tw = reinterpret_cast<cd*>(smem_raw);
   cd* bufA = tw + b;
   cd* bufB = bufA + (size_t)cnt * b;
   const char* xs = reinterpret_cast<const char*>(p.x) +
                    s * p.ld * (p.dtype == AFFT_C64 ? 8 : 16);
-  const cd* res = gather_dft_block(xs, p.dtype, p.n, b, p.plan[c], p.tau + t0, cnt, tw, bufA,
-                                   bufB);
+  const int64_t* taus = p.tau + t0;
+  if (p.shift_table) {  // per-signal shifts (sFFT-DT random shifts), reduced here
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x)
+      s_tau[t] = pymod(p.shift_table[s * p.nshift + t0 + t], p.n);
+    __syncthreads();
+    taus = s_tau;
+  }
+  const cd* res = gather_dft_block(xs, p.dtype, p.n, b, p.plan[c], taus, cnt, tw, bufA, bufB);
   const double inv_b = 1.0 / (double)b;
   double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset[c]);
   const int total = cnt * (int)b;
@@ -67,9 +75,10 @@ __global__ void __launch_bounds__(256) gather_dft_kernel(const __grid_constant__
 static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                              const int64_t* factors, int ncycles, const int64_t* out_offsets,
                              const int64_t* shifts, int nshift, double* out, int64_t oss,
-                             int64_t osh, int64_t obin, cudaStream_t stream) {
+                             int64_t osh, int64_t obin, cudaStream_t stream,
+                             const int64_t* shift_table = nullptr) {
   if (batch == 0 || nshift == 0) return AFFT_OK;
-  if (!x || !out || !factors || !shifts) {
+  if (!x || !out || !factors || (!shifts && !shift_table)) {
     set_error("null pointer argument");
     return AFFT_EINVAL;
   }
@@ -101,7 +110,8 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
   q.out_signal_stride = oss;
   q.out_shift_stride = osh;
   q.out_bin_stride = obin;
-  for (int t = 0; t < nshift; ++t) q.tau[t] = host_pymod(shifts[t], n);
+  q.shift_table = shift_table;
+  for (int t = 0; t < nshift; ++t) q.tau[t] = shifts ? host_pymod(shifts[t], n) : 0;
   const size_t kBudget = 96 * 1024;
   size_t smem_max = 0;
   int total_jobs = 0;
@@ -176,4 +186,15 @@ extern "C" int afft_build_graph(const void* x, int dtype, int64_t n, int64_t bat
   }
   return launch_gather_dft(x, dtype, n, batch, ld, factors, ncycles, offs, shifts, nshift, nodes,
                            total * nshift, 1, nshift, (cudaStream_t)stream);
+}
+
+extern "C" int afft_bucketize_table(const void* x, int dtype, int64_t n, int64_t batch,
+                                    int64_t ld, int64_t b, const int64_t* shift_table,
+                                    int32_t nshift, double* out, int64_t out_signal_stride,
+                                    int64_t out_shift_stride, int64_t out_bin_stride,
+                                    void* stream) {
+  int64_t off = 0;
+  return launch_gather_dft(x, dtype, n, batch, ld, &b, 1, &off, nullptr, nshift, out,
+                           out_signal_stride, out_shift_stride, out_bin_stride,
+                           (cudaStream_t)stream, shift_table);
 }

@@ -1,0 +1,299 @@
+"""One-shot recovery sFFT-DT1.0/2.0/3.0 on the GPU.
+
+Drop-in for /root/reference/pkg/src/aliasfft/oneshot.py.  The configuration and
+the seeded random-shift draw (``rng.choice(n, p, replace=False)``, 93-94) stay
+on the host; measurement collection, the Hankel-SVD vote, localisation (roots /
+grid enumeration / matrix pencil) and subspace pursuit run in csrc/oneshot.cu,
+one thread per bucket for the per-bucket solves.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .bucketize import SampleLedger, record_bucketization
+from .signals import SparseSpectrum
+
+VARIANTS = ("dt1", "dt2", "dt3")
+VARIANT_CODE = {"dt1": 1, "dt2": 2, "dt3": 3}
+_SP_MAX_ITERS = 10
+_TIE_QUANTUM = 1e-12
+
+
+@dataclass
+class OneShotConfig:
+    """Bucketization and pursuit parameters of one run (oneshot.py:27-60)."""
+
+    b: int
+    a_m: int = 4
+    p: int = 12
+    variant: str = "dt3"
+    seed: int = 0
+
+    @classmethod
+    def default(cls, n: int, k: int, variant: str = "dt3", seed: int = 0) -> "OneShotConfig":
+        """B = 32K rounded up to a power of two, raised until N/B <= 1000."""
+        if k < 1:
+            raise ValueError("k must be >= 1")
+        b = 1 << max(0, int(np.ceil(np.log2(32 * k))))
+        while n // b > 1000:
+            b *= 2
+        return cls(b=min(b, n), variant=variant, seed=seed)
+
+    def validate(self, n: int) -> None:
+        if self.variant not in VARIANTS:
+            raise ValueError(f"unknown variant {self.variant!r}")
+        if not 1 <= self.a_m <= 4:
+            raise ValueError("a_m must be in 1..4")
+        if self.b < 1 or n % self.b:
+            raise ValueError(f"bucket count {self.b} does not divide {n}")
+        floor = self.a_m * np.log10(max(n // self.b, 1))
+        if self.p < floor:
+            raise ValueError(f"p={self.p} is below the measurement floor a_m*log10(L)={floor:.2f}")
+
+
+@dataclass
+class BucketMoments:
+    """One bucket's measurements keyed by shift (oneshot.py:63-70)."""
+
+    bucket: int
+    structured: dict[int, complex]
+    random: dict[int, complex] = field(default_factory=dict)
+
+
+@dataclass
+class BucketSolution:
+    bucket: int
+    a: int
+    positions: list[int]
+    values: list[complex]
+
+
+def structured_shifts(a_m: int) -> list[int]:
+    """The 3*a_m consecutive shifts -a_m .. 2*a_m - 1 (oneshot.py:81-83)."""
+    return list(range(-a_m, 2 * a_m))
+
+
+def random_shifts(n: int, config: OneShotConfig) -> list[int]:
+    """The seeded random shift draw of collect_moments (oneshot.py:93-94)."""
+    rng = np.random.default_rng(config.seed)
+    return [int(t) for t in rng.choice(n, size=config.p, replace=False)]
+
+
+# ------------------------------------------------------------------ device helpers
+
+
+def collect_rows_device(xd: torch.Tensor, b: int, a_m: int, rshifts: torch.Tensor) -> torch.Tensor:
+    """rows [batch, b, 3a_m + p] (complex128) from xd [batch, n] and rshifts [batch, p]."""
+    batch, n = int(xd.shape[0]), int(xd.shape[1])
+    p = int(rshifts.shape[1])
+    rows = torch.empty((batch, b, 3 * a_m + p), dtype=torch.complex128, device=xd.device)
+    ld = int(xd.stride(0)) if batch > 1 else n
+    _lib.check(
+        _lib.load().afft_dt_collect(xd.data_ptr(), _device.dtype_code(xd), n, batch, ld, b, a_m,
+                                    p, rshifts.data_ptr() if p else None, rows.data_ptr(),
+                                    _device.stream_ptr()),
+        "collect_moments",
+    )
+    return rows
+
+
+def _rows_from_moments(moments, a_m: int) -> tuple[np.ndarray, list[int]]:
+    shifts = structured_shifts(a_m)
+    rkeys = list(moments[0].random) if moments else []
+    rows = np.empty((len(moments), 3 * a_m + len(rkeys)), dtype=np.complex128)
+    for i, m in enumerate(moments):
+        rows[i, : 3 * a_m] = [m.structured[t] for t in shifts]
+        rows[i, 3 * a_m:] = [m.random[t] for t in rkeys]
+    return rows, rkeys
+
+
+def collect_moments(x, config: OneShotConfig, ledger: SampleLedger | None = None):
+    """Bucketize over the structured and random shift sets (oneshot.py:86-106)."""
+    n = _device.signal_length(x)
+    config.validate(n)
+    shifts = structured_shifts(config.a_m)
+    rsh = random_shifts(n, config)
+    xd = _device.as_device_signal(x).unsqueeze(0)
+    rt = torch.tensor([rsh], dtype=torch.int64, device=xd.device)
+    rows = collect_rows_device(xd, config.b, config.a_m, rt)[0].cpu().numpy()
+    record_bucketization(ledger, n, config.b, shifts + rsh)
+    return [
+        BucketMoments(
+            bucket=i,
+            structured={t: complex(rows[i, j]) for j, t in enumerate(shifts)},
+            random={t: complex(rows[i, 3 * config.a_m + j]) for j, t in enumerate(rsh)},
+        )
+        for i in range(config.b)
+    ]
+
+
+def detect_sparsity(moments, k: int, a_m: int) -> np.ndarray:
+    """Per-bucket tone counts from the global Hankel-sigma vote (oneshot.py:116-140)."""
+    b = len(moments)
+    if k <= 0 or b == 0:
+        return np.zeros(b, dtype=int)
+    dev = _device.require_cuda()
+    rows, _ = _rows_from_moments(moments, a_m)
+    rd = torch.from_numpy(rows).to(dev)
+    counts = torch.empty(b, dtype=torch.int32, device=dev)
+    sig = torch.empty((b, a_m), dtype=torch.float64, device=dev)
+    _lib.check(
+        _lib.load().afft_dt_detect(rd.data_ptr(), 1, b, rows.shape[1], a_m, int(k),
+                                   counts.data_ptr(), sig.data_ptr(), _device.stream_ptr()),
+        "detect_sparsity",
+    )
+    return counts.cpu().numpy().astype(int)
+
+
+def locate(moments: BucketMoments, a: int, method: str, b: int, n: int):
+    """Candidate frequencies for a bucket holding ``a`` tones, or None (oneshot.py:161-200)."""
+    if a < 1:
+        return []
+    if method not in VARIANT_CODE:
+        raise ValueError(f"unknown localization method {method!r}")
+    dev = _device.require_cuda()
+    a_m = max(4, a)
+    # the moment rows need m_{-a..2a-1}; pad the structured window to a_m = 4 layout
+    row = np.zeros(3 * a_m, dtype=np.complex128)
+    for t, v in moments.structured.items():
+        if -a_m <= t < 2 * a_m:
+            row[t + a_m] = v
+    rd = torch.from_numpy(row[None, :]).to(dev)
+    av = torch.tensor([a], dtype=torch.int32, device=dev)
+    bk = torch.tensor([moments.bucket], dtype=torch.int64, device=dev)
+    pos = torch.zeros((1, 4), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(
+        _lib.load().afft_dt_locate(rd.data_ptr(), 1, 3 * a_m, a_m, av.data_ptr(), bk.data_ptr(),
+                                   VARIANT_CODE[method], b, n, pos.data_ptr(), cnt.data_ptr(),
+                                   _device.stream_ptr()),
+        "locate",
+    )
+    c = int(cnt.item())
+    if c < 0:
+        return None
+    return [int(f) for f in pos[0, :c].cpu().numpy()]
+
+
+def estimate_values(moments: BucketMoments, candidates, b: int, n: int) -> BucketSolution:
+    """Subspace pursuit over the random-shift measurements (oneshot.py:203-257)."""
+    cands = sorted(set(int(f) for f in candidates))
+    rkeys = list(moments.random)
+    if len(cands) > 4:
+        raise ValueError("at most 4 candidates per bucket (a_m <= 4)")
+    dev = _device.require_cuda()
+    a_m = 4
+    row = np.zeros(3 * a_m + len(rkeys), dtype=np.complex128)
+    row[3 * a_m:] = [moments.random[t] for t in rkeys]
+    rd = torch.from_numpy(row[None, :]).to(dev)
+    rs = torch.tensor(rkeys if rkeys else [0], dtype=torch.int64, device=dev)
+    cd = torch.zeros((1, 4), dtype=torch.int64)
+    cd[0, : len(cands)] = torch.tensor(cands, dtype=torch.int64)
+    cd = cd.to(dev)
+    nc = torch.tensor([len(cands)], dtype=torch.int32, device=dev)
+    pos = torch.zeros((1, 4), dtype=torch.int64, device=dev)
+    val = torch.zeros((1, 4), dtype=torch.complex128, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(
+        _lib.load().afft_dt_estimate(rd.data_ptr(), rs.data_ptr(), 1, a_m, len(rkeys),
+                                     cd.data_ptr(), nc.data_ptr(), b, n, pos.data_ptr(),
+                                     val.data_ptr(), cnt.data_ptr(), _device.stream_ptr()),
+        "estimate_values",
+    )
+    c = int(cnt.item())
+    return BucketSolution(bucket=moments.bucket, a=c,
+                          positions=[int(f) for f in pos[0, :c].cpu().numpy()],
+                          values=[complex(v) for v in val[0, :c].cpu().numpy()])
+
+
+def truncate_spectrum(entries: dict[int, complex], n: int, k: int) -> SparseSpectrum:
+    """Keep the k largest |v|, ties to the lower frequency (oneshot.py:260-263).
+
+    Host helper for API callers holding a dict; the device paths truncate in-kernel.
+    """
+    ranked = sorted(entries.items(), key=lambda item: (-abs(item[1]), item[0]))
+    return SparseSpectrum(n, dict(ranked[:k]))
+
+
+@dataclass
+class DtBatchResult:
+    n: int
+    k: int
+    pos: torch.Tensor
+    val: torch.Tensor
+    count: torch.Tensor
+    all_pos: torch.Tensor
+    all_val: torch.Tensor
+    all_count: torch.Tensor
+    counts: torch.Tensor  # per-bucket tone counts from the vote
+
+    def spectrum(self, i: int) -> SparseSpectrum:
+        c = int(self.count[i])
+        pos, val = self.pos[i, :c].cpu().numpy(), self.val[i, :c].cpu().numpy()
+        return SparseSpectrum(self.n, {int(f): complex(v) for f, v in zip(pos, val)})
+
+    def full_spectrum(self, i: int) -> SparseSpectrum:
+        c = int(self.all_count[i])
+        pos, val = self.all_pos[i, :c].cpu().numpy(), self.all_val[i, :c].cpu().numpy()
+        return SparseSpectrum(self.n, {int(f): complex(v) for f, v in zip(pos, val)})
+
+
+def sfft_dt_batch(x, k: int, b: int, a_m: int = 4, p: int = 12, variant: str = "dt3",
+                  seeds=None, rand_shifts=None) -> DtBatchResult:
+    """sFFT-DT over a (batch, n) block with per-signal seeds (one launch sequence)."""
+    xd = _device.as_device_batch(x)
+    batch, n = int(xd.shape[0]), int(xd.shape[1])
+    cfg = OneShotConfig(b=b, a_m=a_m, p=p, variant=variant)
+    cfg.validate(n)
+    dev = xd.device
+    if rand_shifts is None:
+        seeds = list(seeds) if seeds is not None else [0] * batch
+        rand_shifts = [random_shifts(n, OneShotConfig(b=b, a_m=a_m, p=p, seed=int(s)))
+                       for s in seeds]
+    rt = torch.as_tensor(np.asarray(rand_shifts, dtype=np.int64).reshape(batch, p)).to(dev)
+    lib = _lib.load()
+    need = int(lib.afft_sfft_dt_workspace_size(n, batch, b, a_m, p))
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    kk = max(int(k), 0)
+    cap = b * a_m
+    out = DtBatchResult(
+        n=n, k=k,
+        pos=torch.empty((batch, kk), dtype=torch.int64, device=dev),
+        val=torch.empty((batch, kk), dtype=torch.complex128, device=dev),
+        count=torch.empty(batch, dtype=torch.int32, device=dev),
+        all_pos=torch.empty((batch, cap), dtype=torch.int64, device=dev),
+        all_val=torch.empty((batch, cap), dtype=torch.complex128, device=dev),
+        all_count=torch.empty(batch, dtype=torch.int32, device=dev),
+        counts=torch.empty((batch, b), dtype=torch.int32, device=dev),
+    )
+    ld = int(xd.stride(0)) if batch > 1 else n
+    _lib.check(
+        lib.afft_sfft_dt(xd.data_ptr(), _device.dtype_code(xd), n, batch, ld, b, a_m, p,
+                         VARIANT_CODE[variant], kk, rt.data_ptr() if p else None,
+                         out.pos.data_ptr(), out.val.data_ptr(), out.count.data_ptr(),
+                         out.all_pos.data_ptr(), out.all_val.data_ptr(), out.all_count.data_ptr(),
+                         out.counts.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream_ptr()),
+        "sfft_dt",
+    )
+    return out
+
+
+def sfft_dt(x, k: int, config: OneShotConfig | None = None,
+            ledger: SampleLedger | None = None) -> SparseSpectrum:
+    """Full one-shot pipeline: collect, detect, locate, estimate, truncate (oneshot.py:266-289)."""
+    n = _device.signal_length(x)
+    if k <= 0:
+        return SparseSpectrum(n, {})
+    if config is None:
+        config = OneShotConfig.default(n, k)
+    config.validate(n)
+    rsh = random_shifts(n, config)
+    res = sfft_dt_batch(_device.as_device_signal(x).unsqueeze(0), k, config.b, config.a_m,
+                        config.p, config.variant, rand_shifts=[rsh])
+    record_bucketization(ledger, n, config.b, structured_shifts(config.a_m) + rsh)
+    return res.spectrum(0)

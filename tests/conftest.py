@@ -89,3 +89,15 @@ def search_plan_of(case):
 
     return SearchPlan(c=case["c"], m=case["m"], anchors=list(case["anchors"]),
                       weights=kay_weights(case["m"]))
+
+
+@pytest.fixture(scope="session")
+def golden_dt():
+    return load_golden("golden_dt.json")
+
+
+def dt_signal(case):
+    from paper_2011_05749_b200.signals import generate_test_case
+
+    x = generate_test_case(case["n"], case["k"], case["snr"], case["seed"]).signal
+    return x.astype(np.complex64) if case.get("c64") else x
