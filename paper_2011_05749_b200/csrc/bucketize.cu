@@ -9,6 +9,7 @@
 // reciprocal — to a caller-strided output, so the same kernel produces the
 // FilteredSpectrum layout [s][t][i] and the peeling-node layout [s][g][t].
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "afft_common.cuh"
@@ -72,6 +73,174 @@ __global__ void __launch_bounds__(256) gather_dft_kernel(const __grid_constant__
   }
 }
 
+// ---------------------------------------------------------------- K2': b > 4096
+//
+// Four-step DFT for large bucket counts, b = b1 * b2 (both <= 4096):
+//   j = j1 + b1*j2, i = i2 + b2*i1
+//   y[i2 + b2*i1] = (1/b) sum_j1 w_b1^{j1*i1} * [ w_b^{j1*i2} * sum_j2 x[(j*L - tau) mod n] w_b2^{j2*i2} ]
+// Pass A: for each (shift, j1) gather the b2 samples at stride b1*L, size-b2 DFT,
+//         twiddle w_b^{j1*i2} (index reduced mod b, sincospi), write z[t][j1][i2].
+// Pass B: for each (shift, block of i2) read z[t][0..b1)[i2..], size-b1 DFT,
+//         scale 1/b, write the caller-strided output.
+struct FourStepParams {
+  const void* x;
+  int dtype;
+  int64_t n, ld, b, b1, b2;
+  int nshift;
+  int cj;       // j1 values per CTA in pass A
+  int wi;       // i2 columns per CTA in pass B
+  DftPlan plan1, plan2;
+  double* z;    // [batch][nshift][b1][b2]
+  double* out;
+  int64_t out_offset, out_signal_stride, out_shift_stride, out_bin_stride;
+  const int64_t* shift_table;
+  int64_t tau[AFFT_MAX_SHIFTS];
+};
+
+__global__ void __launch_bounds__(256) fourstep_a_kernel(const __grid_constant__ FourStepParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t s = blockIdx.z;
+  const int t = blockIdx.y;
+  const int64_t j1_0 = (int64_t)blockIdx.x * p.cj;
+  const int cnt = (int)min((int64_t)p.cj, p.b1 - j1_0);
+  const int b2 = (int)p.b2;
+  cd* tw = reinterpret_cast<cd*>(smem_raw);
+  cd* bufA = tw + b2;
+  cd* bufB = bufA + (size_t)cnt * b2;
+  build_twiddles(tw, b2, threadIdx.x, blockDim.x);
+  const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * (p.dtype == AFFT_C64 ? 8 : 16);
+  const int64_t tau = p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n) : p.tau[t];
+  const int64_t L = p.n / p.b;
+  const int64_t stride = p.b1 * L;
+  const int total = cnt * b2;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int q = e / b2;
+    const int64_t j2 = e - (int64_t)q * b2;
+    int64_t idx = (j1_0 + q) * L + j2 * stride - tau;
+    if (idx < 0) idx += p.n;
+    bufA[e] = load_sample(xs, p.dtype, idx);
+  }
+  __syncthreads();
+  const cd* spec = smem_dft(bufA, bufB, cnt, p.plan2, tw, threadIdx.x, blockDim.x);
+  cd* z = reinterpret_cast<cd*>(p.z) + ((s * p.nshift + t) * p.b1 + j1_0) * p.b2;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int q = e / b2;
+    const int64_t i2 = e - (int64_t)q * b2;
+    const int64_t r = ((j1_0 + q) * i2) % p.b;  // exact index of w_b^{j1*i2}
+    double sn, cs;
+    sincospi(-2.0 * (double)r / (double)p.b, &sn, &cs);
+    z[e] = cmul(spec[e], cd{cs, sn});
+  }
+}
+
+__global__ void __launch_bounds__(256) fourstep_b_kernel(const __grid_constant__ FourStepParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t s = blockIdx.z;
+  const int t = blockIdx.y;
+  const int64_t i2_0 = (int64_t)blockIdx.x * p.wi;
+  const int w = (int)min((int64_t)p.wi, p.b2 - i2_0);
+  const int b1 = (int)p.b1;
+  cd* tw = reinterpret_cast<cd*>(smem_raw);
+  cd* bufA = tw + b1;
+  cd* bufB = bufA + (size_t)w * b1;
+  build_twiddles(tw, b1, threadIdx.x, blockDim.x);
+  const cd* z = reinterpret_cast<const cd*>(p.z) + (s * p.nshift + t) * p.b1 * p.b2;
+  const int total = w * b1;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {  // coalesced along i2
+    const int j1 = e / w;
+    const int q = e - j1 * w;
+    bufA[q * b1 + j1] = z[(int64_t)j1 * p.b2 + i2_0 + q];
+  }
+  __syncthreads();
+  const cd* spec = smem_dft(bufA, bufB, w, p.plan1, tw, threadIdx.x, blockDim.x);
+  const double inv_b = 1.0 / (double)p.b;
+  double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset + t * p.out_shift_stride);
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {  // consecutive i2 per i1
+    const int i1 = e / w;
+    const int q = e - i1 * w;
+    const cd v = cscale(spec[q * b1 + i1], inv_b);
+    const int64_t o = 2 * ((i2_0 + q + p.b2 * (int64_t)i1) * p.out_bin_stride);
+    out[o] = v.re;
+    out[o + 1] = v.im;
+  }
+}
+
+// b = b1 * b2 with both factors <= limit, as balanced as possible; false if none.
+static bool split_size(int64_t b, int64_t limit, int64_t* b1, int64_t* b2) {
+  int64_t best = 0;
+  for (int64_t d = 1; d * d <= b; ++d) {
+    if (b % d) continue;
+    const int64_t e = b / d;
+    if (d <= limit && e <= limit) best = d;  // d grows toward sqrt(b)
+  }
+  if (!best) return false;
+  *b1 = b / best;  // the larger factor on the pass-B side
+  *b2 = best;
+  return true;
+}
+
+static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                           int64_t b, const int64_t* shifts, int nshift, double* out,
+                           int64_t out_offset, int64_t oss, int64_t osh, int64_t obin,
+                           cudaStream_t stream, const int64_t* shift_table) {
+  FourStepParams q;
+  memset(&q, 0, sizeof(q));
+  if (!split_size(b, AFFT_MAX_SMEM_DFT, &q.b1, &q.b2)) {
+    set_error("bucket count %lld has no factorisation into two DFTs of size <= %d",
+              (long long)b, AFFT_MAX_SMEM_DFT);
+    return AFFT_EUNSUPPORTED;
+  }
+  if (!make_dft_plan(q.b1, &q.plan1) || !make_dft_plan(q.b2, &q.plan2)) {
+    set_error("cannot plan DFTs of sizes %lld x %lld", (long long)q.b1, (long long)q.b2);
+    return AFFT_EUNSUPPORTED;
+  }
+  q.x = x;
+  q.dtype = dtype;
+  q.n = n;
+  q.ld = ld;
+  q.b = b;
+  q.nshift = nshift;
+  q.out = out;
+  q.out_offset = out_offset;
+  q.out_signal_stride = oss;
+  q.out_shift_stride = osh;
+  q.out_bin_stride = obin;
+  q.shift_table = shift_table;
+  for (int t = 0; t < nshift; ++t) q.tau[t] = shifts ? host_pymod(shifts[t], n) : 0;
+  const size_t kBudget = 96 * 1024;
+  q.cj = (int)std::max<int64_t>(1, std::min<int64_t>(q.b1, ((int64_t)(kBudget / 16) - q.b2) / (2 * q.b2)));
+  q.wi = (int)std::max<int64_t>(1, std::min<int64_t>(q.b2, ((int64_t)(kBudget / 16) - q.b1) / (2 * q.b1)));
+  const size_t smemA = (size_t)(q.b2 + 2 * (int64_t)q.cj * q.b2) * 16;
+  const size_t smemB = (size_t)(q.b1 + 2 * (int64_t)q.wi * q.b1) * 16;
+  const size_t zbytes = (size_t)batch * nshift * b * 16;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&q.z), zbytes, stream);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(four-step scratch)");
+  e = cudaFuncSetAttribute(fourstep_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smemA);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fourstep_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smemB);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(q.z, stream);
+    return cuda_status(e, "cudaFuncSetAttribute(four-step)");
+  }
+  for (int64_t s0 = 0; s0 < batch; s0 += 65535) {
+    const unsigned cntb = (unsigned)std::min<int64_t>(65535, batch - s0);
+    FourStepParams qs = q;
+    qs.x = reinterpret_cast<const char*>(x) + s0 * ld * (dtype == AFFT_C64 ? 8 : 16);
+    qs.z = q.z + 2 * s0 * nshift * b;
+    qs.out = out + 2 * s0 * oss;
+    qs.shift_table = shift_table ? shift_table + s0 * nshift : nullptr;
+    dim3 ga((unsigned)((q.b1 + q.cj - 1) / q.cj), (unsigned)nshift, cntb);
+    fourstep_a_kernel<<<ga, 256, smemA, stream>>>(qs);
+    dim3 gb((unsigned)((q.b2 + q.wi - 1) / q.wi), (unsigned)nshift, cntb);
+    fourstep_b_kernel<<<gb, 256, smemB, stream>>>(qs);
+  }
+  cudaFreeAsync(q.z, stream);
+  AFFT_CHECK_LAUNCH("fourstep kernels");
+  return AFFT_OK;
+}
+
 static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                              const int64_t* factors, int ncycles, const int64_t* out_offsets,
                              const int64_t* shifts, int nshift, double* out, int64_t oss,
@@ -123,9 +292,20 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
       return AFFT_EINVAL;
     }
     if (b > AFFT_MAX_SMEM_DFT) {
-      set_error("bucket count %lld exceeds the one-CTA DFT limit %d", (long long)b,
-                AFFT_MAX_SMEM_DFT);
-      return AFFT_EUNSUPPORTED;
+      if (nshift > 65535) {
+        set_error("too many shifts for the large-b path");
+        return AFFT_EUNSUPPORTED;
+      }
+      int rc = launch_fourstep(x, dtype, n, batch, ld, b, shifts, nshift, out, out_offsets[c],
+                               oss, osh, obin, stream, shift_table);
+      if (rc) return rc;
+      q.b[c] = b;
+      q.jobs[c] = 0;  // handled above
+      q.chunk[c] = 1;
+      q.out_offset[c] = out_offsets[c];
+      q.plan[c].n = 1;
+      q.plan[c].nstages = 0;
+      continue;
     }
     if (!make_dft_plan(b, &q.plan[c])) {
       set_error("cannot plan a DFT of size %lld", (long long)b);
@@ -141,6 +321,7 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
     size_t bytes = (size_t)(b + 2 * (int64_t)chunk * b) * 16;
     smem_max = std::max(smem_max, bytes);
   }
+  if (total_jobs == 0) return AFFT_OK;  // every cycle went through the four-step path
   if (total_jobs > 65535) {
     set_error("too many (cycle, shift-chunk) jobs per signal: %d", total_jobs);
     return AFFT_EUNSUPPORTED;

@@ -296,11 +296,11 @@ __global__ void subtract_kernel(double* __restrict__ residual, int nshift,
 __global__ void truncate_kernel(const int64_t* __restrict__ pos, const double* __restrict__ val,
                                 const int32_t* __restrict__ count, int cap, int k,
                                 int64_t* __restrict__ out_pos, double* __restrict__ out_val,
-                                int32_t* __restrict__ out_count) {
+                                int32_t* __restrict__ out_count, double* gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t s = blockIdx.x;
   const int m = count[s];
-  double* mag = reinterpret_cast<double*>(smem_raw);
+  double* mag = gscratch ? gscratch + s * (int64_t)cap * 2 : reinterpret_cast<double*>(smem_raw);
   int64_t* fs = reinterpret_cast<int64_t*>(mag + cap);
   const int64_t* ps = pos + s * cap;
   const cd* vs = reinterpret_cast<const cd*>(val) + s * cap;
@@ -389,16 +389,21 @@ static int launch_peel(PeelParams& p, int64_t batch, void* scratch, cudaStream_t
 static int launch_truncate(const int64_t* pos, const double* val, const int32_t* count, int cap,
                            int64_t batch, int k, int64_t* out_pos, double* out_val,
                            int32_t* out_count, cudaStream_t stream) {
-  const size_t smem = (size_t)std::max(cap, 1) * 16;
-  if (smem > kSmemLimit) {
-    set_error("truncate: %d entries per signal exceed the shared-memory ranker", cap);
-    return AFFT_EUNSUPPORTED;
+  size_t smem = (size_t)std::max(cap, 1) * 16;
+  double* scratch = nullptr;
+  if (smem > kSmemLimit) {  // large graphs: rank from global memory
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                    (size_t)batch * cap * 16, stream);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(truncate scratch)");
+    smem = 0;
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(truncate_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(truncate)");
   }
-  cudaError_t e = cudaFuncSetAttribute(truncate_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(truncate)");
-  truncate_kernel<<<(unsigned)batch, 256, smem, stream>>>(pos, val, count, cap, k, out_pos,
-                                                           out_val, out_count);
+  truncate_kernel<<<(unsigned)batch, 1024, smem, stream>>>(pos, val, count, cap, k, out_pos,
+                                                            out_val, out_count, scratch);
+  if (scratch) cudaFreeAsync(scratch, stream);
   AFFT_CHECK_LAUNCH("truncate_kernel");
   return AFFT_OK;
 }

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "afft_common.cuh"
@@ -309,7 +310,8 @@ __global__ void __launch_bounds__(512) noisy_harvest_kernel(
     int8_t* __restrict__ dirty, const int64_t* __restrict__ node_f0,
     const double* __restrict__ node_val, int32_t* __restrict__ done, int64_t* __restrict__ rec_pos,
     double* __restrict__ rec_val, int rec_cap, int32_t* __restrict__ rec_count,
-    int32_t* __restrict__ rounds, int32_t* __restrict__ total_found) {
+    int32_t* __restrict__ rounds, int32_t* __restrict__ total_found, char* gscratch,
+    size_t scratch_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int warp_tmp[32];
   __shared__ int carry;
@@ -317,7 +319,9 @@ __global__ void __launch_bounds__(512) noisy_harvest_kernel(
   if (done[s]) return;
   const int N = P.nodes;
   const int tid = threadIdx.x, nt = blockDim.x;
-  unsigned long long* hash = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned char* mem = gscratch ? reinterpret_cast<unsigned char*>(gscratch) + s * scratch_bytes
+                                : smem_raw;
+  unsigned long long* hash = reinterpret_cast<unsigned long long*>(mem);
   int* flag = reinterpret_cast<int*>(hash + P.hmask + 1);
   int32_t* found_g = flag + N;
   int32_t* found_res = found_g + N;          // [nf][ncycles]
@@ -486,6 +490,85 @@ __global__ void robust_thresholds_kernel(int count, int pow2, const double* __re
   }
 }
 
+// k-th smallest (0-based) of cnt non-negative doubles by 8-bit radix select on the
+// IEEE bit patterns (order-preserving for values >= +0).  One CTA, global data.
+__device__ double radix_select(const double* v, int cnt, int kth, unsigned* hist) {
+  __shared__ unsigned long long prefix;
+  __shared__ int remaining;
+  if (threadIdx.x == 0) {
+    prefix = 0ull;
+    remaining = kth;
+  }
+  __syncthreads();
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const unsigned long long pre = prefix;
+    const unsigned long long mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(v[i]);
+      if ((bits & mask) == pre) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int r = remaining;
+      unsigned d = 0;
+      while (d < 255 && r >= (int)hist[d]) {
+        r -= (int)hist[d];
+        ++d;
+      }
+      remaining = r;
+      prefix = pre | ((unsigned long long)d << shift);
+    }
+    __syncthreads();
+  }
+  return __longlong_as_double((long long)prefix);
+}
+
+__global__ void robust_thresholds_large_kernel(int count, const double* __restrict__ energy,
+                                               const uint8_t* __restrict__ mask, int r,
+                                               double* __restrict__ scratch,
+                                               double* __restrict__ t0, double* __restrict__ t1) {
+  __shared__ unsigned hist[256];
+  __shared__ int m_count;
+  __shared__ double m_max;
+  const int64_t s = blockIdx.x;
+  const double* E = energy + s * (int64_t)count;
+  const uint8_t* M = mask ? mask + s * (int64_t)count : nullptr;
+  double* v = scratch + s * (int64_t)count;
+  if (threadIdx.x == 0) {
+    int cnt = 0;
+    double mx = 0.0;
+    for (int i = 0; i < count; ++i) {
+      mx = fmax(mx, E[i]);
+      if (!M || M[i]) v[cnt++] = E[i];
+    }
+    if (M && cnt == 0) {
+      for (int i = 0; i < count; ++i) v[i] = E[i];
+      cnt = count;
+    }
+    m_count = cnt;
+    m_max = mx;
+  }
+  __syncthreads();
+  const int cnt = m_count;
+  double med;
+  if (cnt & 1) {
+    med = radix_select(v, cnt, cnt / 2, hist);
+  } else {
+    const double lo = radix_select(v, cnt, cnt / 2 - 1, hist);
+    const double hi = radix_select(v, cnt, cnt / 2, hist);
+    med = (lo + hi) / 2.0;
+  }
+  if (threadIdx.x == 0) {
+    const double sigma = sqrt(fmax(med, 0.0) / (double)r);
+    const double floor_ = 1e-8 * sqrt(m_max);
+    const double base = sigma * sqrt((double)r);
+    t0[s] = fmax(1.5 * base, floor_);
+    t1[s] = fmax(2.5 * base, floor_);
+  }
+}
+
 // -------------------------------------------------------------- host side
 
 static int make_noisy_plan(NoisyPlan* P, int64_t n, const int64_t* factors, int ncycles,
@@ -610,7 +693,8 @@ using namespace afft;
 
 extern "C" size_t afft_noisy_workspace_size(int64_t n, int64_t batch, const int64_t* factors,
                                             int32_t ncycles, int32_t c, int32_t m) {
-  NoisyPlan* P = new NoisyPlan();
+  std::unique_ptr<NoisyPlan> P_owner(new NoisyPlan());
+  NoisyPlan* P = P_owner.get();
   std::vector<int64_t> zeros((size_t)std::max(1, c * m), 0);
   double wts[kMaxRounds] = {0};
   int64_t nodes = 0;
@@ -618,7 +702,6 @@ extern "C" size_t afft_noisy_workspace_size(int64_t n, int64_t batch, const int6
   size_t out = 0;
   if (!make_noisy_plan(P, n, factors, ncycles, zeros.data(), c * m, c, m, wts, (int)nodes))
     out = noisy_ws(*P, batch * P->nodes).total;
-  delete P;
   return out;
 }
 
@@ -646,10 +729,16 @@ extern "C" int afft_robust_thresholds(const double* energy, const uint8_t* mask,
   int pow2 = 1;
   while (pow2 < count) pow2 <<= 1;
   const size_t smem = (size_t)pow2 * 8;
-  if (smem > 200 * 1024) {
-    set_error("robust_thresholds: %lld energies per signal exceed the in-smem median",
-              (long long)count);
-    return AFFT_EUNSUPPORTED;
+  if (smem > 200 * 1024) {  // large: radix-select median over a global copy
+    double* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                    (size_t)batch * count * 8, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(median scratch)");
+    robust_thresholds_large_kernel<<<(unsigned)batch, 1024, 0, (cudaStream_t)stream>>>(
+        (int)count, energy, mask, r, scratch, t0, t1);
+    cudaFreeAsync(scratch, (cudaStream_t)stream);
+    AFFT_CHECK_LAUNCH("robust_thresholds_large_kernel");
+    return AFFT_OK;
   }
   cudaError_t e = cudaFuncSetAttribute(robust_thresholds_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -672,15 +761,14 @@ extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t
     set_error("afft_singleton_search_noisy: bad arguments");
     return AFFT_EINVAL;
   }
-  NoisyPlan* P = new NoisyPlan();
+  std::unique_ptr<NoisyPlan> P_owner(new NoisyPlan());
+  NoisyPlan* P = P_owner.get();
   int rc = make_noisy_plan(P, n, &b, 1, shifts, nshift, c, m, weights, 1);
   if (rc) {
-    delete P;
     return rc;
   }
   const NoisyWs w = noisy_ws(*P, count);
   if (!workspace || workspace_bytes < w.total) {
-    delete P;
     set_error("afft_singleton_search_noisy: workspace of %zu bytes needed", w.total);
     return AFFT_ENOMEM;
   }
@@ -700,7 +788,6 @@ extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t
     cudaError_t e = cudaStreamSynchronize(st);  // host vectors above must outlive the copies
     if (e != cudaSuccess) rc = cuda_status(e, "singleton_search_noisy");
   }
-  delete P;
   return rc;
 }
 
@@ -718,22 +805,20 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     set_error("afft_peel_noisy: bad arguments");
     return AFFT_EINVAL;
   }
-  NoisyPlan* P = new NoisyPlan();
+  std::unique_ptr<NoisyPlan> P_owner(new NoisyPlan());
+  NoisyPlan* P = P_owner.get();
   int rc = make_noisy_plan(P, n, factors, ncycles, shifts, nshift, c, m, weights, rec_cap);
   if (rc) {
-    delete P;
     return rc;
   }
   const int N = P->nodes;
   const NoisyWs w = noisy_ws(*P, batch * N);
   if (!workspace || workspace_bytes < w.total) {
-    delete P;
     set_error("afft_peel_noisy: workspace of %zu bytes needed, %zu given", w.total,
               workspace_bytes);
     return AFFT_ENOMEM;
   }
   if ((int64_t)batch * N > INT32_MAX) {
-    delete P;
     set_error("afft_peel_noisy: batch * nodes exceeds 2^31");
     return AFFT_EUNSUPPORTED;
   }
@@ -744,7 +829,6 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
   int32_t* counters = reinterpret_cast<int32_t*>(ws + w.counters);
   int32_t* host = pinned_counter();
   if (!host) {
-    delete P;
     set_error("afft_peel_noisy: cannot allocate a pinned host counter");
     return AFFT_ENOMEM;
   }
@@ -752,21 +836,25 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
   if (e == cudaSuccess) e = cudaMemsetAsync(done, 0, (size_t)batch * 4, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(rounds, 0, (size_t)batch * 4, st);
   if (e != cudaSuccess) {
-    delete P;
     return cuda_status(e, "afft_peel_noisy init");
   }
   int hcap = P->hmask + 1;
-  const size_t hsmem = (size_t)hcap * 8 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64;
-  if (hsmem > 200 * 1024) {
-    delete P;
-    set_error("afft_peel_noisy: graph of %d nodes exceeds the harvest kernel's smem", N);
-    return AFFT_EUNSUPPORTED;
-  }
-  e = cudaFuncSetAttribute(noisy_harvest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)hsmem);
-  if (e != cudaSuccess) {
-    delete P;
-    return cuda_status(e, "cudaFuncSetAttribute(noisy_harvest)");
+  const size_t hbytes =
+      ((size_t)hcap * 8 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64 + 15) & ~size_t(15);
+  size_t hsmem = hbytes;
+  char* hscratch = nullptr;
+  if (hbytes > 200 * 1024) {  // large graphs: harvest state in global memory
+    e = cudaMallocAsync(reinterpret_cast<void**>(&hscratch), (size_t)batch * hbytes, st);
+    if (e != cudaSuccess) {
+      return cuda_status(e, "cudaMallocAsync(noisy harvest scratch)");
+    }
+    hsmem = 0;
+  } else {
+    e = cudaFuncSetAttribute(noisy_harvest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)hsmem);
+    if (e != cudaSuccess) {
+      return cuda_status(e, "cudaFuncSetAttribute(noisy_harvest)");
+    }
   }
   const int64_t total = batch * N;
   for (int it = 0; it < max_rounds; ++it) {
@@ -778,12 +866,12 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     AFFT_CHECK_LAUNCH("noisy_prep_kernel");
     cudaMemcpyAsync(host, counters, 4, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
-      delete P;
+      if (hscratch) cudaFreeAsync(hscratch, st);
       return cuda_status(e, "afft_peel_noisy round sync");
     }
     const int A = host[0];
     if ((rc = run_search(*P, w, ws, A, residual, st))) {
-      delete P;
+      if (hscratch) cudaFreeAsync(hscratch, st);
       return rc;
     }
     if (A > 0) {
@@ -795,18 +883,17 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     }
     noisy_harvest_kernel<<<(unsigned)batch, 512, hsmem, st>>>(
         *P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap,
-        rec_count, rounds, counters + 1);
+        rec_count, rounds, counters + 1, hscratch, hbytes);
     AFFT_CHECK_LAUNCH("noisy_harvest_kernel");
     cudaMemcpyAsync(host + 1, counters + 1, 4, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
-      delete P;
       return cuda_status(e, "afft_peel_noisy round sync");
     }
     if (host[1] == 0) break;  // every signal found nothing: all loops have exited
   }
   count_multi_kernel<<<(unsigned)batch, 256, 0, st>>>(batch, N, state, unresolved);
+  if (hscratch) cudaFreeAsync(hscratch, st);
   AFFT_CHECK_LAUNCH("count_multi_kernel");
-  delete P;
   return AFFT_OK;
 }
 

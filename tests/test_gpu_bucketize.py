@@ -54,7 +54,10 @@ def test_alias_sum_exhaustive_small(rng):
 
 @pytest.mark.parametrize("n,b", [(124950, 49), (124950, 50), (124950, 51), (2097024, 127),
                                  (2097024, 128), (2097024, 129), (1 << 22, 1024),
-                                 (1 << 24, 4096), (511 * 512 * 8, 511), (3 * 17 * 19 * 73, 73 * 17)])
+                                 (1 << 24, 4096), (511 * 512 * 8, 511), (3 * 17 * 19 * 73, 73 * 17),
+                                 # K2' four-step path (b > 4096)
+                                 (9728 * 7, 9728), (13797 * 5, 13797), (1 << 20, 1 << 13),
+                                 (1 << 20, 1 << 20), (3 << 16, 3 << 15)])
 def test_config_sizes_vs_oracle(n, b):
     from paper_2011_05749_b200.bucketize import bucketize_device
 
@@ -103,3 +106,21 @@ def test_errors_and_ledger():
     ledger = SampleLedger(24)
     bucketize_set(np.zeros(24), 6, [0, 1, 2, 3, 10], ledger)
     assert ledger.count == 30 and ledger.unique_count <= 24
+
+
+def test_large_b_batched_and_strided():
+    """Four-step path with a batch, per-signal rows and the node layout."""
+    from paper_2011_05749_b200 import _lib
+    from paper_2011_05749_b200 import peeling
+
+    rng = np.random.default_rng(7)
+    n, factors, shifts = 9728 * 13 * 4, [9728, 13 * 4], [0, 1, 2, 5]
+    xs = (rng.normal(size=(3, n)) + 1j * rng.normal(size=(3, n))).astype(np.complex64)
+    for i in range(3):
+        got = peeling.build_graph_device(torch.from_numpy(xs[i]).cuda(), factors, shifts)
+        want = of.graph_values(xs[i].astype(np.complex128), factors, shifts)
+        assert _close(got.cpu().numpy(), want, 1e-12)
+    with pytest.raises(Exception):
+        # prime bucket count above the one-CTA limit has no two-factor split
+        from paper_2011_05749_b200.bucketize import bucketize_device
+        bucketize_device(torch.zeros(4099 * 2, dtype=torch.complex128).cuda(), 4099, [0])

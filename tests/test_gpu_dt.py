@@ -100,3 +100,21 @@ def test_recovery_and_validation():
     with pytest.raises(ValueError):
         sfft_dt(np.zeros(1 << 22, complex), 10, OneShotConfig(b=1024, p=12, variant="dt2"))
     assert sfft_dt(np.zeros(64, complex), 0).entries == {}
+
+
+def test_default_config_large_b_vs_oracle():
+    """OneShotConfig.default at N=2^20, K=1000 picks B=32768 (four-step bucketization)."""
+    from oracle import oneshot as od
+    from paper_2011_05749_b200 import OneShotConfig, generate_test_case, sfft_dt_batch
+
+    n, k = 1 << 20, 1000
+    case = generate_test_case(n, k, "exact", seed=3)
+    cfg = OneShotConfig.default(n, k, "dt3", seed=3)
+    assert cfg.b == 32768
+    res = sfft_dt_batch(case.signal[None, :], k, cfg.b, cfg.a_m, cfg.p, "dt3", seeds=[3])
+    _, entries, counts = od.sfft_dt(case.signal, k, cfg.b, cfg.a_m, cfg.p, "dt3", 3)
+    assert np.array_equal(res.counts[0].cpu().numpy(), counts)
+    got = {f: v for f, v in res.full_spectrum(0).entries.items() if abs(v) > SIG}
+    want = {f: v for f, v in entries.items() if abs(v) > SIG}
+    assert set(got) == set(want)
+    assert max(abs(got[f] - v) for f, v in want.items()) <= 1e-9
