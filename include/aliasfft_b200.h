@@ -266,6 +266,34 @@ int afft_sfft_dt(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                  double* all_val, int32_t* all_count, int32_t* counts_out, void* workspace,
                  size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------ DSFFT tree layers */
+
+/*
+ * Rows of selected buckets at arbitrary shifts (dsfft.py:118-174, 201-228):
+ * rows[r][t] = bucketize(x, b, shifts[t]).values[bucket_idx[r]] for one signal, with
+ * shifts sharing a coset mod n/b served by one DFT; energy [b] (may be NULL) gets
+ * sum_t |bucketize(x, b, shifts[t]).values[i]|^2 for every bucket.
+ */
+int afft_bucketize_rows(const void* x, int dtype, int64_t n, int64_t b,
+                        const int64_t* shifts /* host */, int32_t nshift,
+                        const int64_t* bucket_idx, int64_t nrows, double* rows, double* energy,
+                        void* stream);
+
+/*
+ * Ascending indices i < b with |values[i]| > thr (dsfft.py:78, 114); with map != NULL the
+ * written value is map[i].  out_count is a device int32.
+ */
+int afft_active_indices(const double* values, int64_t b, double thr, const int64_t* map,
+                        int64_t* out_idx, int32_t* out_count, void* stream);
+
+/* expand_layer's selective direct sums (dsfft.py:99-109) for ncand candidate buckets. */
+int afft_selective_sums(const void* x, int dtype, int64_t n, int64_t b, const int64_t* cand,
+                        int64_t ncand, double* out, void* stream);
+
+/* np.median per row of `count` values: mode 0 real values, mode 1 |complex|^2. */
+int afft_median(const double* values, int32_t mode, int64_t count, int64_t batch, double* out,
+                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

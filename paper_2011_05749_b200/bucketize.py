@@ -64,10 +64,14 @@ def gather_indices(n: int, b: int, tau: int) -> np.ndarray:
 
 
 def record_bucketization(ledger: SampleLedger | None, n: int, b: int, shifts) -> None:
+    """Replay ledger.record for each shift: the index set of one bucketization is the
+    residue class (-tau) mod L of stride L = n/b, so it is recorded as a strided slice."""
     if ledger is None:
         return
+    step = n // b
     for tau in shifts:
-        ledger.record(gather_indices(n, b, int(tau)))
+        ledger.count += b
+        ledger._mask[(-int(tau)) % step::step] = True
 
 
 def shift(x, tau: int):

@@ -1,0 +1,259 @@
+// K6: DSFFT tree-layer primitives (dsfft.py:73-241).
+//
+//   afft_bucketize_rows   bucket values of selected buckets at arbitrary shifts,
+//                         the measurement rows of _classify_active (dsfft.py:118-174)
+//                         and collect_moments for _resolve_aliased (201-228).  Shifts
+//                         in the same coset mod L = n/b share one size-b DFT:
+//                         tau = q*L + r  =>  y_tau[i] = w_b^{i*q} * y_r[i]
+//                         (substitute j' = j - q in the alias sum), so a layer needs
+//                         min(#shifts, L) DFTs instead of #shifts — one at depth log2 n;
+//                         optionally the per-bucket energies sum_t |y_tau[i]|^2 of all
+//                         b buckets (the thresholds' floor / median set);
+//   afft_active_indices   ascending indices i with |values[i]| > thr (initial_layer /
+//                         expand_layer activity, 69-79, 114), a stream compaction;
+//   afft_selective_sums   expand_layer's direct alias sums for candidate buckets
+//                         (Eq. 23, dsfft.py:99-109): (1/b) sum_j x[j*L] w_b^{i*j}.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "afft_common.cuh"
+
+extern "C" int afft_bucketize(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                              int64_t b, const int64_t* shifts, int32_t nshift, double* out,
+                              int64_t out_signal_stride, int64_t out_shift_stride,
+                              int64_t out_bin_stride, void* stream);
+
+namespace afft {
+
+struct RowsParams {
+  int64_t b;
+  int nshift;
+  int64_t nrows;
+  int32_t coset[AFFT_MAX_SHIFTS];  // which distinct-residue DFT serves shift t
+  int64_t q[AFFT_MAX_SHIFTS];      // rotation count: tau mod n = q*L + r
+};
+
+// rows[r][t] = w_b^{(i_r * q_t) mod b} * Y[coset_t][i_r]
+__global__ void rows_gather_kernel(const __grid_constant__ RowsParams p, const cd* __restrict__ Y,
+                                   const int64_t* __restrict__ idx, cd* __restrict__ rows) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.nrows * p.nshift) return;
+  const int64_t r = e / p.nshift;
+  const int t = (int)(e - r * p.nshift);
+  const int64_t i = idx[r];
+  const cd y = Y[(int64_t)p.coset[t] * p.b + i];
+  if (p.q[t] == 0) {
+    rows[e] = y;
+    return;
+  }
+  const int64_t ph = (i * p.q[t]) % p.b;
+  double sn, cs;
+  sincospi(-2.0 * (double)ph / (double)p.b, &sn, &cs);
+  rows[e] = cmul(y, cd{cs, sn});
+}
+
+struct Mult {
+  int32_t m[AFFT_MAX_SHIFTS];
+};
+
+// energy[i] = sum_t |y_tau_t[i]|^2 = sum_u mult_u |Y_u[i]|^2
+__global__ void coset_energy_kernel(int64_t b, int U, const __grid_constant__ Mult mult,
+                                    const cd* __restrict__ Y, double* __restrict__ energy) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  double e = 0.0;
+  for (int u = 0; u < U; ++u) {
+    const cd y = Y[(int64_t)u * b + i];
+    const double m2 = cabs_(y);
+    e += (double)mult.m[u] * (m2 * m2);
+  }
+  energy[i] = e;
+}
+
+// ---------------------------------------------------------------- compaction
+
+constexpr int kCompactThreads = 1024;
+
+__global__ void active_count_kernel(int64_t b, const cd* __restrict__ v, double thr,
+                                    int32_t* __restrict__ block_counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = (i < b) && (cabs_(v[i]) > thr);
+  const int c = __syncthreads_count(f);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
+}
+
+__global__ void scan_counts_kernel(int nblocks, int32_t* __restrict__ counts,
+                                   int32_t* __restrict__ total) {
+  // single thread: nblocks <= 2^24 / 1024 = 16384
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int32_t run = 0;
+    for (int k = 0; k < nblocks; ++k) {
+      const int32_t c = counts[k];
+      counts[k] = run;
+      run += c;
+    }
+    *total = run;
+  }
+}
+
+__global__ void active_write_kernel(int64_t b, const cd* __restrict__ v, double thr,
+                                    const int32_t* __restrict__ offsets,
+                                    const int64_t* __restrict__ map, int64_t* __restrict__ out) {
+  __shared__ int warp_off[kCompactThreads / 32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = (i < b) && (cabs_(v[i]) > thr);
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) warp_off[w] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int k = 0; k < kCompactThreads / 32; ++k) {
+      const int c = warp_off[k];
+      warp_off[k] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (f) out[offsets[blockIdx.x] + warp_off[w] + __popc(m & ((1u << lane) - 1u))] = map ? map[i] : i;
+}
+
+// ---------------------------------------------------------------- selective sums
+
+// out[c] = (1/b) sum_j x[j*L] * w_b^{(i_c * j) mod b}, one CTA per candidate
+__global__ void selective_sum_kernel(const void* __restrict__ x, int dtype, int64_t n, int64_t b,
+                                     const int64_t* __restrict__ cand, double* __restrict__ out) {
+  const int64_t c = blockIdx.x;
+  const int64_t i = cand[c];
+  const int64_t L = n / b;
+  double re = 0.0, im = 0.0;
+  for (int64_t j = threadIdx.x; j < b; j += blockDim.x) {
+    const cd s = load_sample(x, dtype, j * L);
+    double sn, cs;
+    sincospi(-2.0 * (double)((i * j) % b) / (double)b, &sn, &cs);
+    re += s.re * cs - s.im * sn;
+    im += s.re * sn + s.im * cs;
+  }
+  __shared__ double wr[32], wi[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    wr[threadIdx.x >> 5] = re;
+    wi[threadIdx.x >> 5] = im;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tr = 0.0, ti = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      tr += wr[w];
+      ti += wi[w];
+    }
+    const double inv = 1.0 / (double)b;
+    out[2 * c] = tr * inv;
+    out[2 * c + 1] = ti * inv;
+  }
+}
+
+}  // namespace afft
+
+using namespace afft;
+
+extern "C" int afft_bucketize_rows(const void* x, int dtype, int64_t n, int64_t b,
+                                   const int64_t* shifts, int32_t nshift,
+                                   const int64_t* bucket_idx, int64_t nrows, double* rows,
+                                   double* energy, void* stream) {
+  if (nshift == 0) return AFFT_OK;
+  if (!x || !shifts || (nrows > 0 && (!bucket_idx || !rows)) || b < 1 || n % b ||
+      nshift < 0 || nshift > AFFT_MAX_SHIFTS) {
+    set_error("afft_bucketize_rows: bad arguments");
+    return AFFT_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t L = n / b;
+  RowsParams p;
+  memset(&p, 0, sizeof(p));
+  p.b = b;
+  p.nshift = nshift;
+  p.nrows = nrows;
+  std::map<int64_t, int> seen;
+  std::vector<int64_t> residues;
+  std::vector<int32_t> mult;
+  for (int t = 0; t < nshift; ++t) {
+    const int64_t tm = host_pymod(shifts[t], n);
+    const int64_t r = tm % L, q = tm / L;
+    auto it = seen.find(r);
+    int u;
+    if (it == seen.end()) {
+      u = (int)residues.size();
+      seen[r] = u;
+      residues.push_back(r);
+      mult.push_back(0);
+    } else {
+      u = it->second;
+    }
+    ++mult[u];
+    p.coset[t] = u;
+    p.q[t] = q;
+  }
+  const int U = (int)residues.size();
+  cd* Y = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&Y), (size_t)U * b * 16, st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(coset DFTs)");
+  int rc = afft_bucketize(x, dtype, n, 1, n, b, residues.data(), U,
+                          reinterpret_cast<double*>(Y), (int64_t)U * b, b, 1, stream);
+  if (!rc && nrows > 0) {
+    const int64_t tot = nrows * nshift;
+    rows_gather_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        p, Y, bucket_idx, reinterpret_cast<cd*>(rows));
+    if (cudaGetLastError() != cudaSuccess) rc = cuda_status(cudaErrorLaunchFailure, "rows_gather");
+  }
+  if (!rc && energy) {
+    Mult mm;
+    for (int u = 0; u < U; ++u) mm.m[u] = mult[u];
+    coset_energy_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(b, U, mm, Y, energy);
+  }
+  cudaFreeAsync(Y, st);
+  if (!rc) AFFT_CHECK_LAUNCH("afft_bucketize_rows");
+  return rc;
+}
+
+extern "C" int afft_active_indices(const double* values, int64_t b, double thr,
+                                   const int64_t* map, int64_t* out_idx, int32_t* out_count,
+                                   void* stream) {
+  if (!values || !out_idx || !out_count || b < 1) {
+    set_error("afft_active_indices: bad arguments");
+    return AFFT_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nblocks = (int)((b + kCompactThreads - 1) / kCompactThreads);
+  int32_t* counts = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), (size_t)nblocks * 4, st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(compaction)");
+  const cd* v = reinterpret_cast<const cd*>(values);
+  active_count_kernel<<<nblocks, kCompactThreads, 0, st>>>(b, v, thr, counts);
+  scan_counts_kernel<<<1, 32, 0, st>>>(nblocks, counts, out_count);
+  active_write_kernel<<<nblocks, kCompactThreads, 0, st>>>(b, v, thr, counts, map, out_idx);
+  cudaFreeAsync(counts, st);
+  AFFT_CHECK_LAUNCH("afft_active_indices");
+  return AFFT_OK;
+}
+
+extern "C" int afft_selective_sums(const void* x, int dtype, int64_t n, int64_t b,
+                                   const int64_t* cand, int64_t ncand, double* out,
+                                   void* stream) {
+  if (ncand == 0) return AFFT_OK;
+  if (!x || !cand || !out || b < 1 || n % b || ncand < 0 || ncand > INT32_MAX) {
+    set_error("afft_selective_sums: bad arguments");
+    return AFFT_EINVAL;
+  }
+  selective_sum_kernel<<<(unsigned)ncand, 256, 0, (cudaStream_t)stream>>>(x, dtype, n, b, cand,
+                                                                          out);
+  AFFT_CHECK_LAUNCH("selective_sum_kernel");
+  return AFFT_OK;
+}

@@ -103,9 +103,11 @@ __global__ void dt_truncate_kernel(int64_t nrows, int a_m, int k, const int64_t*
                                    const int32_t* __restrict__ cnt, int cap,
                                    int64_t* __restrict__ all_pos, double* __restrict__ all_val,
                                    int32_t* __restrict__ all_count, int64_t* __restrict__ out_pos,
-                                   double* __restrict__ out_val, int32_t* __restrict__ out_count) {
+                                   double* __restrict__ out_val, int32_t* __restrict__ out_count,
+                                   double* gscratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* mag = reinterpret_cast<double*>(smem_raw);
+  double* mag = gscratch ? gscratch + blockIdx.x * (int64_t)cap
+                         : reinterpret_cast<double*>(smem_raw);
   __shared__ int total;
   const int64_t s = blockIdx.x;
   const int32_t* c = cnt + s * nrows;
@@ -270,18 +272,23 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
     set_error("afft_dt_truncate: bad arguments");
     return AFFT_EINVAL;
   }
-  const size_t smem = (size_t)std::max<int64_t>(cap, 1) * 8;
-  if (smem > 200 * 1024) {
-    set_error("afft_dt_truncate: %lld entries per signal exceed the in-smem ranker",
-              (long long)cap);
-    return AFFT_EUNSUPPORTED;
+  size_t smem = (size_t)std::max<int64_t>(cap, 1) * 8;
+  double* scratch = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (smem > 200 * 1024) {  // many buckets: magnitudes in global memory
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                    (size_t)batch * cap * 8, st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(dt_truncate scratch)");
+    smem = 0;
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(dt_truncate_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(dt_truncate)");
   }
-  cudaError_t e = cudaFuncSetAttribute(dt_truncate_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(dt_truncate)");
-  dt_truncate_kernel<<<(unsigned)batch, 256, smem, (cudaStream_t)stream>>>(
+  dt_truncate_kernel<<<(unsigned)batch, 1024, smem, st>>>(
       nrows, a_m, k, pos, val, cnt, (int)cap, all_pos, all_val, all_count, out_pos, out_val,
-      out_count);
+      out_count, scratch);
+  if (scratch) cudaFreeAsync(scratch, st);
   AFFT_CHECK_LAUNCH("dt_truncate_kernel");
   return AFFT_OK;
 }

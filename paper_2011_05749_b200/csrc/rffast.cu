@@ -932,3 +932,48 @@ extern "C" int afft_classify_noisy(const double* residual, const int64_t* index,
   AFFT_CHECK_LAUNCH("noisy_decide_kernel");
   return AFFT_OK;
 }
+
+namespace afft {
+// np.median of |v|^2 (complex input, mode 1) or of v (real, mode 0), one CTA per row.
+__global__ void median_kernel(int count, int mode, const double* __restrict__ in,
+                              double* __restrict__ scratch, double* __restrict__ out) {
+  __shared__ unsigned hist[256];
+  const int64_t s = blockIdx.x;
+  double* v = scratch + s * (int64_t)count;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    if (mode == 1) {
+      const double a = hypot(in[2 * (s * (int64_t)count + i)], in[2 * (s * (int64_t)count + i) + 1]);
+      v[i] = a * a;
+    } else {
+      v[i] = in[s * (int64_t)count + i];
+    }
+  }
+  __syncthreads();
+  double med;
+  if (count & 1) {
+    med = radix_select(v, count, count / 2, hist);
+  } else {
+    const double lo = radix_select(v, count, count / 2 - 1, hist);
+    const double hi = radix_select(v, count, count / 2, hist);
+    med = (lo + hi) / 2.0;
+  }
+  if (threadIdx.x == 0) out[s] = med;
+}
+}  // namespace afft
+
+extern "C" int afft_median(const double* values, int32_t mode, int64_t count, int64_t batch,
+                           double* out, void* stream) {
+  if (batch == 0) return AFFT_OK;
+  if (!values || !out || count < 1 || count > INT32_MAX || (mode != 0 && mode != 1)) {
+    set_error("afft_median: bad arguments");
+    return AFFT_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)batch * count * 8, st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(median)");
+  median_kernel<<<(unsigned)batch, 1024, 0, st>>>((int)count, mode, values, scratch, out);
+  cudaFreeAsync(scratch, st);
+  AFFT_CHECK_LAUNCH("median_kernel");
+  return AFFT_OK;
+}

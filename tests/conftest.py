@@ -101,3 +101,16 @@ def dt_signal(case):
 
     x = generate_test_case(case["n"], case["k"], case["snr"], case["seed"]).signal
     return x.astype(np.complex64) if case.get("c64") else x
+
+
+@pytest.fixture(scope="session")
+def golden_dsfft():
+    return load_golden("golden_dsfft.json")
+
+
+def dsfft_signal(case):
+    from paper_2011_05749_b200.signals import generate_test_case
+
+    x = generate_test_case(case["n"], case["k"], case["snr"], case["seed"],
+                           positions=case.get("positions")).signal
+    return x.astype(np.complex64) if case.get("c64") else x

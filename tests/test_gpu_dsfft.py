@@ -1,0 +1,87 @@
+"""GPU DSFFT parity against the reference goldens (config 4's DSFFT leg included when its
+golden exists).  Bar: identical layer trace (depths, active counts, single/multi counts
+per classification), identical output support, values within 1e-9 (complex128) /
+1e-6 (complex64), identical sample ledger."""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR, cx, dsfft_signal
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(case, trace, out, ledger=None):
+    assert trace == case["trace"]
+    want = {f: cx(v) for f, v in case["truncated"]}
+    assert set(out.entries) == set(want), sorted(set(out.entries) ^ set(want))[:10]
+    tol = 1e-6 if case["c64"] else 1e-9
+    for f, v in want.items():
+        assert abs(out.entries[f] - v) <= tol
+    if ledger is not None:
+        assert [ledger.count, ledger.unique_count] == case["ledger"]
+
+
+def _run(case, with_ledger=True):
+    from paper_2011_05749_b200 import DsfftConfig, SampleLedger, SparseSpectrum, _device
+    from paper_2011_05749_b200.dsfft import dsfft_device
+
+    x = dsfft_signal(case)
+    cfg = DsfftConfig(mode=case["mode"], seed=case["seed"], noise_std=case["noise_std"])
+    ledger = SampleLedger(case["n"]) if with_ledger else None
+    trace = []
+    entries = dsfft_device(_device.as_device_signal(x), case["k"], cfg, ledger, trace)
+    ranked = sorted(entries.items(), key=lambda kv: (-abs(kv[1]), kv[0]))
+    return trace, SparseSpectrum(case["n"], dict(ranked[: case["k"]])), ledger
+
+
+def test_dsfft_goldens(golden_dsfft):
+    for case in golden_dsfft["cases"]:
+        trace, out, ledger = _run(case)
+        _check(case, trace, out, ledger)
+
+
+def test_layer_api_kat(golden_dsfft):
+    from paper_2011_05749_b200 import dsfft, evaluate, expand_layer, generate_test_case, initial_layer
+
+    case = generate_test_case(64, 5, "exact", seed=11, positions=[1, 6, 13, 20, 59])
+    layer = initial_layer(case.signal, 0, None, 1e-6)
+    counts = [layer.m_d]
+    for _ in range(3):
+        layer = expand_layer(case.signal, layer, None, 1e-6)
+        counts.append(layer.m_d)
+    assert counts == [1, 2, 4, 5]
+    assert evaluate(case.truth, dsfft(case.signal, 5)).l2 < 1e-9
+    # parent = sum of children (reference tests/test_dsfft.py:39-48)
+    x = generate_test_case(128, 6, "exact", seed=3).signal
+    parent = initial_layer(x, 3, None, 1e-6)
+    child = initial_layer(x, 4, None, 1e-6)
+    for i in range(parent.b):
+        assert abs(parent.values[i] - (child.values[i] + child.values[i + parent.b])) < 1e-9
+
+
+def test_dsfft_errors_and_probabilities():
+    from paper_2011_05749_b200 import (UnsupportedSizeError, dsfft, non_aliasing_probability,
+                                       non_aliasing_probability_limit)
+
+    with pytest.raises(UnsupportedSizeError):
+        dsfft(np.zeros(100, complex), 3)
+    assert dsfft(np.zeros(64, complex), 0).entries == {}
+    assert abs(non_aliasing_probability_limit(4, 8) - 0.4101) < 5e-3
+    assert abs(non_aliasing_probability(64 * 8, 4, 8) - 0.4101) < 2e-2
+
+
+C4 = sorted(glob.glob(os.path.join(GOLDEN_DIR, "golden_dsfft_c4_*db.json")))
+
+
+@pytest.mark.parametrize("path", C4, ids=[os.path.basename(p) for p in C4])
+def test_config4_dsfft_vs_reference(path):
+    """BASELINE config 4, DSFFT leg: N=2^24, K=4096, complex64, noisy (one seeded signal)."""
+    with open(path) as fh:
+        case = json.load(fh)
+    trace, out, _ = _run(case, with_ledger=False)
+    _check(case, trace, out)
