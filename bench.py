@@ -175,23 +175,23 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2011_05749_b200.shard import gather_slots, max_over_ranks, shard_range
+
     total = args.signals
-    per = total // world
-    first = rank * per
-    lib = _lib.load()
+    first, stop = shard_range(total, rank, world)
+    per = stop - first
+    if total % world:
+        raise SystemExit("--signals must be a multiple of the rank count (equal result slots)")
 
     x = torch.empty((per, N_SIG), dtype=torch.complex64, device=dev)
     truths = synth_signals(x, first, dev)
     torch.cuda.synchronize()
 
+    lib = _lib.load()  # noqa: F841  (fail loudly here if the library is missing)
     code = _lib.AFFT_C64
     ws = torch.empty(ffast_workspace_bytes(N_SIG, code, per, FACTORS), dtype=torch.uint8,
                      device=dev)
     res = ffast_batch(x, K, FACTORS, workspace=ws)
-    if world > 1:
-        gpos = torch.empty((total, K), dtype=torch.int64, device=dev)
-        gval = torch.empty((total, K), dtype=torch.complex128, device=dev)
-        gcnt = torch.empty(total, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -205,9 +205,7 @@ def run_ours(args):
         if i is not None:
             ev[i][1].record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(gpos, res.pos)
-            dist.all_gather_into_tensor(gval, res.val)
-            dist.all_gather_into_tensor(gcnt, res.count)
+            gather_slots(res.pos, res.val, res.count)
 
     launches_per_step = 1  # ffast_fused_kernel
 
@@ -237,10 +235,7 @@ def run_ours(args):
         dist.barrier()
     ms = start.elapsed_time(end)
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, kern_ms = (float(v) for v in t.tolist())
+    ms, kern_ms = max_over_ranks([ms, kern_ms], dev)
     ms_per_step = ms / args.steps
 
     e2e = run_e2e(args, dev, x, world) if rank == 0 else None

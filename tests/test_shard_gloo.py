@@ -1,0 +1,69 @@
+"""Multi-rank path of the signal-sharded bench on CPU: world_size 2 over gloo.
+
+Checks the slice arithmetic and that the result-slot all-gather (NCCL on the GPU
+box) reassembles every rank's [signals, k] slots in rank order, and that the
+timing reduction is a max over ranks.
+"""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2011_05749_b200.shard import gather_slots, max_over_ranks, shard_range
+
+
+def test_shard_range_partitions():
+    for total in (0, 1, 7, 8192, 8193):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(total, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    total, k = 10, 4
+    a, b = shard_range(total, rank, world)
+    sig = torch.arange(a, b)
+    pos = (sig[:, None] * 100 + torch.arange(k)[None, :]).to(torch.int64)
+    val = torch.complex(pos.double(), -pos.double())
+    cnt = torch.full((b - a,), rank + 1, dtype=torch.int32)
+    gp, gv, gc = gather_slots(pos, val, cnt)
+    t = max_over_ranks([float(rank), 10.0 - rank], torch.device("cpu"))
+    q.put((rank, gp.tolist(), gv.real.tolist(), gc.tolist(), t))
+    dist.destroy_process_group()
+
+
+def test_gather_slots_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, gp, gv, gc, t in res:
+        assert [row[0] // 100 for row in gp] == list(range(10))
+        assert gv == [[float(v) for v in row] for row in gp]
+        assert gc == [1] * 5 + [2] * 5
+        assert t == [1.0, 10.0]
