@@ -176,11 +176,14 @@ int afft_robust_thresholds(const double* energy, const uint8_t* mask, int64_t co
 size_t afft_noisy_workspace_size(int64_t n, int64_t batch, const int64_t* factors /* host */,
                                  int32_t ncycles, int32_t c, int32_t m);
 
+/* Workspace bytes for afft_singleton_search_noisy / afft_classify_noisy over `count` nodes. */
+size_t afft_singleton_workspace_size(int64_t n, int64_t count, int64_t b, int32_t c, int32_t m);
+
 /*
  * singleton_search_noisy (peeling.py:222-250) for `count` nodes of one cycle size b:
  * residual [count][c*m], index [count]; shifts (host) = SearchPlan.shifts, weights
  * (host) = kay_weights(m).  Outputs f0, val (complex128), resnorm per node.
- * Workspace: afft_noisy_workspace_size(n, count, &b, 1, c, m).  Synchronises.
+ * Workspace: afft_singleton_workspace_size(n, count, b, c, m).  Synchronises.
  */
 int afft_singleton_search_noisy(const double* residual, const int64_t* index, int64_t count,
                                 int64_t b, int64_t n, const int64_t* shifts, int32_t nshift,

@@ -56,6 +56,7 @@ SIGNATURES = {
     "afft_node_energies": (_INT, [_P, _I32, _I64, _P, _P]),
     "afft_robust_thresholds": (_INT, [_P, _P, _I64, _I64, _I32, _P, _P, _P]),
     "afft_noisy_workspace_size": (_SZ, [_I64, _I64, _P, _I32, _I32, _I32]),
+    "afft_singleton_workspace_size": (_SZ, [_I64, _I64, _I64, _I32, _I32]),
     "afft_singleton_search_noisy": (
         _INT, [_P, _P, _I64, _I64, _I64, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "afft_classify_noisy": (

@@ -114,7 +114,8 @@ struct FusedParams {
   int32_t* all_count;
   int32_t* rounds;
   int32_t* unresolved;
-  double* eps_out;  // may be null
+  double* eps_out;       // may be null
+  const double* eps_in;  // may be null: precomputed thresholds (small batches)
 };
 
 constexpr int kFusedThreads = 256;
@@ -196,7 +197,8 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
   const char* row = reinterpret_cast<const char*>(p.x) + s * p.ld * (p.dtype == AFFT_C64 ? 8 : 16);
 
   // 1. exact_thresholds: eps = 1e-6 * ||x|| / sqrt(n), fixed-order block reduction
-  double acc = stream_sumsq(row, p.dtype, n);
+  //    (skipped when a multi-CTA pre-pass already produced eps for a small batch)
+  double acc = p.eps_in ? 0.0 : stream_sumsq(row, p.dtype, n);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((tid & 31) == 0) wsum[tid >> 5] = acc;
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
   }
   double t = 0.0;
   for (int w = 0; w < kFusedThreads / 32; ++w) t += wsum[w];
-  const double eps = (1e-6 * sqrt(t)) / sqrt((double)n);
+  const double eps = p.eps_in ? p.eps_in[s] : (1e-6 * sqrt(t)) / sqrt((double)n);
   // 3. graph state
   for (int g = tid; g < N; g += nt) {
     M.st[g] = AFFT_UNKNOWN;
@@ -556,7 +558,8 @@ extern "C" size_t afft_ffast_workspace_size(int64_t n, int dtype, int64_t batch,
   PeelGraph G;
   if (setup_graph(&G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1))) return 0;
   size_t total = 0, off = 0;
-  if (fused_smem(G, &total, &off)) return 256;  // fused path: no workspace needed
+  if (fused_smem(G, &total, &off))  // fused path: partials + eps for the small-batch pre-pass
+    return al256((size_t)batch * afft_sumsq_parts(n, dtype) * 8) + al256((size_t)batch * 8);
   const size_t bytes = peel_layout(G.nodes, ncycles, G.hmask + 1, false).total;
   return ffast_ws(n, dtype, batch, nodes, bytes > kSmemLimit ? bytes : 0).total;
 }
@@ -602,6 +605,22 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     fp.all_count = all_count;
     fp.rounds = rounds;
     fp.unresolved = unresolved;
+    // Small batches cannot keep HBM busy with one streaming CTA per signal: run the
+    // |x|^2 pass as a multi-CTA partial sum first and feed eps to the fused decode.
+    const int nparts = afft_sumsq_parts(n, dtype);
+    if (batch < 2 * 148 && nparts > 1) {
+      const size_t need = al256((size_t)batch * nparts * 8) + al256((size_t)batch * 8);
+      if (!workspace || workspace_bytes < need) {
+        set_error("afft_ffast: workspace of %zu bytes needed, %zu given", need, workspace_bytes);
+        return AFFT_ENOMEM;
+      }
+      double* partials = reinterpret_cast<double*>(workspace);
+      double* eps = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) +
+                                              al256((size_t)batch * nparts * 8));
+      if ((rc = afft_sumsq(x, dtype, n, batch, ld, partials, st))) return rc;
+      if ((rc = afft_exact_thresholds(partials, nparts, n, batch, eps, st))) return rc;
+      fp.eps_in = eps;
+    }
     cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ffast_fused)");

@@ -977,3 +977,12 @@ extern "C" int afft_median(const double* values, int32_t mode, int64_t count, in
   AFFT_CHECK_LAUNCH("median_kernel");
   return AFFT_OK;
 }
+
+extern "C" size_t afft_singleton_workspace_size(int64_t n, int64_t count, int64_t b, int32_t c,
+                                                int32_t m) {
+  std::unique_ptr<NoisyPlan> P(new NoisyPlan());
+  std::vector<int64_t> zeros((size_t)std::max(1, c * m), 0);
+  double wts[kMaxRounds] = {0};
+  if (make_noisy_plan(P.get(), n, &b, 1, zeros.data(), c * m, c, m, wts, 1)) return 0;
+  return noisy_ws(*P, count).total;
+}

@@ -3,7 +3,7 @@
 // and is the HBM-bound kernel of the whole path (16.78 MB/signal at
 // config 5 against 22.5 KB of gathered sectors).
 //
-// Each CTA streams one fixed 256 KiB part of one signal with 16-byte loads, 8
+// Each CTA streams one fixed 64 KiB part of one signal with 16-byte loads, 8
 // independent loads in flight per thread, accumulating in float64 (the
 // reference upcasts to complex128 before np.linalg.norm).  Parts are written as
 // fixed-order partials so the final sum, done by afft_exact_thresholds in part
@@ -13,7 +13,7 @@
 namespace afft {
 
 constexpr int kSumsqThreads = 256;
-constexpr int64_t kPartBytes = 256 * 1024;
+constexpr int64_t kPartBytes = 64 * 1024;
 constexpr int kUnroll = 8;
 
 __device__ __forceinline__ double sq4(float4 v) {

@@ -205,8 +205,7 @@ def _classify(xd, layer: _DevLayer, config: DsfftConfig, ledger):
         f0 = torch.full((A,), -1, dtype=torch.int64, device=xd.device)
         val = torch.zeros(A, dtype=torch.complex128, device=xd.device)
         rn = torch.empty(A, dtype=torch.float64, device=xd.device)
-        fb, nc = _lib.host_i64([b])
-        need = int(lib.afft_noisy_workspace_size(n, A, fb, nc, plan.c, plan.m))
+        need = int(lib.afft_singleton_workspace_size(n, A, b, plan.c, plan.m))
         ws = torch.empty(need, dtype=torch.uint8, device=xd.device)
         sb, ns = _lib.host_i64(shifts)
         wb = _lib.host_f64(plan.weights.tolist())

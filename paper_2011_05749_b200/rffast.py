@@ -26,6 +26,13 @@ def _search_args(search):
     return sb, ns, wb
 
 
+def _node_workspace(n, count, b, c, m, dev):
+    need = int(_lib.load().afft_singleton_workspace_size(n, count, b, c, m))
+    if need == 0:
+        _lib.check(_lib.AFFT_EUNSUPPORTED, "noisy search plan")
+    return torch.empty(need, dtype=torch.uint8, device=dev)
+
+
 def _workspace(n, batch, factors, c, m, dev):
     fb, nc = _lib.host_i64(factors)
     need = int(_lib.load().afft_noisy_workspace_size(n, batch, fb, nc, c, m))
@@ -50,7 +57,7 @@ def singleton_search_noisy(node, plan, b: int, n: int):
     f0 = torch.empty(1, dtype=torch.int64, device=dev)
     val = torch.empty(1, dtype=torch.complex128, device=dev)
     rn = torch.empty(1, dtype=torch.float64, device=dev)
-    ws = _workspace(n, 1, [b], c, m, dev)
+    ws = _node_workspace(n, 1, b, c, m, dev)
     sb, ns, wb = _search_args(plan)
     _lib.check(
         _lib.load().afft_singleton_search_noisy(
@@ -77,7 +84,7 @@ def classify_noisy(node, plan, b: int, n: int):
     f0 = torch.empty(1, dtype=torch.int64, device=dev)
     val = torch.empty(1, dtype=torch.complex128, device=dev)
     rn = torch.empty(1, dtype=torch.float64, device=dev)
-    ws = _workspace(n, 1, [b], c, m, dev)
+    ws = _node_workspace(n, 1, b, c, m, dev)
     sb, ns, wb = _search_args(plan)
     _lib.check(
         _lib.load().afft_classify_noisy(

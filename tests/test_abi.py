@@ -41,7 +41,7 @@ def test_ctypes_table_covers_header():
 def test_version_and_host_only_queries():
     lib = _lib.load()
     assert lib.afft_version() >= 1
-    assert lib.afft_sumsq_parts(2097024, _lib.AFFT_C64) == 64
+    assert lib.afft_sumsq_parts(2097024, _lib.AFFT_C64) == 256
     fb, nc = _lib.host_i64([127, 128, 129])
     assert lib.afft_ffast_workspace_size(2097024, _lib.AFFT_C64, 4, fb, nc) > 0
     bad, nb = _lib.host_i64([127, 5])
