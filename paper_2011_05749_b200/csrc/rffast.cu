@@ -603,7 +603,7 @@ static int make_noisy_plan(NoisyPlan* P, int64_t n, const int64_t* factors, int 
     P->base[k] = (int32_t)total;
     total += factors[k];
   }
-  if (total > (1 << 20)) {
+  if (total > (1LL << 30)) {
     set_error("graph with %lld nodes is too large", (long long)total);
     return AFFT_EUNSUPPORTED;
   }
