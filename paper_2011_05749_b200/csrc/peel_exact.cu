@@ -11,7 +11,9 @@
 //   classify / subtract / truncate kernels for the per-node API.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "afft_common.cuh"
 #include "gather_dft.cuh"
@@ -430,6 +432,33 @@ static bool fused_smem(const PeelGraph& G, size_t* total, size_t* dft_off) {
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Auxiliary stream and events for the pipelined FFAST path, one set per device.
+struct AuxStreams {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t chunk[64] = {};
+};
+
+static int aux_streams(AuxStreams** out) {
+  static std::mutex mu;
+  static AuxStreams per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 64) return cuda_status(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  AuxStreams& a = per_dev[dev];
+  if (!a.aux) {
+    e = cudaStreamCreateWithFlags(&a.aux, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming);
+    for (int i = 0; i < 64 && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&a.chunk[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e, "aux stream setup");
+  }
+  *out = &a;
+  return AFFT_OK;
+}
+
 struct FfastWs {
   size_t partials, eps, nodes, state, rec_pos, rec_val, rec_count, rounds, unres, scratch, total;
 };
@@ -558,7 +587,7 @@ extern "C" size_t afft_ffast_workspace_size(int64_t n, int dtype, int64_t batch,
   PeelGraph G;
   if (setup_graph(&G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1))) return 0;
   size_t total = 0, off = 0;
-  if (fused_smem(G, &total, &off))  // fused path: partials + eps for the small-batch pre-pass
+  if (fused_smem(G, &total, &off))  // fused path: partials + eps of the norm pre-pass
     return al256((size_t)batch * afft_sumsq_parts(n, dtype) * 8) + al256((size_t)batch * 8);
   const size_t bytes = peel_layout(G.nodes, ncycles, G.hmask + 1, false).total;
   return ffast_ws(n, dtype, batch, nodes, bytes > kSmemLimit ? bytes : 0).total;
@@ -607,23 +636,71 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     fp.unresolved = unresolved;
     // Small batches cannot keep HBM busy with one streaming CTA per signal: run the
     // |x|^2 pass as a multi-CTA partial sum first and feed eps to the fused decode.
+    // Large batches (mode 2, the default there) pipeline it: the norm stream of
+    // chunk c+1 runs on the caller's stream while chunk c decodes on an auxiliary
+    // stream, so HBM never waits for the latency-bound decode.
     const int nparts = afft_sumsq_parts(n, dtype);
-    if (batch < 2 * 148 && nparts > 1) {
+    const char* env = getenv("AFFT_FFAST_MODE");  // 0 fused, 1 pre-pass, 2 pipelined
+    int mode = batch < 2 * 148 ? 1 : 2;
+    if (env && (env[0] == '0' || env[0] == '1' || env[0] == '2')) mode = env[0] - '0';
+    if (nparts < 2) mode = 0;
+    double* partials = nullptr;
+    double* epsbuf = nullptr;
+    if (mode) {
       const size_t need = al256((size_t)batch * nparts * 8) + al256((size_t)batch * 8);
       if (!workspace || workspace_bytes < need) {
         set_error("afft_ffast: workspace of %zu bytes needed, %zu given", need, workspace_bytes);
         return AFFT_ENOMEM;
       }
-      double* partials = reinterpret_cast<double*>(workspace);
-      double* eps = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) +
-                                              al256((size_t)batch * nparts * 8));
-      if ((rc = afft_sumsq(x, dtype, n, batch, ld, partials, st))) return rc;
-      if ((rc = afft_exact_thresholds(partials, nparts, n, batch, eps, st))) return rc;
-      fp.eps_in = eps;
+      partials = reinterpret_cast<double*>(workspace);
+      epsbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) +
+                                         al256((size_t)batch * nparts * 8));
     }
-    cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ffast_fused)");
+    {
+      cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ffast_fused)");
+    }
+    if (mode == 2) {
+      AuxStreams* A = nullptr;
+      if ((rc = aux_streams(&A))) return rc;
+      const int64_t esz = dtype == AFFT_C64 ? 8 : 16;
+      int64_t nchunks = std::min<int64_t>(32, std::max<int64_t>(2, batch / 256));
+      const int64_t csz = (batch + nchunks - 1) / nchunks;
+      nchunks = (batch + csz - 1) / csz;
+      cudaEventRecord(A->fork, st);
+      cudaStreamWaitEvent(A->aux, A->fork, 0);
+      for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t s0 = c * csz, cnt = std::min(csz, batch - s0);
+        const char* xc = reinterpret_cast<const char*>(x) + s0 * ld * esz;
+        if ((rc = afft_sumsq(xc, dtype, n, cnt, ld, partials + s0 * nparts, st))) return rc;
+        if ((rc = afft_exact_thresholds(partials + s0 * nparts, nparts, n, cnt, epsbuf + s0, st)))
+          return rc;
+        cudaEventRecord(A->chunk[c], st);
+        cudaStreamWaitEvent(A->aux, A->chunk[c], 0);
+        FusedParams fc = fp;
+        fc.x = xc;
+        fc.eps_in = epsbuf + s0;
+        fc.out_pos = out_pos ? out_pos + s0 * k : nullptr;
+        fc.out_val = out_val ? out_val + 2 * s0 * k : nullptr;
+        fc.out_count = out_count + s0;
+        fc.all_pos = all_pos ? all_pos + s0 * nodes : nullptr;
+        fc.all_val = all_val ? all_val + 2 * s0 * nodes : nullptr;
+        fc.all_count = all_count ? all_count + s0 : nullptr;
+        fc.rounds = rounds ? rounds + s0 : nullptr;
+        fc.unresolved = unresolved ? unresolved + s0 : nullptr;
+        ffast_fused_kernel<<<(unsigned)cnt, kFusedThreads, smem, A->aux>>>(fc);
+        AFFT_CHECK_LAUNCH("ffast_fused_kernel");
+      }
+      cudaEventRecord(A->join, A->aux);
+      cudaStreamWaitEvent(st, A->join, 0);
+      return AFFT_OK;
+    }
+    if (mode == 1) {
+      if ((rc = afft_sumsq(x, dtype, n, batch, ld, partials, st))) return rc;
+      if ((rc = afft_exact_thresholds(partials, nparts, n, batch, epsbuf, st))) return rc;
+      fp.eps_in = epsbuf;
+    }
     ffast_fused_kernel<<<(unsigned)batch, kFusedThreads, smem, st>>>(fp);
     AFFT_CHECK_LAUNCH("ffast_fused_kernel");
     return AFFT_OK;
