@@ -19,7 +19,7 @@
 
 namespace afft {
 
-constexpr unsigned long long kEmpty = ~0ull;
+constexpr unsigned kEmpty = ~0u;  // hash keys are positions f < n < 2^32 - 1
 
 struct PeelGraph {
   int64_t n;
@@ -32,8 +32,8 @@ struct PeelGraph {
 };
 
 struct PeelLayout {
-  size_t res, val, f0, found_f, found_v, found_res, hash, flag, hv, st, dirty, rec_f, rec_v,
-      total;
+  size_t res, val, f0, found_f, found_v, found_p, found_res, hash, flag, hv, st, dirty, rec_f,
+      rec_v, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -48,8 +48,9 @@ __host__ __device__ inline PeelLayout peel_layout(int nodes, int ncycles, int hc
   L.f0 = o;        o = align16(o + (size_t)nodes * 8);
   L.found_f = o;   o = align16(o + (size_t)nodes * 8);
   L.found_v = o;   o = align16(o + (size_t)nodes * 16);
+  L.found_p = o;   o = align16(o + (size_t)nodes * 2 * 16);
   L.found_res = o; o = align16(o + (size_t)nodes * ncycles * 4);
-  L.hash = o;      o = align16(o + (size_t)hcap * 8);
+  L.hash = o;      o = align16(o + (size_t)hcap * 4);
   L.flag = o;      o = align16(o + (size_t)nodes * 4);
   L.hv = o;        o = align16(o + (size_t)nodes);
   L.st = o;        o = align16(o + (size_t)nodes);
@@ -66,8 +67,9 @@ struct PeelMem {
   int64_t* f0;
   int64_t* found_f;
   cd* found_v;
+  cd* found_p;  // per found tone: v * w^{tau_1 f}, v * w^{tau_2 f} (tau_0 = 0: v itself)
   int32_t* found_res;
-  unsigned long long* hash;
+  unsigned* hash;
   int* flag;
   int8_t* hv;
   int8_t* st;
@@ -83,8 +85,9 @@ __device__ __forceinline__ PeelMem peel_carve(unsigned char* mem, const PeelLayo
   M.f0 = reinterpret_cast<int64_t*>(mem + L.f0);
   M.found_f = reinterpret_cast<int64_t*>(mem + L.found_f);
   M.found_v = reinterpret_cast<cd*>(mem + L.found_v);
+  M.found_p = reinterpret_cast<cd*>(mem + L.found_p);
   M.found_res = reinterpret_cast<int32_t*>(mem + L.found_res);
-  M.hash = reinterpret_cast<unsigned long long*>(mem + L.hash);
+  M.hash = reinterpret_cast<unsigned*>(mem + L.hash);
   M.flag = reinterpret_cast<int*>(mem + L.flag);
   M.hv = reinterpret_cast<int8_t*>(mem + L.hv);
   M.st = reinterpret_cast<int8_t*>(mem + L.st);
@@ -97,20 +100,20 @@ __device__ __forceinline__ PeelMem peel_carve(unsigned char* mem, const PeelLayo
 __device__ __forceinline__ unsigned hslot(int64_t f, int mask) {
   return (unsigned)(((unsigned long long)f * 0x9E3779B97F4A7C15ull) >> 40) & (unsigned)mask;
 }
-__device__ __forceinline__ bool hash_contains(const unsigned long long* h, int mask, int64_t f) {
+__device__ __forceinline__ bool hash_contains(const unsigned* h, int mask, int64_t f) {
   unsigned i = hslot(f, mask);
   while (true) {
-    const unsigned long long k = h[i];
-    if (k == (unsigned long long)f) return true;
+    const unsigned k = h[i];
+    if (k == (unsigned)f) return true;
     if (k == kEmpty) return false;
     i = (i + 1) & mask;
   }
 }
-__device__ __forceinline__ void hash_insert(unsigned long long* h, int mask, int64_t f) {
+__device__ __forceinline__ void hash_insert(unsigned* h, int mask, int64_t f) {
   unsigned i = hslot(f, mask);
   while (true) {
-    const unsigned long long old = atomicCAS(h + i, kEmpty, (unsigned long long)f);
-    if (old == kEmpty || old == (unsigned long long)f) return;
+    const unsigned old = atomicCAS(h + i, kEmpty, (unsigned)f);
+    if (old == kEmpty || old == (unsigned)f) return;
     i = (i + 1) & mask;
   }
 }
@@ -245,6 +248,13 @@ __device__ inline int peel_rounds(const PeelGraph& G, const PeelMem& M, double e
       }
     }
     __syncthreads();
+    // ---- per found tone (warp-parallel, convergent): v * w^{(tau_r f) mod n} for r = 1, 2
+    for (int i = tid; i < nf; i += nt) {
+      const int64_t f = M.found_f[i];
+      const cd v = M.found_v[i];
+      M.found_p[2 * i] = cmul(v, unit_root(mulmod(G.tau[1], f, n), n));
+      M.found_p[2 * i + 1] = cmul(v, unit_root(mulmod(G.tau[2], f, n), n));
+    }
     // ---- residues of the found tones; mark the nodes they hit (hv reused as "touched")
     for (int e = tid; e < nf * F; e += nt) {
       const int i = e / F, c = e - i * F;
@@ -262,11 +272,10 @@ __device__ inline int peel_rounds(const PeelGraph& G, const PeelMem& M, double e
       cd a0 = M.res[3 * g], a1 = M.res[3 * g + 1], a2 = M.res[3 * g + 2];
       for (int i = 0; i < nf; ++i) {
         if (M.found_res[i * F + c] != idx) continue;
-        const int64_t f = M.found_f[i];
-        const cd v = M.found_v[i];
-        a0 = csub(a0, cmul(v, unit_root(mulmod(G.tau[0], f, n), n)));
-        a1 = csub(a1, cmul(v, unit_root(mulmod(G.tau[1], f, n), n)));
-        a2 = csub(a2, cmul(v, unit_root(mulmod(G.tau[2], f, n), n)));
+        // tau_0 = 0: v * (1, -0) == v exactly, so the first term is v itself
+        a0 = csub(a0, M.found_v[i]);
+        a1 = csub(a1, M.found_p[2 * i]);
+        a2 = csub(a2, M.found_p[2 * i + 1]);
       }
       M.res[3 * g] = a0;
       M.res[3 * g + 1] = a1;

@@ -333,7 +333,7 @@ static int setup_graph(PeelGraph* G, int64_t n, const int64_t* factors, int ncyc
     set_error("number of cycles %d outside 1..%d", ncycles, AFFT_MAX_CYCLES);
     return AFFT_EUNSUPPORTED;
   }
-  if (n < 1 || n > 3000000000LL) {
+  if (n < 1 || n > 3000000000LL) {  // positions fit the 32-bit hash keys
     set_error("signal size %lld outside the supported 1..3e9", (long long)n);
     return AFFT_EUNSUPPORTED;
   }

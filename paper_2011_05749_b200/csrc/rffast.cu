@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(512) noisy_harvest_kernel(
   const int tid = threadIdx.x, nt = blockDim.x;
   unsigned char* mem = gscratch ? reinterpret_cast<unsigned char*>(gscratch) + s * scratch_bytes
                                 : smem_raw;
-  unsigned long long* hash = reinterpret_cast<unsigned long long*>(mem);
+  unsigned* hash = reinterpret_cast<unsigned*>(mem);
   int* flag = reinterpret_cast<int*>(hash + P.hmask + 1);
   int32_t* found_g = flag + N;
   int32_t* found_res = found_g + N;          // [nf][ncycles]
@@ -840,7 +840,7 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
   }
   int hcap = P->hmask + 1;
   const size_t hbytes =
-      ((size_t)hcap * 8 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64 + 15) & ~size_t(15);
+      ((size_t)hcap * 4 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64 + 15) & ~size_t(15);
   size_t hsmem = hbytes;
   char* hscratch = nullptr;
   if (hbytes > 200 * 1024) {  // large graphs: harvest state in global memory
