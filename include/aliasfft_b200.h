@@ -139,6 +139,10 @@ int afft_truncate(const int64_t* pos, const double* val, const int32_t* count, i
                   int64_t batch, int32_t k, int64_t* out_pos, double* out_val,
                   int32_t* out_count, void* stream);
 
+/* Resident ffast_fused_kernel CTAs per SM and its dynamic shared memory for a plan. */
+int afft_ffast_occupancy(int64_t n, const int64_t* factors /* host */, int32_t ncycles,
+                         int32_t* blocks_per_sm /* host */, int32_t* smem_bytes /* host */);
+
 /*
  * ffast (peeling.py:321-332) over a batch with an explicit cycle plan and the
  * exact shift set (0,1,2): fused norm → thresholds → build_graph → peel → truncate.

@@ -183,13 +183,11 @@ __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64
   return a0 + a1;
 }
 
-__global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
-    const __grid_constant__ FusedParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int warp_tmp[32];
-  __shared__ int carry, red;
-  __shared__ double wsum[kFusedThreads / 32];
-  const int64_t s = blockIdx.x;
+__device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s,
+                                                 unsigned char* smem_raw, int* warp_tmp,
+                                                 int* carry_p, int* red_p, double* wsum) {
+  int& carry = *carry_p;
+  int& red = *red_p;
   const int tid = threadIdx.x, nt = blockDim.x;
   const PeelGraph& G = p.G;
   const int N = G.nodes;
@@ -261,6 +259,21 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
     if (p.rounds) p.rounds[s] = rounds;
     if (p.unresolved) p.unresolved[s] = unres;
     if (p.eps_out) p.eps_out[s] = eps;
+  }
+}
+
+// One signal per CTA iteration; a grid smaller than the batch makes the CTAs
+// persistent (grid-stride over signals), which is how the pipelined path caps
+// the decode's SM footprint next to the concurrent norm stream.
+__global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
+    const __grid_constant__ FusedParams p, int64_t batch) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tmp[32];
+  __shared__ int carry, red;
+  __shared__ double wsum[kFusedThreads / 32];
+  for (int64_t s = blockIdx.x; s < batch; s += gridDim.x) {
+    ffast_one_signal(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
+    __syncthreads();
   }
 }
 
@@ -431,6 +444,17 @@ static bool fused_smem(const PeelGraph& G, size_t* total, size_t* dft_off) {
 }
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached = v > 0 ? v : 148;
+  }
+  return cached;
+}
 
 // Auxiliary stream and events for the pipelined FFAST path, one set per device.
 struct AuxStreams {
@@ -689,7 +713,10 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
         fc.all_count = all_count ? all_count + s0 : nullptr;
         fc.rounds = rounds ? rounds + s0 : nullptr;
         fc.unresolved = unresolved ? unresolved + s0 : nullptr;
-        ffast_fused_kernel<<<(unsigned)cnt, kFusedThreads, smem, A->aux>>>(fc);
+        const char* dg = getenv("AFFT_DECODE_CTAS_PER_SM");
+        const int per_sm = dg ? std::max(1, atoi(dg)) : 1;
+        const int64_t grid = std::min<int64_t>(cnt, (int64_t)num_sms() * per_sm);
+        ffast_fused_kernel<<<(unsigned)grid, kFusedThreads, smem, A->aux>>>(fc, cnt);
         AFFT_CHECK_LAUNCH("ffast_fused_kernel");
       }
       cudaEventRecord(A->join, A->aux);
@@ -701,7 +728,7 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
       if ((rc = afft_exact_thresholds(partials, nparts, n, batch, epsbuf, st))) return rc;
       fp.eps_in = epsbuf;
     }
-    ffast_fused_kernel<<<(unsigned)batch, kFusedThreads, smem, st>>>(fp);
+    ffast_fused_kernel<<<(unsigned)batch, kFusedThreads, smem, st>>>(fp, batch);
     AFFT_CHECK_LAUNCH("ffast_fused_kernel");
     return AFFT_OK;
   }
@@ -747,4 +774,29 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
   if ((rc = launch_peel(p, batch, ws + w.scratch, st))) return rc;
   return launch_truncate(rpos, rval, rcount, (int)nodes, batch, k, out_pos, out_val, out_count,
                          st);
+}
+
+extern "C" int afft_ffast_occupancy(int64_t n, const int64_t* factors, int32_t ncycles,
+                                    int32_t* blocks_per_sm, int32_t* smem_bytes) {
+  PeelGraph G;
+  int64_t nodes = 0;
+  for (int c = 0; c < ncycles && factors; ++c) nodes += factors[c];
+  int rc = setup_graph(&G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1));
+  if (rc) return rc;
+  size_t smem = 0, off = 0;
+  if (!fused_smem(G, &smem, &off)) {
+    *blocks_per_sm = 0;
+    *smem_bytes = 0;
+    return AFFT_OK;
+  }
+  cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int blocks = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, ffast_fused_kernel, kFusedThreads,
+                                                      smem);
+  if (e != cudaSuccess) return cuda_status(e, "occupancy query");
+  *blocks_per_sm = blocks;
+  *smem_bytes = (int32_t)smem;
+  return AFFT_OK;
 }

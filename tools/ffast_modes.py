@@ -44,7 +44,23 @@ def main():
     for mode in ("0", "1", "2"):
         os.environ["AFFT_FFAST_MODE"] = mode
         out[mode] = t(lambda: ffast_batch(x, bench.K, bench.FACTORS, workspace=ws, out=res))
-    gb = S * bench.SIGNAL_BYTES / 1e9
+    import ctypes
+    fb, nc = _lib.host_i64(bench.FACTORS)
+    blk, sm = ctypes.c_int32(0), ctypes.c_int32(0)
+    lib.afft_ffast_occupancy(bench.N_SIG, fb, nc, ctypes.byref(blk), ctypes.byref(sm))
+    print(f"fused kernel: {blk.value} CTAs/SM, {sm.value} B dynamic smem")
+    for rep in range(2):
+        for mode in ("0", "1", "2"):
+            os.environ["AFFT_FFAST_MODE"] = mode
+            out[mode] = t(lambda: ffast_batch(x, bench.K, bench.FACTORS, workspace=ws, out=res))
+        print(rep, {k: round(v, 3) for k, v in out.items()})
+    os.environ["AFFT_FFAST_MODE"] = "2"
+    for per_sm in ("1", "2", "3"):
+        os.environ["AFFT_DECODE_CTAS_PER_SM"] = per_sm
+        print("pipelined, decode CTAs/SM", per_sm,
+              round(t(lambda: ffast_batch(x, bench.K, bench.FACTORS, workspace=ws, out=res)), 3))
+    del os.environ["AFFT_DECODE_CTAS_PER_SM"]
+    gb = S * bench.SIGNAL_BYTES / 1e6
     print(f"signals {S}: norm alone {ms_norm:.3f} ms ({gb / ms_norm:.0f} GB/s); "
           f"fused(mode0) {out['0']:.3f}; prepass+decode(mode1) {out['1']:.3f} "
           f"(decode ~{out['1'] - ms_norm:.3f}); pipelined(mode2) {out['2']:.3f} ms")
