@@ -32,19 +32,20 @@ struct PeelGraph {
 };
 
 struct PeelLayout {
-  size_t res, val, f0, found_f, found_v, found_p, found_res, hash, flag, hv, st, dirty, rec_f,
-      rec_v, total;
+  size_t res, val, f0, found_f, found_v, found_p, found_res, hash, flag, hv, st, dirty, cyc,
+      rec_f, rec_v, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// with_rec: keep the cumulative recovered list in the same memory (fused kernel).
+// with_val: keep each node's last decoded value (the graph API writes it back);
+// with_rec: keep the cumulative recovered list in the same memory.
 __host__ __device__ inline PeelLayout peel_layout(int nodes, int ncycles, int hcap,
-                                                  bool with_rec) {
+                                                  bool with_rec, bool with_val = true) {
   PeelLayout L;
   size_t o = 0;
   L.res = o;       o = align16(o + (size_t)nodes * 3 * 16);
-  L.val = o;       o = align16(o + (size_t)nodes * 16);
+  L.val = o;       if (with_val) o = align16(o + (size_t)nodes * 16);
   L.f0 = o;        o = align16(o + (size_t)nodes * 8);
   L.found_f = o;   o = align16(o + (size_t)nodes * 8);
   L.found_v = o;   o = align16(o + (size_t)nodes * 16);
@@ -55,6 +56,7 @@ __host__ __device__ inline PeelLayout peel_layout(int nodes, int ncycles, int hc
   L.hv = o;        o = align16(o + (size_t)nodes);
   L.st = o;        o = align16(o + (size_t)nodes);
   L.dirty = o;     o = align16(o + (size_t)nodes);
+  L.cyc = o;       o = align16(o + (size_t)nodes);
   L.rec_f = o;     if (with_rec) o = align16(o + (size_t)nodes * 8);
   L.rec_v = o;     if (with_rec) o = align16(o + (size_t)nodes * 16);
   L.total = o;
@@ -68,12 +70,14 @@ struct PeelMem {
   int64_t* found_f;
   cd* found_v;
   cd* found_p;  // per found tone: v * w^{tau_1 f}, v * w^{tau_2 f} (tau_0 = 0: v itself)
-  int32_t* found_res;
+  int32_t* found_res;  // per round: found-tone indices grouped by node (counting sort)
   unsigned* hash;
   int* flag;
   int8_t* hv;
   int8_t* st;
   int8_t* dirty;
+  int8_t* cyc;     // node -> cycle
+  cd* valp;        // node values, or null when not kept (fused kernel: value = r0)
   int64_t* rec_f;  // cumulative recovered list (insertion order)
   cd* rec_v;
 };
@@ -92,6 +96,8 @@ __device__ __forceinline__ PeelMem peel_carve(unsigned char* mem, const PeelLayo
   M.hv = reinterpret_cast<int8_t*>(mem + L.hv);
   M.st = reinterpret_cast<int8_t*>(mem + L.st);
   M.dirty = reinterpret_cast<int8_t*>(mem + L.dirty);
+  M.cyc = reinterpret_cast<int8_t*>(mem + L.cyc);
+  M.valp = L.val != L.f0 ? M.val : nullptr;
   M.rec_f = reinterpret_cast<int64_t*>(mem + L.rec_f);
   M.rec_v = reinterpret_cast<cd*>(mem + L.rec_v);
   return M;
@@ -176,7 +182,7 @@ __device__ __forceinline__ int8_t classify_exact_dev(cd r0, cd r1, cd r2, int64_
       const int64_t f = pymod((int64_t)rint(__dmul_rn(ang, cfac)), n);
       if (f % b == index) {
         *f0 = f;
-        *val = r0;
+        if (val) *val = r0;
         return AFFT_SINGLE_TON;
       }
     }
@@ -190,10 +196,15 @@ __device__ __forceinline__ int cycle_of(const PeelGraph& G, int g) {
   return c;
 }
 
-// Round loop.  Expects M.res/st/f0/val initialised, M.dirty = 1, the hash holding
-// the rc prior recovered positions, and rec_f/rec_v (shared or global) holding
-// them.  Appends newly found tones to rec_f/rec_v; returns the round count and
-// updates rc.
+// Node -> cycle table (call once after carving, before the rounds).
+__device__ inline void peel_fill_cycles(const PeelGraph& G, const PeelMem& M) {
+  for (int g = threadIdx.x; g < G.nodes; g += blockDim.x) M.cyc[g] = (int8_t)cycle_of(G, g);
+}
+
+// Round loop.  Expects M.res/st/f0/(val) initialised, M.dirty = 1, M.cyc filled, the
+// hash holding the rc prior recovered positions, and rec_f/rec_v (shared or global)
+// holding them.  Appends newly found tones to rec_f/rec_v; returns the round count
+// and updates rc.
 __device__ inline int peel_rounds(const PeelGraph& G, const PeelMem& M, double eps0, double epsr,
                                   int max_rounds, int64_t* rec_f, cd* rec_v, int& rc,
                                   int* warp_tmp, int* carry) {
@@ -208,10 +219,10 @@ __device__ inline int peel_rounds(const PeelGraph& G, const PeelMem& M, double e
     for (int g = tid; g < N; g += nt) {
       const int8_t s0 = M.st[g];
       if (s0 == AFFT_RESOLVED || s0 == AFFT_ZERO_TON || !M.dirty[g]) continue;
-      const int c = cycle_of(G, g);
+      const int c = M.cyc[g];
       M.st[g] = classify_exact_dev(M.res[3 * g], M.res[3 * g + 1], M.res[3 * g + 2],
                                    g - G.base[c], G.b[c], n, eps0, epsr, cfac, &M.f0[g],
-                                   &M.val[g]);
+                                   M.valp ? &M.valp[g] : nullptr);
       M.dirty[g] = 0;
     }
     __syncthreads();
@@ -222,7 +233,7 @@ __device__ inline int peel_rounds(const PeelGraph& G, const PeelMem& M, double e
         const int64_t f = M.f0[g];
         if (!hash_contains(M.hash, G.hmask, f)) {
           take = 1;
-          const int c = cycle_of(G, g);
+          const int c = M.cyc[g];
           for (int c2 = 0; c2 < c; ++c2) {
             const int g2 = G.base[c2] + (int)(f % G.b[c2]);
             if (M.st[g2] == AFFT_SINGLE_TON && M.f0[g2] == f) {
@@ -238,42 +249,57 @@ __device__ inline int peel_rounds(const PeelGraph& G, const PeelMem& M, double e
     __syncthreads();
     const int nf = block_exclusive_scan(M.flag, N, warp_tmp, carry);
     if (nf == 0) break;
+    // ---- found list in insertion order.  A SINGLE_TON's value is r0 of its current
+    // residual: a node is reclassified whenever its residual changes, so r0 still
+    // equals the value classify_exact stored.
     for (int g = tid; g < N; g += nt) {
       if (M.hv[g]) {
         const int pos = M.flag[g];
         M.found_f[pos] = M.f0[g];
-        M.found_v[pos] = M.val[g];
+        M.found_v[pos] = M.res[3 * g];
         M.st[g] = AFFT_RESOLVED;
         M.hv[g] = 0;
       }
+      M.flag[g] = 0;
     }
     __syncthreads();
-    // ---- per found tone (warp-parallel, convergent): v * w^{(tau_r f) mod n} for r = 1, 2
+    // ---- per found tone (convergent): v * w^{(tau_r f) mod n}, r = 1, 2 (tau_0 = 0);
+    //      and the per-node hit counts of the (tone, cycle) pairs
     for (int i = tid; i < nf; i += nt) {
       const int64_t f = M.found_f[i];
       const cd v = M.found_v[i];
       M.found_p[2 * i] = cmul(v, unit_root(mulmod(G.tau[1], f, n), n));
       M.found_p[2 * i + 1] = cmul(v, unit_root(mulmod(G.tau[2], f, n), n));
     }
-    // ---- residues of the found tones; mark the nodes they hit (hv reused as "touched")
     for (int e = tid; e < nf * F; e += nt) {
       const int i = e / F, c = e - i * F;
-      const int32_t r = (int32_t)(M.found_f[i] % G.b[c]);
-      M.found_res[e] = r;
-      M.hv[G.base[c] + r] = 1;
+      atomicAdd(&M.flag[G.base[c] + (int)(M.found_f[i] % G.b[c])], 1);
     }
     __syncthreads();
-    // ---- subtract in found order from every hit node (any state)
+    block_exclusive_scan(M.flag, N, warp_tmp, carry);  // segment starts
+    for (int e = tid; e < nf * F; e += nt) {             // scatter (unordered within a node)
+      const int i = e / F, c = e - i * F;
+      const int slot = atomicAdd(&M.flag[G.base[c] + (int)(M.found_f[i] % G.b[c])], 1);
+      M.found_res[slot] = i;
+    }
+    __syncthreads();
+    // ---- subtract: each hit node applies its tones in found order (peeling.py:305-307)
     for (int g = tid; g < N; g += nt) {
-      if (!M.hv[g]) continue;
-      M.hv[g] = 0;
-      const int c = cycle_of(G, g);
-      const int idx = g - G.base[c];
+      const int lo = g ? M.flag[g - 1] : 0, hi = M.flag[g];
+      if (lo == hi) continue;
+      for (int a = lo + 1; a < hi; ++a) {  // insertion sort of the (short) segment
+        const int v = M.found_res[a];
+        int b = a - 1;
+        while (b >= lo && M.found_res[b] > v) {
+          M.found_res[b + 1] = M.found_res[b];
+          --b;
+        }
+        M.found_res[b + 1] = v;
+      }
       cd a0 = M.res[3 * g], a1 = M.res[3 * g + 1], a2 = M.res[3 * g + 2];
-      for (int i = 0; i < nf; ++i) {
-        if (M.found_res[i * F + c] != idx) continue;
-        // tau_0 = 0: v * (1, -0) == v exactly, so the first term is v itself
-        a0 = csub(a0, M.found_v[i]);
+      for (int a = lo; a < hi; ++a) {
+        const int i = M.found_res[a];
+        a0 = csub(a0, M.found_v[i]);  // v * (1, -0) == v exactly
         a1 = csub(a1, M.found_p[2 * i]);
         a2 = csub(a2, M.found_p[2 * i + 1]);
       }
@@ -304,6 +330,43 @@ __device__ inline int count_multitons(const PeelGraph& G, const PeelMem& M, int*
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(red, cnt);
   __syncthreads();
   return *red;
+}
+
+// truncate_spectrum order (oneshot.py:260-263) by an in-smem bitonic sort of
+// (|v| descending, f ascending) keys; pads to a power of two with sentinels.
+// key/pos/idx need pow2 entries.  All threads must call it.
+__device__ inline void bitonic_trunc_sort(double* key, int64_t* pos, int32_t* idx, int m,
+                                          int pow2) {
+  for (int i = threadIdx.x + m; i < pow2; i += blockDim.x) {
+    key[i] = -1.0;
+    pos[i] = INT64_MAX;
+    idx[i] = -1;
+  }
+  __syncthreads();
+  for (int k = 2; k <= pow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          // "a before b" iff a.key > b.key, or equal keys and a.pos < b.pos
+          const bool lbefore = key[l] > key[i] || (key[l] == key[i] && pos[l] < pos[i]);
+          const bool up = (i & k) == 0;
+          if (up == lbefore) {
+            const double tk = key[i];
+            key[i] = key[l];
+            key[l] = tk;
+            const int64_t tp = pos[i];
+            pos[i] = pos[l];
+            pos[l] = tp;
+            const int32_t ti = idx[i];
+            idx[i] = idx[l];
+            idx[l] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
 }
 
 // truncate_spectrum (oneshot.py:260-263): rank of entry i by (-|v|, f).

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) peel_exact_kernel(const __grid_constant__
     M.val[g] = p.node_val ? reinterpret_cast<const cd*>(p.node_val)[s * N + g] : cd{0.0, 0.0};
   }
   for (int h = tid; h <= G.hmask; h += nt) M.hash[h] = kEmpty;
+  peel_fill_cycles(G, M);
   __syncthreads();
   int rc = p.rec_count[s];
   int64_t* rpos = p.rec_pos + s * (int64_t)p.rec_cap;
@@ -118,6 +119,7 @@ struct FusedParams {
   int32_t* unresolved;
   double* eps_out;       // may be null
   const double* eps_in;  // may be null: precomputed thresholds (small batches)
+  int rec_in_smem;       // 1: recovered list in shared memory (no all_pos output)
 };
 
 constexpr int kFusedThreads = 256;
@@ -192,8 +194,10 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
   const PeelGraph& G = p.G;
   const int N = G.nodes;
   const int64_t n = G.n;
-  const PeelLayout L = peel_layout(N, G.ncycles, G.hmask + 1, true);
+  const PeelLayout L = peel_layout(N, G.ncycles, G.hmask + 1, p.rec_in_smem != 0, false);
   const PeelMem M = peel_carve(smem_raw, L);
+  int64_t* rec_f = p.rec_in_smem ? M.rec_f : p.all_pos + s * N;
+  cd* rec_v = p.rec_in_smem ? M.rec_v : reinterpret_cast<cd*>(p.all_val) + s * N;
   const char* row = reinterpret_cast<const char*>(p.x) + s * p.ld * (p.dtype == AFFT_C64 ? 8 : 16);
 
   // 1. exact_thresholds: eps = 1e-6 * ||x|| / sqrt(n), fixed-order block reduction
@@ -228,29 +232,35 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
     M.f0[g] = -1;
   }
   for (int h = tid; h <= G.hmask; h += nt) M.hash[h] = kEmpty;
+  peel_fill_cycles(G, M);
   __syncthreads();
   // 4. peel
   int rc = 0;
-  const int rounds =
-      peel_rounds(G, M, eps, eps, p.max_rounds, M.rec_f, M.rec_v, rc, warp_tmp, &carry);
+  const int rounds = peel_rounds(G, M, eps, eps, p.max_rounds, rec_f, rec_v, rc, warp_tmp, &carry);
   const int unres = count_multitons(G, M, &red);
-  // 5. truncate to k by (-|v|, f) and write the fixed-size result slots
-  double* mag = reinterpret_cast<double*>(M.found_v);
-  for (int i = tid; i < rc; i += nt) mag[i] = cabs_(M.rec_v[i]);
-  __syncthreads();
-  cd* ov = reinterpret_cast<cd*>(p.out_val) + s * p.k;
+  // 5. truncate to k by (-|v|, f): bitonic sort in the (now free) found-list memory
+  int pow2 = 1;
+  while (pow2 < rc) pow2 <<= 1;
+  double* key = reinterpret_cast<double*>(M.found_f);
+  int64_t* kpos = reinterpret_cast<int64_t*>(key + pow2);
+  int32_t* kidx = reinterpret_cast<int32_t*>(kpos + pow2);
   for (int i = tid; i < rc; i += nt) {
-    const int r = trunc_rank(mag, M.rec_f, rc, i);
-    if (r < p.k) {
-      p.out_pos[s * p.k + r] = M.rec_f[i];
-      ov[r] = M.rec_v[i];
-    }
+    key[i] = cabs_(rec_v[i]);
+    kpos[i] = rec_f[i];
+    kidx[i] = i;
   }
-  if (p.all_pos) {
+  bitonic_trunc_sort(key, kpos, kidx, rc, pow2);
+  cd* ov = reinterpret_cast<cd*>(p.out_val) + s * p.k;
+  const int kept = rc < p.k ? rc : p.k;
+  for (int r = tid; r < kept; r += nt) {
+    p.out_pos[s * p.k + r] = kpos[r];
+    ov[r] = rec_v[kidx[r]];
+  }
+  if (p.all_pos && p.rec_in_smem) {
     cd* av = reinterpret_cast<cd*>(p.all_val) + s * N;
     for (int i = tid; i < rc; i += nt) {
-      p.all_pos[s * N + i] = M.rec_f[i];
-      av[i] = M.rec_v[i];
+      p.all_pos[s * N + i] = rec_f[i];
+      av[i] = rec_v[i];
     }
   }
   if (tid == 0) {
@@ -317,7 +327,30 @@ __global__ void truncate_kernel(const int64_t* __restrict__ pos, const double* _
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t s = blockIdx.x;
   const int m = count[s];
-  double* mag = gscratch ? gscratch + s * (int64_t)cap * 2 : reinterpret_cast<double*>(smem_raw);
+  if (!gscratch) {  // bitonic sort in shared memory
+    int pow2 = 1;
+    while (pow2 < m) pow2 <<= 1;
+    double* key = reinterpret_cast<double*>(smem_raw);
+    int64_t* kpos = reinterpret_cast<int64_t*>(key + pow2);
+    int32_t* kidx = reinterpret_cast<int32_t*>(kpos + pow2);
+    const int64_t* ps = pos + s * cap;
+    const cd* vs = reinterpret_cast<const cd*>(val) + s * cap;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      key[i] = cabs_(vs[i]);
+      kpos[i] = ps[i];
+      kidx[i] = i;
+    }
+    bitonic_trunc_sort(key, kpos, kidx, m, pow2);
+    cd* ov = reinterpret_cast<cd*>(out_val) + s * k;
+    const int kept = m < k ? m : k;
+    for (int r = threadIdx.x; r < kept; r += blockDim.x) {
+      out_pos[s * k + r] = kpos[r];
+      ov[r] = vs[kidx[r]];
+    }
+    if (threadIdx.x == 0) out_count[s] = kept;
+    return;
+  }
+  double* mag = gscratch + s * (int64_t)cap * 2;
   int64_t* fs = reinterpret_cast<int64_t*>(mag + cap);
   const int64_t* ps = pos + s * cap;
   const cd* vs = reinterpret_cast<const cd*>(val) + s * cap;
@@ -406,7 +439,9 @@ static int launch_peel(PeelParams& p, int64_t batch, void* scratch, cudaStream_t
 static int launch_truncate(const int64_t* pos, const double* val, const int32_t* count, int cap,
                            int64_t batch, int k, int64_t* out_pos, double* out_val,
                            int32_t* out_count, cudaStream_t stream) {
-  size_t smem = (size_t)std::max(cap, 1) * 16;
+  int pow2 = 1;
+  while (pow2 < std::max(cap, 1)) pow2 <<= 1;
+  size_t smem = (size_t)pow2 * 20;
   double* scratch = nullptr;
   if (smem > kSmemLimit) {  // large graphs: rank from global memory
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
@@ -427,8 +462,8 @@ static int launch_truncate(const int64_t* pos, const double* val, const int32_t*
 
 // Fused-kernel shared memory: peel layout (with recovered list) + DFT scratch
 // (tw + 2 x 3 shifts x b) aliased onto found/hash when it fits there.
-static bool fused_smem(const PeelGraph& G, size_t* total, size_t* dft_off) {
-  const PeelLayout L = peel_layout(G.nodes, G.ncycles, G.hmask + 1, true);
+static bool fused_smem(const PeelGraph& G, bool rec_in_smem, size_t* total, size_t* dft_off) {
+  const PeelLayout L = peel_layout(G.nodes, G.ncycles, G.hmask + 1, rec_in_smem, false);
   int64_t bmax = 0;
   for (int c = 0; c < G.ncycles; ++c) bmax = std::max(bmax, G.b[c]);
   if (bmax > AFFT_MAX_SMEM_DFT) return false;
@@ -611,7 +646,7 @@ extern "C" size_t afft_ffast_workspace_size(int64_t n, int dtype, int64_t batch,
   PeelGraph G;
   if (setup_graph(&G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1))) return 0;
   size_t total = 0, off = 0;
-  if (fused_smem(G, &total, &off))  // fused path: partials + eps of the norm pre-pass
+  if (fused_smem(G, true, &total, &off))  // fused path: partials + eps of the norm pre-pass
     return al256((size_t)batch * afft_sumsq_parts(n, dtype) * 8) + al256((size_t)batch * 8);
   const size_t bytes = peel_layout(G.nodes, ncycles, G.hmask + 1, false).total;
   return ffast_ws(n, dtype, batch, nodes, bytes > kSmemLimit ? bytes : 0).total;
@@ -638,7 +673,8 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
   int rc = setup_graph(&fp.G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1));
   if (rc) return rc;
   size_t smem = 0;
-  if (fused_smem(fp.G, &smem, &fp.dft_off)) {
+  fp.rec_in_smem = all_pos == nullptr || all_val == nullptr;
+  if (fused_smem(fp.G, fp.rec_in_smem != 0, &smem, &fp.dft_off)) {
     for (int c = 0; c < ncycles; ++c) {
       if (!make_dft_plan(fp.G.b[c], &fp.plan[c])) {
         set_error("cannot plan a DFT of size %lld", (long long)fp.G.b[c]);
@@ -784,7 +820,7 @@ extern "C" int afft_ffast_occupancy(int64_t n, const int64_t* factors, int32_t n
   int rc = setup_graph(&G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1));
   if (rc) return rc;
   size_t smem = 0, off = 0;
-  if (!fused_smem(G, &smem, &off)) {
+  if (!fused_smem(G, false, &smem, &off)) {
     *blocks_per_sm = 0;
     *smem_bytes = 0;
     return AFFT_OK;
