@@ -8,6 +8,8 @@
 // reference upcasts to complex128 before np.linalg.norm).  Parts are written as
 // fixed-order partials so the final sum, done by afft_exact_thresholds in part
 // order, is deterministic run to run.
+#include <cstdlib>
+
 #include "afft_common.cuh"
 
 namespace afft {
@@ -15,6 +17,23 @@ namespace afft {
 constexpr int kSumsqThreads = 256;
 constexpr int64_t kPartBytes = 64 * 1024;
 constexpr int kUnroll = 8;
+
+// 16-byte streaming load that does not allocate in L1 (the decode CTAs running
+// next to this kernel keep most of the SM's unified L1/shared storage).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
 
 __device__ __forceinline__ double sq4(float4 v) {
   double a = (double)v.x, b = (double)v.y, c = (double)v.z, d = (double)v.w;
@@ -24,7 +43,8 @@ __device__ __forceinline__ double sq2(double2 v) { return __fma_rn(v.x, v.x, v.y
 
 __global__ void __launch_bounds__(kSumsqThreads) sumsq_kernel(const void* __restrict__ x, int dtype,
                                                               int64_t n, int64_t ld, int nparts,
-                                                              double* __restrict__ partials) {
+                                                              double* __restrict__ partials,
+                                                              int use_na) {
   const int64_t s = blockIdx.y;
   const int part = blockIdx.x;
   const int esz = dtype == AFFT_C64 ? 8 : 16;
@@ -51,7 +71,7 @@ __global__ void __launch_bounds__(kSumsqThreads) sumsq_kernel(const void* __rest
     for (; i + (kUnroll - 1) * kSumsqThreads < nvec; i += kUnroll * kSumsqThreads) {
       float4 v[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = __ldcs(xv + i + u * kSumsqThreads);
+      for (int u = 0; u < kUnroll; ++u) v[u] = use_na ? ld_stream(xv + i + u * kSumsqThreads) : __ldcs(xv + i + u * kSumsqThreads);
 #pragma unroll
       for (int u = 0; u < kUnroll; u += 2) {
         acc0 += sq4(v[u]);
@@ -71,7 +91,7 @@ __global__ void __launch_bounds__(kSumsqThreads) sumsq_kernel(const void* __rest
     for (; i + (kUnroll - 1) * kSumsqThreads < nvec; i += kUnroll * kSumsqThreads) {
       double2 v[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = __ldcs(xv + i + u * kSumsqThreads);
+      for (int u = 0; u < kUnroll; ++u) v[u] = use_na ? ld_stream(xv + i + u * kSumsqThreads) : __ldcs(xv + i + u * kSumsqThreads);
 #pragma unroll
       for (int u = 0; u < kUnroll; u += 2) {
         acc0 += sq2(v[u]);
@@ -127,9 +147,13 @@ extern "C" int afft_sumsq(const void* x, int dtype, int64_t n, int64_t batch, in
   for (int64_t s0 = 0; s0 < batch; s0 += 65535) {  // grid.y limit
     const int64_t cnt = batch - s0 < 65535 ? batch - s0 : 65535;
     dim3 grid((unsigned)nparts, (unsigned)cnt);
+    static const int use_na = [] {
+      const char* e = getenv("AFFT_STREAM_NO_ALLOCATE");
+      return e ? atoi(e) : 1;
+    }();
     sumsq_kernel<<<grid, kSumsqThreads, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const char*>(x) + s0 * ld * esz, dtype, n, ld, nparts,
-        partials + s0 * nparts);
+        partials + s0 * nparts, use_na);
     AFFT_CHECK_LAUNCH("sumsq_kernel");
   }
   return AFFT_OK;

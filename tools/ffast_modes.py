@@ -60,6 +60,7 @@ def main():
         print("pipelined, decode CTAs/SM", per_sm,
               round(t(lambda: ffast_batch(x, bench.K, bench.FACTORS, workspace=ws, out=res)), 3))
     del os.environ["AFFT_DECODE_CTAS_PER_SM"]
+    print("(stream loads: AFFT_STREAM_NO_ALLOCATE =", os.environ.get("AFFT_STREAM_NO_ALLOCATE", "1"), ")")
     gb = S * bench.SIGNAL_BYTES / 1e6
     print(f"signals {S}: norm alone {ms_norm:.3f} ms ({gb / ms_norm:.0f} GB/s); "
           f"fused(mode0) {out['0']:.3f}; prepass+decode(mode1) {out['1']:.3f} "
