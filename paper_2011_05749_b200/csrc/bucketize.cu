@@ -97,7 +97,7 @@ struct FourStepParams {
   int64_t tau[AFFT_MAX_SHIFTS];
 };
 
-__global__ void __launch_bounds__(256) fourstep_a_kernel(const __grid_constant__ FourStepParams p) {
+__global__ void __launch_bounds__(1024) fourstep_a_kernel(const __grid_constant__ FourStepParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t s = blockIdx.z;
   const int t = blockIdx.y;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) fourstep_a_kernel(const __grid_constant__
   }
 }
 
-__global__ void __launch_bounds__(256) fourstep_b_kernel(const __grid_constant__ FourStepParams p) {
+__global__ void __launch_bounds__(1024) fourstep_b_kernel(const __grid_constant__ FourStepParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t s = blockIdx.z;
   const int t = blockIdx.y;
@@ -231,10 +231,13 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     qs.z = q.z + 2 * s0 * nshift * b;
     qs.out = out + 2 * s0 * oss;
     qs.shift_table = shift_table ? shift_table + s0 * nshift : nullptr;
+    // large sub-DFTs run one CTA per SM: give it enough warps to hide smem latency
+    const int ta = q.b2 >= 2048 ? 1024 : (q.b2 >= 512 ? 512 : 256);
+    const int tb = q.b1 >= 2048 ? 1024 : (q.b1 >= 512 ? 512 : 256);
     dim3 ga((unsigned)((q.b1 + q.cj - 1) / q.cj), (unsigned)nshift, cntb);
-    fourstep_a_kernel<<<ga, 256, smemA, stream>>>(qs);
+    fourstep_a_kernel<<<ga, ta, smemA, stream>>>(qs);
     dim3 gb((unsigned)((q.b2 + q.wi - 1) / q.wi), (unsigned)nshift, cntb);
-    fourstep_b_kernel<<<gb, 256, smemB, stream>>>(qs);
+    fourstep_b_kernel<<<gb, tb, smemB, stream>>>(qs);
   }
   cudaFreeAsync(q.z, stream);
   AFFT_CHECK_LAUNCH("fourstep kernels");

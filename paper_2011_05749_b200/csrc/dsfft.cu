@@ -85,18 +85,42 @@ __global__ void active_count_kernel(int64_t b, const cd* __restrict__ v, double 
   if (threadIdx.x == 0) block_counts[blockIdx.x] = c;
 }
 
+// Exclusive scan of the per-block counts in one CTA of 1024 threads (chunked).
 __global__ void scan_counts_kernel(int nblocks, int32_t* __restrict__ counts,
                                    int32_t* __restrict__ total) {
-  // single thread: nblocks <= 2^24 / 1024 = 16384
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int32_t run = 0;
-    for (int k = 0; k < nblocks; ++k) {
-      const int32_t c = counts[k];
-      counts[k] = run;
-      run += c;
+  __shared__ int32_t warp_sum[32];
+  __shared__ int32_t carry;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nblocks; base += blockDim.x) {
+    const int i = base + tid;
+    const int32_t v = i < nblocks ? counts[i] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    *total = run;
+    if (lane == 31) warp_sum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int32_t s = lane < (int)(blockDim.x >> 5) ? warp_sum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sum[lane] = s;
+    }
+    __syncthreads();
+    const int32_t c = carry;
+    if (i < nblocks) counts[i] = c + (w ? warp_sum[w - 1] : 0) + x - v;
+    __syncthreads();
+    if (tid == 0) carry = c + warp_sum[(blockDim.x >> 5) - 1];
+    __syncthreads();
   }
+  if (tid == 0) *total = carry;
 }
 
 __global__ void active_write_kernel(int64_t b, const cd* __restrict__ v, double thr,
@@ -237,7 +261,7 @@ extern "C" int afft_active_indices(const double* values, int64_t b, double thr,
   if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(compaction)");
   const cd* v = reinterpret_cast<const cd*>(values);
   active_count_kernel<<<nblocks, kCompactThreads, 0, st>>>(b, v, thr, counts);
-  scan_counts_kernel<<<1, 32, 0, st>>>(nblocks, counts, out_count);
+  scan_counts_kernel<<<1, 1024, 0, st>>>(nblocks, counts, out_count);
   active_write_kernel<<<nblocks, kCompactThreads, 0, st>>>(b, v, thr, counts, map, out_idx);
   cudaFreeAsync(counts, st);
   AFFT_CHECK_LAUNCH("afft_active_indices");

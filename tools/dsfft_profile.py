@@ -13,7 +13,8 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 from bench_suite import make_batch  # noqa: E402
 from paper_2011_05749_b200 import DsfftConfig  # noqa: E402
-from paper_2011_05749_b200 import dsfft as D  # noqa: E402
+import paper_2011_05749_b200.dsfft  # noqa: E402,F401
+D = sys.modules["paper_2011_05749_b200.dsfft"]
 
 acc = collections.defaultdict(float)
 cnt = collections.Counter()
