@@ -20,6 +20,9 @@ namespace afft {
 // ---------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
+// stream-ordered scratch from the library's memory pool (kept across calls)
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
+cudaError_t scratch_free(void* p, cudaStream_t stream);
 
 #define AFFT_CHECK_LAUNCH(what)                                   \
   do {                                                            \

@@ -213,15 +213,15 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
   const size_t smemA = (size_t)(q.b2 + 2 * (int64_t)q.cj * q.b2) * 16;
   const size_t smemB = (size_t)(q.b1 + 2 * (int64_t)q.wi * q.b1) * 16;
   const size_t zbytes = (size_t)batch * nshift * b * 16;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&q.z), zbytes, stream);
-  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(four-step scratch)");
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&q.z), zbytes, stream);
+  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(four-step scratch)");
   e = cudaFuncSetAttribute(fourstep_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smemA);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fourstep_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smemB);
   if (e != cudaSuccess) {
-    cudaFreeAsync(q.z, stream);
+    scratch_free(q.z, stream);
     return cuda_status(e, "cudaFuncSetAttribute(four-step)");
   }
   for (int64_t s0 = 0; s0 < batch; s0 += 65535) {
@@ -239,7 +239,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     dim3 gb((unsigned)((q.b2 + q.wi - 1) / q.wi), (unsigned)nshift, cntb);
     fourstep_b_kernel<<<gb, tb, smemB, stream>>>(qs);
   }
-  cudaFreeAsync(q.z, stream);
+  scratch_free(q.z, stream);
   AFFT_CHECK_LAUNCH("fourstep kernels");
   return AFFT_OK;
 }

@@ -1,5 +1,6 @@
 // Error plumbing and version for the C ABI (include/aliasfft_b200.h).
 #include <cstring>
+#include <mutex>
 
 #include "afft_common.cuh"
 
@@ -18,6 +19,39 @@ int cuda_status(cudaError_t e, const char* what) {
   set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
   return e == cudaErrorMemoryAllocation ? AFFT_ENOMEM : AFFT_ECUDA;
 }
+
+// Stream-ordered scratch from a library-owned pool per device.  The default pool's
+// release threshold is 0, which hands memory back at every synchronisation and
+// re-maps it on the next allocation; this pool keeps it (threshold = max).
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[64] = {};
+
+static cudaMemPool_t library_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    g_pools[dev] = pool;
+  }
+  return g_pools[dev];
+}
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
+  cudaMemPool_t pool = library_pool();
+  if (!pool) return cudaMallocAsync(p, bytes, stream);
+  return cudaMallocFromPoolAsync(p, bytes, pool, stream);
+}
+
+cudaError_t scratch_free(void* p, cudaStream_t stream) { return cudaFreeAsync(p, stream); }
 
 }  // namespace afft
 

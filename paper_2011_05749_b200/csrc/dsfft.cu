@@ -227,8 +227,8 @@ extern "C" int afft_bucketize_rows(const void* x, int dtype, int64_t n, int64_t 
   }
   const int U = (int)residues.size();
   cd* Y = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&Y), (size_t)U * b * 16, st);
-  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(coset DFTs)");
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&Y), (size_t)U * b * 16, st);
+  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(coset DFTs)");
   int rc = afft_bucketize(x, dtype, n, 1, n, b, residues.data(), U,
                           reinterpret_cast<double*>(Y), (int64_t)U * b, b, 1, stream);
   if (!rc && nrows > 0) {
@@ -242,7 +242,7 @@ extern "C" int afft_bucketize_rows(const void* x, int dtype, int64_t n, int64_t 
     for (int u = 0; u < U; ++u) mm.m[u] = mult[u];
     coset_energy_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(b, U, mm, Y, energy);
   }
-  cudaFreeAsync(Y, st);
+  scratch_free(Y, st);
   if (!rc) AFFT_CHECK_LAUNCH("afft_bucketize_rows");
   return rc;
 }
@@ -257,13 +257,13 @@ extern "C" int afft_active_indices(const double* values, int64_t b, double thr,
   cudaStream_t st = (cudaStream_t)stream;
   const int nblocks = (int)((b + kCompactThreads - 1) / kCompactThreads);
   int32_t* counts = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), (size_t)nblocks * 4, st);
-  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(compaction)");
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&counts), (size_t)nblocks * 4, st);
+  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(compaction)");
   const cd* v = reinterpret_cast<const cd*>(values);
   active_count_kernel<<<nblocks, kCompactThreads, 0, st>>>(b, v, thr, counts);
   scan_counts_kernel<<<1, 1024, 0, st>>>(nblocks, counts, out_count);
   active_write_kernel<<<nblocks, kCompactThreads, 0, st>>>(b, v, thr, counts, map, out_idx);
-  cudaFreeAsync(counts, st);
+  scratch_free(counts, st);
   AFFT_CHECK_LAUNCH("afft_active_indices");
   return AFFT_OK;
 }

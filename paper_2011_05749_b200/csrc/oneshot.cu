@@ -276,9 +276,9 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
   double* scratch = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   if (smem > 200 * 1024) {  // many buckets: magnitudes in global memory
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch),
                                     (size_t)batch * cap * 8, st);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(dt_truncate scratch)");
+    if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(dt_truncate scratch)");
     smem = 0;
   } else {
     cudaError_t e = cudaFuncSetAttribute(dt_truncate_kernel,
@@ -288,7 +288,7 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
   dt_truncate_kernel<<<(unsigned)batch, 1024, smem, st>>>(
       nrows, a_m, k, pos, val, cnt, (int)cap, all_pos, all_val, all_count, out_pos, out_val,
       out_count, scratch);
-  if (scratch) cudaFreeAsync(scratch, st);
+  if (scratch) scratch_free(scratch, st);
   AFFT_CHECK_LAUNCH("dt_truncate_kernel");
   return AFFT_OK;
 }

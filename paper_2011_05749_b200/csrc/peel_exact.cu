@@ -444,9 +444,9 @@ static int launch_truncate(const int64_t* pos, const double* val, const int32_t*
   size_t smem = (size_t)pow2 * 20;
   double* scratch = nullptr;
   if (smem > kSmemLimit) {  // large graphs: rank from global memory
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch),
                                     (size_t)batch * cap * 16, stream);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(truncate scratch)");
+    if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(truncate scratch)");
     smem = 0;
   } else {
     cudaError_t e = cudaFuncSetAttribute(truncate_kernel,
@@ -455,7 +455,7 @@ static int launch_truncate(const int64_t* pos, const double* val, const int32_t*
   }
   truncate_kernel<<<(unsigned)batch, 1024, smem, stream>>>(pos, val, count, cap, k, out_pos,
                                                             out_val, out_count, scratch);
-  if (scratch) cudaFreeAsync(scratch, stream);
+  if (scratch) scratch_free(scratch, stream);
   AFFT_CHECK_LAUNCH("truncate_kernel");
   return AFFT_OK;
 }
@@ -583,11 +583,11 @@ extern "C" int afft_peel_exact(int64_t n, int64_t batch, const int64_t* factors,
   void* scratch = nullptr;
   const size_t bytes = peel_layout(p.G.nodes, ncycles, p.G.hmask + 1, false).total;
   if (bytes > kSmemLimit) {
-    cudaError_t e = cudaMallocAsync(&scratch, (size_t)batch * bytes, st);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(peel scratch)");
+    cudaError_t e = scratch_alloc(&scratch, (size_t)batch * bytes, st);
+    if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(peel scratch)");
   }
   rc = launch_peel(p, batch, scratch, st);
-  if (scratch) cudaFreeAsync(scratch, st);
+  if (scratch) scratch_free(scratch, st);
   return rc;
 }
 

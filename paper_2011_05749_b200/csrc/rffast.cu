@@ -731,12 +731,12 @@ extern "C" int afft_robust_thresholds(const double* energy, const uint8_t* mask,
   const size_t smem = (size_t)pow2 * 8;
   if (smem > 200 * 1024) {  // large: radix-select median over a global copy
     double* scratch = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch),
                                     (size_t)batch * count * 8, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(median scratch)");
+    if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(median scratch)");
     robust_thresholds_large_kernel<<<(unsigned)batch, 1024, 0, (cudaStream_t)stream>>>(
         (int)count, energy, mask, r, scratch, t0, t1);
-    cudaFreeAsync(scratch, (cudaStream_t)stream);
+    scratch_free(scratch, (cudaStream_t)stream);
     AFFT_CHECK_LAUNCH("robust_thresholds_large_kernel");
     return AFFT_OK;
   }
@@ -844,9 +844,9 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
   size_t hsmem = hbytes;
   char* hscratch = nullptr;
   if (hbytes > 200 * 1024) {  // large graphs: harvest state in global memory
-    e = cudaMallocAsync(reinterpret_cast<void**>(&hscratch), (size_t)batch * hbytes, st);
+    e = scratch_alloc(reinterpret_cast<void**>(&hscratch), (size_t)batch * hbytes, st);
     if (e != cudaSuccess) {
-      return cuda_status(e, "cudaMallocAsync(noisy harvest scratch)");
+      return cuda_status(e, "scratch_alloc(noisy harvest scratch)");
     }
     hsmem = 0;
   } else {
@@ -866,12 +866,12 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     AFFT_CHECK_LAUNCH("noisy_prep_kernel");
     cudaMemcpyAsync(host, counters, 4, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
-      if (hscratch) cudaFreeAsync(hscratch, st);
+      if (hscratch) scratch_free(hscratch, st);
       return cuda_status(e, "afft_peel_noisy round sync");
     }
     const int A = host[0];
     if ((rc = run_search(*P, w, ws, A, residual, st))) {
-      if (hscratch) cudaFreeAsync(hscratch, st);
+      if (hscratch) scratch_free(hscratch, st);
       return rc;
     }
     if (A > 0) {
@@ -892,7 +892,7 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     if (host[1] == 0) break;  // every signal found nothing: all loops have exited
   }
   count_multi_kernel<<<(unsigned)batch, 256, 0, st>>>(batch, N, state, unresolved);
-  if (hscratch) cudaFreeAsync(hscratch, st);
+  if (hscratch) scratch_free(hscratch, st);
   AFFT_CHECK_LAUNCH("count_multi_kernel");
   return AFFT_OK;
 }
@@ -970,10 +970,10 @@ extern "C" int afft_median(const double* values, int32_t mode, int64_t count, in
   }
   cudaStream_t st = (cudaStream_t)stream;
   double* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (size_t)batch * count * 8, st);
-  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(median)");
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch), (size_t)batch * count * 8, st);
+  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(median)");
   median_kernel<<<(unsigned)batch, 1024, 0, st>>>((int)count, mode, values, scratch, out);
-  cudaFreeAsync(scratch, st);
+  scratch_free(scratch, st);
   AFFT_CHECK_LAUNCH("median_kernel");
   return AFFT_OK;
 }
