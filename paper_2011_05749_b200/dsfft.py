@@ -21,7 +21,7 @@ from . import _device, _lib
 from .bucketize import SampleLedger, gather_indices, record_bucketization
 from .oneshot import OneShotConfig, random_shifts, structured_shifts
 from .peeling import (
-    CODE_STATE,
+    STATE_CODE,
     NodeState,
     SearchPlan,
     UnsupportedSizeError,
@@ -29,6 +29,9 @@ from .peeling import (
     kay_weights,
 )
 from .signals import SparseSpectrum
+
+STATE_SINGLE = STATE_CODE[NodeState.SINGLE_TON]
+STATE_MULTI = STATE_CODE[NodeState.MULTI_TON]
 
 
 @dataclass
@@ -215,13 +218,12 @@ def _classify(xd, layer: _DevLayer, config: DsfftConfig, ledger):
                                            rn.data_ptr(), ws.data_ptr(), ws.numel(), sp),
                    "classify_noisy")
     st_h = st.cpu().numpy()
+    single = st_h == STATE_SINGLE
+    multi = st_h == STATE_MULTI
     f0_h, val_h, act_h = f0.cpu().numpy(), val.cpu().numpy(), act.cpu().numpy()
-    for g in range(A):
-        state = CODE_STATE[int(st_h[g])]
-        if state is NodeState.SINGLE_TON:
-            entries[int(f0_h[g])] = complex(val_h[g])
-        elif state is NodeState.MULTI_TON:
-            multitons.append(int(act_h[g]))
+    # entries in ascending-bucket order, as the reference inserts them
+    entries.update(zip(f0_h[single].tolist(), val_h[single].tolist()))
+    multitons.extend(act_h[multi].tolist())
     return entries, multitons
 
 

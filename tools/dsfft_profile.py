@@ -53,3 +53,35 @@ total = time.perf_counter() - t0
 print(f"total {total * 1e3:.1f} ms")
 for name, v in sorted(acc.items(), key=lambda kv: -kv[1]):
     print(f"  {name:18s} {v * 1e3:8.2f} ms  x{cnt[name]}")
+
+# ---- per C-ABI entry point (synchronised wall time per call)
+from paper_2011_05749_b200 import _lib  # noqa: E402
+
+lib = _lib.load()
+cacc = collections.defaultdict(float)
+ccnt = collections.Counter()
+
+
+class Timed:
+    def __init__(self, fn, name):
+        self.fn, self.name = fn, name
+
+    def __call__(self, *a):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        r = self.fn(*a)
+        torch.cuda.synchronize()
+        cacc[self.name] += time.perf_counter() - t
+        ccnt[self.name] += 1
+        return r
+
+
+for name in list(_lib.SIGNATURES):
+    setattr(lib, name, Timed(getattr(lib, name), name))
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+D.dsfft_device(x[1], k, cfg)
+torch.cuda.synchronize()
+print(f"total (C calls synchronised) {(time.perf_counter() - t0) * 1e3:.1f} ms")
+for name, v in sorted(cacc.items(), key=lambda kv: -kv[1]):
+    print(f"  {name:32s} {v * 1e3:8.2f} ms  x{ccnt[name]}")
