@@ -701,7 +701,10 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     // stream, so HBM never waits for the latency-bound decode.
     const int nparts = afft_sumsq_parts(n, dtype);
     const char* env = getenv("AFFT_FFAST_MODE");  // 0 fused, 1 pre-pass, 2 pipelined
-    int mode = batch < 2 * 148 ? 1 : 2;
+    // pipelining pays when each signal's stream dwarfs its decode (config 5: 16.8 MB);
+    // small signals (config 1: 2 MB) are best served by the single fused launch
+    const int64_t sig_bytes = n * (dtype == AFFT_C64 ? 8 : 16);
+    int mode = batch < 2 * 148 ? 1 : (sig_bytes >= (8 << 20) ? 2 : 0);
     if (env && (env[0] == '0' || env[0] == '1' || env[0] == '2')) mode = env[0] - '0';
     if (nparts < 2) mode = 0;
     double* partials = nullptr;
