@@ -217,6 +217,20 @@ int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors /* host */,
                     int32_t* rec_count, int32_t* rounds, int32_t* unresolved, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------------------ smallnum */
+/*
+ * smallnum.py:54-142 for one row-major complex128 matrix a (m x n), single-thread
+ * device kernel over the hot path's small-LA code.  op: 0 svd (u m x m, s, v n x n),
+ * 1 lstsq with numpy's cutoff (b [m], x [n], s [n], out_i[0] = rank; m >= n),
+ * 2 eigvals (n x n; x [n], out_i[0] = converged), 3 poly_roots (a = n non-leading
+ * coefficients, m = 1; x, out_i[0] = count), 4 pencil_eigenvalues (a = full
+ * (r+1) x (r+1) pencil, rank; x, out_i = {rank used, ok}).  Caps: short side <= 8,
+ * long side <= 32.
+ */
+int afft_small_la(int32_t op, int32_t m, int32_t n, const double* a, const double* b,
+                  int32_t rank, double* out_u, double* out_s, double* out_v, double* out_x,
+                  int32_t* out_i, void* stream);
+
 /* ------------------------------------------------------------------ sFFT-DT1/2/3 */
 /*
  * Measurement rows (oneshot.py:86-106): rows[s][bucket][3*a_m + p] = bucket values at the
