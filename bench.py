@@ -252,6 +252,7 @@ def run_ours(args):
     del os.environ["AFFT_FFAST_MODE"]
 
     e2e = run_e2e(args, dev, x, world) if rank == 0 else None
+    context = dense_fft_context(x, dev) if rank == 0 else None
     cpu = cpu_baseline_sample(x[: args.cpu_signals]) if (rank == 0 and world == 1) else None
 
     if rank == 0:
@@ -295,6 +296,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "context": context,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -339,6 +341,37 @@ def run_e2e(args, dev, x, world):
     return {"value": m / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": m * SIGNAL_BYTES,
             "d2h_bytes_per_step": m * K * (8 + 16) + m * 4, "signals_per_step": m,
             "ms_per_step": ms, "api": "paper_2011_05749_b200.ffast_batch (afft_ffast) on pinned host"}
+
+
+def dense_fft_context(x, dev):
+    """Context only (north_star): a dense full-length FFT of the same N — cuFFT on this
+    B200 (via torch, c64) and numpy on one host core — in signals/s."""
+    import torch
+
+    m = min(512, x.shape[0])
+    xs = x[:m]
+    out = torch.empty_like(xs)
+
+    def run():
+        out.copy_(torch.fft.fft(xs, dim=1))
+
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    gpu_ms = a.elapsed_time(b) / 3
+    host = x[0].cpu().numpy()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        np.fft.fft(host.astype(np.complex128))
+    cpu_s = (time.perf_counter() - t0) / 3
+    return {"dense_fft_gpu_signals_per_s": m / (gpu_ms * 1e-3), "dense_fft_gpu": "cuFFT c64 (torch.fft)",
+            "dense_fft_cpu_signals_per_s": 1.0 / cpu_s, "dense_fft_cpu": "numpy pocketfft c128, 1 core",
+            "note": "context only; not part of the measured path"}
 
 
 def cpu_baseline_sample(xs):
