@@ -124,3 +124,15 @@ def test_large_b_batched_and_strided():
         # prime bucket count above the one-CTA limit has no two-factor split
         from paper_2011_05749_b200.bucketize import bucketize_device
         bucketize_device(torch.zeros(4099 * 2, dtype=torch.complex128).cuda(), 4099, [0])
+
+
+def test_device_input_synthesis_matches_host_model():
+    """§8f item 1: device-synthesised inputs equal generate_test_case to ~1e-15."""
+    from paper_2011_05749_b200.signals import generate_test_case, generate_test_case_device
+
+    for n, k, snr, seed in [(124950, 40, "exact", 3), (1 << 16, 16, 20.0, 2), (4095, 4, 10.0, 0)]:
+        ref = generate_test_case(n, k, snr, seed)
+        x, truth = generate_test_case_device(n, k, snr, seed)
+        assert truth.entries == ref.truth.entries
+        d = np.max(np.abs(x.cpu().numpy() - ref.signal))
+        assert d <= 1e-12 * max(1.0, np.max(np.abs(ref.signal))), d
