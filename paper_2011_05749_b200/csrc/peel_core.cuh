@@ -125,40 +125,43 @@ __device__ __forceinline__ void hash_insert(unsigned* h, int mask, int64_t f) {
 }
 
 // In-place exclusive prefix sum of a[0..N) across the block; returns the total.
+// Each thread scans a contiguous chunk of ceil(N / blockDim) elements, the chunk
+// sums are scanned across the block with warp shuffles: two barriers for any N.
 __device__ inline int block_exclusive_scan(int* a, int N, int* warp_tmp, int* carry) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int nwarps = (nt + 31) >> 5;
-  if (tid == 0) *carry = 0;
+  const int per = (N + nt - 1) / nt;
+  const int lo = min(N, tid * per), hi = min(N, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += a[i];
+  int x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tmp[wid] = x;
   __syncthreads();
-  for (int base = 0; base < N; base += nt) {
-    const int i = base + tid;
-    const int v = i < N ? a[i] : 0;
-    int x = v;
+  if (wid == 0) {
+    int w = lane < nwarps ? warp_tmp[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
     }
-    if (lane == 31) warp_tmp[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      int w = lane < nwarps ? warp_tmp[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      if (lane < nwarps) warp_tmp[lane] = w;
-    }
-    __syncthreads();
-    const int c = *carry;
-    const int wprefix = wid > 0 ? warp_tmp[wid - 1] : 0;
-    if (i < N) a[i] = c + wprefix + x - v;
-    __syncthreads();
-    if (tid == 0) *carry = c + warp_tmp[nwarps - 1];
-    __syncthreads();
+    if (lane < nwarps) warp_tmp[lane] = w;
+    if (lane == 31) *carry = w;
   }
-  return *carry;
+  __syncthreads();
+  int run = (wid ? warp_tmp[wid - 1] : 0) + x - sum;
+  for (int i = lo; i < hi; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  const int total = *carry;
+  __syncthreads();  // a[] and carry are read back by the caller's next phase
+  return total;
 }
 
 // classify_exact (peeling.py:193-215) for one residual (r0, r1, r2): ZERO_TON if

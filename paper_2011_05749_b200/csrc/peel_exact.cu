@@ -185,6 +185,7 @@ __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64
   return a0 + a1;
 }
 
+template <bool kStream>
 __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s,
                                                  unsigned char* smem_raw, int* warp_tmp,
                                                  int* carry_p, int* red_p, double* wsum) {
@@ -202,7 +203,7 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
 
   // 1. exact_thresholds: eps = 1e-6 * ||x|| / sqrt(n), fixed-order block reduction
   //    (skipped when a multi-CTA pre-pass already produced eps for a small batch)
-  double acc = p.eps_in ? 0.0 : stream_sumsq(row, p.dtype, n);
+  double acc = (!kStream || p.eps_in) ? 0.0 : stream_sumsq(row, p.dtype, n);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((tid & 31) == 0) wsum[tid >> 5] = acc;
@@ -223,7 +224,7 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
   }
   double t = 0.0;
   for (int w = 0; w < kFusedThreads / 32; ++w) t += wsum[w];
-  const double eps = p.eps_in ? p.eps_in[s] : (1e-6 * sqrt(t)) / sqrt((double)n);
+  const double eps = (!kStream || p.eps_in) ? p.eps_in[s] : (1e-6 * sqrt(t)) / sqrt((double)n);
   // 3. graph state
   for (int g = tid; g < N; g += nt) {
     M.st[g] = AFFT_UNKNOWN;
@@ -282,7 +283,21 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
   __shared__ int carry, red;
   __shared__ double wsum[kFusedThreads / 32];
   for (int64_t s = blockIdx.x; s < batch; s += gridDim.x) {
-    ffast_one_signal(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
+    ffast_one_signal<true>(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
+    __syncthreads();
+  }
+}
+
+// Decode only (eps precomputed by the multi-CTA norm pass): the fused body with the
+// stream compiled out, so fewer registers are live across the decode.
+__global__ void __launch_bounds__(kFusedThreads, 3) ffast_decode_kernel(
+    const __grid_constant__ FusedParams p, int64_t batch) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tmp[32];
+  __shared__ int carry, red;
+  __shared__ double wsum[kFusedThreads / 32];
+  for (int64_t s = blockIdx.x; s < batch; s += gridDim.x) {
+    ffast_one_signal<false>(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
     __syncthreads();
   }
 }
@@ -722,6 +737,9 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     {
       cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ffast_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ffast_fused)");
     }
     if (mode == 2) {
@@ -755,7 +773,7 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
         const char* dg = getenv("AFFT_DECODE_CTAS_PER_SM");
         const int per_sm = dg ? std::max(1, atoi(dg)) : 1;
         const int64_t grid = std::min<int64_t>(cnt, (int64_t)num_sms() * per_sm);
-        ffast_fused_kernel<<<(unsigned)grid, kFusedThreads, smem, A->aux>>>(fc, cnt);
+        ffast_decode_kernel<<<(unsigned)grid, kFusedThreads, smem, A->aux>>>(fc, cnt);
         AFFT_CHECK_LAUNCH("ffast_fused_kernel");
       }
       cudaEventRecord(A->join, A->aux);
@@ -767,7 +785,10 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
       if ((rc = afft_exact_thresholds(partials, nparts, n, batch, epsbuf, st))) return rc;
       fp.eps_in = epsbuf;
     }
-    ffast_fused_kernel<<<(unsigned)batch, kFusedThreads, smem, st>>>(fp, batch);
+    if (fp.eps_in)
+      ffast_decode_kernel<<<(unsigned)batch, kFusedThreads, smem, st>>>(fp, batch);
+    else
+      ffast_fused_kernel<<<(unsigned)batch, kFusedThreads, smem, st>>>(fp, batch);
     AFFT_CHECK_LAUNCH("ffast_fused_kernel");
     return AFFT_OK;
   }
