@@ -125,6 +125,23 @@ struct FusedParams {
 constexpr int kFusedThreads = 256;
 constexpr int kStreamUnroll = 8;
 
+// 16-byte streaming loads that do not allocate in L1: the CTA's own shared memory
+// leaves little L1 next to it, and nothing in the stream is re-read.
+__device__ __forceinline__ float4 ld_na(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_na(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
 // Per-thread partial of sum |x|^2 over one signal: 16-byte streaming loads,
 // kStreamUnroll in flight per thread, float64 accumulation.
 __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64_t n) {
@@ -146,7 +163,7 @@ __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64
     for (; i + (kStreamUnroll - 1) * nt < nvec; i += kStreamUnroll * nt) {
       float4 v[kStreamUnroll];
 #pragma unroll
-      for (int u = 0; u < kStreamUnroll; ++u) v[u] = __ldcs(xv + i + u * nt);
+      for (int u = 0; u < kStreamUnroll; ++u) v[u] = ld_na(xv + i + u * nt);
 #pragma unroll
       for (int u = 0; u < kStreamUnroll; u += 2) {
         a0 += (double)v[u].x * v[u].x + (double)v[u].y * v[u].y + (double)v[u].z * v[u].z +
@@ -156,7 +173,7 @@ __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64
       }
     }
     for (; i < nvec; i += nt) {
-      const float4 v = __ldcs(xv + i);
+      const float4 v = ld_na(xv + i);
       a0 += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
     }
     const int64_t tail = e + 2 * nvec;
@@ -170,7 +187,7 @@ __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64
     for (; i + (kStreamUnroll - 1) * nt < n; i += kStreamUnroll * nt) {
       double2 v[kStreamUnroll];
 #pragma unroll
-      for (int u = 0; u < kStreamUnroll; ++u) v[u] = __ldcs(xv + i + u * nt);
+      for (int u = 0; u < kStreamUnroll; ++u) v[u] = ld_na(xv + i + u * nt);
 #pragma unroll
       for (int u = 0; u < kStreamUnroll; u += 2) {
         a0 += v[u].x * v[u].x + v[u].y * v[u].y;
@@ -178,7 +195,7 @@ __device__ __forceinline__ double stream_sumsq(const char* row, int dtype, int64
       }
     }
     for (; i < n; i += nt) {
-      const double2 v = __ldcs(xv + i);
+      const double2 v = ld_na(xv + i);
       a0 += v.x * v.x + v.y * v.y;
     }
   }
@@ -716,10 +733,10 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     // stream, so HBM never waits for the latency-bound decode.
     const int nparts = afft_sumsq_parts(n, dtype);
     const char* env = getenv("AFFT_FFAST_MODE");  // 0 fused, 1 pre-pass, 2 pipelined
-    // pipelining pays when each signal's stream dwarfs its decode (config 5: 16.8 MB);
-    // small signals (config 1: 2 MB) are best served by the single fused launch
-    const int64_t sig_bytes = n * (dtype == AFFT_C64 ? 8 : 16);
-    int mode = batch < 2 * 148 ? 1 : (sig_bytes >= (8 << 20) ? 2 : 0);
+    // Measured on B200 (tools/ffast_modes.py, config 5, 8192 signals): fused 20.44 ms,
+    // pipelined 20.96 ms, pre-pass + decode 22.25 ms, stream alone 18.65 ms.  Small
+    // batches (< 2 waves) cannot keep HBM busy with one streaming CTA per signal.
+    int mode = batch < 2 * 148 ? 1 : 0;
     if (env && (env[0] == '0' || env[0] == '1' || env[0] == '2')) mode = env[0] - '0';
     if (nparts < 2) mode = 0;
     double* partials = nullptr;
