@@ -396,7 +396,6 @@ def cpu_baseline_sample(xs):
 
 def _ref_worker(args_tuple):
     wid, per_step, steps, warmup, barrier, q = args_tuple
-    os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import ffast as oracle_ffast
     from paper_2011_05749_b200.signals import generate_test_case
 
@@ -424,9 +423,12 @@ def run_reference(args):
         return
     import multiprocessing as mp
 
+    # one BLAS / OpenMP thread per worker process, fixed before the workers import numpy
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
     cores = os.cpu_count() or 1
-    per_step = 1
-    ctx = mp.get_context("fork")
+    per_step = 4  # signals per core per step: amortises the per-step barrier
+    ctx = mp.get_context("spawn")
     barrier = ctx.Barrier(cores)
     q = ctx.Queue()
     procs = [ctx.Process(target=_ref_worker,
@@ -452,7 +454,7 @@ def run_reference(args):
         "config": {"workload": "config5_ffast_n2097024_k256_127x128x129_c64", "n": N_SIG, "k": K,
                    "factors": FACTORS, "signals_per_step": cores * per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{cores * per_step} signals per step (one per core), "
+                         "sample": f"{cores * per_step} signals per step ({per_step} per core), "
                                    "oracle/ffast.py numpy port of the reference FFAST path, "
                                    "signal generation excluded as bench.py:172-176 does"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
