@@ -73,7 +73,7 @@ def ffast_batch(x, k: int, factors, max_rounds: int | None = None,
     dev = xd.device
     code = _device.dtype_code(xd)
     ld = int(xd.stride(0)) if batch > 1 else n
-    need = ffast_workspace_bytes(n, code, batch, factors)
+    need = ffast_workspace_bytes(n, code, max(batch, 1), factors)
     if need == 0:
         # planning failed inside the library: surface its message
         _lib.check(_lib.AFFT_EINVAL if any(b < 1 or n % b for b in factors) else
@@ -92,6 +92,8 @@ def ffast_batch(x, k: int, factors, max_rounds: int | None = None,
             rounds=torch.empty(batch, dtype=torch.int32, device=dev),
             unresolved=torch.empty(batch, dtype=torch.int32, device=dev),
         )
+    if batch == 0:
+        return out
     fb, nc = _lib.host_i64(factors)
     mr = int(max_rounds) if max_rounds else 0
     _lib.check(

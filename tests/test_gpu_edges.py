@@ -1,0 +1,98 @@
+"""Edge cases of the device paths: strided and misaligned rows, empty batches, k = 0,
+graphs too large for shared memory (global-scratch fallback), bucket counts on the
+four-step DFT path — each checked against the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ffast as of
+
+pytestmark = pytest.mark.gpu
+
+
+def _signals(n, k, count, seed0=0, dtype=np.complex128):
+    from paper_2011_05749_b200 import generate_test_case
+
+    return np.stack([generate_test_case(n, k, "exact", seed0 + i).signal for i in range(count)]
+                    ).astype(dtype)
+
+
+def test_strided_rows_equal_contiguous():
+    from paper_2011_05749_b200 import ffast_batch
+
+    n, k, f = 4095, 8, [63, 65]
+    xs = _signals(n, k, 5)
+    wide = torch.zeros((5, n + 37), dtype=torch.complex128, device="cuda")
+    wide[:, :n] = torch.from_numpy(xs).cuda()
+    strided = wide[:, :n]  # ld = n + 37
+    assert strided.stride(0) == n + 37
+    a = ffast_batch(strided, k, f)
+    b = ffast_batch(torch.from_numpy(xs).cuda(), k, f)
+    for i in range(5):
+        assert a.full_spectrum(i).entries == b.full_spectrum(i).entries
+
+
+def test_misaligned_complex64_rows():
+    """n odd => every other c64 row starts 8 bytes off a 16-byte boundary (stream head path)."""
+    from paper_2011_05749_b200 import ffast_batch
+
+    n, k, f = 4095, 8, [63, 65]
+    xs = _signals(n, k, 6, seed0=10, dtype=np.complex64)
+    for mode in ("0", "1"):
+        import os
+
+        os.environ["AFFT_FFAST_MODE"] = mode
+        try:
+            res = ffast_batch(torch.from_numpy(xs).cuda(), k, f)
+        finally:
+            del os.environ["AFFT_FFAST_MODE"]
+        for i in range(6):
+            _, o = of.ffast(xs[i].astype(np.complex128), k, f)
+            assert list(res.full_spectrum(i).entries) == list(o["recovered"])
+
+
+def test_empty_and_k0():
+    from paper_2011_05749_b200 import ffast, ffast_batch
+
+    res = ffast_batch(torch.zeros((0, 4095), dtype=torch.complex128, device="cuda"), 4, [63, 65])
+    assert res.count.numel() == 0
+    x = _signals(4095, 4, 1)[0]
+    assert ffast(x, 0).entries == {}
+    res = ffast_batch(x[None, :], 0, [63, 65])
+    assert int(res.count[0]) == 0 and int(res.all_count[0]) > 0  # decoded, then truncated to 0
+
+
+def test_large_graph_fallback_and_four_step():
+    """b = 8192 > 4096: four-step graph build, global-memory peeling scratch, large truncation."""
+    from paper_2011_05749_b200 import CyclePlan, ffast, plan_cycles
+
+    n, k = 8192 * 5, 6
+    plan, _ = plan_cycles(n, k, "exact")
+    assert max(plan.factors) > 4096
+    for seed in range(3):
+        x = _signals(n, k, 1, seed0=seed)[0]
+        out = ffast(x, k, plan=CyclePlan(plan.factors, [0, 1, 2]))
+        trunc, o = of.ffast(x, k, plan.factors)
+        assert set(out.entries) == set(trunc)
+        for f, v in trunc.items():
+            assert abs(out.entries[f] - v) < 1e-9
+
+
+def test_peel_decode_resumes_with_prior_recovered():
+    """peel_decode on a graph that already holds recovered tones (peeling.py:281-282 default
+    max_rounds = len(recovered) + 8; prior entries must not be re-harvested)."""
+    from paper_2011_05749_b200 import CyclePlan, generate_test_case, peel_decode
+    from paper_2011_05749_b200.peeling import build_graph, exact_thresholds
+
+    case = generate_test_case(504, 6, "exact", seed=2)
+    g = build_graph(case.signal, CyclePlan([7, 8, 9], [0, 1, 2]))
+    e = exact_thresholds(case.signal)
+    r1 = peel_decode(g, "exact", eps_zero=e, eps_ratio=e, max_rounds=1)
+    first = dict(g.recovered)
+    r2 = peel_decode(g, "exact", eps_zero=e, eps_ratio=e)
+    assert list(g.recovered)[: len(first)] == list(first)
+    g_all = build_graph(case.signal, CyclePlan([7, 8, 9], [0, 1, 2]))
+    r_all = peel_decode(g_all, "exact", eps_zero=e, eps_ratio=e, max_rounds=12)
+    assert set(r2.spectrum.entries) == set(r_all.spectrum.entries)
+    assert r1.rounds == 1
