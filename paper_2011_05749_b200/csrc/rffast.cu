@@ -305,7 +305,7 @@ __global__ void noisy_apply_kernel(int A, const __grid_constant__ NoisyPlan P,
 }
 
 // Harvest (first-found) + subtract for one signal per CTA (peeling.py:296-308).
-__global__ void __launch_bounds__(512) noisy_harvest_kernel(
+__global__ void __launch_bounds__(1024) noisy_harvest_kernel(
     const __grid_constant__ NoisyPlan P, double* __restrict__ residual, int8_t* __restrict__ state,
     int8_t* __restrict__ dirty, const int64_t* __restrict__ node_f0,
     const double* __restrict__ node_val, int32_t* __restrict__ done, int64_t* __restrict__ rec_pos,
@@ -369,24 +369,44 @@ __global__ void __launch_bounds__(512) noisy_harvest_kernel(
   }
   __syncthreads();
   for (int i = tid; i < nf; i += nt) state[so + found_g[i]] = AFFT_RESOLVED;
-  for (int e = tid; e < nf * P.ncycles; e += nt) {
-    const int i = e / P.ncycles, c = e - i * P.ncycles;
-    const int32_t r = (int32_t)(node_f0[so + found_g[i]] % P.b[c]);
-    found_res[e] = r;
-    hv[P.base[c] + r] = 1;
+  for (int g = tid; g < N; g += nt) flag[g] = 0;
+  __syncthreads();
+  // per-node lists of the found tones hitting it: count, scan, scatter
+  const int F = P.ncycles;
+  for (int e = tid; e < nf * F; e += nt) {
+    const int i = e / F, c = e - i * F;
+    atomicAdd(&flag[P.base[c] + (int)(node_f0[so + found_g[i]] % P.b[c])], 1);
   }
   __syncthreads();
-  // subtract: one warp per hit node, lanes over the R measurements, found order
+  block_exclusive_scan(flag, N, warp_tmp, &carry);
+  for (int e = tid; e < nf * F; e += nt) {
+    const int i = e / F, c = e - i * F;
+    const int slot = atomicAdd(&flag[P.base[c] + (int)(node_f0[so + found_g[i]] % P.b[c])], 1);
+    found_res[slot] = i;
+  }
+  __syncthreads();
+  // subtract: one warp per hit node, lanes over the R measurements, tones in found order
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   for (int g = wid; g < N; g += nw) {
-    if (!hv[g]) continue;
-    const int c = noisy_cycle(P, g);
-    const int idx = g - P.base[c];
+    const int lo = g ? flag[g - 1] : 0, hi = flag[g];
+    if (lo == hi) continue;
+    if (lane == 0) {  // insertion sort of the (short) segment restores found order
+      for (int a2 = lo + 1; a2 < hi; ++a2) {
+        const int v = found_res[a2];
+        int b2 = a2 - 1;
+        while (b2 >= lo && found_res[b2] > v) {
+          found_res[b2 + 1] = found_res[b2];
+          --b2;
+        }
+        found_res[b2 + 1] = v;
+      }
+    }
+    __syncwarp();
     cd* y = reinterpret_cast<cd*>(residual) + (so + g) * P.R;
     for (int r = lane; r < P.R; r += 32) {
       cd acc = y[r];
-      for (int i = 0; i < nf; ++i) {
-        if (found_res[i * P.ncycles + c] != idx) continue;
+      for (int a2 = lo; a2 < hi; ++a2) {
+        const int i = found_res[a2];
         const int64_t f = node_f0[so + found_g[i]];
         const cd v = reinterpret_cast<const cd*>(node_val)[so + found_g[i]];
         acc = csub(acc, cmul(v, unit_root(mulmod(P.tau[r], f, P.n), P.n)));
@@ -536,21 +556,31 @@ __global__ void robust_thresholds_large_kernel(int count, const double* __restri
   const double* E = energy + s * (int64_t)count;
   const uint8_t* M = mask ? mask + s * (int64_t)count : nullptr;
   double* v = scratch + s * (int64_t)count;
+  // max over all energies and the (masked) median set, compacted in parallel
+  // (order is irrelevant to a selection)
+  __shared__ int m_fill;
   if (threadIdx.x == 0) {
-    int cnt = 0;
-    double mx = 0.0;
-    for (int i = 0; i < count; ++i) {
-      mx = fmax(mx, E[i]);
-      if (!M || M[i]) v[cnt++] = E[i];
-    }
-    if (M && cnt == 0) {
-      for (int i = 0; i < count; ++i) v[i] = E[i];
-      cnt = count;
-    }
-    m_count = cnt;
-    m_max = mx;
+    m_fill = 0;
+    m_max = 0.0;
   }
   __syncthreads();
+  double mx = 0.0;  // scale.max(initial=0.0)
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    mx = fmax(mx, E[i]);
+    if (!M || M[i]) v[atomicAdd(&m_fill, 1)] = E[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&m_max), (unsigned long long)__double_as_longlong(mx));
+  __syncthreads();
+  if (threadIdx.x == 0) m_count = m_fill;
+  __syncthreads();
+  if (M && m_count == 0) {  // empty reference set: fall back to all energies
+    for (int i = threadIdx.x; i < count; i += blockDim.x) v[i] = E[i];
+    __syncthreads();
+    if (threadIdx.x == 0) m_count = count;
+    __syncthreads();
+  }
   const int cnt = m_count;
   double med;
   if (cnt & 1) {
@@ -839,6 +869,7 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     return cuda_status(e, "afft_peel_noisy init");
   }
   int hcap = P->hmask + 1;
+  // hash, flag[N], found_g[N], found_res[N * ncycles] (per-node tone lists), hv[N]
   const size_t hbytes =
       ((size_t)hcap * 4 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64 + 15) & ~size_t(15);
   size_t hsmem = hbytes;
@@ -881,7 +912,7 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
           reinterpret_cast<const double*>(ws + w.res), t1, state, dirty, node_f0, node_val);
       AFFT_CHECK_LAUNCH("noisy_apply_kernel");
     }
-    noisy_harvest_kernel<<<(unsigned)batch, 512, hsmem, st>>>(
+    noisy_harvest_kernel<<<(unsigned)batch, 1024, hsmem, st>>>(
         *P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap,
         rec_count, rounds, counters + 1, hscratch, hbytes);
     AFFT_CHECK_LAUNCH("noisy_harvest_kernel");
