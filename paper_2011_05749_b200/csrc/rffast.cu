@@ -116,24 +116,43 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
   __syncthreads();
   const int64_t idx = act_index[a];
   const double dn = (double)n;
+  // score of candidate t, summed in stride order exactly as the reference does;
+  // stops (returns > bound) once the partial sum exceeds bound: every term is
+  // >= 0, so such a candidate is strictly worse than the candidate that set bound
+  // and can be neither the minimum nor a tie.
+  auto score = [&](int64_t t, double bound) -> double {
+    int64_t r = idx + b * t;  // cand = (index + b*t) mod n, already < n
+    double sc = 0.0;
+    for (int j = 0; j < c; ++j) {
+      const double tgt = __ddiv_rn(__dmul_rn(-kTwoPi, (double)r), dn);
+      const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
+      sc = __dadd_rn(sc, __dmul_rn(wv, wv));
+      if (sc > bound) return sc;
+      r <<= 1;
+      if (r >= n) r -= n;
+    }
+    return sc;
+  };
   double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   int32_t bt = INT32_MAX;
   if (t0 < L) {
+    // pruning bound: the full score of the candidate nearest the stride-0 estimate
+    const double fe = (-s_est[0] * dn) / kTwoPi;
+    double dd = (fe - (double)idx) / (double)b;
+    int64_t th = (int64_t)floor(dd + 0.5);
+    th %= L;
+    if (th < 0) th += L;
+    double bound = score(th, __longlong_as_double(0x7ff0000000000000LL));
+    if (!(bound == bound)) bound = __longlong_as_double(0x7ff0000000000000LL);  // NaN: no pruning
     const int64_t t1 = min(L, t0 + (int64_t)kChunk);
     for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads) {
-      int64_t r = idx + b * t;  // cand = (index + b*t) mod n, already < n
-      double sc = 0.0;
-      for (int j = 0; j < c; ++j) {
-        const double tgt = __ddiv_rn(__dmul_rn(-kTwoPi, (double)r), dn);
-        const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
-        sc = __dadd_rn(sc, __dmul_rn(wv, wv));
-        r <<= 1;
-        if (r >= n) r -= n;
-      }
+      const double sc = score(t, bound);
+      if (sc > bound) continue;  // pruned / worse than a candidate that is scored in full
       if (sc < best) {
         best = sc;
         bt = (int32_t)t;
       }
+      if (sc < bound) bound = sc;
     }
   }
   // block argmin, ties -> smaller t
