@@ -17,10 +17,11 @@
 
 #include "afft_common.cuh"
 #include "oneshot_core.cuh"
+#include "peel_core.cuh"
 
 namespace afft {
 
-constexpr int kDtSolveThreads = 128;
+constexpr int kDtSolveThreads = 64;
 
 // ------------------------------------------------------------------ detect
 
@@ -39,40 +40,211 @@ __global__ void dt_sigma_kernel(int64_t rows, int R, int a_m, const double* __re
   for (int i = 0; i < a_m; ++i) sigmas[e * a_m + i] = s[i];
 }
 
-// Vote: key i of signal s (i = bucket*a_m + slot) is chosen iff its rank under
-// (-q, bucket, slot) is < k, with q = rint(sigma / 1e-12) (oneshot.py:131-139).
-__global__ void dt_vote_kernel(int M, int a_m, int k, const double* __restrict__ sigmas,
-                               int32_t* __restrict__ counts) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  long long* q = reinterpret_cast<long long*>(smem_raw);
-  const int64_t s = blockIdx.y;
+// Vote (oneshot.py:131-139): keys i = bucket*a_m + slot with q_i = rint(sigma_i/1e-12);
+// the first k keys under (-q, i) are chosen.  One CTA per signal: a radix select
+// finds the k-th largest q (q*) and the count above it; among keys equal to q* the
+// lowest indices fill the remaining places (a block scan over the equality flags).
+constexpr int kVoteThreads = 1024;
+
+__global__ void __launch_bounds__(kVoteThreads) dt_vote_kernel(int M, int a_m, int k,
+                                                               const double* __restrict__ sigmas,
+                                                               int32_t* __restrict__ counts,
+                                                               long long* __restrict__ qbuf) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long prefix;
+  __shared__ int remaining;
+  __shared__ int warp_sum[32];
+  __shared__ int carry;
+  const int64_t s = blockIdx.x;
   const double* sg = sigmas + s * (int64_t)M;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const long long qi = i < M ? (long long)rint(__ddiv_rn(sg[i], 1e-12)) : 0;
-  int rank = 0;
-  constexpr int kTile = 2048;
-  for (int base = 0; base < M; base += kTile) {
-    const int cnt = min(kTile, M - base);
-    __syncthreads();
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x)
-      q[t] = (long long)rint(__ddiv_rn(sg[base + t], 1e-12));
-    __syncthreads();
-    if (i < M) {
-      for (int t = 0; t < cnt; ++t) {
-        const long long qt = q[t];
-        rank += (qt > qi) || (qt == qi && base + t < i);
-      }
-    }
+  long long* q = qbuf + s * (int64_t)M;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int kk = k < M ? k : M;
+  for (int i = tid; i < M; i += nt) q[i] = (long long)rint(__ddiv_rn(sg[i], 1e-12));
+  if (tid == 0) {
+    prefix = 0ull;
+    remaining = kk - 1;  // 0-based rank of the k-th largest
   }
-  if (i < M && rank < k) atomicAdd(&counts[s * (M / a_m) + i / a_m], 1);
+  __syncthreads();
+  // radix select of the kk-th largest q (keys are >= 0: unsigned order = value order)
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += nt) hist[i] = 0u;
+    __syncthreads();
+    const unsigned long long pre = prefix;
+    const unsigned long long mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (int i = tid; i < M; i += nt) {
+      const unsigned long long v = (unsigned long long)q[i];
+      if ((v & mask) == pre) atomicAdd(&hist[255u - ((v >> shift) & 255u)], 1u);  // descending
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int r = remaining;
+      unsigned d = 0;
+      while (d < 255 && r >= (int)hist[d]) {
+        r -= (int)hist[d];
+        ++d;
+      }
+      remaining = r;
+      prefix = pre | ((unsigned long long)(255u - d) << shift);
+    }
+    __syncthreads();
+  }
+  const long long qs = (long long)prefix;
+  const int need_eq = remaining + 1;  // keys equal to q* that are chosen (lowest indices)
+  // scan of equality flags in index order; per-thread contiguous chunks
+  const int per = (M + nt - 1) / nt;
+  const int lo = min(M, tid * per), hi = min(M, lo + per);
+  int local = 0;
+  for (int i = lo; i < hi; ++i) local += q[i] == qs;
+  const int lane = tid & 31, w = tid >> 5;
+  int x = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < (nt >> 5) ? warp_sum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    warp_sum[lane] = v;
+  }
+  __syncthreads();
+  int run = (w ? warp_sum[w - 1] : 0) + x - local;  // equal keys before this chunk
+  (void)carry;
+  int32_t* cnt = counts + s * (int64_t)(M / a_m);
+  for (int i = lo; i < hi; ++i) {
+    bool chosen = false;
+    if (q[i] > qs) {
+      chosen = true;
+    } else if (q[i] == qs) {
+      chosen = run < need_eq;
+      ++run;
+    }
+    if (chosen && kk > 0) atomicAdd(&cnt[i / a_m], 1);
+  }
 }
 
 // ------------------------------------------------------------------ solve
 
+// dt2 locate with one warp per bucket (oneshot.py:182-198): lane 0 solves the
+// moment coefficients, the lanes split the n/b grid candidates, and a butterfly
+// merge of per-lane sorted lists keeps the `take` smallest |P| under (|P|, j) —
+// exactly the stable argsort's first `take`.  cands[e][0..4) sorted; ncand[e] =
+// count, 0 for an empty bucket, -1 for None.
+constexpr int kDt2LocateThreads = 256;
+
+__global__ void __launch_bounds__(kDt2LocateThreads) dt2_locate_warp_kernel(
+    int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
+    const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
+    int64_t b, int64_t n, int64_t* __restrict__ cands, int32_t* __restrict__ ncand) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= total) return;
+  int a = counts[e];
+  if (a_cap > 0 && a > a_cap) a = a_cap;
+  if (a <= 0) {
+    if (lane == 0) ncand[e] = 0;
+    return;
+  }
+  const int64_t s = e / nrows;
+  const int64_t bucket = bucket_ids ? bucket_ids[e] : e - s * nrows;
+  la::c2 coeffs[dt::kMaxAm];
+  int ok = 0;
+  if (lane == 0) {
+    dt::Moments M{reinterpret_cast<const la::c2*>(meas) + e * R, a_m};
+    ok = dt::moment_coeffs(M, a, coeffs);
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (!ok) {
+    if (lane == 0) ncand[e] = -1;
+    return;
+  }
+  for (int k = 0; k < a; ++k) {
+    coeffs[k].re = __shfl_sync(0xffffffffu, coeffs[k].re, 0);
+    coeffs[k].im = __shfl_sync(0xffffffffu, coeffs[k].im, 0);
+  }
+  const int64_t step = n / b;
+  const int take = (int64_t)a < step ? a : (int)step;
+  constexpr int64_t kNone = INT64_MAX;
+  double bv[dt::kMaxAm];
+  int64_t bj[dt::kMaxAm];
+#pragma unroll
+  for (int i = 0; i < dt::kMaxAm; ++i) {
+    bv[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    bj[i] = kNone;
+  }
+  for (int64_t j = lane; j < step; j += 32) {
+    const double v = dt::poly_abs_at(coeffs, a, dt::pmod(bucket + b * j, n), n);
+    // j ascends within a lane: strict < keeps the earlier j among equal values
+    if (v < bv[take - 1] || bj[take - 1] == kNone) {
+      int i = take - 1;
+      while (i > 0 && (bv[i - 1] > v || bj[i - 1] == kNone)) {
+        bv[i] = bv[i - 1];
+        bj[i] = bj[i - 1];
+        --i;
+      }
+      bv[i] = v;
+      bj[i] = j;
+    }
+  }
+  // butterfly merge of sorted (value, j) lists; lists of different lanes are disjoint
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov[dt::kMaxAm];
+    int64_t oj[dt::kMaxAm];
+#pragma unroll
+    for (int i = 0; i < dt::kMaxAm; ++i) {
+      ov[i] = __shfl_xor_sync(0xffffffffu, bv[i], o);
+      oj[i] = __shfl_xor_sync(0xffffffffu, bj[i], o);
+    }
+    double mv[dt::kMaxAm];
+    int64_t mj[dt::kMaxAm];
+    int x = 0, y = 0;
+#pragma unroll
+    for (int i = 0; i < dt::kMaxAm; ++i) {
+      if (i >= take) break;
+      // (value, j) lexicographic; an empty slot (j = kNone) sorts last
+      const bool left = oj[y] == kNone ||
+                        (bj[x] != kNone && (bv[x] < ov[y] || (bv[x] == ov[y] && bj[x] < oj[y])));
+      if (left) {
+        mv[i] = bv[x];
+        mj[i] = bj[x];
+        ++x;
+      } else {
+        mv[i] = ov[y];
+        mj[i] = oj[y];
+        ++y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < dt::kMaxAm; ++i)
+      if (i < take) {
+        bv[i] = mv[i];
+        bj[i] = mj[i];
+      }
+  }
+  if (lane == 0) {
+    int64_t pos[dt::kMaxAm];
+    int have = 0;
+    for (int i = 0; i < take; ++i)
+      if (bj[i] != kNone) pos[have++] = dt::pmod(bucket + b * bj[i], n);
+    have = dt::sort_unique(pos, have);
+    for (int i = 0; i < have; ++i) cands[e * dt::kMaxAm + i] = pos[i];
+    ncand[e] = have;
+  }
+}
+
+// Per-bucket solve, one thread per bucket.  kLocated: candidates come from a
+// previous locate kernel (dt2's warp enumeration); else locate runs here (dt1/dt3).
+template <bool kLocated>
 __global__ void __launch_bounds__(kDtSolveThreads, 4) dt_solve_kernel(
     int64_t batch, int64_t nrows, int R, int a_m, int p, const double* __restrict__ meas,
     const int64_t* __restrict__ rshifts, const int32_t* __restrict__ counts,
     const int64_t* __restrict__ bucket_ids, int variant, int a_cap, int64_t b, int64_t n,
+    const int64_t* __restrict__ cands, const int32_t* __restrict__ ncand,
     int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_cnt) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= batch * nrows) return;
@@ -85,7 +257,14 @@ __global__ void __launch_bounds__(kDtSolveThreads, 4) dt_solve_kernel(
     const la::c2* row = reinterpret_cast<const la::c2*>(meas) + e * R;
     int64_t pos[dt::kMaxAm];
     la::c2 val[dt::kMaxAm];
-    cnt = dt::solve_bucket(row, a_m, p, rshifts + s * p, a, variant, bucket, b, n, pos, val);
+    if (kLocated) {
+      int64_t c[dt::kMaxAm];
+      const int nc = ncand[e];
+      for (int i = 0; i < nc; ++i) c[i] = cands[e * dt::kMaxAm + i];
+      cnt = dt::estimate_bucket(row, a_m, p, rshifts + s * p, c, nc, b, n, pos, val);
+    } else {
+      cnt = dt::solve_bucket(row, a_m, p, rshifts + s * p, a, variant, bucket, b, n, pos, val);
+    }
     for (int i = 0; i < cnt; ++i) {
       out_pos[e * a_m + i] = pos[i];
       reinterpret_cast<la::c2*>(out_val)[e * a_m + i] = val[i];
@@ -96,52 +275,74 @@ __global__ void __launch_bounds__(kDtSolveThreads, 4) dt_solve_kernel(
 
 // ------------------------------------------------------------------ truncate
 
-// Compact the per-bucket entries of each signal (bucket order) and keep the k
-// largest by (-|v|, f).  One CTA per signal.
-__global__ void dt_truncate_kernel(int64_t nrows, int a_m, int k, const int64_t* __restrict__ pos,
-                                   const double* __restrict__ val,
-                                   const int32_t* __restrict__ cnt, int cap,
-                                   int64_t* __restrict__ all_pos, double* __restrict__ all_val,
-                                   int32_t* __restrict__ all_count, int64_t* __restrict__ out_pos,
-                                   double* __restrict__ out_val, int32_t* __restrict__ out_count,
-                                   double* gscratch) {
+// Compact the per-bucket entries of each signal (bucket order, block scan over the
+// per-row counts) and keep the k largest by (-|v|, f) with a bitonic sort — in
+// shared memory when it fits, else in a global scratch.  One CTA per signal.
+__global__ void __launch_bounds__(1024) dt_truncate_kernel(
+    int64_t nrows, int a_m, int k, const int64_t* __restrict__ pos,
+    const double* __restrict__ val, const int32_t* __restrict__ cnt, int cap,
+    int64_t* __restrict__ all_pos, double* __restrict__ all_val, int32_t* __restrict__ all_count,
+    int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_count,
+    unsigned char* gscratch, size_t scratch_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* mag = gscratch ? gscratch + blockIdx.x * (int64_t)cap
-                         : reinterpret_cast<double*>(smem_raw);
-  __shared__ int total;
+  __shared__ int warp_sum[32];
   const int64_t s = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
   const int32_t* c = cnt + s * nrows;
   int64_t* ap = all_pos + s * (int64_t)cap;
   la::c2* av = reinterpret_cast<la::c2*>(all_val) + s * (int64_t)cap;
-  if (threadIdx.x == 0) {
-    int m = 0;
-    for (int64_t r = 0; r < nrows; ++r) {
-      for (int i = 0; i < c[r]; ++i) {
-        const int64_t src = (s * nrows + r) * a_m + i;
-        ap[m] = pos[src];
-        av[m] = reinterpret_cast<const la::c2*>(val)[src];
-        ++m;
-      }
+  // exclusive scan of the row counts (contiguous chunk per thread)
+  const int64_t per = (nrows + nt - 1) / nt;
+  const int64_t lo = min(nrows, tid * per), hi = min(nrows, lo + per);
+  int local = 0;
+  for (int64_t r = lo; r < hi; ++r) local += c[r];
+  int x = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < (nt >> 5) ? warp_sum[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
     }
-    total = m;
-    all_count[s] = m;
+    warp_sum[lane] = v;
   }
   __syncthreads();
-  const int m = total;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) mag[i] = la::cabs(av[i]);
+  int off = (w ? warp_sum[w - 1] : 0) + x - local;
+  const int m = warp_sum[31];
+  for (int64_t r = lo; r < hi; ++r) {
+    for (int i = 0; i < c[r]; ++i) {
+      const int64_t src = (s * nrows + r) * a_m + i;
+      ap[off] = pos[src];
+      av[off] = reinterpret_cast<const la::c2*>(val)[src];
+      ++off;
+    }
+  }
+  if (tid == 0) all_count[s] = m;
   __syncthreads();
+  int pow2 = 1;
+  while (pow2 < m) pow2 <<= 1;
+  unsigned char* mem = gscratch ? gscratch + s * scratch_bytes : smem_raw;
+  double* key = reinterpret_cast<double*>(mem);
+  int64_t* kpos = reinterpret_cast<int64_t*>(key + pow2);
+  int32_t* kidx = reinterpret_cast<int32_t*>(kpos + pow2);
+  for (int i = tid; i < m; i += nt) {
+    key[i] = la::cabs(av[i]);
+    kpos[i] = ap[i];
+    kidx[i] = i;
+  }
+  bitonic_trunc_sort(key, kpos, kidx, m, pow2);
   la::c2* ov = reinterpret_cast<la::c2*>(out_val) + s * k;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const double a = mag[i];
-    const int64_t f = ap[i];
-    int rank = 0;
-    for (int j = 0; j < m; ++j) rank += (mag[j] > a) || (mag[j] == a && ap[j] < f);
-    if (rank < k) {
-      out_pos[s * k + rank] = f;
-      ov[rank] = av[i];
-    }
+  const int kept = m < k ? m : k;
+  for (int r = tid; r < kept; r += nt) {
+    out_pos[s * k + r] = kpos[r];
+    ov[r] = av[kidx[r]];
   }
-  if (threadIdx.x == 0) out_count[s] = m < k ? m : k;
+  if (tid == 0) out_count[s] = kept;
 }
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -233,8 +434,11 @@ extern "C" int afft_dt_detect(const double* rows, int64_t batch, int64_t nrows, 
     set_error("afft_dt_detect: too many keys");
     return AFFT_EUNSUPPORTED;
   }
-  dim3 grid((unsigned)((M + 255) / 256), (unsigned)batch);
-  dt_vote_kernel<<<grid, 256, 2048 * 8, st>>>((int)M, a_m, k, sigmas, counts);
+  long long* qbuf = nullptr;
+  e = scratch_alloc(reinterpret_cast<void**>(&qbuf), (size_t)batch * M * 8, st);
+  if (e != cudaSuccess) return cuda_status(e, "scratch (vote keys)");
+  dt_vote_kernel<<<(unsigned)batch, kVoteThreads, 0, st>>>((int)M, a_m, k, sigmas, counts, qbuf);
+  scratch_free(qbuf, st);
   AFFT_CHECK_LAUNCH("dt_vote_kernel");
   return AFFT_OK;
 }
@@ -252,10 +456,28 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
     return AFFT_EINVAL;
   }
   const int64_t total = batch * nrows;
-  dt_solve_kernel<<<(unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads), kDtSolveThreads,
-                    0, (cudaStream_t)stream>>>(batch, nrows, 3 * a_m + p, a_m, p, rows,
-                                               rand_shifts, counts, bucket_ids, variant, a_cap, b,
-                                               n, out_pos, out_val, out_cnt);
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads);
+  if (variant == dt::VAR_DT2) {
+    int64_t* cands = nullptr;
+    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands),
+                                  (size_t)total * (dt::kMaxAm * 8 + 4), st);
+    if (e != cudaSuccess) return cuda_status(e, "scratch (dt2 candidates)");
+    int32_t* ncand = reinterpret_cast<int32_t*>(cands + total * dt::kMaxAm);
+    const int64_t threads = total * 32;
+    dt2_locate_warp_kernel<<<(unsigned)((threads + kDt2LocateThreads - 1) / kDt2LocateThreads),
+                             kDt2LocateThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
+                                                         counts, bucket_ids, a_cap, b, n, cands,
+                                                         ncand);
+    dt_solve_kernel<true><<<grid, kDtSolveThreads, 0, st>>>(
+        batch, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, counts, bucket_ids, variant, a_cap,
+        b, n, cands, ncand, out_pos, out_val, out_cnt);
+    scratch_free(cands, st);
+  } else {
+    dt_solve_kernel<false><<<grid, kDtSolveThreads, 0, st>>>(
+        batch, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, counts, bucket_ids, variant, a_cap,
+        b, n, nullptr, nullptr, out_pos, out_val, out_cnt);
+  }
   AFFT_CHECK_LAUNCH("dt_solve_kernel");
   return AFFT_OK;
 }
@@ -272,12 +494,14 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
     set_error("afft_dt_truncate: bad arguments");
     return AFFT_EINVAL;
   }
-  size_t smem = (size_t)std::max<int64_t>(cap, 1) * 8;
-  double* scratch = nullptr;
+  int64_t pow2 = 1;
+  while (pow2 < std::max<int64_t>(cap, 1)) pow2 <<= 1;
+  const size_t need = ((size_t)pow2 * 20 + 255) / 256 * 256;
+  size_t smem = need;
+  unsigned char* scratch = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  if (smem > 200 * 1024) {  // many buckets: magnitudes in global memory
-    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch),
-                                    (size_t)batch * cap * 8, st);
+  if (smem > 200 * 1024) {  // many buckets: bitonic sort in global memory
+    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch), (size_t)batch * need, st);
     if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(dt_truncate scratch)");
     smem = 0;
   } else {
@@ -287,7 +511,7 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
   }
   dt_truncate_kernel<<<(unsigned)batch, 1024, smem, st>>>(
       nrows, a_m, k, pos, val, cnt, (int)cap, all_pos, all_val, all_count, out_pos, out_val,
-      out_count, scratch);
+      out_count, scratch, need);
   if (scratch) scratch_free(scratch, st);
   AFFT_CHECK_LAUNCH("dt_truncate_kernel");
   return AFFT_OK;

@@ -138,6 +138,34 @@ __host__ __device__ inline int pencil_roots(const Moments& M, int a, c2* roots) 
   return rank;
 }
 
+// Prony coefficients of the a-tone moment recursion (oneshot.py:182-188): the a x a
+// Hankel lstsq H c = -m[a..2a).  False when a coefficient is not finite (-> None).
+__host__ __device__ inline bool moment_coeffs(const Moments& M, int a, c2* coeffs) {
+  M4 H;
+  H.m = H.n = a;
+  c2 rhs[kMaxAm];
+  for (int r = 0; r < a; ++r) {
+    for (int c = 0; c < a; ++c) H.at(r, c) = M.m(r + c);
+    const c2 v = M.m(a + r);
+    rhs[r] = la::C(-v.re, -v.im);
+  }
+  la::lstsq(H, rhs, coeffs, nullptr);
+  for (int i = 0; i < a; ++i)
+    if (!la::finite(coeffs[i])) return false;
+  return true;
+}
+
+// |P(w^cand)| for the dt2 grid enumeration (oneshot.py:193-198), Horner from the
+// leading 1.
+__host__ __device__ __forceinline__ double poly_abs_at(const c2* coeffs, int a, int64_t cand,
+                                                       int64_t n) {
+  const c2 z = unit_root_(cand, n);
+  c2 y = la::C(0.0);
+  y = la::add(la::mul(y, z), la::C(1.0));
+  for (int k = a - 1; k >= 0; --k) y = la::add(la::mul(y, z), coeffs[k]);
+  return la::cabs(y);
+}
+
 // locate (oneshot.py:161-200).  Returns the number of candidate positions
 // (sorted, unique), or -1 for "None" (degenerate bucket).
 __host__ __device__ inline int locate(const Moments& M, int a, int variant, int64_t bucket,
@@ -151,17 +179,8 @@ __host__ __device__ inline int locate(const Moments& M, int a, int variant, int6
     for (int i = 0; i < nr; ++i) pos[i] = snap_to_grid(roots[i], bucket, b, n);
     return sort_unique(pos, nr);
   }
-  M4 H;
-  H.m = H.n = a;
-  c2 rhs[kMaxAm], coeffs[kMaxAm];
-  for (int r = 0; r < a; ++r) {
-    for (int c = 0; c < a; ++c) H.at(r, c) = M.m(r + c);
-    const c2 v = M.m(a + r);
-    rhs[r] = la::C(-v.re, -v.im);
-  }
-  la::lstsq(H, rhs, coeffs, nullptr);
-  for (int i = 0; i < a; ++i)
-    if (!la::finite(coeffs[i])) return -1;
+  c2 coeffs[kMaxAm];
+  if (!moment_coeffs(M, a, coeffs)) return -1;
   if (variant == VAR_DT1) {
     const int nr = la::poly_roots(coeffs, a, roots);
     for (int i = 0; i < nr; ++i) pos[i] = snap_to_grid(roots[i], bucket, b, n);
@@ -173,12 +192,7 @@ __host__ __device__ inline int locate(const Moments& M, int a, int variant, int6
   int64_t bj[kMaxAm];
   int have = 0;
   for (int64_t j = 0; j < step; ++j) {
-    const int64_t cand = pmod(bucket + b * j, n);
-    const c2 z = unit_root_(cand, n);
-    c2 y = la::C(0.0);
-    y = la::add(la::mul(y, z), la::C(1.0));
-    for (int k = a - 1; k >= 0; --k) y = la::add(la::mul(y, z), coeffs[k]);
-    const double v = la::cabs(y);
+    const double v = poly_abs_at(coeffs, a, pmod(bucket + b * j, n), n);
     // insert into the sorted top-`take` list; equal values keep the earlier j
     if (have < take || v < best[have - 1]) {
       int i = have < take ? have++ : have - 1;
@@ -325,6 +339,15 @@ __host__ __device__ inline int estimate_values(const c2* rand, const int64_t* sh
     out_val[i] = best_coef[i];
   }
   return want;
+}
+
+// One bucket's estimate step given located candidates (nc < 0 = None).
+__host__ __device__ inline int estimate_bucket(const c2* row, int a_m, int P,
+                                               const int64_t* rshifts, const int64_t* cands,
+                                               int nc, int64_t b, int64_t n, int64_t* out_pos,
+                                               c2* out_val) {
+  if (nc < 0) return 0;
+  return estimate_values(row + 3 * a_m, rshifts, P, cands, nc, b, n, out_pos, out_val);
 }
 
 // One bucket of sfft_dt's main loop (oneshot.py:279-288): locate then estimate.
