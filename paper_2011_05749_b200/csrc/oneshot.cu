@@ -16,6 +16,7 @@
 #include <cstring>
 
 #include "afft_common.cuh"
+#include "dt_warp.cuh"
 #include "oneshot_core.cuh"
 #include "peel_core.cuh"
 
@@ -237,40 +238,63 @@ __global__ void __launch_bounds__(kDt2LocateThreads) dt2_locate_warp_kernel(
   }
 }
 
-// Per-bucket solve, one thread per bucket.  kLocated: candidates come from a
-// previous locate kernel (dt2's warp enumeration); else locate runs here (dt1/dt3).
-template <bool kLocated>
-__global__ void __launch_bounds__(kDtSolveThreads, 4) dt_solve_kernel(
-    int64_t batch, int64_t nrows, int R, int a_m, int p, const double* __restrict__ meas,
-    const int64_t* __restrict__ rshifts, const int32_t* __restrict__ counts,
-    const int64_t* __restrict__ bucket_ids, int variant, int a_cap, int64_t b, int64_t n,
-    const int64_t* __restrict__ cands, const int32_t* __restrict__ ncand,
-    int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_cnt) {
+// dt1 / dt3 locate (oneshot.py:161-191), one thread per bucket: ncand[e] = count,
+// 0 for an empty bucket, -1 for None.
+__global__ void __launch_bounds__(kDtSolveThreads) dt_locate_rows_kernel(
+    int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
+    const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
+    int variant, int64_t b, int64_t n, int64_t* __restrict__ cands, int32_t* __restrict__ ncand) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= batch * nrows) return;
-  const int64_t s = e / nrows;
+  if (e >= total) return;
   int a = counts[e];
   if (a_cap > 0 && a > a_cap) a = a_cap;  // dsfft.py:219 caps at a_m
-  int cnt = 0;
-  if (a > 0) {
-    const int64_t bucket = bucket_ids ? bucket_ids[e] : e - s * nrows;
-    const la::c2* row = reinterpret_cast<const la::c2*>(meas) + e * R;
-    int64_t pos[dt::kMaxAm];
-    la::c2 val[dt::kMaxAm];
-    if (kLocated) {
-      int64_t c[dt::kMaxAm];
-      const int nc = ncand[e];
-      for (int i = 0; i < nc; ++i) c[i] = cands[e * dt::kMaxAm + i];
-      cnt = dt::estimate_bucket(row, a_m, p, rshifts + s * p, c, nc, b, n, pos, val);
-    } else {
-      cnt = dt::solve_bucket(row, a_m, p, rshifts + s * p, a, variant, bucket, b, n, pos, val);
-    }
-    for (int i = 0; i < cnt; ++i) {
-      out_pos[e * a_m + i] = pos[i];
-      reinterpret_cast<la::c2*>(out_val)[e * a_m + i] = val[i];
-    }
+  if (a <= 0) {
+    ncand[e] = 0;
+    return;
   }
-  out_cnt[e] = cnt;
+  const int64_t s = e / nrows;
+  const int64_t bucket = bucket_ids ? bucket_ids[e] : e - s * nrows;
+  dt::Moments M{reinterpret_cast<const la::c2*>(meas) + e * R, a_m};
+  int64_t pos[5];
+  const int c = dt::locate(M, a, variant, bucket, b, n, pos);
+  for (int k = 0; k < c && k < dt::kMaxAm; ++k) cands[e * dt::kMaxAm + k] = pos[k];
+  ncand[e] = c;
+}
+
+// estimate_values for every row, one warp per row (dt_warp.cuh).  Row e belongs
+// to signal e / nrows, whose random shifts start at rshifts + signal * shift_stride.
+constexpr int kDtEstWarps = 4;
+
+__global__ void __launch_bounds__(kDtEstWarps * 32) dt_estimate_warp_kernel(
+    int64_t total, int64_t nrows, int R, int a_m, int p, const double* __restrict__ meas,
+    const int64_t* __restrict__ rshifts, int64_t shift_stride, const int64_t* __restrict__ cands,
+    const int32_t* __restrict__ ncand, int64_t b, int64_t n, int out_stride,
+    int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_cnt) {
+  __shared__ dtw::WarpPursuit pursuit[kDtEstWarps];
+  __shared__ int64_t cand_s[kDtEstWarps][dt::kMaxAm];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * kDtEstWarps + wid;
+  if (e >= total) return;
+  int nc = 0;
+  if (lane == 0) {
+    nc = ncand[e];
+    if (nc > dt::kMaxAm) nc = dt::kMaxAm;
+    int64_t c[dt::kMaxAm];
+    for (int k = 0; k < nc; ++k) c[k] = cands[e * dt::kMaxAm + k];
+    if (nc > 0) nc = dt::sort_unique(c, nc);
+    for (int k = 0; k < nc; ++k) cand_s[wid][k] = c[k];
+  }
+  nc = __shfl_sync(0xffffffffu, nc, 0);
+  __syncwarp();
+  int cnt = 0;
+  if (nc > 0) {
+    const int64_t s = e / nrows;
+    const la::c2* row = reinterpret_cast<const la::c2*>(meas) + e * R;
+    cnt = dtw::warp_estimate(pursuit[wid], row + 3 * a_m, rshifts + s * shift_stride, p,
+                             cand_s[wid], nc, b, n, out_pos + e * out_stride,
+                             reinterpret_cast<la::c2*>(out_val) + e * out_stride);
+  }
+  if (lane == 0) out_cnt[e] = cnt;
 }
 
 // ------------------------------------------------------------------ truncate
@@ -457,28 +481,29 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
   }
   const int64_t total = batch * nrows;
   cudaStream_t st = (cudaStream_t)stream;
-  const unsigned grid = (unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads);
+  int64_t* cands = nullptr;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands),
+                                (size_t)total * (dt::kMaxAm * 8 + 4), st);
+  if (e != cudaSuccess) return cuda_status(e, "scratch (dt candidates)");
+  int32_t* ncand = reinterpret_cast<int32_t*>(cands + total * dt::kMaxAm);
   if (variant == dt::VAR_DT2) {
-    int64_t* cands = nullptr;
-    cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands),
-                                  (size_t)total * (dt::kMaxAm * 8 + 4), st);
-    if (e != cudaSuccess) return cuda_status(e, "scratch (dt2 candidates)");
-    int32_t* ncand = reinterpret_cast<int32_t*>(cands + total * dt::kMaxAm);
     const int64_t threads = total * 32;
     dt2_locate_warp_kernel<<<(unsigned)((threads + kDt2LocateThreads - 1) / kDt2LocateThreads),
                              kDt2LocateThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
                                                          counts, bucket_ids, a_cap, b, n, cands,
                                                          ncand);
-    dt_solve_kernel<true><<<grid, kDtSolveThreads, 0, st>>>(
-        batch, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, counts, bucket_ids, variant, a_cap,
-        b, n, cands, ncand, out_pos, out_val, out_cnt);
-    scratch_free(cands, st);
   } else {
-    dt_solve_kernel<false><<<grid, kDtSolveThreads, 0, st>>>(
-        batch, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, counts, bucket_ids, variant, a_cap,
-        b, n, nullptr, nullptr, out_pos, out_val, out_cnt);
+    dt_locate_rows_kernel<<<(unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads),
+                            kDtSolveThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
+                                                      counts, bucket_ids, a_cap, variant, b, n,
+                                                      cands, ncand);
   }
-  AFFT_CHECK_LAUNCH("dt_solve_kernel");
+  dt_estimate_warp_kernel<<<(unsigned)((total + kDtEstWarps - 1) / kDtEstWarps),
+                            kDtEstWarps * 32, 0, st>>>(total, nrows, 3 * a_m + p, a_m, p, rows,
+                                                       rand_shifts, p, cands, ncand, b, n, a_m,
+                                                       out_pos, out_val, out_cnt);
+  scratch_free(cands, st);
+  AFFT_CHECK_LAUNCH("dt_estimate_warp_kernel");
   return AFFT_OK;
 }
 
@@ -571,30 +596,6 @@ __global__ void dt_locate_kernel(int64_t count, int R, int a_m, const double* __
   out_n[i] = c;
 }
 
-// estimate_values (oneshot.py:203-257) for `count` rows given their candidates.
-__global__ void dt_estimate_kernel(int64_t count, int R, int a_m, int p,
-                                   const double* __restrict__ rows,
-                                   const int64_t* __restrict__ rshifts,
-                                   const int64_t* __restrict__ cands,
-                                   const int32_t* __restrict__ ncand, int64_t b, int64_t n,
-                                   int64_t* __restrict__ out_pos, double* __restrict__ out_val,
-                                   int32_t* __restrict__ out_n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  int64_t c[dt::kMaxAm];
-  int nc = 0;
-  for (int k = 0; k < ncand[i] && k < dt::kMaxAm; ++k) c[nc++] = cands[i * dt::kMaxAm + k];
-  nc = dt::sort_unique(c, nc);
-  int64_t pos[dt::kMaxAm];
-  la::c2 val[dt::kMaxAm];
-  const la::c2* row = reinterpret_cast<const la::c2*>(rows) + i * R;
-  const int m = dt::estimate_values(row + 3 * a_m, rshifts, p, c, nc, b, n, pos, val);
-  for (int k = 0; k < m; ++k) {
-    out_pos[i * dt::kMaxAm + k] = pos[k];
-    reinterpret_cast<la::c2*>(out_val)[i * dt::kMaxAm + k] = val[k];
-  }
-  out_n[i] = m;
-}
 }  // namespace afft
 
 extern "C" int afft_dt_locate(const double* rows, int64_t count, int32_t R, int32_t a_m,
@@ -624,8 +625,10 @@ extern "C" int afft_dt_estimate(const double* rows, const int64_t* rand_shifts, 
     set_error("afft_dt_estimate: bad arguments");
     return AFFT_EINVAL;
   }
-  dt_estimate_kernel<<<(unsigned)((count + 63) / 64), 64, 0, (cudaStream_t)stream>>>(
-      count, 3 * a_m + p, a_m, p, rows, rand_shifts, cands, ncand, b, n, out_pos, out_val, out_n);
-  AFFT_CHECK_LAUNCH("dt_estimate_kernel");
+  dt_estimate_warp_kernel<<<(unsigned)((count + kDtEstWarps - 1) / kDtEstWarps),
+                            kDtEstWarps * 32, 0, (cudaStream_t)stream>>>(
+      count, count, 3 * a_m + p, a_m, p, rows, rand_shifts, 0, cands, ncand, b, n, dt::kMaxAm,
+      out_pos, out_val, out_n);
+  AFFT_CHECK_LAUNCH("dt_estimate_warp_kernel");
   return AFFT_OK;
 }
