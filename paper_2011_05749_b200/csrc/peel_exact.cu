@@ -119,6 +119,8 @@ struct FusedParams {
   int32_t* unresolved;
   double* eps_out;       // may be null
   const double* eps_in;  // may be null: precomputed thresholds (small batches)
+  int order_mode;        // fused kernel: 0 stream first, 1 alternate by CTA, 2 DFTs first
+  const unsigned* ready; // split-role kernel: ready[s] != 0 once eps_in[s] is published
   int rec_in_smem;       // 1: recovered list in shared memory (no all_pos output)
 };
 
@@ -140,6 +142,15 @@ __device__ __forceinline__ double2 ld_na(const double2* p) {
                : "=d"(v.x), "=d"(v.y)
                : "l"(p));
   return v;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Per-thread partial of sum |x|^2 over one signal: 16-byte streaming loads,
@@ -220,10 +231,15 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
 
   // 1. exact_thresholds: eps = 1e-6 * ||x|| / sqrt(n), fixed-order block reduction
   //    (skipped when a multi-CTA pre-pass already produced eps for a small batch)
-  double acc = (!kStream || p.eps_in) ? 0.0 : stream_sumsq(row, p.dtype, n);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((tid & 31) == 0) wsum[tid >> 5] = acc;
+  //    By default (order_mode 2) the stream runs after the gather + DFTs and before
+  //    the peeling, splitting the latency-bound decode around it: CTAs of one wave
+  //    otherwise stream together and then all decode at the same moment, leaving HBM
+  //    idle.  Measured at config 5 (tools/fused_order.py, 8192 signals, 15 reps x 5):
+  //    stream first 20.47 ms, alternating by CTA 20.48 ms, DFTs first 20.26 ms.
+  const bool do_stream = kStream && !p.eps_in;
+  const bool stream_first =
+      p.order_mode == 0 || (p.order_mode == 1 && (blockIdx.x & 1) == 0);
+  double acc = (do_stream && stream_first) ? stream_sumsq(row, p.dtype, n) : 0.0;
   // 2. build_graph: gather + DFT of every cycle at shifts (0, 1, 2), node layout
   cd* tw = reinterpret_cast<cd*>(smem_raw + p.dft_off);
   for (int c = 0; c < G.ncycles; ++c) {
@@ -239,9 +255,20 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
     }
     __syncthreads();
   }
+  if (do_stream && !stream_first) acc = stream_sumsq(row, p.dtype, n);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) wsum[tid >> 5] = acc;
+  __syncthreads();
+  if (p.ready) {  // split-role kernel: wait for the streaming CTA that owns signal s
+    if (tid == 0)
+      while (ld_acquire_u32(p.ready + s) == 0u) __nanosleep(128);
+    __syncthreads();
+  }
   double t = 0.0;
   for (int w = 0; w < kFusedThreads / 32; ++w) t += wsum[w];
-  const double eps = (!kStream || p.eps_in) ? p.eps_in[s] : (1e-6 * sqrt(t)) / sqrt((double)n);
+  const double eps =
+      (!kStream || p.eps_in) ? __ldcg(p.eps_in + s) : (1e-6 * sqrt(t)) / sqrt((double)n);
   // 3. graph state
   for (int g = tid; g < N; g += nt) {
     M.st[g] = AFFT_UNKNOWN;
@@ -301,6 +328,49 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
   __shared__ double wsum[kFusedThreads / 32];
   for (int64_t s = blockIdx.x; s < batch; s += gridDim.x) {
     ffast_one_signal<true>(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
+    __syncthreads();
+  }
+}
+
+// Split roles (mode 3, selectable; slower at config 5): a persistent, co-resident grid
+// whose first n_stream CTAs (two per SM) only stream |x|^2 and publish each
+// signal's eps with a release flag, while the remaining CTAs (one per SM) decode
+// signals in order — gather + DFTs first, then an acquire wait on the flag, then
+// peeling.  The fused kernel's CTAs alternate stream and decode phases and tend
+// to fall into step, leaving HBM idle while whole waves decode; here HBM is fed
+// by the streaming CTAs continuously and the decode runs beside them.
+__global__ void __launch_bounds__(kFusedThreads, 3) ffast_split_kernel(
+    const __grid_constant__ FusedParams p, int64_t batch, int n_stream, double* eps_buf,
+    unsigned* ready) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tmp[32];
+  __shared__ int carry, red;
+  __shared__ double wsum[kFusedThreads / 32];
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x < n_stream) {
+    const int64_t n = p.G.n;
+    const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
+    for (int64_t s = blockIdx.x; s < batch; s += n_stream) {
+      const char* row = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
+      double acc = stream_sumsq(row, p.dtype, n);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if ((tid & 31) == 0) wsum[tid >> 5] = acc;
+      __syncthreads();
+      if (tid == 0) {  // same fixed-order reduction as the fused kernel
+        double t = 0.0;
+        for (int w = 0; w < kFusedThreads / 32; ++w) t += wsum[w];
+        eps_buf[s] = (1e-6 * sqrt(t)) / sqrt((double)n);
+        if (p.eps_out) p.eps_out[s] = eps_buf[s];
+        st_release_u32(ready + s, 1u);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const int nd = gridDim.x - n_stream;
+  for (int64_t s = (int)blockIdx.x - n_stream; s < batch; s += nd) {
+    ffast_one_signal<false>(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
     __syncthreads();
   }
 }
@@ -726,19 +796,39 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     fp.all_count = all_count;
     fp.rounds = rounds;
     fp.unresolved = unresolved;
+    {
+      const char* om = getenv("AFFT_FUSED_ORDER");
+      fp.order_mode = om && om[0] >= '0' && om[0] <= '2' ? om[0] - '0' : 2;
+    }
     // Small batches cannot keep HBM busy with one streaming CTA per signal: run the
     // |x|^2 pass as a multi-CTA partial sum first and feed eps to the fused decode.
     // Large batches (mode 2, the default there) pipeline it: the norm stream of
     // chunk c+1 runs on the caller's stream while chunk c decodes on an auxiliary
     // stream, so HBM never waits for the latency-bound decode.
     const int nparts = afft_sumsq_parts(n, dtype);
-    const char* env = getenv("AFFT_FFAST_MODE");  // 0 fused, 1 pre-pass, 2 pipelined
+    const char* env = getenv("AFFT_FFAST_MODE");  // 0 fused, 1 pre-pass, 2 pipelined, 3 split
     // Measured on B200 (tools/ffast_modes.py, config 5, 8192 signals): fused 20.44 ms,
-    // pipelined 20.96 ms, pre-pass + decode 22.25 ms, stream alone 18.65 ms.  Small
-    // batches (< 2 waves) cannot keep HBM busy with one streaming CTA per signal.
-    int mode = batch < 2 * 148 ? 1 : 0;
-    if (env && (env[0] == '0' || env[0] == '1' || env[0] == '2')) mode = env[0] - '0';
+    // pipelined 20.96 ms, split roles 22.5 ms (one decoding CTA per SM cannot keep
+    // up: ~0.2 ms per signal), pre-pass + decode 22.25 ms, stream alone 18.65 ms.
+    // Small batches (< 2 waves) cannot keep HBM busy with one streaming CTA per signal.
+    const int sms = num_sms();
+    int mode = batch < 2 * sms ? 1 : 0;
+    if (env && env[0] >= '0' && env[0] <= '3') mode = env[0] - '0';
     if (nparts < 2) mode = 0;
+    if (mode == 3) {
+      // the split roles spin-wait across CTAs: every CTA must be resident (cooperative
+      // launch below) with room for two streaming CTAs and one decoding CTA per SM
+      int per_sm = 0;
+      cudaError_t e = cudaFuncSetAttribute(ffast_split_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffast_split_kernel,
+                                                          kFusedThreads, smem);
+      if (e != cudaSuccess || per_sm < 3) {
+        cudaGetLastError();
+        mode = 0;
+      }
+    }
     double* partials = nullptr;
     double* epsbuf = nullptr;
     if (mode) {
@@ -795,6 +885,21 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
       }
       cudaEventRecord(A->join, A->aux);
       cudaStreamWaitEvent(st, A->join, 0);
+      return AFFT_OK;
+    }
+    if (mode == 3) {
+      unsigned* ready = reinterpret_cast<unsigned*>(partials);  // batch * 4 <= partials
+      cudaError_t e = cudaMemsetAsync(ready, 0, (size_t)batch * 4, st);
+      if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(ready flags)");
+      fp.eps_in = epsbuf;
+      fp.ready = ready;
+      int n_stream = 2 * sms;
+      unsigned grid = (unsigned)(3 * sms);
+      if (batch < n_stream) n_stream = (int)batch;
+      void* args[] = {&fp, &batch, &n_stream, &epsbuf, &ready};
+      e = cudaLaunchCooperativeKernel((const void*)ffast_split_kernel, grid, kFusedThreads, args,
+                                      smem, st);
+      if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(ffast_split)");
       return AFFT_OK;
     }
     if (mode == 1) {

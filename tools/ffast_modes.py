@@ -41,7 +41,7 @@ def main():
                      device=dev)
     res = ffast_batch(x, bench.K, bench.FACTORS, workspace=ws)
     out = {}
-    for mode in ("0", "1", "2"):
+    for mode in ("0", "1", "2", "3"):
         os.environ["AFFT_FFAST_MODE"] = mode
         out[mode] = t(lambda: ffast_batch(x, bench.K, bench.FACTORS, workspace=ws, out=res))
     import ctypes
@@ -50,7 +50,7 @@ def main():
     lib.afft_ffast_occupancy(bench.N_SIG, fb, nc, ctypes.byref(blk), ctypes.byref(sm))
     print(f"fused kernel: {blk.value} CTAs/SM, {sm.value} B dynamic smem")
     for rep in range(2):
-        for mode in ("0", "1", "2"):
+        for mode in ("0", "1", "2", "3"):
             os.environ["AFFT_FFAST_MODE"] = mode
             out[mode] = t(lambda: ffast_batch(x, bench.K, bench.FACTORS, workspace=ws, out=res))
         print(rep, {k: round(v, 3) for k, v in out.items()})
@@ -64,7 +64,8 @@ def main():
     gb = S * bench.SIGNAL_BYTES / 1e6
     print(f"signals {S}: norm alone {ms_norm:.3f} ms ({gb / ms_norm:.0f} GB/s); "
           f"fused(mode0) {out['0']:.3f}; prepass+decode(mode1) {out['1']:.3f} "
-          f"(decode ~{out['1'] - ms_norm:.3f}); pipelined(mode2) {out['2']:.3f} ms")
+          f"(decode ~{out['1'] - ms_norm:.3f}); pipelined(mode2) {out['2']:.3f} ms; "
+          f"split roles(mode3) {out['3']:.3f} ms")
 
 
 if __name__ == "__main__":
