@@ -363,12 +363,48 @@ def dense_fft_context(x, dev):
     b.record()
     torch.cuda.synchronize()
     gpu_ms = a.elapsed_time(b) / 3
+    # the same transform in float64 arithmetic: cuFFT c128 and this library's
+    # four-step K2' (afft_bucketize with b = N, tau = 0 — y = fft(x) / N)
+    from paper_2011_05749_b200 import _device, _lib
+
+    m2 = min(64, x.shape[0])
+    x2 = x[:m2]
+    x2c = x2.to(torch.complex128)
+    out2 = torch.empty((m2, N_SIG), dtype=torch.complex128, device=dev)
+    lib = _lib.load()
+    sb, ns = _lib.host_i64([0])
+
+    def run_c128():
+        out2.copy_(torch.fft.fft(x2c, dim=1))
+
+    def run_ours():
+        _lib.check(lib.afft_bucketize(x2.data_ptr(), _device.dtype_code(x2), N_SIG, m2, N_SIG, N_SIG,
+                                      sb, ns, out2.data_ptr(), N_SIG, N_SIG, 1,
+                                      _device.stream_ptr()), "bucketize(b=N)")
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    c128_ms = timed(run_c128)
+    ours_ms = timed(run_ours)
+    del x2c, out2
     host = x[0].cpu().numpy()
     t0 = time.perf_counter()
     for _ in range(3):
         np.fft.fft(host.astype(np.complex128))
     cpu_s = (time.perf_counter() - t0) / 3
     return {"dense_fft_gpu_signals_per_s": m / (gpu_ms * 1e-3), "dense_fft_gpu": "cuFFT c64 (torch.fft)",
+            "dense_fft_gpu_c128_signals_per_s": m2 / (c128_ms * 1e-3),
+            "dense_fft_ours_signals_per_s": m2 / (ours_ms * 1e-3),
+            "dense_fft_ours": "four-step K2' (afft_bucketize, b = N), c64 in, f64 compute, c128 out",
             "dense_fft_cpu_signals_per_s": 1.0 / cpu_s, "dense_fft_cpu": "numpy pocketfft c128, 1 core",
             "note": "context only; not part of the measured path"}
 

@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(256) gather_dft_kernel(const __grid_constant__
     __syncthreads();
     taus = s_tau;
   }
-  const cd* res = gather_dft_block(xs, p.dtype, p.n, b, p.plan[c], taus, cnt, tw, bufA, bufB);
+  const cd* res =
+      gather_dft_block<16>(xs, p.dtype, p.n, b, p.plan[c], taus, cnt, tw, bufA, bufB);
   const double inv_b = 1.0 / (double)b;
   double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset[c]);
   const int total = cnt * (int)b;
@@ -87,81 +88,126 @@ struct FourStepParams {
   int dtype;
   int64_t n, ld, b, b1, b2;
   int nshift;
-  int cj;       // j1 values per CTA in pass A
-  int wi;       // i2 columns per CTA in pass B
+  int64_t batch;
+  int cj;       // j1 values per tile in pass A
+  int wi;       // i2 columns per tile in pass B
+  int lgb2;     // log2(b2) if a power of two, else -1 (index splits by shift)
+  int lgb1;
   DftPlan plan1, plan2;
   double* z;    // [batch][nshift][b1][b2]
   double* out;
   int64_t out_offset, out_signal_stride, out_shift_stride, out_bin_stride;
   const int64_t* shift_table;
+  const cd* tlo;  // w_b^r for r < 4096
+  const cd* thi;  // w_b^(4096 q)
   int64_t tau[AFFT_MAX_SHIFTS];
 };
 
-__global__ void __launch_bounds__(1024) fourstep_a_kernel(const __grid_constant__ FourStepParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t s = blockIdx.z;
-  const int t = blockIdx.y;
-  const int64_t j1_0 = (int64_t)blockIdx.x * p.cj;
-  const int cnt = (int)min((int64_t)p.cj, p.b1 - j1_0);
-  const int b2 = (int)p.b2;
-  cd* tw = reinterpret_cast<cd*>(smem_raw);
-  cd* bufA = tw + b2;
-  cd* bufB = bufA + (size_t)cnt * b2;
-  build_twiddles(tw, b2, threadIdx.x, blockDim.x);
-  const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * (p.dtype == AFFT_C64 ? 8 : 16);
-  const int64_t tau = p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n) : p.tau[t];
-  const int64_t L = p.n / p.b;
-  const int64_t stride = p.b1 * L;
-  const int total = cnt * b2;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int q = e / b2;
-    const int64_t j2 = e - (int64_t)q * b2;
-    int64_t idx = (j1_0 + q) * L + j2 * stride - tau;
-    if (idx < 0) idx += p.n;
-    bufA[e] = load_sample(xs, p.dtype, idx);
+constexpr int kTwLoBits = 12;
+
+// w_b^r = w_b^(4096 q) * w_b^(r mod 4096): two table entries (L2/L1 resident, 64 KB
+// each at most) and one complex product instead of a float64 sincospi per element.
+__global__ void fourstep_tables_kernel(int64_t b, cd* __restrict__ tlo, int nlo,
+                                       cd* __restrict__ thi, int nhi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double sn, cs;
+  if (i < nlo) {
+    sincospi(-2.0 * (double)i / (double)b, &sn, &cs);
+    tlo[i] = cd{cs, sn};
   }
-  __syncthreads();
-  const cd* spec = smem_dft(bufA, bufB, cnt, p.plan2, tw, threadIdx.x, blockDim.x);
-  cd* z = reinterpret_cast<cd*>(p.z) + ((s * p.nshift + t) * p.b1 + j1_0) * p.b2;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const int q = e / b2;
-    const int64_t i2 = e - (int64_t)q * b2;
-    const int64_t r = ((j1_0 + q) * i2) % p.b;  // exact index of w_b^{j1*i2}
-    double sn, cs;
-    sincospi(-2.0 * (double)r / (double)p.b, &sn, &cs);
-    z[e] = cmul(spec[e], cd{cs, sn});
+  if (i < nhi) {
+    const int64_t k = (int64_t)i << kTwLoBits;
+    sincospi(-2.0 * (double)k / (double)b, &sn, &cs);
+    thi[i] = cd{cs, sn};
   }
 }
 
+__device__ __forceinline__ cd tw_b(const cd* tlo, const cd* thi, int64_t r) {
+  const cd lo = tlo[r & ((1 << kTwLoBits) - 1)];
+  return (r >> kTwLoBits) ? cmul(thi[r >> kTwLoBits], lo) : lo;
+}
+
+// Pass A, persistent over tiles (signal, shift, chunk of cj j1 values); the size-b2
+// twiddle table is built once per CTA.
+__global__ void __launch_bounds__(1024) fourstep_a_kernel(const __grid_constant__ FourStepParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b2 = (int)p.b2;
+  cd* tw = reinterpret_cast<cd*>(smem_raw);
+  cd* bufA = tw + b2;
+  cd* bufB = bufA + (size_t)p.cj * b2;
+  build_twiddles(tw, b2, threadIdx.x, blockDim.x);
+  const int64_t nchunks = (p.b1 + p.cj - 1) / p.cj;
+  const int64_t ntiles = p.batch * p.nshift * nchunks;
+  const int64_t L = p.n / p.b;
+  const int64_t stride = p.b1 * L;
+  const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t chunk = tile % nchunks;
+    const int64_t st_ = tile / nchunks;
+    const int t = (int)(st_ % p.nshift);
+    const int64_t s = st_ / p.nshift;
+    const int64_t j1_0 = chunk * p.cj;
+    const int cnt = (int)min((int64_t)p.cj, p.b1 - j1_0);
+    const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
+    const int64_t tau = p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n) : p.tau[t];
+    const int total = cnt * b2;
+    __syncthreads();  // tw ready / previous tile's buffers consumed
+    // consecutive threads take consecutive j1 (addresses L apart) within a row j2
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int j2 = e / cnt;
+      const int q = e - j2 * cnt;
+      int64_t idx = (j1_0 + q) * L + (int64_t)j2 * stride - tau;
+      if (idx < 0) idx += p.n;
+      bufA[q * b2 + j2] = load_sample(xs, p.dtype, idx);
+    }
+    __syncthreads();
+    const cd* spec = smem_dft(bufA, bufB, cnt, p.plan2, tw, threadIdx.x, blockDim.x);
+    cd* z = reinterpret_cast<cd*>(p.z) + ((s * p.nshift + t) * p.b1 + j1_0) * p.b2;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int q = p.lgb2 >= 0 ? e >> p.lgb2 : e / b2;
+      const int i2 = e - q * b2;
+      z[e] = cmul(spec[e], tw_b(p.tlo, p.thi, (j1_0 + q) * i2));  // j1*i2 < b: no reduction
+    }
+  }
+}
+
+// Pass B, persistent over tiles (signal, shift, block of wi i2 columns).
 __global__ void __launch_bounds__(1024) fourstep_b_kernel(const __grid_constant__ FourStepParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t s = blockIdx.z;
-  const int t = blockIdx.y;
-  const int64_t i2_0 = (int64_t)blockIdx.x * p.wi;
-  const int w = (int)min((int64_t)p.wi, p.b2 - i2_0);
   const int b1 = (int)p.b1;
   cd* tw = reinterpret_cast<cd*>(smem_raw);
   cd* bufA = tw + b1;
-  cd* bufB = bufA + (size_t)w * b1;
+  cd* bufB = bufA + (size_t)p.wi * b1;
   build_twiddles(tw, b1, threadIdx.x, blockDim.x);
-  const cd* z = reinterpret_cast<const cd*>(p.z) + (s * p.nshift + t) * p.b1 * p.b2;
-  const int total = w * b1;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {  // coalesced along i2
-    const int j1 = e / w;
-    const int q = e - j1 * w;
-    bufA[q * b1 + j1] = z[(int64_t)j1 * p.b2 + i2_0 + q];
-  }
-  __syncthreads();
-  const cd* spec = smem_dft(bufA, bufB, w, p.plan1, tw, threadIdx.x, blockDim.x);
+  const int64_t nchunks = (p.b2 + p.wi - 1) / p.wi;
+  const int64_t ntiles = p.batch * p.nshift * nchunks;
   const double inv_b = 1.0 / (double)p.b;
-  double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset + t * p.out_shift_stride);
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {  // consecutive i2 per i1
-    const int i1 = e / w;
-    const int q = e - i1 * w;
-    const cd v = cscale(spec[q * b1 + i1], inv_b);
-    const int64_t o = 2 * ((i2_0 + q + p.b2 * (int64_t)i1) * p.out_bin_stride);
-    out[o] = v.re;
-    out[o + 1] = v.im;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t chunk = tile % nchunks;
+    const int64_t st_ = tile / nchunks;
+    const int t = (int)(st_ % p.nshift);
+    const int64_t s = st_ / p.nshift;
+    const int64_t i2_0 = chunk * p.wi;
+    const int w = (int)min((int64_t)p.wi, p.b2 - i2_0);
+    const cd* z = reinterpret_cast<const cd*>(p.z) + (s * p.nshift + t) * p.b1 * p.b2;
+    const int total = w * b1;
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // coalesced along i2
+      const int j1 = e / w;
+      const int q = e - j1 * w;
+      bufA[q * b1 + j1] = z[(int64_t)j1 * p.b2 + i2_0 + q];
+    }
+    __syncthreads();
+    const cd* spec = smem_dft(bufA, bufB, w, p.plan1, tw, threadIdx.x, blockDim.x);
+    double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset + t * p.out_shift_stride);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // consecutive i2 per i1
+      const int i1 = e / w;
+      const int q = e - i1 * w;
+      const cd v = cscale(spec[q * b1 + i1], inv_b);
+      const int64_t o = 2 * ((i2_0 + q + p.b2 * (int64_t)i1) * p.out_bin_stride);
+      out[o] = v.re;
+      out[o + 1] = v.im;
+    }
   }
 }
 
@@ -210,35 +256,50 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
   const size_t kBudget = 96 * 1024;
   q.cj = (int)std::max<int64_t>(1, std::min<int64_t>(q.b1, ((int64_t)(kBudget / 16) - q.b2) / (2 * q.b2)));
   q.wi = (int)std::max<int64_t>(1, std::min<int64_t>(q.b2, ((int64_t)(kBudget / 16) - q.b1) / (2 * q.b1)));
+  q.lgb2 = q.plan2.lgn;
+  q.lgb1 = q.plan1.lgn;
+  q.batch = batch;
   const size_t smemA = (size_t)(q.b2 + 2 * (int64_t)q.cj * q.b2) * 16;
   const size_t smemB = (size_t)(q.b1 + 2 * (int64_t)q.wi * q.b1) * 16;
+  const int nlo = (int)std::min<int64_t>(b, 1 << kTwLoBits);
+  const int nhi = (int)((b + (1 << kTwLoBits) - 1) >> kTwLoBits);
   const size_t zbytes = (size_t)batch * nshift * b * 16;
-  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&q.z), zbytes, stream);
+  const size_t tbytes = (size_t)(nlo + nhi) * 16;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&q.z), zbytes + tbytes, stream);
   if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(four-step scratch)");
+  cd* tlo = reinterpret_cast<cd*>(reinterpret_cast<char*>(q.z) + zbytes);
+  cd* thi = tlo + nlo;
+  q.tlo = tlo;
+  q.thi = thi;
   e = cudaFuncSetAttribute(fourstep_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smemA);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(fourstep_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smemB);
-  if (e != cudaSuccess) {
+  // large sub-DFTs run one CTA per SM: give it enough warps to hide smem latency
+  const int ta = q.b2 >= 2048 ? 1024 : (q.b2 >= 512 ? 512 : 256);
+  const int tb = q.b1 >= 2048 ? 1024 : (q.b1 >= 512 ? 512 : 256);
+  int occA = 0, occB = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occA, fourstep_a_kernel, ta, smemA);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, fourstep_b_kernel, tb, smemB);
+  if (e != cudaSuccess || occA < 1 || occB < 1) {
     scratch_free(q.z, stream);
-    return cuda_status(e, "cudaFuncSetAttribute(four-step)");
+    return cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration,
+                       "four-step occupancy");
   }
-  for (int64_t s0 = 0; s0 < batch; s0 += 65535) {
-    const unsigned cntb = (unsigned)std::min<int64_t>(65535, batch - s0);
-    FourStepParams qs = q;
-    qs.x = reinterpret_cast<const char*>(x) + s0 * ld * (dtype == AFFT_C64 ? 8 : 16);
-    qs.z = q.z + 2 * s0 * nshift * b;
-    qs.out = out + 2 * s0 * oss;
-    qs.shift_table = shift_table ? shift_table + s0 * nshift : nullptr;
-    // large sub-DFTs run one CTA per SM: give it enough warps to hide smem latency
-    const int ta = q.b2 >= 2048 ? 1024 : (q.b2 >= 512 ? 512 : 256);
-    const int tb = q.b1 >= 2048 ? 1024 : (q.b1 >= 512 ? 512 : 256);
-    dim3 ga((unsigned)((q.b1 + q.cj - 1) / q.cj), (unsigned)nshift, cntb);
-    fourstep_a_kernel<<<ga, ta, smemA, stream>>>(qs);
-    dim3 gb((unsigned)((q.b2 + q.wi - 1) / q.wi), (unsigned)nshift, cntb);
-    fourstep_b_kernel<<<gb, tb, smemB, stream>>>(qs);
-  }
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  fourstep_tables_kernel<<<(unsigned)((std::max(nlo, nhi) + 255) / 256), 256, 0, stream>>>(
+      b, tlo, nlo, thi, nhi);
+  const int64_t tilesA = batch * nshift * ((q.b1 + q.cj - 1) / q.cj);
+  const int64_t tilesB = batch * nshift * ((q.b2 + q.wi - 1) / q.wi);
+  const unsigned ga = (unsigned)std::min<int64_t>(tilesA, (int64_t)sms * occA);
+  const unsigned gb = (unsigned)std::min<int64_t>(tilesB, (int64_t)sms * occB);
+  fourstep_a_kernel<<<ga, ta, smemA, stream>>>(q);
+  fourstep_b_kernel<<<gb, tb, smemB, stream>>>(q);
   scratch_free(q.z, stream);
   AFFT_CHECK_LAUNCH("fourstep kernels");
   return AFFT_OK;
@@ -310,7 +371,7 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
       q.plan[c].nstages = 0;
       continue;
     }
-    if (!make_dft_plan(b, &q.plan[c])) {
+    if (!make_dft_plan(b, &q.plan[c], 16)) {
       set_error("cannot plan a DFT of size %lld", (long long)b);
       return AFFT_EUNSUPPORTED;
     }

@@ -10,6 +10,7 @@
 
 namespace afft {
 
+template <int kMaxR = 8>
 __device__ inline cd* gather_dft_block(const char* xs, int dtype, int64_t n, int64_t b,
                                        const DftPlan& plan, const int64_t* tau, int cnt, cd* tw,
                                        cd* bufA, cd* bufB) {
@@ -25,7 +26,7 @@ __device__ inline cd* gather_dft_block(const char* xs, int dtype, int64_t n, int
     bufA[e] = load_sample(xs, dtype, idx);
   }
   __syncthreads();
-  return smem_dft(bufA, bufB, cnt, plan, tw, tid, nt);
+  return smem_dft<kMaxR>(bufA, bufB, cnt, plan, tw, tid, nt);
 }
 
 }  // namespace afft

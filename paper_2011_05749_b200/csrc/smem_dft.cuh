@@ -20,14 +20,38 @@ constexpr int kMaxStages = 40;
 struct DftPlan {
   int32_t n;
   int32_t nstages;
+  int32_t lgn;  // log2(n) when n is a power of two (radix 4/2 only), else -1
   int16_t radix[kMaxStages];
 };
 
-// Host: factor n into radices (4s first, then 2, then odd primes ascending).
-inline bool make_dft_plan(int64_t n, DftPlan* p) {
+// Host: factor n into radices (powers of two: 16/8 first, then 4 or 2; other sizes:
+// 4s first, then 2, then odd primes ascending).
+// max_radix: largest register butterfly for power-of-two sizes (16 needs ~128
+// registers of data per thread; kernels capped at 64-80 registers use 8).
+inline bool make_dft_plan(int64_t n, DftPlan* p, int max_radix = 8) {
   if (n < 1 || n > (1 << 30)) return false;
   p->n = (int32_t)n;
   p->nstages = 0;
+  p->lgn = -1;
+  if ((n & (n - 1)) == 0) {
+    int lg = 0;
+    while ((1ll << lg) < n) ++lg;
+    p->lgn = lg;
+  }
+  if (p->lgn >= 0) {  // powers of two: radix-16 register butterflies, then 8 / 4 / 2
+    int lg = p->lgn;
+    while (max_radix >= 16 && lg >= 4) {
+      p->radix[p->nstages++] = 16;
+      lg -= 4;
+    }
+    while (lg >= 3) {
+      p->radix[p->nstages++] = 8;
+      lg -= 3;
+    }
+    if (lg == 2) p->radix[p->nstages++] = 4;
+    if (lg == 1) p->radix[p->nstages++] = 2;
+    return true;
+  }
   int64_t m = n;
   while (m % 4 == 0) {
     if (p->nstages >= kMaxStages) return false;
@@ -120,11 +144,116 @@ __device__ __forceinline__ void out_generic(const cd* src, cd* dst, const cd* tw
   dst[(j / Ns) * Ns * R + jm + q * Ns] = acc;
 }
 
+// In-register forward DFT of R = 2, 4, 8, 16 points (radix-2 decimation in time
+// with compile-time twiddles w_R^k; multiplications by -i are exact swaps).
+template <int R>
+__device__ __forceinline__ void dft_reg(cd* v) {
+  if constexpr (R == 2) {
+    const cd a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const cd a = cadd(v[0], v[2]), b = csub(v[0], v[2]);
+    const cd c = cadd(v[1], v[3]), d = csub(v[1], v[3]);
+    v[0] = cadd(a, c);
+    v[2] = csub(a, c);
+    v[1] = cd{b.re + d.im, b.im - d.re};  // b - i*d
+    v[3] = cd{b.re - d.im, b.im + d.re};  // b + i*d
+  } else {
+    constexpr int H = R / 2;
+    cd e[H], o[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      e[i] = v[2 * i];
+      o[i] = v[2 * i + 1];
+    }
+    dft_reg<H>(e);
+    dft_reg<H>(o);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      cd t;
+      if (k == 0) {
+        t = o[0];
+      } else if (2 * k == H) {  // w_R^(R/4) = -i
+        t = cd{o[k].im, -o[k].re};
+      } else {
+        // w_R^k = exp(-2 pi i k / R), k < R/2 (constants fold at compile time)
+        constexpr double kTwoPiOverR = 6.283185307179586 / R;
+        const cd w{cos(kTwoPiOverR * k), -sin(kTwoPiOverR * k)};
+        t = cmul(o[k], w);
+      }
+      v[k] = cadd(e[k], t);
+      v[k + H] = csub(e[k], t);
+    }
+  }
+}
+
+// Power-of-two sizes: Stockham stages with every index division a shift.
+template <int R, int LGR>
+__device__ __forceinline__ void bfly_pow2(const cd* __restrict__ src, cd* __restrict__ dst,
+                                          const cd* __restrict__ tw, int nb, int lgNs,
+                                          int lgtstep, int j) {
+  const int jm = j & ((1 << lgNs) - 1);
+  const int Ns = 1 << lgNs;
+  cd v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    cd a = src[j + r * nb];
+    v[r] = (r == 0 || jm == 0) ? a : cmul(a, tw[(jm * r) << lgtstep]);
+  }
+  dft_reg<R>(v);
+  const int idxD = ((j >> lgNs) << (lgNs + LGR)) + jm;
+#pragma unroll
+  for (int q = 0; q < R; ++q) dst[idxD + q * Ns] = v[q];
+}
+
+template <int kMaxR>
+__device__ inline cd* smem_dft_pow2(cd* a, cd* b, int count, const DftPlan& p, const cd* tw,
+                                    int tid, int nthreads) {
+  const int lgn = p.lgn;
+  int lgNs = 0;
+  for (int s = 0; s < p.nstages; ++s) {
+    const int R = p.radix[s];
+    const int lgR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
+    const int lgnb = lgn - lgR;
+    const int nb = 1 << lgnb;
+    const int total = count << lgnb;
+    const int lgtstep = lgn - lgNs - lgR;  // tstep = n / (Ns * R)
+#define AFFT_POW2_STAGE(RR, LG)                                                         \
+  for (int w = tid; w < total; w += nthreads) {                                         \
+    const int seq = w >> lgnb, j = w & (nb - 1);                                        \
+    bfly_pow2<RR, LG>(a + (seq << lgn), b + (seq << lgn), tw, nb, lgNs, lgtstep, j);    \
+  }
+    if (kMaxR >= 16 && R == 16) {
+      AFFT_POW2_STAGE(16, 4)
+    } else if (R == 8) {
+      AFFT_POW2_STAGE(8, 3)
+    } else if (R == 4) {
+      AFFT_POW2_STAGE(4, 2)
+    } else if (R == 2) {
+      AFFT_POW2_STAGE(2, 1)
+    } else {
+      __trap();  // plan built with a larger max_radix than this kernel compiles in
+    }
+#undef AFFT_POW2_STAGE
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+    lgNs += lgR;
+  }
+  return a;
+}
+
 // Forward DFT of `count` contiguous length-n sequences in smem buffer `a`,
 // ping-ponging with `b`.  Returns the buffer that holds the result.  Must be
 // called by all threads of the block (contains __syncthreads).
+// kMaxR: the largest power-of-two register butterfly compiled in (must cover the
+// plan's, see make_dft_plan's max_radix).
+template <int kMaxR = 8>
 __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const cd* tw, int tid,
                         int nthreads) {
+  if (p.lgn >= 0) return smem_dft_pow2<kMaxR>(a, b, count, p, tw, tid, nthreads);
   const int n = p.n;
   int Ns = 1;
   for (int s = 0; s < p.nstages; ++s) {

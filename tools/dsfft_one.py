@@ -1,0 +1,25 @@
+"""One warm config-4 DSFFT decode bracketed by cudaProfilerStart/Stop (for ncu launch lists)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from bench_suite import make_batch  # noqa: E402
+from paper_2011_05749_b200 import DsfftConfig  # noqa: E402
+import paper_2011_05749_b200.dsfft  # noqa: E402,F401
+
+D = sys.modules["paper_2011_05749_b200.dsfft"]
+n, k, snr = 1 << 24, 4096, float(sys.argv[1]) if len(sys.argv) > 1 else 20.0
+x, _ = make_batch(n, k, snr, 2, torch.complex64, torch.device("cuda", 0), chunk=2)
+cfg = DsfftConfig(mode="noisy", seed=0, noise_std=float(np.sqrt(k * 10 ** (-snr / 10))))
+D.dsfft_device(x[0], k, cfg)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
+D.dsfft_device(x[1], k, cfg)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
+print("ok")
