@@ -80,6 +80,7 @@ SIGNATURES = {
     "afft_sfft_dt": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P,
                             _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "afft_bucketize_rows": (_INT, [_P, _INT, _I64, _I64, _P, _I32, _P, _I64, _P, _P, _P]),
+    "afft_alias_rows": (_INT, [_P, _I64, _I64, _P, _I32, _P, _I64, _P, _P, _P, _P]),
     "afft_active_indices": (_INT, [_P, _I64, _D, _P, _P, _P, _P]),
     "afft_selective_sums": (_INT, [_P, _INT, _I64, _I64, _P, _I64, _P, _P]),
     "afft_median": (_INT, [_P, _I32, _I64, _I64, _P, _P]),

@@ -76,39 +76,47 @@ __global__ void __launch_bounds__(256) gather_dft_kernel(const __grid_constant__
 
 // ---------------------------------------------------------------- K2': b > 4096
 //
-// Four-step DFT for large bucket counts, b = b1 * b2 (both <= 4096):
-//   j = j1 + b1*j2, i = i2 + b2*i1
-//   y[i2 + b2*i1] = (1/b) sum_j1 w_b1^{j1*i1} * [ w_b^{j1*i2} * sum_j2 x[(j*L - tau) mod n] w_b2^{j2*i2} ]
-// Pass A: for each (shift, j1) gather the b2 samples at stride b1*L, size-b2 DFT,
-//         twiddle w_b^{j1*i2} (index reduced mod b, sincospi), write z[t][j1][i2].
-// Pass B: for each (shift, block of i2) read z[t][0..b1)[i2..], size-b1 DFT,
-//         scale 1/b, write the caller-strided output.
-struct FourStepParams {
+// Large bucket counts (DSFFT's deep layers up to b = 2^24, R-FFAST's auto plans,
+// the dense full-length transform): global-memory Stockham passes.  b is split
+// into radices R_1 >= R_2 >= ... (each <= 256 unless a prime factor is larger),
+// and pass s computes, for every butterfly j < b/R_s with k = j mod N_s
+// (N_s = R_1 ... R_{s-1}):
+//   v[r] = in[j + r b/R_s] * w_b^(k r b/(N_s R_s)),  V = DFT_{R_s}(v),
+//   out[(j / N_s) N_s R_s + k + q N_s] = V[q]
+// — the smem Stockham of smem_dft.cuh run over HBM, so the result lands in natural
+// order.  A CTA takes `cnt` consecutive butterflies (cnt * R_s ~ 2048 points):
+// every row r it loads is cnt contiguous elements and every output row q is cnt
+// contiguous elements, so all global traffic is coalesced; each pass reads and
+// writes the data once.  The first pass gathers x[(e L - tau) mod n] directly
+// (bucketize.py:96) and the last applies numpy's 1/b and the caller's strides.
+// Twiddles w_b^m come from two 4096-entry tables (w_b^(4096 q) * w_b^(m mod 4096)).
+struct GStockParams {
   const void* x;
   int dtype;
-  int64_t n, ld, b, b1, b2;
-  int nshift;
+  int64_t n, ld, L, b;
   int64_t batch;
-  int cj;       // j1 values per tile in pass A
-  int wi;       // i2 columns per tile in pass B
-  int lgb2;     // log2(b2) if a power of two, else -1 (index splits by shift)
-  int lgb1;
-  DftPlan plan1, plan2;
-  double* z;    // [batch][nshift][b1][b2]
+  int nshift;
+  const int64_t* shift_table;
+  const cd* tlo;
+  const cd* thi;
+  const cd* in;   // previous pass (null on the first pass)
+  cd* tmp;        // this pass's output (null on the last pass)
   double* out;
   int64_t out_offset, out_signal_stride, out_shift_stride, out_bin_stride;
-  const int64_t* shift_table;
-  const cd* tlo;  // w_b^r for r < 4096
-  const cd* thi;  // w_b^(4096 q)
+  int R;
+  int64_t Ns;
+  int cnt;
+  DftPlan plan;
   int64_t tau[AFFT_MAX_SHIFTS];
 };
 
 constexpr int kTwLoBits = 12;
+constexpr int kGStockThreads = 256;
+constexpr int kGStockPoints = 2048;  // points per tile (cnt * R)
+constexpr int kPer = 1;  // loads per thread batched in the gather loop (more spills at 85 regs)
 
-// w_b^r = w_b^(4096 q) * w_b^(r mod 4096): two table entries (L2/L1 resident, 64 KB
-// each at most) and one complex product instead of a float64 sincospi per element.
-__global__ void fourstep_tables_kernel(int64_t b, cd* __restrict__ tlo, int nlo,
-                                       cd* __restrict__ thi, int nhi) {
+__global__ void twiddle_tables_kernel(int64_t b, cd* __restrict__ tlo, int nlo,
+                                      cd* __restrict__ thi, int nhi) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double sn, cs;
   if (i < nlo) {
@@ -122,106 +130,130 @@ __global__ void fourstep_tables_kernel(int64_t b, cd* __restrict__ tlo, int nlo,
   }
 }
 
-__device__ __forceinline__ cd tw_b(const cd* tlo, const cd* thi, int64_t r) {
-  const cd lo = tlo[r & ((1 << kTwLoBits) - 1)];
-  return (r >> kTwLoBits) ? cmul(thi[r >> kTwLoBits], lo) : lo;
+__device__ __forceinline__ cd tw_b(const cd* tlo, const cd* thi, int64_t m) {
+  const cd lo = tlo[m & ((1 << kTwLoBits) - 1)];
+  return (m >> kTwLoBits) ? cmul(thi[m >> kTwLoBits], lo) : lo;
 }
 
-// Pass A, persistent over tiles (signal, shift, chunk of cj j1 values); the size-b2
-// twiddle table is built once per CTA.
-__global__ void __launch_bounds__(1024) fourstep_a_kernel(const __grid_constant__ FourStepParams p) {
+__global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
+    const __grid_constant__ GStockParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int b2 = (int)p.b2;
+  const int R = p.R, cnt = p.cnt;
+  const int tid = threadIdx.x, nt = blockDim.x;
   cd* tw = reinterpret_cast<cd*>(smem_raw);
-  cd* bufA = tw + b2;
-  cd* bufB = bufA + (size_t)p.cj * b2;
-  build_twiddles(tw, b2, threadIdx.x, blockDim.x);
-  const int64_t nchunks = (p.b1 + p.cj - 1) / p.cj;
+  cd* bufA = tw + R;
+  cd* bufB = bufA + (size_t)cnt * R;
+  build_twiddles(tw, R, tid, nt);
+  const int64_t nb = p.b / R;
+  const int64_t nchunks = (nb + cnt - 1) / cnt;
   const int64_t ntiles = p.batch * p.nshift * nchunks;
-  const int64_t L = p.n / p.b;
-  const int64_t stride = p.b1 * L;
+  const int64_t tstep = p.b / (p.Ns * R);
   const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t chunk = tile % nchunks;
-    const int64_t st_ = tile / nchunks;
-    const int t = (int)(st_ % p.nshift);
-    const int64_t s = st_ / p.nshift;
-    const int64_t j1_0 = chunk * p.cj;
-    const int cnt = (int)min((int64_t)p.cj, p.b1 - j1_0);
-    const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
-    const int64_t tau = p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n) : p.tau[t];
-    const int total = cnt * b2;
-    __syncthreads();  // tw ready / previous tile's buffers consumed
-    // consecutive threads take consecutive j1 (addresses L apart) within a row j2
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int j2 = e / cnt;
-      const int q = e - j2 * cnt;
-      int64_t idx = (j1_0 + q) * L + (int64_t)j2 * stride - tau;
-      if (idx < 0) idx += p.n;
-      bufA[q * b2 + j2] = load_sample(xs, p.dtype, idx);
-    }
-    __syncthreads();
-    const cd* spec = smem_dft(bufA, bufB, cnt, p.plan2, tw, threadIdx.x, blockDim.x);
-    cd* z = reinterpret_cast<cd*>(p.z) + ((s * p.nshift + t) * p.b1 + j1_0) * p.b2;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int q = p.lgb2 >= 0 ? e >> p.lgb2 : e / b2;
-      const int i2 = e - q * b2;
-      z[e] = cmul(spec[e], tw_b(p.tlo, p.thi, (j1_0 + q) * i2));  // j1*i2 < b: no reduction
-    }
-  }
-}
-
-// Pass B, persistent over tiles (signal, shift, block of wi i2 columns).
-__global__ void __launch_bounds__(1024) fourstep_b_kernel(const __grid_constant__ FourStepParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int b1 = (int)p.b1;
-  cd* tw = reinterpret_cast<cd*>(smem_raw);
-  cd* bufA = tw + b1;
-  cd* bufB = bufA + (size_t)p.wi * b1;
-  build_twiddles(tw, b1, threadIdx.x, blockDim.x);
-  const int64_t nchunks = (p.b2 + p.wi - 1) / p.wi;
-  const int64_t ntiles = p.batch * p.nshift * nchunks;
   const double inv_b = 1.0 / (double)p.b;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t chunk = tile % nchunks;
     const int64_t st_ = tile / nchunks;
     const int t = (int)(st_ % p.nshift);
     const int64_t s = st_ / p.nshift;
-    const int64_t i2_0 = chunk * p.wi;
-    const int w = (int)min((int64_t)p.wi, p.b2 - i2_0);
-    const cd* z = reinterpret_cast<const cd*>(p.z) + (s * p.nshift + t) * p.b1 * p.b2;
-    const int total = w * b1;
-    __syncthreads();
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // coalesced along i2
-      const int j1 = e / w;
-      const int q = e - j1 * w;
-      bufA[q * b1 + j1] = z[(int64_t)j1 * p.b2 + i2_0 + q];
+    const int64_t j0 = chunk * cnt;
+    const int c = (int)min((int64_t)cnt, nb - j0);
+    const int64_t seq = s * p.nshift + t;
+    const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
+    const int64_t tau = p.in ? 0
+                             : (p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n)
+                                              : p.tau[t]);
+    __syncthreads();  // twiddles ready / previous tile consumed
+    // row r: c contiguous butterflies (kPer > 1 batches loads per thread; at the
+    // 85-register cap that spilled and measured slower)
+    const int total = c * R;
+    for (int base = 0; base < total; base += nt * kPer) {
+      cd v[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = base + tid + u * nt;
+        if (e < total) {
+          const int r = e / c;
+          const int64_t src = j0 + (e - r * c) + r * nb;
+          if (p.in) {
+            v[u] = p.in[seq * p.b + src];
+          } else {
+            int64_t idx = src * p.L - tau;
+            if (idx < 0) idx += p.n;
+            v[u] = load_sample(xs, p.dtype, idx);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = base + tid + u * nt;
+        if (e < total) {
+          const int r = e / c;
+          const int jj = e - r * c;
+          const int64_t j = j0 + jj;
+          const int64_t k = p.Ns == 1 ? 0 : j % p.Ns;
+          cd a = v[u];
+          if (r && k) a = cmul(a, tw_b(p.tlo, p.thi, k * r * tstep));
+          bufA[jj * R + r] = a;
+        }
+      }
     }
     __syncthreads();
-    const cd* spec = smem_dft(bufA, bufB, w, p.plan1, tw, threadIdx.x, blockDim.x);
-    double* out = p.out + 2 * (s * p.out_signal_stride + p.out_offset + t * p.out_shift_stride);
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {  // consecutive i2 per i1
-      const int i1 = e / w;
-      const int q = e - i1 * w;
-      const cd v = cscale(spec[q * b1 + i1], inv_b);
-      const int64_t o = 2 * ((i2_0 + q + p.b2 * (int64_t)i1) * p.out_bin_stride);
-      out[o] = v.re;
-      out[o + 1] = v.im;
+    const cd* spec = smem_dft(bufA, bufB, c, p.plan, tw, tid, nt);
+    double* out = p.out ? p.out + 2 * (s * p.out_signal_stride + p.out_offset +
+                                       t * p.out_shift_stride)
+                        : nullptr;
+    cd* tmp = p.tmp ? p.tmp + seq * p.b : nullptr;
+    for (int e = tid; e < c * R; e += nt) {
+      int jj, q;
+      if (p.Ns == 1) {  // first pass: butterfly j's outputs are the contiguous j*R + q
+        jj = e / R;
+        q = e - jj * R;
+      } else {          // output row q: c contiguous k
+        q = e / c;
+        jj = e - q * c;
+      }
+      const int64_t j = j0 + jj;
+      const int64_t k = p.Ns == 1 ? 0 : j % p.Ns;
+      const int64_t dst = (j - k) * R + k + q * p.Ns;  // (j / Ns) Ns R + k + q Ns
+      const cd v = spec[jj * R + q];
+      if (tmp) {
+        tmp[dst] = v;
+      } else {
+        const cd w = cscale(v, inv_b);
+        const int64_t o = 2 * dst * p.out_bin_stride;
+        out[o] = w.re;
+        out[o + 1] = w.im;
+      }
     }
   }
 }
 
-// b = b1 * b2 with both factors <= limit, as balanced as possible; false if none.
-static bool split_size(int64_t b, int64_t limit, int64_t* b1, int64_t* b2) {
-  int64_t best = 0;
-  for (int64_t d = 1; d * d <= b; ++d) {
-    if (b % d) continue;
-    const int64_t e = b / d;
-    if (d <= limit && e <= limit) best = d;  // d grows toward sqrt(b)
+// Radices for b: first-fit decreasing of the prime factors into groups <= 256
+// (a prime above 256 forms its own radix, up to AFFT_MAX_SMEM_DFT); descending.
+static bool plan_radices(int64_t b, std::vector<int>* radices) {
+  std::vector<int64_t> primes;
+  int64_t m = b;
+  for (int64_t q = 2; q * q <= m; ++q)
+    while (m % q == 0) {
+      primes.push_back(q);
+      m /= q;
+    }
+  if (m > 1) primes.push_back(m);
+  std::sort(primes.rbegin(), primes.rend());
+  if (!primes.empty() && primes[0] > AFFT_MAX_SMEM_DFT) return false;
+  std::vector<int64_t> groups;
+  for (int64_t pr : primes) {
+    bool placed = false;
+    for (auto& g : groups)
+      if (g * pr <= 256) {
+        g *= pr;
+        placed = true;
+        break;
+      }
+    if (!placed) groups.push_back(pr);
   }
-  if (!best) return false;
-  *b1 = b / best;  // the larger factor on the pass-B side
-  *b2 = best;
+  std::sort(groups.rbegin(), groups.rend());
+  radices->assign(groups.begin(), groups.end());
   return true;
 }
 
@@ -229,80 +261,82 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
                            int64_t b, const int64_t* shifts, int nshift, double* out,
                            int64_t out_offset, int64_t oss, int64_t osh, int64_t obin,
                            cudaStream_t stream, const int64_t* shift_table) {
-  FourStepParams q;
+  std::vector<int> radices;
+  if (!plan_radices(b, &radices)) {
+    set_error("bucket count %lld has a prime factor above %d", (long long)b, AFFT_MAX_SMEM_DFT);
+    return AFFT_EUNSUPPORTED;
+  }
+  GStockParams q;
   memset(&q, 0, sizeof(q));
-  if (!split_size(b, AFFT_MAX_SMEM_DFT, &q.b1, &q.b2)) {
-    set_error("bucket count %lld has no factorisation into two DFTs of size <= %d",
-              (long long)b, AFFT_MAX_SMEM_DFT);
-    return AFFT_EUNSUPPORTED;
-  }
-  if (!make_dft_plan(q.b1, &q.plan1) || !make_dft_plan(q.b2, &q.plan2)) {
-    set_error("cannot plan DFTs of sizes %lld x %lld", (long long)q.b1, (long long)q.b2);
-    return AFFT_EUNSUPPORTED;
-  }
   q.x = x;
   q.dtype = dtype;
   q.n = n;
   q.ld = ld;
+  q.L = n / b;
   q.b = b;
+  q.batch = batch;
   q.nshift = nshift;
-  q.out = out;
+  q.shift_table = shift_table;
   q.out_offset = out_offset;
   q.out_signal_stride = oss;
   q.out_shift_stride = osh;
   q.out_bin_stride = obin;
-  q.shift_table = shift_table;
   for (int t = 0; t < nshift; ++t) q.tau[t] = shifts ? host_pymod(shifts[t], n) : 0;
-  const size_t kBudget = 96 * 1024;
-  q.cj = (int)std::max<int64_t>(1, std::min<int64_t>(q.b1, ((int64_t)(kBudget / 16) - q.b2) / (2 * q.b2)));
-  q.wi = (int)std::max<int64_t>(1, std::min<int64_t>(q.b2, ((int64_t)(kBudget / 16) - q.b1) / (2 * q.b1)));
-  q.lgb2 = q.plan2.lgn;
-  q.lgb1 = q.plan1.lgn;
-  q.batch = batch;
-  const size_t smemA = (size_t)(q.b2 + 2 * (int64_t)q.cj * q.b2) * 16;
-  const size_t smemB = (size_t)(q.b1 + 2 * (int64_t)q.wi * q.b1) * 16;
+  const int P = (int)radices.size();
   const int nlo = (int)std::min<int64_t>(b, 1 << kTwLoBits);
   const int nhi = (int)((b + (1 << kTwLoBits) - 1) >> kTwLoBits);
-  const size_t zbytes = (size_t)batch * nshift * b * 16;
-  const size_t tbytes = (size_t)(nlo + nhi) * 16;
-  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&q.z), zbytes + tbytes, stream);
-  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(four-step scratch)");
-  cd* tlo = reinterpret_cast<cd*>(reinterpret_cast<char*>(q.z) + zbytes);
+  const size_t seqs = (size_t)batch * nshift;
+  const size_t buf = (seqs * b * 16 + 255) / 256 * 256;
+  const size_t nbufs = P >= 3 ? 2 : (P == 2 ? 1 : 0);
+  char* scratch = nullptr;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch),
+                                nbufs * buf + (size_t)(nlo + nhi) * 16, stream);
+  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(large-b DFT)");
+  cd* bufs[2] = {reinterpret_cast<cd*>(scratch), reinterpret_cast<cd*>(scratch + buf)};
+  cd* tlo = reinterpret_cast<cd*>(scratch + nbufs * buf);
   cd* thi = tlo + nlo;
   q.tlo = tlo;
   q.thi = thi;
-  e = cudaFuncSetAttribute(fourstep_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smemA);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(fourstep_b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smemB);
-  // large sub-DFTs run one CTA per SM: give it enough warps to hide smem latency
-  const int ta = q.b2 >= 2048 ? 1024 : (q.b2 >= 512 ? 512 : 256);
-  const int tb = q.b1 >= 2048 ? 1024 : (q.b1 >= 512 ? 512 : 256);
-  int occA = 0, occB = 0;
-  if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occA, fourstep_a_kernel, ta, smemA);
-  if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, fourstep_b_kernel, tb, smemB);
-  if (e != cudaSuccess || occA < 1 || occB < 1) {
-    scratch_free(q.z, stream);
-    return cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration,
-                       "four-step occupancy");
-  }
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  fourstep_tables_kernel<<<(unsigned)((std::max(nlo, nhi) + 255) / 256), 256, 0, stream>>>(
+  twiddle_tables_kernel<<<(unsigned)((std::max(nlo, nhi) + 255) / 256), 256, 0, stream>>>(
       b, tlo, nlo, thi, nhi);
-  const int64_t tilesA = batch * nshift * ((q.b1 + q.cj - 1) / q.cj);
-  const int64_t tilesB = batch * nshift * ((q.b2 + q.wi - 1) / q.wi);
-  const unsigned ga = (unsigned)std::min<int64_t>(tilesA, (int64_t)sms * occA);
-  const unsigned gb = (unsigned)std::min<int64_t>(tilesB, (int64_t)sms * occB);
-  fourstep_a_kernel<<<ga, ta, smemA, stream>>>(q);
-  fourstep_b_kernel<<<gb, tb, smemB, stream>>>(q);
-  scratch_free(q.z, stream);
-  AFFT_CHECK_LAUNCH("fourstep kernels");
-  return AFFT_OK;
+  int64_t Ns = 1;
+  int rc = AFFT_OK;
+  for (int s = 0; s < P && !rc; ++s) {
+    const int R = radices[s];
+    GStockParams g = q;
+    g.R = R;
+    g.Ns = Ns;
+    g.cnt = std::max(1, kGStockPoints / R);
+    if (!make_dft_plan(R, &g.plan)) {
+      rc = AFFT_EUNSUPPORTED;
+      set_error("cannot plan a DFT of size %d", R);
+      break;
+    }
+    g.in = s == 0 ? nullptr : bufs[(s - 1) & 1];
+    g.tmp = s == P - 1 ? nullptr : bufs[s & 1];
+    g.out = s == P - 1 ? out : nullptr;
+    const size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * R) * 16;
+    e = cudaFuncSetAttribute(gstockham_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    int occ = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gstockham_kernel, kGStockThreads,
+                                                        smem);
+    if (e != cudaSuccess || occ < 1) {
+      rc = cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "large-b DFT pass");
+      break;
+    }
+    const int64_t tiles = (int64_t)seqs * ((b / R + g.cnt - 1) / g.cnt);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * occ);
+    gstockham_kernel<<<grid, kGStockThreads, smem, stream>>>(g);
+    Ns *= R;
+  }
+  scratch_free(scratch, stream);
+  if (!rc) AFFT_CHECK_LAUNCH("gstockham_kernel");
+  return rc;
 }
 
 static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,

@@ -184,6 +184,109 @@ __global__ void selective_sum_kernel(const void* __restrict__ x, int dtype, int6
   }
 }
 
+
+// ---------------------------------------------------------------- alias rows
+//
+// Deep layers from the resident spectrum.  With Y = fft(x)/n (the signal's full
+// normalised spectrum, computed once per decode) and L = n/b, substituting the
+// inverse DFT into bucketize.py:96-99 gives the alias identity
+//   bucketize(x, b, tau)[i] = w_n^(i tau) * sum_{l<L} Y[i + l b] * w_L^(l tau mod L),
+// so a layer with small L needs L loads and L complex products per value instead
+// of min(#shifts, L) size-b DFTs over the whole signal.  Used for L <= 32
+// (kAliasMaxL), i.e. DSFFT's deepest layers, which otherwise each cost a full
+// n-point transform's worth of passes.
+constexpr int kAliasMaxL = 32;
+constexpr int kAliasWarps = 8;
+
+struct AliasShifts {
+  int32_t nshift;
+  int64_t tau[AFFT_MAX_SHIFTS];  // reduced into [0, n)
+};
+
+__device__ __forceinline__ cd root_pi(int64_t m, int64_t q) {  // exp(-2 pi i m / q)
+  double sn, cs;
+  sincospi(-2.0 * (double)m / (double)q, &sn, &cs);
+  return cd{cs, sn};
+}
+
+// rows[r][t] for selected buckets: one warp per row, lanes over the L spectrum
+// terms (load) and then over the shifts (sum).
+__global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_kernel(
+    const cd* __restrict__ Y, int64_t n, int64_t b, int L, const __grid_constant__ AliasShifts sh,
+    const int64_t* __restrict__ idx, int64_t nrows, cd* __restrict__ rows) {
+  __shared__ cd rootL[kAliasMaxL];
+  __shared__ cd ys[kAliasWarps][kAliasMaxL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x < L) rootL[threadIdx.x] = root_pi(threadIdx.x, L);
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * kAliasWarps + w;
+  if (r >= nrows) return;
+  const int64_t i = idx[r];
+  if (lane < L) ys[w][lane] = Y[i + (int64_t)lane * b];
+  __syncwarp();
+  for (int t = lane; t < sh.nshift; t += 32) {
+    const int64_t tau = sh.tau[t];
+    const int rl = (int)(tau % L);
+    cd acc = ys[w][0];
+    int m = 0;
+    for (int l = 1; l < L; ++l) {
+      m += rl;
+      if (m >= L) m -= L;
+      acc = cadd(acc, cmul(ys[w][l], rootL[m]));
+    }
+    rows[r * sh.nshift + t] = cmul(acc, root_pi(mulmod(i, tau, n), n));
+  }
+}
+
+struct AliasCosets {
+  int32_t U;
+  int32_t r[kAliasMaxL];     // distinct tau mod L
+  int32_t mult[kAliasMaxL];  // shifts per residue
+};
+
+// All b buckets: energy[i] = sum_t |y_tau_t[i]|^2 (the w_n^(i tau) factor has modulus 1,
+// so shifts with equal tau mod L contribute equal terms); vals0 (optional) = the
+// tau = 0 values sum_l Y[i + l b].
+__global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y, int64_t b, int L,
+                                                        const __grid_constant__ AliasCosets cs,
+                                                        double* __restrict__ energy,
+                                                        cd* __restrict__ vals0) {
+  __shared__ cd rootL[kAliasMaxL];
+  if (threadIdx.x < L) rootL[threadIdx.x] = root_pi(threadIdx.x, L);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  cd y[kAliasMaxL];
+#pragma unroll
+  for (int l = 0; l < kAliasMaxL; ++l)
+    if (l < L) y[l] = Y[i + (int64_t)l * b];
+  if (vals0) {
+    cd acc = y[0];
+#pragma unroll
+    for (int l = 1; l < kAliasMaxL; ++l)
+      if (l < L) acc = cadd(acc, y[l]);
+    vals0[i] = acc;
+  }
+  if (energy) {
+    double e = 0.0;
+    for (int u = 0; u < cs.U; ++u) {
+      cd acc = y[0];
+      int m = 0;
+#pragma unroll
+      for (int l = 1; l < kAliasMaxL; ++l) {
+        if (l < L) {
+          m += cs.r[u];
+          if (m >= L) m -= L;
+          acc = cadd(acc, cmul(y[l], rootL[m]));
+        }
+      }
+      const double m2 = cabs_(acc);
+      e += (double)cs.mult[u] * (m2 * m2);
+    }
+    energy[i] = e;
+  }
+}
+
 }  // namespace afft
 
 using namespace afft;
@@ -279,5 +382,48 @@ extern "C" int afft_selective_sums(const void* x, int dtype, int64_t n, int64_t 
   selective_sum_kernel<<<(unsigned)ncand, 256, 0, (cudaStream_t)stream>>>(x, dtype, n, b, cand,
                                                                           out);
   AFFT_CHECK_LAUNCH("selective_sum_kernel");
+  return AFFT_OK;
+}
+
+extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
+                               const int64_t* shifts, int32_t nshift, const int64_t* bucket_idx,
+                               int64_t nrows, double* rows, double* energy, double* values0,
+                               void* stream) {
+  if (!spectrum || b < 1 || n % b || nshift < 0 || nshift > AFFT_MAX_SHIFTS ||
+      (nrows > 0 && (!bucket_idx || !rows || !shifts))) {
+    set_error("afft_alias_rows: bad arguments");
+    return AFFT_EINVAL;
+  }
+  const int64_t L = n / b;
+  if (L > kAliasMaxL) {
+    set_error("afft_alias_rows: n/b = %lld above %d", (long long)L, kAliasMaxL);
+    return AFFT_EUNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const cd* Y = reinterpret_cast<const cd*>(spectrum);
+  if (nrows > 0 && nshift > 0) {
+    AliasShifts sh;
+    sh.nshift = nshift;
+    for (int t = 0; t < nshift; ++t) sh.tau[t] = host_pymod(shifts[t], n);
+    alias_rows_kernel<<<(unsigned)((nrows + kAliasWarps - 1) / kAliasWarps), kAliasWarps * 32, 0,
+                        st>>>(Y, n, b, (int)L, sh, bucket_idx, nrows, reinterpret_cast<cd*>(rows));
+  }
+  if (energy || values0) {
+    AliasCosets cs;
+    memset(&cs, 0, sizeof(cs));
+    for (int t = 0; t < nshift && energy; ++t) {
+      const int r = (int)(host_pymod(shifts[t], n) % L);
+      int u = 0;
+      while (u < cs.U && cs.r[u] != r) ++u;
+      if (u == cs.U) {
+        cs.r[cs.U] = r;
+        cs.mult[cs.U++] = 0;
+      }
+      ++cs.mult[u];
+    }
+    alias_all_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
+        Y, b, (int)L, cs, energy, reinterpret_cast<cd*>(values0));
+  }
+  AFFT_CHECK_LAUNCH("afft_alias_rows");
   return AFFT_OK;
 }
