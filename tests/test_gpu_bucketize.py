@@ -136,3 +136,40 @@ def test_device_input_synthesis_matches_host_model():
         assert truth.entries == ref.truth.entries
         d = np.max(np.abs(x.cpu().numpy() - ref.signal))
         assert d <= 1e-12 * max(1.0, np.max(np.abs(ref.signal))), d
+
+
+@pytest.mark.parametrize("L", [1, 2, 8, 32])
+def test_alias_rows_match_bucketize_rows(L):
+    """afft_alias_rows (rows from the resident spectrum by the alias identity) equals
+    afft_bucketize_rows (coset DFTs of the signal) for DSFFT's deep layers."""
+    import torch
+
+    from paper_2011_05749_b200 import _device, _lib
+
+    n = 1 << 14
+    b = n // L
+    rng = np.random.default_rng(L)
+    x = torch.from_numpy(rng.normal(size=n) + 1j * rng.normal(size=n)).cuda()
+    shifts = [int(t) for t in rng.integers(-n, 2 * n, size=40)] + [0, 1, 2]
+    idx = torch.from_numpy(np.sort(rng.choice(b, size=min(b, 300), replace=False))).cuda()
+    lib = _lib.load()
+    sp = _device.stream_ptr()
+    sb, ns = _lib.host_i64(shifts)
+    rows_ref = torch.empty((idx.numel(), len(shifts)), dtype=torch.complex128, device="cuda")
+    en_ref = torch.empty(b, dtype=torch.float64, device="cuda")
+    _lib.check(lib.afft_bucketize_rows(x.data_ptr(), 1, n, b, sb, ns, idx.data_ptr(), idx.numel(),
+                                       rows_ref.data_ptr(), en_ref.data_ptr(), sp), "rows")
+    Y = torch.empty(n, dtype=torch.complex128, device="cuda")
+    s0, n0 = _lib.host_i64([0])
+    _lib.check(lib.afft_bucketize(x.data_ptr(), 1, n, 1, n, n, s0, n0, Y.data_ptr(), n, n, 1, sp),
+               "spectrum")
+    rows = torch.empty_like(rows_ref)
+    en = torch.empty_like(en_ref)
+    v0 = torch.empty(b, dtype=torch.complex128, device="cuda")
+    _lib.check(lib.afft_alias_rows(Y.data_ptr(), n, b, sb, ns, idx.data_ptr(), idx.numel(),
+                                   rows.data_ptr(), en.data_ptr(), v0.data_ptr(), sp), "alias")
+    scale = float(rows_ref.abs().max())
+    assert float((rows - rows_ref).abs().max()) <= 1e-12 * scale
+    assert torch.allclose(en, en_ref, rtol=1e-11, atol=0)
+    ref0 = np.fft.fft(x.cpu().numpy()[::L]) / b
+    assert np.allclose(v0.cpu().numpy(), ref0, rtol=0, atol=1e-12 * np.abs(ref0).max())
