@@ -812,7 +812,10 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     // up: ~0.2 ms per signal), pre-pass + decode 22.25 ms, stream alone 18.65 ms.
     // Small batches (< 2 waves) cannot keep HBM busy with one streaming CTA per signal.
     const int sms = num_sms();
-    int mode = batch < 2 * sms ? 1 : 0;
+    // Below ~3 waves of fused CTAs (3 per SM) the last partial wave streams with too
+    // few CTAs; the multi-CTA pre-pass wins there (tools/batch_sweep.py: 512 signals
+    // 1.52 vs 1.75 ms, 1024 2.93 vs 3.01 ms; from 1536 up the fused kernel wins).
+    int mode = batch < 9 * sms ? 1 : 0;
     if (env && env[0] >= '0' && env[0] <= '3') mode = env[0] - '0';
     if (nparts < 2) mode = 0;
     if (mode == 3) {
