@@ -113,7 +113,6 @@ struct GStockParams {
 constexpr int kTwLoBits = 12;
 constexpr int kGStockThreads = 256;
 constexpr int kGStockPoints = 2048;  // points per tile (cnt * R)
-constexpr int kPer = 1;  // loads per thread batched in the gather loop (more spills at 85 regs)
 
 __global__ void twiddle_tables_kernel(int64_t b, cd* __restrict__ tlo, int nlo,
                                       cd* __restrict__ thi, int nhi) {
@@ -135,20 +134,40 @@ __device__ __forceinline__ cd tw_b(const cd* tlo, const cd* thi, int64_t m) {
   return (m >> kTwLoBits) ? cmul(thi[m >> kTwLoBits], lo) : lo;
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+
+// One pass.  The tile's rows arrive by cp.async into a staging copy (every request
+// in flight at once, no registers held), a second smem pass applies the inter-pass
+// twiddles while transposing into sequences of stride ld = R + 1 (bank-conflict
+// free column access), the smem Stockham runs on that stride, and the output rows
+// leave coalesced.
 __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     const __grid_constant__ GStockParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int R = p.R, cnt = p.cnt;
+  const int ld = (R & 1) ? R : R + 1;
   const int tid = threadIdx.x, nt = blockDim.x;
   cd* tw = reinterpret_cast<cd*>(smem_raw);
   cd* bufA = tw + R;
-  cd* bufB = bufA + (size_t)cnt * R;
+  cd* bufB = bufA + (size_t)cnt * ld;
   build_twiddles(tw, R, tid, nt);
   const int64_t nb = p.b / R;
   const int64_t nchunks = (nb + cnt - 1) / cnt;
   const int64_t ntiles = p.batch * p.nshift * nchunks;
   const int64_t tstep = p.b / (p.Ns * R);
   const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
+  const bool first = p.in == nullptr;
+  const bool c64 = first && p.dtype == AFFT_C64;
   const double inv_b = 1.0 / (double)p.b;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t chunk = tile % nchunks;
@@ -159,63 +178,77 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     const int c = (int)min((int64_t)cnt, nb - j0);
     const int64_t seq = s * p.nshift + t;
     const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
-    const int64_t tau = p.in ? 0
-                             : (p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n)
-                                              : p.tau[t]);
-    __syncthreads();  // twiddles ready / previous tile consumed
-    // row r: c contiguous butterflies (kPer > 1 batches loads per thread; at the
-    // 85-register cap that spilled and measured slower)
+    const int64_t tau = first ? (p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n)
+                                               : p.tau[t])
+                              : 0;
     const int total = c * R;
-    for (int base = 0; base < total; base += nt * kPer) {
-      cd v[kPer];
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int e = base + tid + u * nt;
-        if (e < total) {
-          const int r = e / c;
-          const int64_t src = j0 + (e - r * c) + r * nb;
-          if (p.in) {
-            v[u] = p.in[seq * p.b + src];
-          } else {
-            int64_t idx = src * p.L - tau;
-            if (idx < 0) idx += p.n;
-            v[u] = load_sample(xs, p.dtype, idx);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int e = base + tid + u * nt;
-        if (e < total) {
-          const int r = e / c;
-          const int jj = e - r * c;
-          const int64_t j = j0 + jj;
-          const int64_t k = p.Ns == 1 ? 0 : j % p.Ns;
-          cd a = v[u];
-          if (r && k) a = cmul(a, tw_b(p.tlo, p.thi, k * r * tstep));
-          bufA[jj * R + r] = a;
-        }
+    // e / c and e / R by multiply-high (e < 2^13, divisors < 2^13: exact)
+    const unsigned Mc = c > 1 ? (unsigned)((0xffffffffull + c) / c) : 0u;
+    const unsigned MR = (unsigned)((0xffffffffull + R) / R);
+    // k = (j0 + jj) mod N_s for jj < c, from one 64-bit reduction per tile
+    const int64_t k0 = p.Ns > 1 ? j0 % p.Ns : 0;
+    __syncthreads();  // twiddles ready / previous tile's buffers consumed
+    // 1. rows r = 0..R-1, each c contiguous butterflies, into staging (bufB) in
+    //    arrival order e = r * c + jj
+    for (int e = tid; e < total; e += nt) {
+      const int r = c > 1 ? (int)__umulhi((unsigned)e, Mc) : e;
+      const int64_t src = j0 + (e - r * c) + r * nb;
+      if (first) {
+        int64_t idx = src * p.L - tau;
+        if (idx < 0) idx += p.n;
+        if (c64)
+          cp_async8(reinterpret_cast<float2*>(bufB) + e, xs + idx * 8);
+        else
+          cp_async16(bufB + e, xs + idx * 16);
+      } else {
+        cp_async16(bufB + e, p.in + seq * p.b + src);
       }
     }
+    cp_async_wait_all();
     __syncthreads();
-    const cd* spec = smem_dft(bufA, bufB, c, p.plan, tw, tid, nt);
+    // 2. twiddle w_b^(k r b/(N_s R)) and transpose into sequences of stride ld
+#pragma unroll 4
+    for (int e = tid; e < total; e += nt) {
+      const int r = c > 1 ? (int)__umulhi((unsigned)e, Mc) : e;
+      const int jj = e - r * c;
+      cd a;
+      if (c64) {
+        const float2 f = reinterpret_cast<const float2*>(bufB)[e];
+        a = cd{(double)f.x, (double)f.y};
+      } else {
+        a = bufB[e];
+      }
+      if (p.Ns > 1 && r) {
+        int64_t k = k0 + jj;
+        while (k >= p.Ns) k -= p.Ns;
+        if (k) a = cmul(a, tw_b(p.tlo, p.thi, k * r * tstep));
+      }
+      bufA[jj * ld + r] = a;
+    }
+    __syncthreads();
+    const cd* spec = smem_dft(bufA, bufB, c, p.plan, tw, tid, nt, ld);
     double* out = p.out ? p.out + 2 * (s * p.out_signal_stride + p.out_offset +
                                        t * p.out_shift_stride)
                         : nullptr;
     cd* tmp = p.tmp ? p.tmp + seq * p.b : nullptr;
-    for (int e = tid; e < c * R; e += nt) {
+    // 3. outputs: butterfly j's V[q] goes to (j / N_s) N_s R + k + q N_s
+    for (int e = tid; e < total; e += nt) {
       int jj, q;
       if (p.Ns == 1) {  // first pass: butterfly j's outputs are the contiguous j*R + q
-        jj = e / R;
+        jj = (int)__umulhi((unsigned)e, MR);
         q = e - jj * R;
       } else {          // output row q: c contiguous k
-        q = e / c;
+        q = c > 1 ? (int)__umulhi((unsigned)e, Mc) : e;
         jj = e - q * c;
       }
       const int64_t j = j0 + jj;
-      const int64_t k = p.Ns == 1 ? 0 : j % p.Ns;
-      const int64_t dst = (j - k) * R + k + q * p.Ns;  // (j / Ns) Ns R + k + q Ns
-      const cd v = spec[jj * R + q];
+      int64_t k = 0;
+      if (p.Ns > 1) {
+        k = k0 + jj;
+        while (k >= p.Ns) k -= p.Ns;
+      }
+      const int64_t dst = (j - k) * R + k + q * p.Ns;
+      const cd v = spec[jj * ld + q];
       if (tmp) {
         tmp[dst] = v;
       } else {
@@ -318,7 +351,8 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     g.in = s == 0 ? nullptr : bufs[(s - 1) & 1];
     g.tmp = s == P - 1 ? nullptr : bufs[s & 1];
     g.out = s == P - 1 ? out : nullptr;
-    const size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * R) * 16;
+    const int ldR = (R & 1) ? R : R + 1;
+    const size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
     e = cudaFuncSetAttribute(gstockham_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     int occ = 0;

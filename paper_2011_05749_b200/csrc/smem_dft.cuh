@@ -209,7 +209,7 @@ __device__ __forceinline__ void bfly_pow2(const cd* __restrict__ src, cd* __rest
 
 template <int kMaxR>
 __device__ inline cd* smem_dft_pow2(cd* a, cd* b, int count, const DftPlan& p, const cd* tw,
-                                    int tid, int nthreads) {
+                                    int tid, int nthreads, int ld) {
   const int lgn = p.lgn;
   int lgNs = 0;
   for (int s = 0; s < p.nstages; ++s) {
@@ -222,7 +222,7 @@ __device__ inline cd* smem_dft_pow2(cd* a, cd* b, int count, const DftPlan& p, c
 #define AFFT_POW2_STAGE(RR, LG)                                                         \
   for (int w = tid; w < total; w += nthreads) {                                         \
     const int seq = w >> lgnb, j = w & (nb - 1);                                        \
-    bfly_pow2<RR, LG>(a + (seq << lgn), b + (seq << lgn), tw, nb, lgNs, lgtstep, j);    \
+    bfly_pow2<RR, LG>(a + seq * ld, b + seq * ld, tw, nb, lgNs, lgtstep, j);            \
   }
     if (kMaxR >= 16 && R == 16) {
       AFFT_POW2_STAGE(16, 4)
@@ -250,10 +250,13 @@ __device__ inline cd* smem_dft_pow2(cd* a, cd* b, int count, const DftPlan& p, c
 // called by all threads of the block (contains __syncthreads).
 // kMaxR: the largest power-of-two register butterfly compiled in (must cover the
 // plan's, see make_dft_plan's max_radix).
+// ld: distance between consecutive sequences (>= n; n + 1 avoids bank conflicts when
+// a caller writes or reads the buffer column-wise).
 template <int kMaxR = 8>
 __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const cd* tw, int tid,
-                        int nthreads) {
-  if (p.lgn >= 0) return smem_dft_pow2<kMaxR>(a, b, count, p, tw, tid, nthreads);
+                        int nthreads, int ld = 0) {
+  if (ld <= 0) ld = p.n;
+  if (p.lgn >= 0) return smem_dft_pow2<kMaxR>(a, b, count, p, tw, tid, nthreads, ld);
   const int n = p.n;
   int Ns = 1;
   for (int s = 0; s < p.nstages; ++s) {
@@ -268,8 +271,8 @@ __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const 
       case 7:
         for (int w = tid; w < total; w += nthreads) {
           const int seq = w / nb, j = w - seq * nb;
-          const cd* src = a + (size_t)seq * n;
-          cd* dst = b + (size_t)seq * n;
+          const cd* src = a + (size_t)seq * ld;
+          cd* dst = b + (size_t)seq * ld;
           if (R == 2) bfly_small<2>(src, dst, tw, n, nb, Ns, j);
           else if (R == 3) bfly_small<3>(src, dst, tw, n, nb, Ns, j);
           else if (R == 4) bfly_small<4>(src, dst, tw, n, nb, Ns, j);
@@ -280,7 +283,7 @@ __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const 
       default: {
         for (int w = tid; w < total; w += nthreads) {
           const int seq = w / nb, j = w - seq * nb;
-          scale_generic(a + (size_t)seq * n, tw, n, R, nb, Ns, j);
+          scale_generic(a + (size_t)seq * ld, tw, n, R, nb, Ns, j);
         }
         __syncthreads();
         const int outs = total * R;
@@ -288,7 +291,7 @@ __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const 
           const int q = w % R;
           const int bw = w / R;
           const int seq = bw / nb, j = bw - seq * nb;
-          out_generic(a + (size_t)seq * n, b + (size_t)seq * n, tw, n, R, nb, Ns, j, q);
+          out_generic(a + (size_t)seq * ld, b + (size_t)seq * ld, tw, n, R, nb, Ns, j, q);
         }
       }
     }
