@@ -131,6 +131,18 @@ __global__ void __launch_bounds__(kVoteThreads) dt_vote_kernel(int M, int a_m, i
 
 // ------------------------------------------------------------------ solve
 
+// Out of line so its small-matrix frame does not crowd the enumeration loop's registers.
+__device__ __noinline__ int moment_coeffs_call(const la::c2* row, int a_m, int a, la::c2* out) {
+  dt::Moments M{row, a_m};
+  return dt::moment_coeffs(M, a, out) ? 1 : 0;
+}
+
+// w_L^j = exp(-2 pi i j / L), j < L: the grid-candidate roots shared by every bucket.
+__global__ void roots_kernel(int64_t L, la::c2* __restrict__ roots) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < L) roots[j] = dt::root_pi_(j, L);
+}
+
 // dt2 locate with one warp per bucket (oneshot.py:182-198): lane 0 solves the
 // moment coefficients, the lanes split the n/b grid candidates, and a butterfly
 // merge of per-lane sorted lists keeps the `take` smallest |P| under (|P|, j) —
@@ -138,10 +150,11 @@ __global__ void __launch_bounds__(kVoteThreads) dt_vote_kernel(int M, int a_m, i
 // count, 0 for an empty bucket, -1 for None.
 constexpr int kDt2LocateThreads = 256;
 
-__global__ void __launch_bounds__(kDt2LocateThreads) dt2_locate_warp_kernel(
+__global__ void __launch_bounds__(kDt2LocateThreads, 3) dt2_locate_warp_kernel(
     int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
     const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
-    int64_t b, int64_t n, int64_t* __restrict__ cands, int32_t* __restrict__ ncand) {
+    int64_t b, int64_t n, const la::c2* __restrict__ rootsL, int64_t* __restrict__ cands,
+    int32_t* __restrict__ ncand) {
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (e >= total) return;
@@ -155,10 +168,8 @@ __global__ void __launch_bounds__(kDt2LocateThreads) dt2_locate_warp_kernel(
   const int64_t bucket = bucket_ids ? bucket_ids[e] : e - s * nrows;
   la::c2 coeffs[dt::kMaxAm];
   int ok = 0;
-  if (lane == 0) {
-    dt::Moments M{reinterpret_cast<const la::c2*>(meas) + e * R, a_m};
-    ok = dt::moment_coeffs(M, a, coeffs);
-  }
+  if (lane == 0) ok = moment_coeffs_call(reinterpret_cast<const la::c2*>(meas) + e * R, a_m, a,
+                                         coeffs);
   ok = __shfl_sync(0xffffffffu, ok, 0);
   if (!ok) {
     if (lane == 0) ncand[e] = -1;
@@ -178,21 +189,61 @@ __global__ void __launch_bounds__(kDt2LocateThreads) dt2_locate_warp_kernel(
     bv[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     bj[i] = kNone;
   }
-  for (int64_t j = lane; j < step; j += 32) {
-    const double v = dt::poly_abs_at(coeffs, a, dt::pmod(bucket + b * j, n), n);
-    // j ascends within a lane: strict < keeps the earlier j among equal values
-    if (v < bv[take - 1] || bj[take - 1] == kNone) {
-      int i = take - 1;
-      while (i > 0 && (bv[i - 1] > v || bj[i - 1] == kNone)) {
-        bv[i] = bv[i - 1];
-        bj[i] = bj[i - 1];
-        --i;
+  // insert (v, j) into the sorted (value, j) list of the first `take` slots; the
+  // displaced element carries on and the last one drops (compile-time indices only)
+  auto insert = [&](double v, int64_t j) {
+#pragma unroll
+    for (int i = 0; i < dt::kMaxAm; ++i) {
+      const bool before = i < take && j != kNone &&
+                          (bj[i] == kNone || v < bv[i] || (v == bv[i] && j < bj[i]));
+      if (before) {
+        const double tv = bv[i];
+        const int64_t tj = bj[i];
+        bv[i] = v;
+        bj[i] = j;
+        v = tv;
+        j = tj;
       }
-      bv[i] = v;
-      bj[i] = j;
     }
+  };
+  // candidate z_j = w_n^(bucket + b j) = w_n^bucket * w_L^j  (L = n/b, table roots)
+  const la::c2 z0 = dt::root_pi_(bucket, n);
+  double worst = __longlong_as_double(0x7ff0000000000000ll);  // value in slot take-1
+  double worst_sq = worst;  // worst^2 (1 + 1e-13): a safe cheap reject on |y|^2
+  bool full = false;
+  auto consider = [&](la::c2 y, int64_t j) {
+    if (full && !(la::abs2(y) <= worst_sq)) return;  // |y| > worst beyond any rounding
+    const double v = la::cabs(y);
+    // j ascends within a lane, so an equal value never displaces (earlier j wins)
+    if (full && !(v < worst)) return;
+    insert(v, j);
+#pragma unroll
+    for (int i = 0; i < dt::kMaxAm; ++i)
+      if (i == take - 1) {
+        worst = bv[i];
+        full = bj[i] != kNone;
+      }
+    worst_sq = worst * worst * (1.0 + 1e-13);
+  };
+  // two independent candidates per iteration (the Horner chains are latency-bound)
+  int64_t j = lane;
+  for (; j + 32 < step; j += 64) {
+    const la::c2 za = la::mul(z0, rootsL[j]), zb = la::mul(z0, rootsL[j + 32]);
+    la::c2 ya = la::C(1.0), yb = la::C(1.0);
+    for (int k = a - 1; k >= 0; --k) {
+      ya = la::add(la::mul(ya, za), coeffs[k]);
+      yb = la::add(la::mul(yb, zb), coeffs[k]);
+    }
+    consider(ya, j);
+    consider(yb, j + 32);
   }
-  // butterfly merge of sorted (value, j) lists; lists of different lanes are disjoint
+  for (; j < step; j += 32) {
+    const la::c2 z = la::mul(z0, rootsL[j]);
+    la::c2 y = la::C(1.0);
+    for (int k = a - 1; k >= 0; --k) y = la::add(la::mul(y, z), coeffs[k]);
+    consider(y, j);
+  }
+  // butterfly merge: insert the partner lane's list (lists of different lanes are disjoint)
   for (int o = 16; o > 0; o >>= 1) {
     double ov[dt::kMaxAm];
     int64_t oj[dt::kMaxAm];
@@ -201,31 +252,8 @@ __global__ void __launch_bounds__(kDt2LocateThreads) dt2_locate_warp_kernel(
       ov[i] = __shfl_xor_sync(0xffffffffu, bv[i], o);
       oj[i] = __shfl_xor_sync(0xffffffffu, bj[i], o);
     }
-    double mv[dt::kMaxAm];
-    int64_t mj[dt::kMaxAm];
-    int x = 0, y = 0;
 #pragma unroll
-    for (int i = 0; i < dt::kMaxAm; ++i) {
-      if (i >= take) break;
-      // (value, j) lexicographic; an empty slot (j = kNone) sorts last
-      const bool left = oj[y] == kNone ||
-                        (bj[x] != kNone && (bv[x] < ov[y] || (bv[x] == ov[y] && bj[x] < oj[y])));
-      if (left) {
-        mv[i] = bv[x];
-        mj[i] = bj[x];
-        ++x;
-      } else {
-        mv[i] = ov[y];
-        mj[i] = oj[y];
-        ++y;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < dt::kMaxAm; ++i)
-      if (i < take) {
-        bv[i] = mv[i];
-        bj[i] = mj[i];
-      }
+    for (int i = 0; i < dt::kMaxAm; ++i) insert(ov[i], oj[i]);
   }
   if (lane == 0) {
     int64_t pos[dt::kMaxAm];
@@ -482,16 +510,20 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
   const int64_t total = batch * nrows;
   cudaStream_t st = (cudaStream_t)stream;
   int64_t* cands = nullptr;
-  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands),
-                                (size_t)total * (dt::kMaxAm * 8 + 4), st);
+  const int64_t L = n / b;
+  const size_t cbytes = ((size_t)total * (dt::kMaxAm * 8 + 4) + 255) / 256 * 256;
+  const size_t rbytes = variant == dt::VAR_DT2 ? (size_t)L * 16 : 0;
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands), cbytes + rbytes, st);
   if (e != cudaSuccess) return cuda_status(e, "scratch (dt candidates)");
   int32_t* ncand = reinterpret_cast<int32_t*>(cands + total * dt::kMaxAm);
   if (variant == dt::VAR_DT2) {
+    la::c2* roots = reinterpret_cast<la::c2*>(reinterpret_cast<char*>(cands) + cbytes);
+    roots_kernel<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(L, roots);
     const int64_t threads = total * 32;
     dt2_locate_warp_kernel<<<(unsigned)((threads + kDt2LocateThreads - 1) / kDt2LocateThreads),
                              kDt2LocateThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
-                                                         counts, bucket_ids, a_cap, b, n, cands,
-                                                         ncand);
+                                                         counts, bucket_ids, a_cap, b, n, roots,
+                                                         cands, ncand);
   } else {
     dt_locate_rows_kernel<<<(unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads),
                             kDtSolveThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,

@@ -43,6 +43,19 @@ __host__ __device__ __forceinline__ c2 unit_root_(int64_t prod, int64_t n) {
   return c2{c, s};
 }
 
+// exp(-2 pi i m / q) with the argument reduced exactly (sincospi), m in [0, q)
+__host__ __device__ __forceinline__ c2 root_pi_(int64_t m, int64_t q) {
+  double s, c;
+#ifdef __CUDA_ARCH__
+  sincospi(-2.0 * (double)m / (double)q, &s, &c);
+#else
+  const double th = -6.283185307179586 * ((double)m / (double)q);
+  s = sin(th);
+  c = cos(th);
+#endif
+  return c2{c, s};
+}
+
 // Python float modulo x % y for y > 0 (result in [0, y)).
 __host__ __device__ __forceinline__ double pyfmod(double x, double y) {
   double m = fmod(x, y);
