@@ -380,18 +380,40 @@ def dsfft(x, k: int, config: DsfftConfig | None = None,
     return SparseSpectrum(n, dict(ranked[:k]))
 
 
-def dsfft_batch(xs, k: int, configs) -> list[SparseSpectrum]:
-    """DSFFT over several signals (per-signal layer paths differ, so signals run in turn)."""
+def dsfft_batch(xs, k: int, configs, streams: int = 1) -> list[SparseSpectrum]:
+    """DSFFT over several signals, in input order.  Each signal's layer path is
+    data-dependent host control flow; with streams > 1 signals run on worker threads,
+    each with its own CUDA stream (the library is reentrant per stream).  Measured at
+    config 4 (tools/bench_suite.py): 4 streams are no faster than 1 — the per-layer
+    host work holds the GIL — and give identical results, so the default is 1."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
     xd = _device.as_device_batch(xs)
-    out = []
-    for i in range(int(xd.shape[0])):
-        cfg = configs[i] if isinstance(configs, (list, tuple)) else configs
-        out.append(dsfft(xd[i], k, cfg))
+    count = int(xd.shape[0])
+    cfgs = [configs[i] if isinstance(configs, (list, tuple)) else configs for i in range(count)]
+    workers = max(1, min(int(streams), count))
+    if workers == 1:
+        return [dsfft(xd[i], k, cfgs[i]) for i in range(count)]
+    main = torch.cuda.current_stream(xd.device)
+    local = threading.local()
+    made: list = []
+    lock = threading.Lock()
+
+    def work(i):
+        if not hasattr(local, "stream"):
+            local.stream = torch.cuda.Stream(device=xd.device)
+            local.stream.wait_stream(main)  # the batch was produced on the caller's stream
+            with lock:
+                made.append(local.stream)
+        with torch.cuda.stream(local.stream):
+            return dsfft(xd[i], k, cfgs[i])
+
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        out = list(ex.map(work, range(count)))
+    for st in made:
+        main.wait_stream(st)
     return out
-
-
-# ------------------------------------------------------------------ host-visible layer API
-
 
 def _to_tree_layer(layer: _DevLayer) -> TreeLayer:
     if layer.cand is None:
