@@ -114,3 +114,41 @@ def dsfft_signal(case):
     x = generate_test_case(case["n"], case["k"], case["snr"], case["seed"],
                            positions=case.get("positions")).signal
     return x.astype(np.complex64) if case.get("c64") else x
+
+
+# ---- fixtures mirroring the reference suite's inputs (tests/conftest.py of the
+# reference: the same seeds and fixed tone positions, regenerated with our model)
+
+@pytest.fixture
+def five_tone_n20():
+    """20-point exact case with tones at {1, 3, 5, 10, 13}."""
+    from paper_2011_05749_b200 import generate_test_case
+
+    return generate_test_case(20, 5, "exact", seed=7, positions=[1, 3, 5, 10, 13])
+
+
+@pytest.fixture
+def five_tone_n64():
+    """64-point exact case with tones at {1, 6, 13, 20, 59}."""
+    from paper_2011_05749_b200 import generate_test_case
+
+    return generate_test_case(64, 5, "exact", seed=11, positions=[1, 6, 13, 20, 59])
+
+
+def brute_dft(x):
+    """O(n^2) forward transform, 1/n scaled (independent of every FFT under test)."""
+    x = np.asarray(x, dtype=np.complex128)
+    n = x.size
+    idx = np.arange(n)
+    return np.exp(-2j * np.pi * np.outer(idx, idx) / n) @ x / n
+
+
+def alias_sum(spectrum, b, tau):
+    """Bucket values from a full spectrum: sum over the residue class of i mod b of
+    X[f] * w^(tau f) (the aliasing identity, evaluated term by term)."""
+    spectrum = np.asarray(spectrum, dtype=np.complex128)
+    n = spectrum.size
+    out = np.zeros(b, dtype=np.complex128)
+    for f in range(n):
+        out[f % b] += spectrum[f] * np.exp(-2j * np.pi * ((tau * f) % n) / n)
+    return out
