@@ -120,11 +120,19 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
   // stops (returns > bound) once the partial sum exceeds bound: every term is
   // >= 0, so such a candidate is strictly worse than the candidate that set bound
   // and can be neither the minimum nor a tie.
+  // target = RN(RN(-2 pi r) / n) by Markstein's sequence with the correctly rounded
+  // reciprocal: q0 = RN(x inv), rem = x - q0 n (exact, fma), q = RN(q0 + rem inv).
+  // Bit-identical to the IEEE quotient for every r in [0, n) at n <= 2^28 and a
+  // 2^28-point sweep at n = 3e9 (tools/div_check.cu; r = 0 keeps the -0.0 of x / n).
+  const double inv = 1.0 / dn;
   auto score = [&](int64_t t, double bound) -> double {
     int64_t r = idx + b * t;  // cand = (index + b*t) mod n, already < n
     double sc = 0.0;
     for (int j = 0; j < c; ++j) {
-      const double tgt = __ddiv_rn(__dmul_rn(-kTwoPi, (double)r), dn);
+      const double x = __dmul_rn(-kTwoPi, (double)r);
+      const double q0 = __dmul_rn(x, inv);
+      const double q = __fma_rn(__fma_rn(-q0, dn, x), inv, q0);
+      const double tgt = r ? q : x;
       const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
       sc = __dadd_rn(sc, __dmul_rn(wv, wv));
       if (sc > bound) return sc;
