@@ -56,7 +56,7 @@ __device__ __forceinline__ double warp_vnorm(c2 v, int P, int lane) {
 
 // refit (oneshot.py:229-232): x = lstsq(A[:, sup], y) with numpy's cutoff; returns
 // ||y - A_s x||.  S.sup[0..cnt) are atom indices; the solution lands in S.x.
-__device__ inline double warp_refit(WarpPursuit& S, int P, int cnt, int lane) {
+__device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int lane) {
   c2 w[kCols], v[kCols];
 #pragma unroll
   for (int c = 0; c < kCols; ++c) {

@@ -291,9 +291,9 @@ __global__ void __launch_bounds__(kDtSolveThreads) dt_locate_rows_kernel(
 
 // estimate_values for every row, one warp per row (dt_warp.cuh).  Row e belongs
 // to signal e / nrows, whose random shifts start at rshifts + signal * shift_stride.
-constexpr int kDtEstWarps = 4;
+constexpr int kDtEstWarps = 1;
 
-__global__ void __launch_bounds__(kDtEstWarps * 32) dt_estimate_warp_kernel(
+__global__ void __launch_bounds__(kDtEstWarps * 32, 24) dt_estimate_warp_kernel(
     int64_t total, int64_t nrows, int R, int a_m, int p, const double* __restrict__ meas,
     const int64_t* __restrict__ rshifts, int64_t shift_stride, const int64_t* __restrict__ cands,
     const int32_t* __restrict__ ncand, int64_t b, int64_t n, int out_stride,
