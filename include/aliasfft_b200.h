@@ -187,7 +187,7 @@ size_t afft_singleton_workspace_size(int64_t n, int64_t count, int64_t b, int32_
  * singleton_search_noisy (peeling.py:222-250) for `count` nodes of one cycle size b:
  * residual [count][c*m], index [count]; shifts (host) = SearchPlan.shifts, weights
  * (host) = kay_weights(m).  Outputs f0, val (complex128), resnorm per node.
- * Workspace: afft_singleton_workspace_size(n, count, b, c, m).  Synchronises.
+ * Workspace: afft_singleton_workspace_size(n, count, b, c, m).  Stream-ordered.
  */
 int afft_singleton_search_noisy(const double* residual, const int64_t* index, int64_t count,
                                 int64_t b, int64_t n, const int64_t* shifts, int32_t nshift,
@@ -326,6 +326,35 @@ int afft_selective_sums(const void* x, int dtype, int64_t n, int64_t b, const in
 /* np.median per row of `count` values: mode 0 real values, mode 1 |complex|^2. */
 int afft_median(const double* values, int32_t mode, int64_t count, int64_t batch, double* out,
                 void* stream);
+
+/*
+ * The whole DSFFT decode of one signal (dsfft.py:244-267 with 69-241): the layer loop
+ * runs natively (one read-back per layer), every layer on the primitives above.
+ * Host inputs drawn from numpy's PCG64 by the caller: the noisy search plan
+ * (anchors [c], Kay weights [m-1]; dsfft.py:142-150) and, for every possible stop
+ * depth d, the DT3 random shifts dt_shifts[dt_shift_off[d] .. dt_shift_off[d+1])
+ * (dsfft.py:207-212).  Output: the entries dict in insertion order (host arrays,
+ * out_count set even on AFFT_ENOMEM) and a trace of [kind, depth, a, b] records:
+ * 0 calibrate, 1 initial (m_d), 2 expand (m_d, candidates or -1), 3 classify
+ * (#single, #multi), 4 resolve (#buckets, p), 5 classify read set (R, mode).
+ */
+typedef struct {
+  double theta;          /* DsfftConfig.theta (stop rule) */
+  int32_t mode;          /* 0 exact, 1 noisy */
+  int32_t a_m;
+  double noise_std;      /* <= 0: calibrate (noisy mode) */
+  double activity_floor; /* DsfftConfig.activity_floor */
+  int32_t c, m;          /* noisy search plan */
+  const int64_t* anchors;
+  const double* weights;
+  const int64_t* dt_shifts;
+  const int32_t* dt_shift_off; /* [log2(n) + 2] */
+} AfftDsfftParams;
+
+int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k, const AfftDsfftParams* params,
+               int64_t* out_pos /* host */, double* out_val /* host */, int64_t capacity,
+               int64_t* out_count /* host */, int32_t* trace /* host */, int32_t trace_capacity,
+               int32_t* trace_len /* host */, void* stream);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,7 @@ SIGNATURES = {
     "afft_active_indices": (_INT, [_P, _I64, _D, _P, _P, _P, _P]),
     "afft_selective_sums": (_INT, [_P, _INT, _I64, _I64, _P, _I64, _P, _P]),
     "afft_median": (_INT, [_P, _I32, _I64, _I64, _P, _P]),
+    "afft_dsfft": (_INT, [_P, _INT, _I64, _I32, _P, _P, _P, _I64, _P, _P, _I32, _P, _P]),
 }
 
 _lock = threading.Lock()
@@ -92,6 +93,24 @@ _lib = None
 
 class LibraryNotBuilt(ImportError):
     """The CUDA library is missing: build it with __graft_entry__.build()."""
+
+
+class DsfftParams(ctypes.Structure):
+    """AfftDsfftParams (include/aliasfft_b200.h)."""
+
+    _fields_ = [
+        ("theta", ctypes.c_double),
+        ("mode", ctypes.c_int32),
+        ("a_m", ctypes.c_int32),
+        ("noise_std", ctypes.c_double),
+        ("activity_floor", ctypes.c_double),
+        ("c", ctypes.c_int32),
+        ("m", ctypes.c_int32),
+        ("anchors", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+        ("dt_shifts", ctypes.c_void_p),
+        ("dt_shift_off", ctypes.c_void_p),
+    ]
 
 
 def load():

@@ -1,0 +1,546 @@
+// Native DSFFT layer loop (dsfft.py:244-267 and its helpers 69-241) over the device
+// primitives of dsfft.cu / rffast.cu / oneshot.cu.
+//
+// The tree search is data-dependent host control flow: every layer reads back one
+// active count, every classification one small result block.  Run from Python, the
+// per-layer interpreter work and the tensor bookkeeping around ~20 library calls
+// left the GPU idle for about half of a config-4 decode; here the same sequence of
+// launches is issued from C++ with one synchronisation per read-back.  The control
+// flow, thresholds and insertion orders follow the reference line by line:
+//
+//   calibrate   (231-241)  noise_std = sqrt(b * median|v|^2 / ln 2) when absent;
+//   initial     (69-79)    full layer at depth ceil(log2 k), active by |v| > thr;
+//   expand      (82-115)   children {i, i + 2^(d-1)}: direct alias sums when
+//                          2 m_{d-1} <= d, else the full layer;
+//   classify    (118-174)  exact: shifts 0,1,2 + classify_exact with the signal's
+//                          exact threshold; noisy: the c*m search-plan shifts,
+//                          T0/T1 from noise_std (floor 1e-8 sqrt(max energy)) or
+//                          the quiet-bucket median, then classify_noisy;
+//   loop        (258-264)  expand while m_d < theta k; then (noisy) re-expand while
+//                          multitons remain; entries come from the last classify;
+//   resolve     (201-228)  leftover multitons through the DT3 detect + solve with
+//                          p = max(12, ceil(a_m log10 max(n/b, 10))) random shifts.
+//
+// Host inputs that must come from numpy's PCG64 (the search-plan anchors and the
+// DT3 random shifts for every possible stop depth) are drawn by the Python caller.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "afft_common.cuh"
+
+namespace afft {
+
+__global__ void dsfft_cand_kernel(const int64_t* __restrict__ act, int64_t m, int64_t half,
+                                  int64_t* __restrict__ cand) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) {
+    cand[i] = act[i];
+    cand[m + i] = act[i] + half;
+  }
+}
+
+__global__ void dsfft_quiet_kernel(int64_t b, const int64_t* __restrict__ act, int64_t m,
+                                   uint8_t* __restrict__ quiet) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b;
+       i += (int64_t)gridDim.x * blockDim.x)
+    quiet[i] = 1;
+}
+__global__ void dsfft_unquiet_kernel(const int64_t* __restrict__ act, int64_t m,
+                                     uint8_t* __restrict__ quiet) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) quiet[act[i]] = 0;
+}
+
+// max of v[0..n) (all >= 0) into *out, one CTA.
+__global__ void __launch_bounds__(1024) dsfft_max_kernel(const double* __restrict__ v, int64_t n,
+                                                         double* __restrict__ out) {
+  __shared__ double part[32];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, part[w]);
+    *out = r;
+  }
+}
+
+// sum |Y|^2 for the floor bound (order irrelevant: a bound with a wide margin)
+__global__ void __launch_bounds__(1024) dsfft_norm2_kernel(const cd* __restrict__ y, int64_t n,
+                                                           double* __restrict__ out) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s += y[i].re * y[i].re + y[i].im * y[i].im;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += part[w];
+    atomicAdd(out, r);
+  }
+}
+
+namespace {
+
+// Stream-ordered device buffer from the library pool.
+struct DBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) scratch_free(p, st);
+    p = nullptr;
+  }
+  int alloc(size_t bytes, cudaStream_t s, const char* what) {
+    reset();
+    st = s;
+    cudaError_t e = scratch_alloc(&p, std::max<size_t>(bytes, 16), s);
+    return e == cudaSuccess ? AFFT_OK : cuda_status(e, what);
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+template <class T>
+int d2h(std::vector<T>& h, const void* d, size_t count, cudaStream_t st) {
+  h.resize(count);
+  if (!count) return AFFT_OK;
+  cudaError_t e = cudaMemcpyAsync(h.data(), d, count * sizeof(T), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? AFFT_OK : cuda_status(e, "dsfft read-back");
+}
+
+#define RC(expr)          \
+  do {                    \
+    int _rc = (expr);     \
+    if (_rc) return _rc;  \
+  } while (0)
+
+struct Layer {
+  int depth = 0;
+  int64_t m = 0;     // active count
+  DBuf active;       // ascending bucket indices (device int64)
+};
+
+void swap_layers(Layer& a, Layer& b) {
+  std::swap(a.depth, b.depth);
+  std::swap(a.m, b.m);
+  std::swap(a.active.p, b.active.p);
+  std::swap(a.active.st, b.active.st);
+}
+
+// Python dict insertion semantics for the entries: a new key appends, a repeated
+// key keeps its position and takes the new value.
+struct Entries {
+  std::vector<int64_t> f;
+  std::vector<cd> v;
+  std::unordered_map<int64_t, size_t> at;
+  void clear() {
+    f.clear();
+    v.clear();
+    at.clear();
+  }
+  void put(int64_t key, cd val) {
+    auto it = at.find(key);
+    if (it == at.end()) {
+      at.emplace(key, f.size());
+      f.push_back(key);
+      v.push_back(val);
+    } else {
+      v[it->second] = val;
+    }
+  }
+};
+
+struct Tracer {
+  int32_t* buf;
+  int32_t cap;
+  int32_t len = 0;
+  void add(int kind, int64_t a, int64_t b, int64_t c) {
+    if (buf && len < cap) {
+      buf[4 * len + 0] = kind;
+      buf[4 * len + 1] = (int32_t)a;
+      buf[4 * len + 2] = (int32_t)b;
+      buf[4 * len + 3] = (int32_t)c;
+    }
+    ++len;
+  }
+};
+
+struct Dsfft {
+  const void* x;
+  int dtype;
+  int64_t n;
+  int k;
+  const AfftDsfftParams& P;
+  cudaStream_t st;
+  Tracer tr;
+  int max_depth = 0;
+  double noise_std = 0.0;
+  DBuf Y;             // resident spectrum fft(x)/n (lazy)
+  double normY = -1;  // ||Y||^2 (lazy)
+
+  static constexpr int64_t kAliasMaxL = 32;
+
+  bool alias_ok(int64_t b) const { return n / b <= kAliasMaxL; }
+
+  int spectrum() {
+    if (Y.p) return AFFT_OK;
+    RC(Y.alloc((size_t)n * 16, st, "dsfft spectrum"));
+    const int64_t zero = 0;
+    return afft_bucketize(x, dtype, n, 1, n, n, &zero, 1, Y.as<double>(), n, n, 1, st);
+  }
+
+  // full layer values at tau = 0 (bucketize.py:83-99)
+  int full_values(int64_t b, DBuf& vals) {
+    RC(vals.alloc((size_t)b * 16, st, "dsfft layer values"));
+    if (alias_ok(b)) {
+      RC(spectrum());
+      return afft_alias_rows(Y.as<double>(), n, b, nullptr, 0, nullptr, 0, nullptr, nullptr,
+                             vals.as<double>(), st);
+    }
+    const int64_t zero = 0;
+    return afft_bucketize(x, dtype, n, 1, n, b, &zero, 1, vals.as<double>(), b, b, 1, st);
+  }
+
+  int active(const DBuf& vals, int64_t count, double thr, const int64_t* map, Layer& out) {
+    RC(out.active.alloc((size_t)std::max<int64_t>(count, 1) * 8, st, "dsfft active"));
+    DBuf cnt;
+    RC(cnt.alloc(4, st, "dsfft count"));
+    RC(afft_active_indices(vals.as<double>(), count, thr, map, out.active.as<int64_t>(),
+                           cnt.as<int32_t>(), st));
+    std::vector<int32_t> h;
+    RC(d2h(h, cnt.p, 1, st));
+    out.m = h[0];
+    return AFFT_OK;
+  }
+
+  double threshold(int depth) const {  // dsfft.py:69-71
+    return std::max(P.activity_floor, 3.0 * noise_std / std::sqrt((double)(1LL << depth)));
+  }
+
+  int initial(int depth, Layer& out) {
+    DBuf vals;
+    RC(full_values(1LL << depth, vals));
+    out.depth = depth;
+    RC(active(vals, 1LL << depth, threshold(depth), nullptr, out));
+    tr.add(1, depth, out.m, -1);
+    return AFFT_OK;
+  }
+
+  int expand(const Layer& prev, Layer& out) {
+    const int depth = prev.depth + 1;
+    const int64_t b = 1LL << depth;
+    if (b > n) {
+      set_error("layer depth exceeds log2 of the signal size");
+      return AFFT_EINVAL;
+    }
+    out.depth = depth;
+    const double thr = threshold(depth);
+    if (2 * prev.m <= depth) {  // selective: only the children of active buckets
+      const int64_t nc = 2 * prev.m;
+      DBuf cand, vals;
+      RC(cand.alloc((size_t)std::max<int64_t>(nc, 1) * 8, st, "dsfft candidates"));
+      RC(vals.alloc((size_t)std::max<int64_t>(nc, 1) * 16, st, "dsfft candidate values"));
+      if (nc) {
+        dsfft_cand_kernel<<<(unsigned)((prev.m + 255) / 256), 256, 0, st>>>(
+            prev.active.as<int64_t>(), prev.m, b >> 1, cand.as<int64_t>());
+        RC(afft_selective_sums(x, dtype, n, b, cand.as<int64_t>(), nc, vals.as<double>(), st));
+        RC(active(vals, nc, thr, cand.as<int64_t>(), out));
+      } else {
+        RC(out.active.alloc(8, st, "dsfft active"));
+        out.m = 0;
+      }
+      tr.add(2, depth, out.m, nc);
+      return AFFT_OK;
+    }
+    DBuf vals;
+    RC(full_values(b, vals));
+    RC(active(vals, b, thr, nullptr, out));
+    tr.add(2, depth, out.m, -1);
+    return AFFT_OK;
+  }
+
+  int rows(int64_t b, const std::vector<int64_t>& shifts, const int64_t* idx, int64_t count,
+           DBuf& out, double* energy) {
+    const int ns = (int)shifts.size();
+    RC(out.alloc((size_t)std::max<int64_t>(count, 1) * ns * 16, st, "dsfft rows"));
+    if (alias_ok(b)) {
+      RC(spectrum());
+      return afft_alias_rows(Y.as<double>(), n, b, shifts.data(), ns, count ? idx : nullptr, count,
+                             out.as<double>(), energy, nullptr, st);
+    }
+    return afft_bucketize_rows(x, dtype, n, b, shifts.data(), ns, count ? idx : nullptr, count,
+                               out.as<double>(), energy, st);
+  }
+
+  // _classify_active: entries (ascending bucket order) and multiton buckets
+  int classify(const Layer& L, Entries& E, std::vector<int64_t>& multi) {
+    E.clear();
+    multi.clear();
+    const int64_t b = 1LL << L.depth;
+    const int64_t A = L.m;
+    DBuf st8, f0, val, rowsb;
+    if (A) {
+      RC(st8.alloc((size_t)A, st, "dsfft states"));
+      RC(f0.alloc((size_t)A * 8, st, "dsfft f0"));
+      RC(val.alloc((size_t)A * 16, st, "dsfft values"));
+    }
+    if (P.mode == 0) {
+      tr.add(5, L.depth, 3, 0);  // ledger: shifts 0, 1, 2
+      if (A == 0) return finish_classify(L, E, multi, st8, f0, val);
+      const std::vector<int64_t> shifts = {0, 1, 2};
+      RC(rows(b, shifts, L.active.as<int64_t>(), A, rowsb, nullptr));
+      // exact_thresholds (peeling.py:316-318)
+      const int nparts = afft_sumsq_parts(n, dtype);
+      DBuf parts, eps;
+      RC(parts.alloc((size_t)std::max(nparts, 1) * 8, st, "dsfft partials"));
+      RC(eps.alloc(8, st, "dsfft eps"));
+      RC(afft_sumsq(x, dtype, n, 1, n, parts.as<double>(), st));
+      RC(afft_exact_thresholds(parts.as<double>(), nparts, n, 1, eps.as<double>(), st));
+      std::vector<double> he;
+      RC(d2h(he, eps.p, 1, st));
+      cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st);  // -1
+      cudaMemsetAsync(val.p, 0, (size_t)A * 16, st);
+      RC(afft_classify_exact(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, he[0], he[0],
+                             st8.as<int8_t>(), f0.as<int64_t>(), val.as<double>(), st));
+      return finish_classify(L, E, multi, st8, f0, val);
+    }
+    // noisy: the search plan of dsfft.py:142-150 (anchors drawn by the caller)
+    std::vector<int64_t> shifts;
+    for (int j = 0; j < P.c; ++j)
+      for (int t = 0; t < P.m; ++t) shifts.push_back(P.anchors[j] + (int64_t(1) << j) * t);
+    const int R = (int)shifts.size();
+    tr.add(5, L.depth, R, 1);  // ledger: the plan shifts
+    const double base = noise_std / std::sqrt((double)b) * std::sqrt((double)R);
+    bool skip = false;
+    if (noise_std > 0.0 && alias_ok(b)) {
+      if (normY < 0) {
+        RC(spectrum());
+        DBuf s;
+        RC(s.alloc(8, st, "dsfft norm"));
+        cudaMemsetAsync(s.p, 0, 8, st);
+        dsfft_norm2_kernel<<<148 * 4, 1024, 0, st>>>(Y.as<cd>(), n, s.as<double>());
+        std::vector<double> h;
+        RC(d2h(h, s.p, 1, st));
+        normY = h[0];
+      }
+      skip = 1e-8 * std::sqrt((double)R * (double)(n / b) * normY) < 1.5 * base;
+    }
+    DBuf energy;
+    if (!skip) RC(energy.alloc((size_t)b * 8, st, "dsfft energies"));
+    RC(rows(b, shifts, L.active.as<int64_t>(), A, rowsb, skip ? nullptr : energy.as<double>()));
+    double t0 = 0.0, t1 = 0.0;
+    if (noise_std > 0.0) {
+      double floor = 0.0;
+      if (!skip) {
+        DBuf mx;
+        RC(mx.alloc(8, st, "dsfft max"));
+        dsfft_max_kernel<<<1, 1024, 0, st>>>(energy.as<double>(), b, mx.as<double>());
+        std::vector<double> h;
+        RC(d2h(h, mx.p, 1, st));
+        floor = 1e-8 * std::sqrt(h[0]);
+      }
+      t0 = std::max(1.5 * base, floor);
+      t1 = std::max(2.5 * base, floor);
+    } else {
+      DBuf quiet, d0, d1;
+      RC(quiet.alloc((size_t)b, st, "dsfft quiet mask"));
+      RC(d0.alloc(8, st, "dsfft t0"));
+      RC(d1.alloc(8, st, "dsfft t1"));
+      dsfft_quiet_kernel<<<148 * 4, 256, 0, st>>>(b, nullptr, 0, quiet.as<uint8_t>());
+      if (A)
+        dsfft_unquiet_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(
+            L.active.as<int64_t>(), A, quiet.as<uint8_t>());
+      RC(afft_robust_thresholds(energy.as<double>(), quiet.as<uint8_t>(), b, 1, R, d0.as<double>(),
+                                d1.as<double>(), st));
+      std::vector<double> h0, h1;
+      RC(d2h(h0, d0.p, 1, st));
+      RC(d2h(h1, d1.p, 1, st));
+      t0 = h0[0];
+      t1 = h1[0];
+    }
+    if (A == 0) return finish_classify(L, E, multi, st8, f0, val);
+    cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st);
+    cudaMemsetAsync(val.p, 0, (size_t)A * 16, st);
+    DBuf rn, ws;
+    RC(rn.alloc((size_t)A * 8, st, "dsfft resnorm"));
+    const size_t need = afft_singleton_workspace_size(n, A, b, P.c, P.m);
+    RC(ws.alloc(need, st, "dsfft search workspace"));
+    RC(afft_classify_noisy(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, shifts.data(), R,
+                           P.c, P.m, P.weights, t0, t1, st8.as<int8_t>(), f0.as<int64_t>(),
+                           val.as<double>(), rn.as<double>(), ws.p, need, st));
+    return finish_classify(L, E, multi, st8, f0, val);
+  }
+
+  int finish_classify(const Layer& L, Entries& E, std::vector<int64_t>& multi,
+                      const DBuf& st8, const DBuf& f0, const DBuf& val) {
+    const int64_t A = L.m;
+    if (A) {
+      // one read-back: pack f0 | value | bucket | state on the device first
+      DBuf pack;
+      const size_t of = 0, ov = (size_t)A * 8, oa = ov + (size_t)A * 16, os = oa + (size_t)A * 8;
+      RC(pack.alloc(os + (size_t)A, st, "dsfft result pack"));
+      char* pk = pack.as<char>();
+      cudaMemcpyAsync(pk + of, f0.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(pk + ov, val.p, (size_t)A * 16, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(pk + oa, L.active.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(pk + os, st8.p, (size_t)A, cudaMemcpyDeviceToDevice, st);
+      std::vector<char> h;
+      RC(d2h(h, pk, os + (size_t)A, st));
+      const int64_t* hf = reinterpret_cast<const int64_t*>(h.data() + of);
+      const cd* hv = reinterpret_cast<const cd*>(h.data() + ov);
+      const int64_t* ha = reinterpret_cast<const int64_t*>(h.data() + oa);
+      const int8_t* hs = reinterpret_cast<const int8_t*>(h.data() + os);
+      for (int64_t i = 0; i < A; ++i) {
+        if (hs[i] == AFFT_SINGLE_TON) {  // ascending bucket order, as the reference inserts
+          E.put(hf[i], hv[i]);
+        } else if (hs[i] == AFFT_MULTI_TON) {
+          multi.push_back(ha[i]);
+        }
+      }
+    }
+    tr.add(3, L.depth, (int64_t)E.f.size(), (int64_t)multi.size());
+    return AFFT_OK;
+  }
+
+  // _resolve_aliased: DT3 detect + solve on the leftover multi-ton buckets
+  int resolve(int depth, const std::vector<int64_t>& buckets, int64_t remaining, Entries& E) {
+    const int64_t b = 1LL << depth;
+    const int a_m = P.a_m;
+    const int32_t off0 = P.dt_shift_off[depth], off1 = P.dt_shift_off[depth + 1];
+    const int p = off1 - off0;
+    std::vector<int64_t> shifts;
+    for (int t = -a_m; t < 2 * a_m; ++t) shifts.push_back(t);
+    for (int i = off0; i < off1; ++i) shifts.push_back(P.dt_shifts[i]);
+    tr.add(4, depth, (int64_t)buckets.size(), p);
+    const int64_t nm = (int64_t)buckets.size();
+    const int R = (int)shifts.size();
+    DBuf idx, rowsb, counts, sig, rs, pos, val, cnt;
+    RC(idx.alloc((size_t)nm * 8, st, "dsfft resolve ids"));
+    cudaMemcpyAsync(idx.p, buckets.data(), (size_t)nm * 8, cudaMemcpyHostToDevice, st);
+    RC(rows(b, shifts, idx.as<int64_t>(), nm, rowsb, nullptr));
+    RC(counts.alloc((size_t)nm * 4, st, "dsfft counts"));
+    RC(sig.alloc((size_t)nm * a_m * 8, st, "dsfft sigmas"));
+    const int64_t kk = std::min<int64_t>(remaining, (int64_t)a_m * nm);
+    RC(afft_dt_detect(rowsb.as<double>(), 1, nm, R, a_m, (int32_t)kk, counts.as<int32_t>(),
+                      sig.as<double>(), st));
+    RC(rs.alloc((size_t)std::max(p, 1) * 8, st, "dsfft random shifts"));
+    if (p)
+      cudaMemcpyAsync(rs.p, P.dt_shifts + off0, (size_t)p * 8, cudaMemcpyHostToDevice, st);
+    RC(pos.alloc((size_t)nm * a_m * 8, st, "dsfft pos"));
+    RC(val.alloc((size_t)nm * a_m * 16, st, "dsfft val"));
+    RC(cnt.alloc((size_t)nm * 4, st, "dsfft cnt"));
+    RC(afft_dt_solve(rowsb.as<double>(), rs.as<int64_t>(), 1, nm, a_m, p, counts.as<int32_t>(),
+                     idx.as<int64_t>(), 3, a_m, b, n, pos.as<int64_t>(), val.as<double>(),
+                     cnt.as<int32_t>(), st));
+    DBuf pack;  // one read-back: positions | values | counts
+    const size_t ov = (size_t)nm * a_m * 8, oc = ov + (size_t)nm * a_m * 16;
+    RC(pack.alloc(oc + (size_t)nm * 4, st, "dsfft resolve pack"));
+    char* pk = pack.as<char>();
+    cudaMemcpyAsync(pk, pos.p, ov, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(pk + ov, val.p, (size_t)nm * a_m * 16, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(pk + oc, cnt.p, (size_t)nm * 4, cudaMemcpyDeviceToDevice, st);
+    std::vector<char> h;
+    RC(d2h(h, pk, oc + (size_t)nm * 4, st));
+    const int64_t* hp = reinterpret_cast<const int64_t*>(h.data());
+    const cd* hv = reinterpret_cast<const cd*>(h.data() + ov);
+    const int32_t* hc = reinterpret_cast<const int32_t*>(h.data() + oc);
+    for (int64_t r = 0; r < nm; ++r)
+      for (int j = 0; j < hc[r]; ++j) E.put(hp[r * a_m + j], hv[r * a_m + j]);  // .update()
+    return AFFT_OK;
+  }
+
+  int calibrate() {  // dsfft.py:231-241
+    int e = 0;
+    while ((1LL << e) < 32LL * k) ++e;
+    const int64_t b = std::min<int64_t>(n, 1LL << e);
+    DBuf vals, med;
+    RC(full_values(b, vals));
+    RC(med.alloc(8, st, "dsfft median"));
+    RC(afft_median(vals.as<double>(), 1, b, 1, med.as<double>(), st));
+    std::vector<double> h;
+    RC(d2h(h, med.p, 1, st));
+    tr.add(0, (int64_t)std::log2((double)b), 0, 0);
+    noise_std = std::sqrt((double)b * h[0] / std::log(2.0));
+    return AFFT_OK;
+  }
+
+  int run(Entries& E) {
+    max_depth = 0;
+    while ((2LL << max_depth) <= n) ++max_depth;  // n.bit_length() - 1
+    noise_std = P.noise_std;
+    if (P.mode != 0 && noise_std <= 0.0) RC(calibrate());
+    int depth = 0;
+    while ((1LL << depth) < k) ++depth;  // ceil(log2 k), k >= 1
+    depth = std::min(depth, max_depth);
+    Layer layer, next;
+    RC(initial(depth, layer));
+    while ((double)layer.m < P.theta * k && layer.depth < max_depth) {
+      RC(expand(layer, next));
+      swap_layers(layer, next);
+    }
+    std::vector<int64_t> multi;
+    RC(classify(layer, E, multi));
+    while (P.mode != 0 && !multi.empty() && layer.depth < max_depth) {
+      RC(expand(layer, next));
+      swap_layers(layer, next);
+      RC(classify(layer, E, multi));
+    }
+    const int64_t remaining = (int64_t)k - (int64_t)E.f.size();
+    if (!multi.empty() && remaining > 0) RC(resolve(layer.depth, multi, remaining, E));
+    return AFFT_OK;
+  }
+};
+
+}  // namespace
+}  // namespace afft
+
+using namespace afft;
+
+extern "C" int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k,
+                          const AfftDsfftParams* params, int64_t* out_pos, double* out_val,
+                          int64_t capacity, int64_t* out_count, int32_t* trace,
+                          int32_t trace_capacity, int32_t* trace_len, void* stream) {
+  if (!x || !params || !out_count || n < 1 || (n & (n - 1)) || k < 1 ||
+      (dtype != AFFT_C64 && dtype != AFFT_C128) ||
+      (params->mode != 0 && (params->c < 1 || params->m < 2 || !params->anchors ||
+                             !params->weights)) ||
+      !params->dt_shift_off || (capacity > 0 && (!out_pos || !out_val))) {
+    set_error("afft_dsfft: bad arguments");
+    return AFFT_EINVAL;
+  }
+  Entries E;
+  Dsfft D{x, dtype, n, k, *params, (cudaStream_t)stream, Tracer{trace, trace_capacity}};
+  const int rc = D.run(E);
+  const std::vector<int64_t>& ef = E.f;
+  const std::vector<cd>& ev = E.v;
+  if (trace_len) *trace_len = D.tr.len;
+  if (rc) return rc;
+  *out_count = (int64_t)ef.size();
+  if ((int64_t)ef.size() > capacity) {
+    set_error("afft_dsfft: %zu entries, capacity %lld", ef.size(), (long long)capacity);
+    return AFFT_ENOMEM;
+  }
+  for (size_t i = 0; i < ef.size(); ++i) {
+    out_pos[i] = ef[i];
+    out_val[2 * i] = ev[i].re;
+    out_val[2 * i + 1] = ev[i].im;
+  }
+  return AFFT_OK;
+}

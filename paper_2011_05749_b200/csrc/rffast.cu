@@ -806,6 +806,19 @@ extern "C" int afft_robust_thresholds(const double* energy, const uint8_t* mask,
   return AFFT_OK;
 }
 
+namespace afft {
+__global__ void search_list_kernel(int64_t count, int64_t b, const int64_t* __restrict__ index,
+                                   int64_t* __restrict__ rows, int64_t* __restrict__ idx,
+                                   int64_t* __restrict__ bs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) {
+    rows[i] = i;
+    idx[i] = index[i];
+    bs[i] = b;
+  }
+}
+}  // namespace afft
+
 extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t* index,
                                            int64_t count, int64_t b, int64_t n,
                                            const int64_t* shifts, int32_t nshift, int32_t c,
@@ -831,19 +844,17 @@ extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t
   }
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = reinterpret_cast<char*>(workspace);
-  // active list = the given nodes, rows 0..count-1 of `residual`
-  std::vector<int64_t> rows((size_t)count), bs((size_t)count, b);
-  for (int64_t i = 0; i < count; ++i) rows[i] = i;
-  cudaMemcpyAsync(ws + w.act_row, rows.data(), count * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(ws + w.act_index, index, count * 8, cudaMemcpyDeviceToDevice, st);
-  cudaMemcpyAsync(ws + w.act_b, bs.data(), count * 8, cudaMemcpyHostToDevice, st);
+  // active list = the given nodes, rows 0..count-1 of `residual` (filled on the device:
+  // no host staging, no synchronisation)
+  search_list_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(
+      count, b, index, reinterpret_cast<int64_t*>(ws + w.act_row),
+      reinterpret_cast<int64_t*>(ws + w.act_index), reinterpret_cast<int64_t*>(ws + w.act_b));
   rc = run_search(*P, w, ws, (int)count, residual, st);
   if (!rc) {
     cudaMemcpyAsync(f0, ws + w.f0, count * 8, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(val, ws + w.val, count * 16, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(resnorm, ws + w.res, count * 8, cudaMemcpyDeviceToDevice, st);
-    cudaError_t e = cudaStreamSynchronize(st);  // host vectors above must outlive the copies
-    if (e != cudaSuccess) rc = cuda_status(e, "singleton_search_noisy");
+    AFFT_CHECK_LAUNCH("singleton_search_noisy");
   }
   return rc;
 }

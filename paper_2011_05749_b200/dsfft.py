@@ -1,18 +1,21 @@
 """Deterministic binary-tree search (DSFFT) on the GPU.
 
-Drop-in for /root/reference/pkg/src/aliasfft/dsfft.py.  The layer loop is
-host control flow (one small count read per layer); every layer's data stays on
-the device: full layers are size-2^d bucketizations (one-CTA or four-step
-DFT), selective layers are direct alias sums, activity is a device stream
-compaction, classification reuses the exact / noisy singleton kernels on
-measurement rows built with coset reuse (csrc/dsfft.cu), and leftover aliased
-buckets go through the sFFT-DT3 kernels.
+Drop-in for /root/reference/pkg/src/aliasfft/dsfft.py.  `dsfft` runs the whole
+layer loop natively (afft_dsfft, csrc/dsfft_host.cu: one read-back per layer);
+every layer's data stays on the device: full layers are size-2^d bucketizations,
+selective layers are direct alias sums, deep layers read the resident spectrum
+through the alias identity, activity is a device stream compaction,
+classification reuses the exact / noisy singleton kernels on measurement rows
+built with coset reuse (csrc/dsfft.cu), and leftover aliased buckets go through
+the sFFT-DT3 kernels.  This module draws the numpy-PCG64 inputs, replays the
+ledger, and keeps the reference's layer-level API (initial_layer / expand_layer).
 """
 
 from __future__ import annotations
 
+import ctypes
 import warnings
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -20,18 +23,9 @@ import torch
 from . import _device, _lib
 from .bucketize import SampleLedger, gather_indices, record_bucketization
 from .oneshot import OneShotConfig, random_shifts, structured_shifts
-from .peeling import (
-    STATE_CODE,
-    NodeState,
-    SearchPlan,
-    UnsupportedSizeError,
-    exact_thresholds_device,
-    kay_weights,
-)
+from .peeling import SearchPlan, UnsupportedSizeError, kay_weights
 from .signals import SparseSpectrum
 
-STATE_SINGLE = STATE_CODE[NodeState.SINGLE_TON]
-STATE_MULTI = STATE_CODE[NodeState.MULTI_TON]
 
 
 @dataclass
@@ -59,10 +53,6 @@ class DsfftConfig:
     seed: int = 0
     noise_std: float = 0.0
     activity_floor: float = 1e-6
-
-
-def _threshold(config: DsfftConfig, depth: int) -> float:
-    return max(config.activity_floor, 3.0 * config.noise_std / np.sqrt(1 << depth))
 
 
 # ------------------------------------------------------------------ device layer
@@ -96,37 +86,7 @@ def _active(values: torch.Tensor, thr: float, cand: torch.Tensor | None = None) 
     return out[: int(count.item())]
 
 
-# Deep layers (n/b <= 32) read the signal's normalised spectrum Y = fft(x)/n, computed
-# once per dsfft_device call, through the alias identity (afft_alias_rows) instead of
-# running min(#shifts, n/b) size-b DFTs over the whole signal at every layer.
-_ALIAS_MAX_L = 32
-_SPECTRA: dict[tuple, list] = {}  # (data_ptr, numel) -> [Y or None, ||Y||^2 or None]
-
-
-def _spectrum(xd: torch.Tensor):
-    """[Y, ||Y||^2] for a signal registered by dsfft_device, else None."""
-    ent = _SPECTRA.get((xd.data_ptr(), xd.numel()))
-    if ent is None:
-        return None
-    if ent[0] is None:
-        from .bucketize import bucketize_device
-
-        ent[0] = bucketize_device(xd, int(xd.numel()), [0])[0]
-    return ent
-
-
-def _alias_ok(xd: torch.Tensor, b: int) -> bool:
-    return int(xd.numel()) // b <= _ALIAS_MAX_L and (xd.data_ptr(), xd.numel()) in _SPECTRA
-
-
 def _full_values(xd: torch.Tensor, b: int) -> torch.Tensor:
-    if _alias_ok(xd, b):
-        Y = _spectrum(xd)[0]
-        vals = torch.empty(b, dtype=torch.complex128, device=xd.device)
-        _lib.check(_lib.load().afft_alias_rows(Y.data_ptr(), int(xd.numel()), b, None, 0, None, 0,
-                                               None, None, vals.data_ptr(), _device.stream_ptr()),
-                   "alias_rows")
-        return vals
     from .bucketize import bucketize_device
 
     return bucketize_device(xd, b, [0])[0]
@@ -166,32 +126,6 @@ def _expand(xd, prev: _DevLayer, thr, ledger) -> _DevLayer:
     return _DevLayer(depth, _active(vals, thr), vals)
 
 
-def _rows(xd, b, shifts, idx, energy=False):
-    n = int(xd.numel())
-    rows = torch.empty((max(1, idx.numel()), len(shifts)), dtype=torch.complex128,
-                       device=xd.device)
-    en = torch.empty(b, dtype=torch.float64, device=xd.device) if energy else None
-    sb, ns = _lib.host_i64(shifts)
-    if _alias_ok(xd, b):
-        Y = _spectrum(xd)[0]
-        _lib.check(
-            _lib.load().afft_alias_rows(Y.data_ptr(), n, b, sb, ns,
-                                        idx.data_ptr() if idx.numel() else None, idx.numel(),
-                                        rows.data_ptr(), None if en is None else en.data_ptr(),
-                                        None, _device.stream_ptr()),
-            "alias_rows",
-        )
-        return rows[: idx.numel()], en
-    _lib.check(
-        _lib.load().afft_bucketize_rows(xd.data_ptr(), _device.dtype_code(xd), n, b, sb, ns,
-                                        idx.data_ptr() if idx.numel() else None, idx.numel(),
-                                        rows.data_ptr(), None if en is None else en.data_ptr(),
-                                        _device.stream_ptr()),
-        "bucketize_rows",
-    )
-    return rows[: idx.numel()], en
-
-
 def _search_plan(n: int, seed: int) -> SearchPlan:
     """The noisy plan of _classify_active (dsfft.py:142-150)."""
     c = int(np.ceil(np.log2(n)))
@@ -201,168 +135,93 @@ def _search_plan(n: int, seed: int) -> SearchPlan:
                       weights=kay_weights(m))
 
 
-def _classify(xd, layer: _DevLayer, config: DsfftConfig, ledger):
-    """_classify_active (dsfft.py:118-174): decoded single-tons and multi-ton buckets."""
-    n = int(xd.numel())
-    b = layer.b
-    lib = _lib.load()
-    sp = _device.stream_ptr()
-    act = layer.active
-    A = int(act.numel())
-    entries: dict[int, complex] = {}
-    multitons: list[int] = []
-    if config.mode == "exact":
-        shifts = [0, 1, 2]
-        record_bucketization(ledger, n, b, shifts)
-        if A == 0:
-            return entries, multitons
-        rows, _ = _rows(xd, b, shifts, act)
-        eps = float(exact_thresholds_device(xd).item())
-        st = torch.empty(A, dtype=torch.int8, device=xd.device)
-        f0 = torch.full((A,), -1, dtype=torch.int64, device=xd.device)
-        val = torch.zeros(A, dtype=torch.complex128, device=xd.device)
-        _lib.check(lib.afft_classify_exact(rows.data_ptr(), act.data_ptr(), A, b, n, eps, eps,
-                                           st.data_ptr(), f0.data_ptr(), val.data_ptr(), sp),
-                   "classify_exact")
-    else:
-        plan = _search_plan(n, config.seed)
-        shifts = plan.shifts
-        record_bucketization(ledger, n, b, shifts)
-        R = len(shifts)
-        base = config.noise_std / np.sqrt(b) * np.sqrt(R)
-        # the floor 1e-8 sqrt(max energy) only matters above 1.5 base; with the
-        # spectrum resident, max energy <= R (n/b) ||Y||^2 bounds it without the
-        # all-bucket energy pass (thresholds identical either way)
-        skip = False
-        if config.noise_std > 0.0 and _alias_ok(xd, b):
-            ent = _spectrum(xd)
-            if ent[1] is None:
-                ent[1] = float((ent[0].abs() ** 2).sum().item())
-            skip = 1e-8 * np.sqrt(R * (n // b) * ent[1]) < 1.5 * base
-        rows, energy = _rows(xd, b, shifts, act, energy=not skip)
-        if config.noise_std > 0.0:
-            floor = 0.0 if skip else 1e-8 * np.sqrt(float(energy.max().item()))
-            t0, t1 = max(1.5 * base, floor), max(2.5 * base, floor)
-        else:
-            from .rffast import robust_thresholds_device
-
-            quiet = torch.ones(b, dtype=torch.uint8, device=xd.device)
-            if A:
-                quiet[act] = 0
-            a0, a1 = robust_thresholds_device(energy.unsqueeze(0), R, quiet.unsqueeze(0))
-            t0, t1 = float(a0.item()), float(a1.item())
-        if A == 0:
-            return entries, multitons
-        st = torch.empty(A, dtype=torch.int8, device=xd.device)
-        f0 = torch.full((A,), -1, dtype=torch.int64, device=xd.device)
-        val = torch.zeros(A, dtype=torch.complex128, device=xd.device)
-        rn = torch.empty(A, dtype=torch.float64, device=xd.device)
-        need = int(lib.afft_singleton_workspace_size(n, A, b, plan.c, plan.m))
-        ws = torch.empty(need, dtype=torch.uint8, device=xd.device)
-        sb, ns = _lib.host_i64(shifts)
-        wb = _lib.host_f64(plan.weights.tolist())
-        _lib.check(lib.afft_classify_noisy(rows.data_ptr(), act.data_ptr(), A, b, n, sb, ns,
-                                           plan.c, plan.m, wb, float(t0), float(t1),
-                                           st.data_ptr(), f0.data_ptr(), val.data_ptr(),
-                                           rn.data_ptr(), ws.data_ptr(), ws.numel(), sp),
-                   "classify_noisy")
-    # one synchronisation for the four result arrays (pinned, non-blocking copies)
-    host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (st, f0, val, act)]
-    for h, t in zip(host, (st, f0, val, act)):
-        h.copy_(t, non_blocking=True)
-    torch.cuda.current_stream(xd.device).synchronize()
-    st_h, f0_h, val_h, act_h = (h.numpy() for h in host)
-    single = st_h == STATE_SINGLE
-    multi = st_h == STATE_MULTI
-    # entries in ascending-bucket order, as the reference inserts them
-    entries.update(zip(f0_h[single].tolist(), val_h[single].tolist()))
-    multitons.extend(act_h[multi].tolist())
-    return entries, multitons
+def _dt3_shift_table(n: int, config: DsfftConfig):
+    """The DT3 fallback's random shifts (dsfft.py:207-212) for every possible stop depth d:
+    p = max(12, ceil(a_m log10 max(n/2^d, 10))) draws of default_rng(seed).choice."""
+    max_depth = n.bit_length() - 1
+    offs, flat = [0], []
+    for d in range(max_depth + 1):
+        b = 1 << d
+        step = n // b
+        p = max(12, int(np.ceil(config.a_m * np.log10(max(step, 10)))))
+        cfg = OneShotConfig(b=b, a_m=config.a_m, p=p, variant="dt3", seed=config.seed)
+        try:
+            cfg.validate(n)
+            flat.extend(random_shifts(n, cfg))
+        except ValueError:  # not reachable as a stop depth (too few samples)
+            pass
+        offs.append(len(flat))
+    return np.asarray(flat, dtype=np.int64), np.asarray(offs, dtype=np.int32)
 
 
-def _resolve_aliased(xd, b, buckets, k_remaining, config, ledger):
-    """Pencil + pursuit for buckets still holding several tones (dsfft.py:201-228)."""
-    n = int(xd.numel())
-    step = n // b
-    p = max(12, int(np.ceil(config.a_m * np.log10(max(step, 10)))))
-    cfg = OneShotConfig(b=b, a_m=config.a_m, p=p, variant="dt3", seed=config.seed)
-    cfg.validate(n)
-    rsh = random_shifts(n, cfg)
-    shifts = structured_shifts(config.a_m) + rsh
-    record_bucketization(ledger, n, b, shifts)
-    idx = torch.tensor(buckets, dtype=torch.int64, device=xd.device)
-    rows, _ = _rows(xd, b, shifts, idx)
-    nm, R, a_m = len(buckets), len(shifts), config.a_m
-    lib = _lib.load()
-    sp = _device.stream_ptr()
-    counts = torch.empty(nm, dtype=torch.int32, device=xd.device)
-    sig = torch.empty((nm, a_m), dtype=torch.float64, device=xd.device)
-    kk = min(k_remaining, a_m * nm)
-    _lib.check(lib.afft_dt_detect(rows.data_ptr(), 1, nm, R, a_m, int(kk), counts.data_ptr(),
-                                  sig.data_ptr(), sp), "detect_sparsity")
-    rs = torch.tensor(rsh, dtype=torch.int64, device=xd.device)
-    pos = torch.empty((nm, a_m), dtype=torch.int64, device=xd.device)
-    val = torch.empty((nm, a_m), dtype=torch.complex128, device=xd.device)
-    cnt = torch.empty(nm, dtype=torch.int32, device=xd.device)
-    _lib.check(lib.afft_dt_solve(rows.data_ptr(), rs.data_ptr(), 1, nm, a_m, p, counts.data_ptr(),
-                                 idx.data_ptr(), 3, a_m, b, n, pos.data_ptr(), val.data_ptr(),
-                                 cnt.data_ptr(), sp), "dt3 solve")
-    cnt_h, pos_h, val_h = cnt.cpu().numpy(), pos.cpu().numpy(), val.cpu().numpy()
-    out: dict[int, complex] = {}
-    for r in range(nm):
-        for j in range(int(cnt_h[r])):
-            out[int(pos_h[r, j])] = complex(val_h[r, j])
-    return out
-
-
-def _calibrate_noise_device(xd, k, ledger) -> float:
-    """Time-domain noise std from one wide bucketization (dsfft.py:231-241)."""
-    n = int(xd.numel())
-    b = min(n, 1 << max(0, int(np.ceil(np.log2(32 * k)))))
-    vals = _full_values(xd, b)
-    record_bucketization(ledger, n, b, [0])
-    med = torch.empty(1, dtype=torch.float64, device=xd.device)
-    _lib.check(_lib.load().afft_median(vals.data_ptr(), 1, b, 1, med.data_ptr(),
-                                       _device.stream_ptr()), "median")
-    return float(np.sqrt(b * float(med.item()) / np.log(2.0)))
+def _replay(trace_rec, n, config, plan, dt_table, ledger, trace):
+    """Ledger records and the Python trace from the native trace records."""
+    flat, offs = dt_table
+    for kind, depth, a, c in trace_rec:
+        b = 1 << depth
+        if kind in (0, 1):
+            record_bucketization(ledger, n, b, [0])
+        elif kind == 2:
+            for _ in range(c if c >= 0 else 1):
+                record_bucketization(ledger, n, b, [0])
+            if trace is not None:
+                trace.append(["expand", depth, a])
+        elif kind == 3:
+            if trace is not None:
+                trace.append(["classify", depth, a, c])
+        elif kind == 4:
+            rsh = flat[offs[depth]:offs[depth + 1]].tolist()
+            record_bucketization(ledger, n, b, structured_shifts(config.a_m) + rsh)
+        elif kind == 5:
+            record_bucketization(ledger, n, b, [0, 1, 2] if c == 0 else plan.shifts)
 
 
 def dsfft_device(xd: torch.Tensor, k: int, config: DsfftConfig,
                  ledger: SampleLedger | None = None, trace: list | None = None
                  ) -> dict[int, complex]:
     """dsfft body (dsfft.py:250-266) for one device signal; returns the entries dict.
-    ``trace`` (optional) collects ["expand", depth, m_d] / ["classify", depth, #single,
-    #multi] records in the order the reference executes them."""
-    key = (xd.data_ptr(), xd.numel())
-    _SPECTRA[key] = [None, None]
-    try:
-        return _dsfft_layers(xd, k, config, ledger, trace)
-    finally:
-        _SPECTRA.pop(key, None)
 
-
-def _dsfft_layers(xd, k, config, ledger, trace):
+    The layer loop runs natively (afft_dsfft, csrc/dsfft_host.cu); this wrapper draws
+    the numpy-PCG64 inputs it needs (search-plan anchors, DT3 random shifts per stop
+    depth), then replays the ledger and the optional ``trace`` (["expand", depth, m_d]
+    / ["classify", depth, #single, #multi] in the reference's order)."""
     n = int(xd.numel())
-    max_depth = n.bit_length() - 1
-    log = trace.append if trace is not None else (lambda rec: None)
-    if config.mode != "exact" and config.noise_std <= 0.0:
-        config = replace(config, noise_std=_calibrate_noise_device(xd, k, ledger))
-    depth = min(max(0, int(np.ceil(np.log2(k)))), max_depth)
-    layer = _initial(xd, depth, _threshold(config, depth), ledger)
-    while layer.m_d < config.theta * k and layer.depth < max_depth:
-        layer = _expand(xd, layer, _threshold(config, layer.depth + 1), ledger)
-        log(["expand", layer.depth, layer.m_d])
-    entries, multitons = _classify(xd, layer, config, ledger)
-    log(["classify", layer.depth, len(entries), len(multitons)])
-    while config.mode != "exact" and multitons and layer.depth < max_depth:
-        layer = _expand(xd, layer, _threshold(config, layer.depth + 1), ledger)
-        log(["expand", layer.depth, layer.m_d])
-        entries, multitons = _classify(xd, layer, config, ledger)
-        log(["classify", layer.depth, len(entries), len(multitons)])
-    remaining = k - len(entries)
-    if multitons and remaining > 0:
-        entries.update(_resolve_aliased(xd, layer.b, multitons, remaining, config, ledger))
-    return entries
+    xd = xd.contiguous()
+    noisy = config.mode != "exact"
+    plan = _search_plan(n, config.seed) if noisy else None
+    dt_table = _dt3_shift_table(n, config)
+    anchors = np.asarray(plan.anchors if noisy else [0], dtype=np.int64)
+    weights = np.asarray(plan.weights if noisy else [0.0], dtype=np.float64)
+    prm = _lib.DsfftParams(
+        theta=float(config.theta), mode=1 if noisy else 0, a_m=int(config.a_m),
+        noise_std=float(config.noise_std), activity_floor=float(config.activity_floor),
+        c=int(plan.c) if noisy else 0, m=int(plan.m) if noisy else 0,
+        anchors=anchors.ctypes.data, weights=weights.ctypes.data,
+        dt_shifts=dt_table[0].ctypes.data if dt_table[0].size else None,
+        dt_shift_off=dt_table[1].ctypes.data)
+    lib = _lib.load()
+    cap = max(8 * k, 1024)
+    tcap = 4 * (n.bit_length() + 8)
+    while True:
+        pos = np.empty(cap, dtype=np.int64)
+        val = np.empty(cap, dtype=np.complex128)
+        cnt = ctypes.c_int64(0)
+        tr = np.empty((tcap, 4), dtype=np.int32)
+        tlen = ctypes.c_int32(0)
+        rc = lib.afft_dsfft(xd.data_ptr(), _device.dtype_code(xd), n, int(k), ctypes.byref(prm),
+                            pos.ctypes.data, val.ctypes.data, cap, ctypes.byref(cnt),
+                            tr.ctypes.data, tcap, ctypes.byref(tlen), _device.stream_ptr())
+        if rc == _lib.AFFT_ENOMEM and cnt.value > cap:
+            cap = int(cnt.value)
+            continue
+        if rc == _lib.AFFT_OK and tlen.value > tcap:
+            tcap = int(tlen.value)  # trace truncated: rerun with room (rare)
+            continue
+        _lib.check(rc, "dsfft")
+        break
+    _replay(tr[: tlen.value].tolist(), n, config, plan, dt_table, ledger, trace)
+    m = int(cnt.value)
+    return dict(zip(pos[:m].tolist(), val[:m].tolist()))
 
 
 def dsfft(x, k: int, config: DsfftConfig | None = None,
