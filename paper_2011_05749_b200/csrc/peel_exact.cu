@@ -124,7 +124,11 @@ struct FusedParams {
   int rec_in_smem;       // 1: recovered list in shared memory (no all_pos output)
 };
 
-constexpr int kFusedThreads = 256;
+#ifndef AFFT_FUSED_THREADS
+#define AFFT_FUSED_THREADS 256
+#define AFFT_FUSED_MIN_BLOCKS 3
+#endif
+constexpr int kFusedThreads = AFFT_FUSED_THREADS;
 constexpr int kStreamUnroll = 8;
 
 // 16-byte streaming loads that do not allocate in L1: the CTA's own shared memory
@@ -320,7 +324,7 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
 // One signal per CTA iteration; a grid smaller than the batch makes the CTAs
 // persistent (grid-stride over signals), which is how the pipelined path caps
 // the decode's SM footprint next to the concurrent norm stream.
-__global__ void __launch_bounds__(kFusedThreads, 3) ffast_fused_kernel(
+__global__ void __launch_bounds__(kFusedThreads, AFFT_FUSED_MIN_BLOCKS) ffast_fused_kernel(
     const __grid_constant__ FusedParams p, int64_t batch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int warp_tmp[32];
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_split_kernel(
 
 // Decode only (eps precomputed by the multi-CTA norm pass): the fused body with the
 // stream compiled out, so fewer registers are live across the decode.
-__global__ void __launch_bounds__(kFusedThreads, 3) ffast_decode_kernel(
+__global__ void __launch_bounds__(kFusedThreads, AFFT_FUSED_MIN_BLOCKS) ffast_decode_kernel(
     const __grid_constant__ FusedParams p, int64_t batch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int warp_tmp[32];
