@@ -225,24 +225,25 @@ __global__ void __launch_bounds__(kDt2LocateThreads, 3) dt2_locate_warp_kernel(
       }
     worst_sq = worst * worst * (1.0 + 1e-13);
   };
-  // two independent candidates per iteration (the Horner chains are latency-bound)
+  // Horner from the leading 1 with compile-time coefficient indices (a runtime index
+  // into coeffs[] would live in local memory); two independent candidates per
+  // iteration, since each chain is a dependent sequence of complex products (four
+  // spill at the 80-register cap and measured slower)
+  auto horner = [&](la::c2 z) {
+    la::c2 y = la::C(1.0);
+#pragma unroll
+    for (int kk = dt::kMaxAm - 1; kk >= 0; --kk)
+      if (kk < a) y = la::add(la::mul(y, z), coeffs[kk]);
+    return y;
+  };
   int64_t j = lane;
   for (; j + 32 < step; j += 64) {
-    const la::c2 za = la::mul(z0, rootsL[j]), zb = la::mul(z0, rootsL[j + 32]);
-    la::c2 ya = la::C(1.0), yb = la::C(1.0);
-    for (int k = a - 1; k >= 0; --k) {
-      ya = la::add(la::mul(ya, za), coeffs[k]);
-      yb = la::add(la::mul(yb, zb), coeffs[k]);
-    }
-    consider(ya, j);
-    consider(yb, j + 32);
+    const la::c2 y0 = horner(la::mul(z0, rootsL[j]));
+    const la::c2 y1 = horner(la::mul(z0, rootsL[j + 32]));
+    consider(y0, j);
+    consider(y1, j + 32);
   }
-  for (; j < step; j += 32) {
-    const la::c2 z = la::mul(z0, rootsL[j]);
-    la::c2 y = la::C(1.0);
-    for (int k = a - 1; k >= 0; --k) y = la::add(la::mul(y, z), coeffs[k]);
-    consider(y, j);
-  }
+  for (; j < step; j += 32) consider(horner(la::mul(z0, rootsL[j])), j);
   // butterfly merge: insert the partner lane's list (lists of different lanes are disjoint)
   for (int o = 16; o > 0; o >>= 1) {
     double ov[dt::kMaxAm];
