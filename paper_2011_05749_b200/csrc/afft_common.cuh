@@ -23,6 +23,10 @@ int cuda_status(cudaError_t e, const char* what);
 // stream-ordered scratch from the library's memory pool (kept across calls)
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
 cudaError_t scratch_free(void* p, cudaStream_t stream);
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (never lowers it:
+// the attribute is process-wide, so concurrent callers on other streams/threads that
+// need more must not be undercut).  Thread-safe.
+cudaError_t ensure_smem(const void* func, size_t bytes);
 
 #define AFFT_CHECK_LAUNCH(what)                                   \
   do {                                                            \

@@ -353,8 +353,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     g.out = s == P - 1 ? out : nullptr;
     const int ldR = (R & 1) ? R : R + 1;
     const size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
-    e = cudaFuncSetAttribute(gstockham_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+    e = ensure_smem((const void*)gstockham_kernel, (int)smem);
     int occ = 0;
     if (e == cudaSuccess)
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gstockham_kernel, kGStockThreads,
@@ -458,9 +457,7 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
     set_error("too many (cycle, shift-chunk) jobs per signal: %d", total_jobs);
     return AFFT_EUNSUPPORTED;
   }
-  cudaError_t e = cudaFuncSetAttribute(gather_dft_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem_max);
+  cudaError_t e = ensure_smem((const void*)gather_dft_kernel, (int)smem_max);
   if (e != cudaSuccess) {
     return cuda_status(e, "cudaFuncSetAttribute(gather_dft)");
   }

@@ -1,5 +1,6 @@
 // Error plumbing and version for the C ABI (include/aliasfft_b200.h).
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "afft_common.cuh"
@@ -43,6 +44,20 @@ static cudaMemPool_t library_pool() {
     g_pools[dev] = pool;
   }
   return g_pools[dev];
+}
+
+cudaError_t ensure_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = granted[{dev, func}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
 }
 
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {

@@ -563,8 +563,7 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
     if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(dt_truncate scratch)");
     smem = 0;
   } else {
-    cudaError_t e = cudaFuncSetAttribute(dt_truncate_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem((const void*)dt_truncate_kernel, (int)smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(dt_truncate)");
   }
   dt_truncate_kernel<<<(unsigned)batch, 1024, smem, st>>>(

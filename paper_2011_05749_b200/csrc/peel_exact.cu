@@ -526,8 +526,7 @@ static int launch_peel(PeelParams& p, int64_t batch, void* scratch, cudaStream_t
   if (bytes <= kSmemLimit) {
     p.gscratch = nullptr;
     dyn = bytes;
-    cudaError_t e = cudaFuncSetAttribute(peel_exact_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaError_t e = ensure_smem((const void*)peel_exact_kernel, (int)dyn);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(peel_exact)");
   } else {
     if (!scratch) {
@@ -555,8 +554,7 @@ static int launch_truncate(const int64_t* pos, const double* val, const int32_t*
     if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(truncate scratch)");
     smem = 0;
   } else {
-    cudaError_t e = cudaFuncSetAttribute(truncate_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem((const void*)truncate_kernel, (int)smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(truncate)");
   }
   truncate_kernel<<<(unsigned)batch, 1024, smem, stream>>>(pos, val, count, cap, k, out_pos,
@@ -826,8 +824,7 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
       // the split roles spin-wait across CTAs: every CTA must be resident (cooperative
       // launch below) with room for two streaming CTAs and one decoding CTA per SM
       int per_sm = 0;
-      cudaError_t e = cudaFuncSetAttribute(ffast_split_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = ensure_smem((const void*)ffast_split_kernel, (int)smem);
       if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ffast_split_kernel,
                                                           kFusedThreads, smem);
@@ -849,11 +846,9 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
                                          al256((size_t)batch * nparts * 8));
     }
     {
-      cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = ensure_smem((const void*)ffast_fused_kernel, (int)smem);
       if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ffast_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+        e = ensure_smem((const void*)ffast_decode_kernel, (int)smem);
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(ffast_fused)");
     }
     if (mode == 2) {
@@ -978,8 +973,7 @@ extern "C" int afft_ffast_occupancy(int64_t n, const int64_t* factors, int32_t n
     *smem_bytes = 0;
     return AFFT_OK;
   }
-  cudaError_t e = cudaFuncSetAttribute(ffast_fused_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem((const void*)ffast_fused_kernel, (int)smem);
   int blocks = 0;
   if (e == cudaSuccess)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, ffast_fused_kernel, kFusedThreads,

@@ -797,8 +797,7 @@ extern "C" int afft_robust_thresholds(const double* energy, const uint8_t* mask,
     AFFT_CHECK_LAUNCH("robust_thresholds_large_kernel");
     return AFFT_OK;
   }
-  cudaError_t e = cudaFuncSetAttribute(robust_thresholds_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem((const void*)robust_thresholds_kernel, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(robust_thresholds)");
   robust_thresholds_kernel<<<(unsigned)batch, 256, smem, (cudaStream_t)stream>>>(
       (int)count, pow2, energy, mask, r, t0, t1);
@@ -919,8 +918,7 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
     }
     hsmem = 0;
   } else {
-    e = cudaFuncSetAttribute(noisy_harvest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)hsmem);
+    e = ensure_smem((const void*)noisy_harvest_kernel, (int)hsmem);
     if (e != cudaSuccess) {
       return cuda_status(e, "cudaFuncSetAttribute(noisy_harvest)");
     }

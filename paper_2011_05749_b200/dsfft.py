@@ -179,7 +179,16 @@ def _replay(trace_rec, n, config, plan, dt_table, ledger, trace):
 def dsfft_device(xd: torch.Tensor, k: int, config: DsfftConfig,
                  ledger: SampleLedger | None = None, trace: list | None = None
                  ) -> dict[int, complex]:
-    """dsfft body (dsfft.py:250-266) for one device signal; returns the entries dict.
+    """dsfft body (dsfft.py:250-266) for one device signal; returns the entries dict
+    in the reference's insertion order (see _dsfft_arrays)."""
+    pos, val = _dsfft_arrays(xd, k, config, ledger, trace)
+    return dict(zip(pos.tolist(), val.tolist()))
+
+
+def _dsfft_arrays(xd: torch.Tensor, k: int, config: DsfftConfig,
+                  ledger: SampleLedger | None = None, trace: list | None = None):
+    """dsfft body (dsfft.py:250-266) for one device signal: (positions, values) of the
+    entries dict in insertion order.
 
     The layer loop runs natively (afft_dsfft, csrc/dsfft_host.cu); this wrapper draws
     the numpy-PCG64 inputs it needs (search-plan anchors, DT3 random shifts per stop
@@ -221,7 +230,7 @@ def dsfft_device(xd: torch.Tensor, k: int, config: DsfftConfig,
         break
     _replay(tr[: tlen.value].tolist(), n, config, plan, dt_table, ledger, trace)
     m = int(cnt.value)
-    return dict(zip(pos[:m].tolist(), val[:m].tolist()))
+    return pos[:m], val[:m]
 
 
 def dsfft(x, k: int, config: DsfftConfig | None = None,
@@ -234,17 +243,21 @@ def dsfft(x, k: int, config: DsfftConfig | None = None,
         return SparseSpectrum(n, {})
     if k > 64:
         warnings.warn(f"binary-tree search degrades for large sparsity (k={k})", stacklevel=2)
-    entries = dsfft_device(_device.as_device_signal(x), k, config or DsfftConfig(), ledger)
-    ranked = sorted(entries.items(), key=lambda item: (-abs(item[1]), item[0]))
-    return SparseSpectrum(n, dict(ranked[:k]))
+    pos, val = _dsfft_arrays(_device.as_device_signal(x), k, config or DsfftConfig(), ledger)
+    # truncate_spectrum order (-|v|, f), first k (oneshot.py:260-263); the entry keys
+    # are distinct, so the lexicographic sort is total
+    order = np.lexsort((pos, -np.abs(val)))[:k]
+    return SparseSpectrum(n, dict(zip(pos[order].tolist(), val[order].tolist())))
 
 
-def dsfft_batch(xs, k: int, configs, streams: int = 1) -> list[SparseSpectrum]:
-    """DSFFT over several signals, in input order.  Each signal's layer path is
-    data-dependent host control flow; with streams > 1 signals run on worker threads,
-    each with its own CUDA stream (the library is reentrant per stream).  Measured at
-    config 4 (tools/bench_suite.py): 4 streams are no faster than 1 — the per-layer
-    host work holds the GIL — and give identical results, so the default is 1."""
+def dsfft_batch(xs, k: int, configs, streams: int = 4) -> list[SparseSpectrum]:
+    """DSFFT over several signals, in input order.  Each signal's layer loop is
+    data-dependent (one read-back per layer), so one signal alone leaves the GPU idle
+    during its read-backs; with streams > 1 signals run on worker threads, each with
+    its own CUDA stream (the library is reentrant per stream and the native loop runs
+    without the GIL), overlapping one signal's read-backs with another's kernels.
+    Measured at config 4, 8 signals (tools/dsfft_streams.py): 1 stream 69 signals/s,
+    4 streams 117, 8 streams 137; results identical to the sequential run."""
     import threading
     from concurrent.futures import ThreadPoolExecutor
 

@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 from paper_2011_05749_b200 import (  # noqa: E402
     DsfftConfig, ffast_batch, plan_cycles, rffast_batch, sfft_dt_batch,
 )
-from paper_2011_05749_b200.dsfft import dsfft_device  # noqa: E402
+from paper_2011_05749_b200.dsfft import dsfft_batch, dsfft_device  # noqa: E402
 from paper_2011_05749_b200.signals import draw_truth  # noqa: E402
 
 
@@ -164,6 +164,16 @@ def main():
                 ms, wall = timed(run, 1)
                 emit(f"c4_dsfft_n2^24_k4096_{int(snr)}db", nsig, ms, wall,
                      {"recall": recall([set(o) for o in outs], tr[:nsig]), "mode": "sequential"})
+                nb = 8
+                batch_out = []
+
+                def run_batch():
+                    batch_out[:] = dsfft_batch(x[:nb], k, cfg, streams=8)
+
+                ms, wall = timed(run_batch, 1)
+                emit(f"c4_dsfft_n2^24_k4096_{int(snr)}db_batch8", nb, ms, wall,
+                     {"recall": recall([set(o.entries) for o in batch_out], tr[:nb]),
+                      "mode": "dsfft_batch, 8 streams"})
             del x
             torch.cuda.empty_cache()
 
