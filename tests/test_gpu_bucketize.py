@@ -173,3 +173,24 @@ def test_alias_rows_match_bucketize_rows(L):
     assert torch.allclose(en, en_ref, rtol=1e-11, atol=0)
     ref0 = np.fft.fft(x.cpu().numpy()[::L]) / b
     assert np.allclose(v0.cpu().numpy(), ref0, rtol=0, atol=1e-12 * np.abs(ref0).max())
+
+
+@pytest.mark.parametrize("b", [8186, 15015, 6480, 12288, 32766, 8168, 65536 * 3, 4097 * 2])
+def test_large_b_mixed_radix_sizes(b):
+    """K2' global passes at b > 4096 with mixed prime factors (radix groups <= 256, a
+    prime above 256 as its own radix, 4097 = 17 * 241): against numpy on a shifted,
+    subsampled signal."""
+    import torch
+
+    from paper_2011_05749_b200.bucketize import bucketize_device
+
+    L = 3
+    n = b * L
+    rng = np.random.default_rng(b)
+    x = rng.normal(size=n) + 1j * rng.normal(size=n)
+    shifts = [0, 1, -7, n + 5]
+    got = bucketize_device(torch.from_numpy(x).cuda(), b, shifts).cpu().numpy()
+    for t, tau in enumerate(shifts):
+        idx = (np.arange(b) * L - tau) % n
+        want = np.fft.fft(x[idx]) / b
+        assert np.max(np.abs(got[t] - want)) <= 1e-12 * np.max(np.abs(want)) * np.log2(b)
