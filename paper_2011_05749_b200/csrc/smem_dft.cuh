@@ -144,6 +144,17 @@ __device__ __forceinline__ void out_generic(const cd* src, cd* dst, const cd* tw
   dst[(j / Ns) * Ns * R + jm + q * Ns] = acc;
 }
 
+// cos(pi m / 8) for m = 0..15 as correctly rounded literals; sin(pi m / 8) =
+// cos16(m + 12).  A selection chain (not a table) so that the unrolled callers'
+// constant m folds to immediates.
+__host__ __device__ __forceinline__ constexpr double cos16(int m) {
+  m &= 15;
+  const double c1 = 0.9238795325112867, h = 0.7071067811865476, s1 = 0.3826834323650898;
+  return m == 0 ? 1.0 : m == 1 ? c1 : m == 2 ? h : m == 3 ? s1 : m == 4 ? 0.0
+       : m == 5 ? -s1 : m == 6 ? -h : m == 7 ? -c1 : m == 8 ? -1.0 : m == 9 ? -c1
+       : m == 10 ? -h : m == 11 ? -s1 : m == 12 ? 0.0 : m == 13 ? s1 : m == 14 ? h : c1;
+}
+
 // In-register forward DFT of R = 2, 4, 8, 16 points (radix-2 decimation in time
 // with compile-time twiddles w_R^k; multiplications by -i are exact swaps).
 template <int R>
@@ -177,9 +188,11 @@ __device__ __forceinline__ void dft_reg(cd* v) {
       } else if (2 * k == H) {  // w_R^(R/4) = -i
         t = cd{o[k].im, -o[k].re};
       } else {
-        // w_R^k = exp(-2 pi i k / R), k < R/2 (constants fold at compile time)
-        constexpr double kTwoPiOverR = 6.283185307179586 / R;
-        const cd w{cos(kTwoPiOverR * k), -sin(kTwoPiOverR * k)};
+        // w_R^k = exp(-2 pi i k / R) = cos(pi m / 8) - i sin(pi m / 8), m = 16 k / R,
+        // from correctly rounded literals (a device cos()/sin() call here is not
+        // constant-folded and cost ~20 instructions per point per stage)
+        const int m = 16 / R * k;
+        const cd w{cos16(m), -cos16(m + 12)};
         t = cmul(o[k], w);
       }
       v[k] = cadd(e[k], t);
