@@ -151,10 +151,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // twiddles while transposing into sequences of stride ld = R + 1 (bank-conflict
 // free column access), the smem Stockham runs on that stride, and the output rows
 // leave coalesced.
+// LGR >= 0: R = 2^LGR and cnt = kGStockPoints / R fixed at compile time (every tile
+// full), so index splits are shifts, loops have constant trip counts and the DFT
+// stages are dft_fixed — the runtime-shaped variant (LGR = -1) spent ~80% of its
+// instructions on integer index math and control flow (ncu SASS mix).
+template <int LGR>
 __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     const __grid_constant__ GStockParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int R = p.R, cnt = p.cnt;
+  constexpr bool kFixed = LGR >= 0;
+  constexpr int kR = kFixed ? (1 << LGR) : 1;
+  constexpr int kCnt = kFixed ? kGStockPoints / kR : 1;
+  constexpr int kLgCnt = kFixed ? 11 - LGR : 0;  // kGStockPoints = 2^11
+  const int R = kFixed ? kR : p.R, cnt = kFixed ? kCnt : p.cnt;
   const int ld = (R & 1) ? R : R + 1;
   const int tid = threadIdx.x, nt = blockDim.x;
   cd* tw = reinterpret_cast<cd*>(smem_raw);
@@ -175,13 +184,13 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     const int t = (int)(st_ % p.nshift);
     const int64_t s = st_ / p.nshift;
     const int64_t j0 = chunk * cnt;
-    const int c = (int)min((int64_t)cnt, nb - j0);
+    const int c = kFixed ? kCnt : (int)min((int64_t)cnt, nb - j0);
     const int64_t seq = s * p.nshift + t;
     const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
     const int64_t tau = first ? (p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n)
                                                : p.tau[t])
                               : 0;
-    const int total = c * R;
+    const int total = kFixed ? kGStockPoints : c * R;
     // e / c and e / R by multiply-high (e < 2^13, divisors < 2^13: exact)
     const unsigned Mc = c > 1 ? (unsigned)((0xffffffffull + c) / c) : 0u;
     const unsigned MR = (unsigned)((0xffffffffull + R) / R);
@@ -191,7 +200,7 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     // 1. rows r = 0..R-1, each c contiguous butterflies, into staging (bufB) in
     //    arrival order e = r * c + jj
     for (int e = tid; e < total; e += nt) {
-      const int r = c > 1 ? (int)__umulhi((unsigned)e, Mc) : e;
+      const int r = kFixed ? e >> kLgCnt : (c > 1 ? (int)__umulhi((unsigned)e, Mc) : e);
       const int64_t src = j0 + (e - r * c) + r * nb;
       if (first) {
         int64_t idx = src * p.L - tau;
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     // 2. twiddle w_b^(k r b/(N_s R)) and transpose into sequences of stride ld
 #pragma unroll 4
     for (int e = tid; e < total; e += nt) {
-      const int r = c > 1 ? (int)__umulhi((unsigned)e, Mc) : e;
+      const int r = kFixed ? e >> kLgCnt : (c > 1 ? (int)__umulhi((unsigned)e, Mc) : e);
       const int jj = e - r * c;
       cd a;
       if (c64) {
@@ -226,7 +235,11 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
       bufA[jj * ld + r] = a;
     }
     __syncthreads();
-    const cd* spec = smem_dft(bufA, bufB, c, p.plan, tw, tid, nt, ld);
+    const cd* spec;
+    if constexpr (kFixed)
+      spec = dft_fixed<(LGR > 0 ? LGR : 1), 0, kCnt, kGStockThreads>(bufA, bufB, tw, ld);
+    else
+      spec = smem_dft(bufA, bufB, c, p.plan, tw, tid, nt, ld);
     double* out = p.out ? p.out + 2 * (s * p.out_signal_stride + p.out_offset +
                                        t * p.out_shift_stride)
                         : nullptr;
@@ -235,10 +248,10 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
     for (int e = tid; e < total; e += nt) {
       int jj, q;
       if (p.Ns == 1) {  // first pass: butterfly j's outputs are the contiguous j*R + q
-        jj = (int)__umulhi((unsigned)e, MR);
+        jj = kFixed ? e >> LGR : (int)__umulhi((unsigned)e, MR);
         q = e - jj * R;
       } else {          // output row q: c contiguous k
-        q = c > 1 ? (int)__umulhi((unsigned)e, Mc) : e;
+        q = kFixed ? e >> kLgCnt : (c > 1 ? (int)__umulhi((unsigned)e, Mc) : e);
         jj = e - q * c;
       }
       const int64_t j = j0 + jj;
@@ -259,6 +272,16 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
       }
     }
   }
+}
+
+static const void* const* gstockham_fixed_table() {
+  static const void* const t[9] = {
+      nullptr,
+      (const void*)gstockham_kernel<1>, (const void*)gstockham_kernel<2>,
+      (const void*)gstockham_kernel<3>, (const void*)gstockham_kernel<4>,
+      (const void*)gstockham_kernel<5>, (const void*)gstockham_kernel<6>,
+      (const void*)gstockham_kernel<7>, (const void*)gstockham_kernel<8>};
+  return t;
 }
 
 // Radices for b: first-fit decreasing of the prime factors into groups <= 256
@@ -352,19 +375,31 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     g.tmp = s == P - 1 ? nullptr : bufs[s & 1];
     g.out = s == P - 1 ? out : nullptr;
     const int ldR = (R & 1) ? R : R + 1;
+    // compile-time shape for power-of-two radices whose tiles are always full
+    int lgr = -1;
+    if ((R & (R - 1)) == 0 && R >= 2 && R <= 256 && (b / R) % (kGStockPoints / R) == 0) {
+      lgr = 0;
+      while ((1 << lgr) < R) ++lgr;
+      g.cnt = kGStockPoints / R;
+    }
+    const void* kfn = lgr < 0 ? (const void*)gstockham_kernel<-1> : gstockham_fixed_table()[lgr];
     const size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
-    e = ensure_smem((const void*)gstockham_kernel, (int)smem);
+    e = ensure_smem(kfn, (int)smem);
     int occ = 0;
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gstockham_kernel, kGStockThreads,
-                                                        smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kGStockThreads, smem);
     if (e != cudaSuccess || occ < 1) {
       rc = cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "large-b DFT pass");
       break;
     }
     const int64_t tiles = (int64_t)seqs * ((b / R + g.cnt - 1) / g.cnt);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * occ);
-    gstockham_kernel<<<grid, kGStockThreads, smem, stream>>>(g);
+    void* args[] = {&g};
+    e = cudaLaunchKernel(kfn, dim3(grid), dim3(kGStockThreads), args, smem, stream);
+    if (e != cudaSuccess) {
+      rc = cuda_status(e, "large-b DFT launch");
+      break;
+    }
     Ns *= R;
   }
   scratch_free(scratch, stream);

@@ -258,6 +258,37 @@ __device__ inline cd* smem_dft_pow2(cd* a, cd* b, int count, const DftPlan& p, c
   return a;
 }
 
+// Compile-time variant for power-of-two n = 2^LGN, CNT sequences of stride `ld`, NT
+// threads: the same radix-8-first stage sequence as make_dft_plan (so the same
+// arithmetic, bit for bit) with every loop bound and index split a constant.
+template <int LGN, int LGR, int LGNS, int CNT, int NT>
+__device__ __forceinline__ void stage_fixed(const cd* src, cd* dst, const cd* tw, int ld) {
+  constexpr int NB = 1 << (LGN - LGR);
+  constexpr int TOTAL = CNT * NB;
+  constexpr int LGTSTEP = LGN - LGNS - LGR;
+#pragma unroll
+  for (int it = 0; it < (TOTAL + NT - 1) / NT; ++it) {
+    const int w = threadIdx.x + it * NT;
+    if (TOTAL % NT == 0 || w < TOTAL) {
+      const int seq = w >> (LGN - LGR), j = w & (NB - 1);
+      bfly_pow2<(1 << LGR), LGR>(src + seq * ld, dst + seq * ld, tw, NB, LGNS, LGTSTEP, j);
+    }
+  }
+}
+
+template <int LGN, int LGNS, int CNT, int NT>
+__device__ __forceinline__ cd* dft_fixed(cd* a, cd* b, const cd* tw, int ld) {
+  if constexpr (LGNS >= LGN) {
+    return a;
+  } else {
+    constexpr int REM = LGN - LGNS;
+    constexpr int LGR = REM >= 3 ? 3 : REM;
+    stage_fixed<LGN, LGR, LGNS, CNT, NT>(a, b, tw, ld);
+    __syncthreads();
+    return dft_fixed<LGN, LGNS + LGR, CNT, NT>(b, a, tw, ld);
+  }
+}
+
 // Forward DFT of `count` contiguous length-n sequences in smem buffer `a`,
 // ping-ponging with `b`.  Returns the buffer that holds the result.  Must be
 // called by all threads of the block (contains __syncthreads).
