@@ -379,6 +379,51 @@ __global__ void __launch_bounds__(kFusedThreads, 3) ffast_split_kernel(
   }
 }
 
+// Split streams (mode 4): `parts` CTAs per signal each stream 1/parts of its |x|^2
+// and leave a partial; the CTA that arrives last (atomic ticket) sums the partials
+// in part order — deterministic — and decodes the signal.  Finer CTAs balance the
+// tail of small batches and scatter the decode phases across the grid.
+__global__ void __launch_bounds__(kFusedThreads, AFFT_FUSED_MIN_BLOCKS) ffast_parts_kernel(
+    const __grid_constant__ FusedParams p, int64_t batch, int parts, double* part_sums,
+    unsigned* tickets, double* eps_buf) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tmp[32];
+  __shared__ int carry, red, last;
+  __shared__ double wsum[kFusedThreads / 32];
+  const int tid = threadIdx.x;
+  const int64_t s = blockIdx.x / parts;
+  const int part = (int)(blockIdx.x - s * parts);
+  if (s >= batch) return;
+  const int64_t n = p.G.n;
+  const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
+  const int64_t chunk = (n + parts - 1) / parts;
+  const int64_t lo = min(n, part * chunk), hi = min(n, lo + chunk);
+  const char* row = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
+  double acc = hi > lo ? stream_sumsq(row + lo * esz, p.dtype, hi - lo) : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((tid & 31) == 0) wsum[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kFusedThreads / 32; ++w) t += wsum[w];
+    part_sums[s * parts + part] = t;
+    __threadfence();
+    last = atomicAdd(tickets + s, 1u) == (unsigned)(parts - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  if (tid == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (int q = 0; q < parts; ++q) t += __ldcg(part_sums + s * parts + q);
+    eps_buf[s] = (1e-6 * sqrt(t)) / sqrt((double)n);
+    __threadfence_block();
+  }
+  __syncthreads();
+  ffast_one_signal<false>(p, s, smem_raw, warp_tmp, &carry, &red, wsum);
+}
+
 // Decode only (eps precomputed by the multi-CTA norm pass): the fused body with the
 // stream compiled out, so fewer registers are live across the decode.
 __global__ void __launch_bounds__(kFusedThreads, AFFT_FUSED_MIN_BLOCKS) ffast_decode_kernel(
@@ -814,11 +859,13 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     // up: ~0.2 ms per signal), pre-pass + decode 22.25 ms, stream alone 18.65 ms.
     // Small batches (< 2 waves) cannot keep HBM busy with one streaming CTA per signal.
     const int sms = num_sms();
-    // Below ~3 waves of fused CTAs (3 per SM) the last partial wave streams with too
-    // few CTAs; the multi-CTA pre-pass wins there (tools/batch_sweep.py: 512 signals
-    // 1.52 vs 1.75 ms, 1024 2.93 vs 3.01 ms; from 1536 up the fused kernel wins).
-    int mode = batch < 9 * sms ? 1 : 0;
-    if (env && env[0] >= '0' && env[0] <= '3') mode = env[0] - '0';
+    // Below ~13 waves of fused CTAs (3 per SM) the last partial waves stream with too
+    // few CTAs; split streams (mode 4: several CTAs per signal, the last one decodes)
+    // keep ~20 CTAs per SM in flight instead (tools/parts_sweep.py, config 5:
+    // 1024 signals 2.67 vs 3.05 ms fused / 2.95 ms pre-pass; 4096 10.12 vs 10.35;
+    // 512 1.40 vs 1.56; from ~6000 signals the single fused launch wins).
+    int mode = batch < 40 * sms ? 4 : 0;
+    if (env && env[0] >= '0' && env[0] <= '4') mode = env[0] - '0';
     if (nparts < 2) mode = 0;
     if (mode == 3) {
       // the split roles spin-wait across CTAs: every CTA must be resident (cooperative
@@ -902,6 +949,22 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
       e = cudaLaunchCooperativeKernel((const void*)ffast_split_kernel, grid, kFusedThreads, args,
                                       smem, st);
       if (e != cudaSuccess) return cuda_status(e, "cudaLaunchCooperativeKernel(ffast_split)");
+      return AFFT_OK;
+    }
+    if (mode == 4) {
+      const char* pe = getenv("AFFT_FFAST_PARTS");
+      const int64_t want = (21LL * sms + batch / 2) / std::max<int64_t>(batch, 1);
+      const int parts = pe ? std::max(1, std::min(16, atoi(pe)))
+                           : (int)std::max<int64_t>(2, std::min<int64_t>(12, want));
+      double* part_sums = partials;                               // batch * parts
+      unsigned* tickets = reinterpret_cast<unsigned*>(part_sums + batch * parts);  // batch
+      cudaError_t e = cudaMemsetAsync(tickets, 0, (size_t)batch * 4, st);
+      if (e == cudaSuccess) e = ensure_smem((const void*)ffast_parts_kernel, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e, "ffast parts setup");
+      fp.eps_in = epsbuf;
+      ffast_parts_kernel<<<(unsigned)(batch * parts), kFusedThreads, smem, st>>>(
+          fp, batch, parts, part_sums, tickets, epsbuf);
+      AFFT_CHECK_LAUNCH("ffast_parts_kernel");
       return AFFT_OK;
     }
     if (mode == 1) {

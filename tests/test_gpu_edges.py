@@ -39,7 +39,7 @@ def test_misaligned_complex64_rows():
 
     n, k, f = 4095, 8, [63, 65]
     xs = _signals(n, k, 6, seed0=10, dtype=np.complex64)
-    for mode in ("0", "1", "2", "3"):
+    for mode in ("0", "1", "2", "3", "4"):
         import os
 
         os.environ["AFFT_FFAST_MODE"] = mode
