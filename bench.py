@@ -207,7 +207,12 @@ def run_ours(args):
         if world > 1:
             gather_slots(res.pos, res.val, res.count)
 
-    launches_per_step = 1 if per >= 2 * 148 else 3  # fused; small batches: sumsq+thresholds+decode
+    # afft_ffast's default for this batch: one ffast_fused_kernel launch (>= 40 signals
+    # per SM) or one ffast_parts_kernel launch (split streams, smaller per-rank batches)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fused = per >= 40 * sms
+    kernel_name = "ffast_fused_kernel" if fused else "ffast_parts_kernel"
+    launches_per_step = 1
 
     for _ in range(args.warmup):
         step()
@@ -279,12 +284,15 @@ def run_ours(args):
                 "parallelism": f"signal-sharded x{world}, NCCL all-gather of result slots",
                 "exact_recovered_fraction": exact / per, "true_tone_fraction": true_kept / max(1, kept),
                 "step_kernels_ms": kern_ms,
-                "step": "one ffast_fused_kernel launch per step (afft_ffast mode 0): each CTA "
-                        "streams its signal's |x|^2 then decodes it",
+                "step": ("one ffast_fused_kernel launch per step (afft_ffast mode 0): each CTA "
+                         "gathers + transforms its signal, streams its |x|^2, then peels it"
+                         if fused else
+                         "one ffast_parts_kernel launch per step (afft_ffast mode 4): several "
+                         "CTAs stream parts of each signal's |x|^2, the last one decodes it"),
                 "pipelined_two_stream_ms": fused_ms,
             },
             "roofline": {
-                "kernel": "ffast_fused_kernel (|x|^2 stream + gather/DFT + peel + truncate)",
+                "kernel": f"{kernel_name} (|x|^2 stream + gather/DFT + peel + truncate)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes, "traffic": traffic,
