@@ -287,23 +287,42 @@ __device__ __forceinline__ void ffast_one_signal(const FusedParams& p, int64_t s
   int rc = 0;
   const int rounds = peel_rounds(G, M, eps, eps, p.max_rounds, rec_f, rec_v, rc, warp_tmp, &carry);
   const int unres = count_multitons(G, M, &red);
-  // 5. truncate to k by (-|v|, f): bitonic sort in the (now free) found-list memory
-  int pow2 = 1;
-  while (pow2 < rc) pow2 <<= 1;
-  double* key = reinterpret_cast<double*>(M.found_f);
-  int64_t* kpos = reinterpret_cast<int64_t*>(key + pow2);
-  int32_t* kidx = reinterpret_cast<int32_t*>(kpos + pow2);
-  for (int i = tid; i < rc; i += nt) {
-    key[i] = cabs_(rec_v[i]);
-    kpos[i] = rec_f[i];
-    kidx[i] = i;
-  }
-  bitonic_trunc_sort(key, kpos, kidx, rc, pow2);
+  // 5. truncate to k by (-|v|, f) in the (now free) found-list memory.  Up to 1024
+  //    entries (every config-5-sized graph) each thread ranks its entries against all
+  //    of them — one barrier; larger lists take the bitonic sort (log^2 barriers).
   cd* ov = reinterpret_cast<cd*>(p.out_val) + s * p.k;
   const int kept = rc < p.k ? rc : p.k;
-  for (int r = tid; r < kept; r += nt) {
-    p.out_pos[s * p.k + r] = kpos[r];
-    ov[r] = rec_v[kidx[r]];
+  if (rc <= 1024) {
+    double* key = reinterpret_cast<double*>(M.found_f);
+    int64_t* kpos = reinterpret_cast<int64_t*>(key + rc);
+    for (int i = tid; i < rc; i += nt) {
+      key[i] = cabs_(rec_v[i]);
+      kpos[i] = rec_f[i];
+    }
+    __syncthreads();
+    for (int i = tid; i < rc; i += nt) {
+      const int r = trunc_rank(key, kpos, rc, i);  // distinct positions: a permutation
+      if (r < kept) {
+        p.out_pos[s * p.k + r] = kpos[i];
+        ov[r] = rec_v[i];
+      }
+    }
+  } else {
+    int pow2 = 1;
+    while (pow2 < rc) pow2 <<= 1;
+    double* key = reinterpret_cast<double*>(M.found_f);
+    int64_t* kpos = reinterpret_cast<int64_t*>(key + pow2);
+    int32_t* kidx = reinterpret_cast<int32_t*>(kpos + pow2);
+    for (int i = tid; i < rc; i += nt) {
+      key[i] = cabs_(rec_v[i]);
+      kpos[i] = rec_f[i];
+      kidx[i] = i;
+    }
+    bitonic_trunc_sort(key, kpos, kidx, rc, pow2);
+    for (int r = tid; r < kept; r += nt) {
+      p.out_pos[s * p.k + r] = kpos[r];
+      ov[r] = rec_v[kidx[r]];
+    }
   }
   if (p.all_pos && p.rec_in_smem) {
     cd* av = reinterpret_cast<cd*>(p.all_val) + s * N;
