@@ -22,6 +22,7 @@
 #include <climits>
 #include <cstring>
 #include <memory>
+#include <type_traits>
 #include <vector>
 
 #include "afft_common.cuh"
@@ -100,6 +101,9 @@ __device__ __forceinline__ int noisy_cycle(const NoisyPlan& P, int g) {
 
 // One CTA scores kChunk consecutive candidates t of one active node.
 // Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
+// k32: n < 2^31, so the doubled residue 2r < 2^32 fits in 32 bits (the 64-bit
+// doubling-and-reduce was ~15% of the kernel's instructions; the kernel is issue-bound).
+template <bool k32>
 __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
     int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
     const double* __restrict__ est, int chunks, double* __restrict__ part_score,
@@ -125,8 +129,10 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
   // Bit-identical to the IEEE quotient for every r in [0, n) at n <= 2^28 and a
   // 2^28-point sweep at n = 3e9 (tools/div_check.cu; r = 0 keeps the -0.0 of x / n).
   const double inv = 1.0 / dn;
+  using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
+  const rt nn = (rt)n;
   auto score = [&](int64_t t, double bound) -> double {
-    int64_t r = idx + b * t;  // cand = (index + b*t) mod n, already < n
+    rt r = (rt)(idx + b * t);  // cand = (index + b*t) mod n, already < n
     double sc = 0.0;
     for (int j = 0; j < c; ++j) {
       const double x = __dmul_rn(-kTwoPi, (double)r);
@@ -137,7 +143,7 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
       sc = __dadd_rn(sc, __dmul_rn(wv, wv));
       if (sc > bound) return sc;
       r <<= 1;
-      if (r >= n) r -= n;
+      if (r >= nn) r -= nn;
     }
     return sc;
   };
@@ -721,7 +727,8 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   for (int a0 = 0; a0 < A; a0 += 65535) {
     const int cnt = std::min(65535, A - a0);
     dim3 grid((unsigned)w.chunks, (unsigned)cnt);
-    noisy_search_kernel<<<grid, kSearchThreads, 0, st>>>(
+    auto kfn = P.n < (int64_t(1) << 31) ? noisy_search_kernel<true> : noisy_search_kernel<false>;
+    kfn<<<grid, kSearchThreads, 0, st>>>(
         P.n, P.c, act_index + a0, act_b + a0, est + (int64_t)a0 * P.c, w.chunks,
         reinterpret_cast<double*>(ws + w.part_s) + (int64_t)a0 * w.chunks,
         reinterpret_cast<int32_t*>(ws + w.part_t) + (int64_t)a0 * w.chunks);
