@@ -51,7 +51,8 @@ struct NoisyPlan {
   int64_t tau[AFFT_MAX_SHIFTS];  // shifts reduced mod n
 };
 
-// numpy: np.remainder(p + pi, 2pi) - pi
+// numpy: np.remainder(p + pi, 2pi) - pi.  The common ranges need no sign-of-zero fix:
+// x >= 0 there and x - k 2pi is exact (Sterbenz), so a zero result is +0 already.
 __device__ __forceinline__ double wrap_phase(double p) {
   const double x = __dadd_rn(p, kPi);
   double r;
@@ -63,11 +64,12 @@ __device__ __forceinline__ double wrap_phase(double p) {
     r = __dsub_rn(x, 2.0 * kTwoPi);  // exact (Sterbenz), 2*2pi exact
   } else if (x < 0.0 && x >= -kTwoPi) {
     r = __dadd_rn(x, kTwoPi);  // fmod(x) = x (<0): numpy adds the divisor
+    if (r == 0.0) r = 0.0;     // copysign(0, +2pi)
   } else {
     r = fmod(x, kTwoPi);
     if (r != 0.0 && r < 0.0) r = __dadd_rn(r, kTwoPi);
+    if (r == 0.0) r = 0.0;  // copysign(0, +2pi)
   }
-  if (r == 0.0) r = 0.0;  // copysign(0, +2pi)
   return __dsub_rn(r, kPi);
 }
 
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
   // target = RN(RN(-2 pi r) / n) by Markstein's sequence with the correctly rounded
   // reciprocal: q0 = RN(x inv), rem = x - q0 n (exact, fma), q = RN(q0 + rem inv).
   // Bit-identical to the IEEE quotient for every r in [0, n) at n <= 2^28 and a
-  // 2^28-point sweep at n = 3e9 (tools/div_check.cu; r = 0 keeps the -0.0 of x / n).
+  // 2^28-point sweep at n = 3e9 (tools/div_check.cu), up to the sign of a zero at r = 0.
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
   const rt nn = (rt)n;
@@ -137,8 +139,9 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
     for (int j = 0; j < c; ++j) {
       const double x = __dmul_rn(-kTwoPi, (double)r);
       const double q0 = __dmul_rn(x, inv);
-      const double q = __fma_rn(__fma_rn(-q0, dn, x), inv, q0);
-      const double tgt = r ? q : x;
+      // (r = 0 gives +0.0 here where x / n is -0.0; est - tgt differs only in the sign
+      // of a zero, which the + pi inside wrap_phase erases — the score is bit-identical)
+      const double tgt = __fma_rn(__fma_rn(-q0, dn, x), inv, q0);
       const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
       sc = __dadd_rn(sc, __dmul_rn(wv, wv));
       if (sc > bound) return sc;
