@@ -131,6 +131,13 @@ int d2h(std::vector<T>& h, const void* d, size_t count, cudaStream_t st) {
     if (_rc) return _rc;  \
   } while (0)
 
+// CUDA runtime call in the layer loop: map a failure to the library's status
+#define CK(expr)                                             \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return cuda_status(_e, #expr);    \
+  } while (0)
+
 struct Layer {
   int depth = 0;
   int64_t m = 0;     // active count
@@ -315,8 +322,8 @@ struct Dsfft {
       RC(afft_exact_thresholds(parts.as<double>(), nparts, n, 1, eps.as<double>(), st));
       std::vector<double> he;
       RC(d2h(he, eps.p, 1, st));
-      cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st);  // -1
-      cudaMemsetAsync(val.p, 0, (size_t)A * 16, st);
+      CK(cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st));  // -1
+      CK(cudaMemsetAsync(val.p, 0, (size_t)A * 16, st));
       RC(afft_classify_exact(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, he[0], he[0],
                              st8.as<int8_t>(), f0.as<int64_t>(), val.as<double>(), st));
       return finish_classify(L, E, multi, st8, f0, val);
@@ -334,7 +341,7 @@ struct Dsfft {
         RC(spectrum());
         DBuf s;
         RC(s.alloc(8, st, "dsfft norm"));
-        cudaMemsetAsync(s.p, 0, 8, st);
+        CK(cudaMemsetAsync(s.p, 0, 8, st));
         dsfft_norm2_kernel<<<148 * 4, 1024, 0, st>>>(Y.as<cd>(), n, s.as<double>());
         std::vector<double> h;
         RC(d2h(h, s.p, 1, st));
@@ -376,8 +383,8 @@ struct Dsfft {
       t1 = h1[0];
     }
     if (A == 0) return finish_classify(L, E, multi, st8, f0, val);
-    cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st);
-    cudaMemsetAsync(val.p, 0, (size_t)A * 16, st);
+    CK(cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st));
+    CK(cudaMemsetAsync(val.p, 0, (size_t)A * 16, st));
     DBuf rn, ws;
     RC(rn.alloc((size_t)A * 8, st, "dsfft resnorm"));
     const size_t need = afft_singleton_workspace_size(n, A, b, P.c, P.m);
@@ -397,10 +404,10 @@ struct Dsfft {
       const size_t of = 0, ov = (size_t)A * 8, oa = ov + (size_t)A * 16, os = oa + (size_t)A * 8;
       RC(pack.alloc(os + (size_t)A, st, "dsfft result pack"));
       char* pk = pack.as<char>();
-      cudaMemcpyAsync(pk + of, f0.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(pk + ov, val.p, (size_t)A * 16, cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(pk + oa, L.active.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(pk + os, st8.p, (size_t)A, cudaMemcpyDeviceToDevice, st);
+      CK(cudaMemcpyAsync(pk + of, f0.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(pk + ov, val.p, (size_t)A * 16, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(pk + oa, L.active.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(pk + os, st8.p, (size_t)A, cudaMemcpyDeviceToDevice, st));
       std::vector<char> h;
       RC(d2h(h, pk, os + (size_t)A, st));
       const int64_t* hf = reinterpret_cast<const int64_t*>(h.data() + of);
@@ -433,7 +440,7 @@ struct Dsfft {
     const int R = (int)shifts.size();
     DBuf idx, rowsb, counts, sig, rs, pos, val, cnt;
     RC(idx.alloc((size_t)nm * 8, st, "dsfft resolve ids"));
-    cudaMemcpyAsync(idx.p, buckets.data(), (size_t)nm * 8, cudaMemcpyHostToDevice, st);
+    CK(cudaMemcpyAsync(idx.p, buckets.data(), (size_t)nm * 8, cudaMemcpyHostToDevice, st));
     RC(rows(b, shifts, idx.as<int64_t>(), nm, rowsb, nullptr));
     RC(counts.alloc((size_t)nm * 4, st, "dsfft counts"));
     RC(sig.alloc((size_t)nm * a_m * 8, st, "dsfft sigmas"));
@@ -442,7 +449,7 @@ struct Dsfft {
                       sig.as<double>(), st));
     RC(rs.alloc((size_t)std::max(p, 1) * 8, st, "dsfft random shifts"));
     if (p)
-      cudaMemcpyAsync(rs.p, P.dt_shifts + off0, (size_t)p * 8, cudaMemcpyHostToDevice, st);
+      CK(cudaMemcpyAsync(rs.p, P.dt_shifts + off0, (size_t)p * 8, cudaMemcpyHostToDevice, st));
     RC(pos.alloc((size_t)nm * a_m * 8, st, "dsfft pos"));
     RC(val.alloc((size_t)nm * a_m * 16, st, "dsfft val"));
     RC(cnt.alloc((size_t)nm * 4, st, "dsfft cnt"));
@@ -453,9 +460,9 @@ struct Dsfft {
     const size_t ov = (size_t)nm * a_m * 8, oc = ov + (size_t)nm * a_m * 16;
     RC(pack.alloc(oc + (size_t)nm * 4, st, "dsfft resolve pack"));
     char* pk = pack.as<char>();
-    cudaMemcpyAsync(pk, pos.p, ov, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(pk + ov, val.p, (size_t)nm * a_m * 16, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(pk + oc, cnt.p, (size_t)nm * 4, cudaMemcpyDeviceToDevice, st);
+    CK(cudaMemcpyAsync(pk, pos.p, ov, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(pk + ov, val.p, (size_t)nm * a_m * 16, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(pk + oc, cnt.p, (size_t)nm * 4, cudaMemcpyDeviceToDevice, st));
     std::vector<char> h;
     RC(d2h(h, pk, oc + (size_t)nm * 4, st));
     const int64_t* hp = reinterpret_cast<const int64_t*>(h.data());
