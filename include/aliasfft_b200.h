@@ -176,6 +176,33 @@ int afft_node_energies(const double* vec, int32_t nshift, int64_t count, double*
 int afft_robust_thresholds(const double* energy, const uint8_t* mask, int64_t count,
                            int64_t batch, int32_t r, double* t0, double* t1, void* stream);
 
+/*
+ * One huge R-FFAST decode across ranks (SURVEY §8(e) stretch row): every rank holds the
+ * whole graph and the same state; the singleton search's candidate chunks are split
+ * round-robin over the ranks, and once per round `exchange` must replace each of the
+ * `count` partial slots (score double, candidate int32, on the device, stream-ordered on
+ * `stream`) by its minimum over all ranks — e.g. two NCCL all-reduces with op MIN.
+ * Slots a rank did not scan hold (+inf, INT32_MAX).  Returns 0 on success.  Results are
+ * identical to the single-rank decode.
+ */
+typedef int (*afft_exchange_fn)(void* ctx, double* part_score, int32_t* part_t, int64_t count,
+                                void* stream);
+typedef struct {
+  int32_t rank, world;
+  afft_exchange_fn exchange;
+  void* ctx;
+} AfftSearchShard;
+
+int afft_peel_noisy_sharded(int64_t n, int64_t batch, const int64_t* factors /* host */,
+                            int32_t ncycles, const int64_t* shifts /* host */, int32_t nshift,
+                            int32_t c, int32_t m, const double* weights /* host */,
+                            double* residual, int8_t* state, int64_t* node_f0, double* node_val,
+                            const double* t0, const double* t1, int32_t max_rounds,
+                            int64_t* rec_pos, double* rec_val, int32_t rec_cap,
+                            int32_t* rec_count, int32_t* rounds, int32_t* unresolved,
+                            void* workspace, size_t workspace_bytes, void* stream,
+                            const AfftSearchShard* shard);
+
 /* Workspace bytes for afft_peel_noisy / (with batch = node count) the per-node search. */
 size_t afft_noisy_workspace_size(int64_t n, int64_t batch, const int64_t* factors /* host */,
                                  int32_t ncycles, int32_t c, int32_t m);

@@ -66,6 +66,9 @@ SIGNATURES = {
     "afft_peel_noisy": (
         _INT, [_I64, _I64, _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P,
                _P, _I32, _P, _P, _P, _P, _SZ, _P]),
+    "afft_peel_noisy_sharded": (
+        _INT, [_I64, _I64, _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P,
+               _P, _I32, _P, _P, _P, _P, _SZ, _P, _P]),
     "afft_small_la": (_INT, [_I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
     "afft_bucketize_table": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _P, _I32, _P, _I64, _I64,
                                     _I64, _P]),
@@ -93,6 +96,18 @@ _lib = None
 
 class LibraryNotBuilt(ImportError):
     """The CUDA library is missing: build it with __graft_entry__.build()."""
+
+
+# afft_exchange_fn(ctx, part_score, part_t, count, stream) -> int
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_int64, ctypes.c_void_p)
+
+
+class SearchShardC(ctypes.Structure):
+    """AfftSearchShard (include/aliasfft_b200.h)."""
+
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("exchange", EXCHANGE_FN), ("ctx", ctypes.c_void_p)]
 
 
 class DsfftParams(ctypes.Structure):

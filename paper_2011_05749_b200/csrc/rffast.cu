@@ -25,6 +25,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "afft_common.cuh"
 #include "peel_core.cuh"
 
@@ -109,12 +111,12 @@ template <bool k32>
 __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
     int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
     const double* __restrict__ est, int chunks, double* __restrict__ part_score,
-    int32_t* __restrict__ part_t) {
+    int32_t* __restrict__ part_t, int chunk_rank, int chunk_world) {
   __shared__ double s_est[kMaxStrides];
   __shared__ double w_score[kSearchThreads / 32];
   __shared__ int32_t w_t[kSearchThreads / 32];
   const int a = blockIdx.y;
-  const int chunk = blockIdx.x;
+  const int chunk = chunk_rank + (int)blockIdx.x * chunk_world;  // this rank's chunks
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t t0 = (int64_t)chunk * kChunk;
@@ -716,9 +718,69 @@ static NoisyWs noisy_ws(const NoisyPlan& P, int64_t rows) {
 }
 
 // est → scan → reduce + LS fit for A active rows already listed in the workspace.
+__global__ void part_fill_kernel(int64_t count, double* __restrict__ part_score,
+                                 int32_t* __restrict__ part_t) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) {
+    part_score[i] = __longlong_as_double(0x7ff0000000000000LL);  // +inf: not this rank's
+    part_t[i] = INT32_MAX;
+  }
+}
+
+// Rewrite the active list from rows sorted ascending (keys[a] = row): the prep kernel
+// compacts with an atomic, so slot order differs from run to run and rank to rank —
+// harmless for one rank, but a split search exchanges partials by slot.
+__global__ void act_from_rows_kernel(int A, const __grid_constant__ NoisyPlan P,
+                                     const int64_t* __restrict__ rows, int64_t* __restrict__ act_row,
+                                     int64_t* __restrict__ act_index, int64_t* __restrict__ act_b) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const int64_t e = rows[a];
+  const int g = (int)(e % P.nodes);
+  const int c = noisy_cycle(P, g);
+  act_row[a] = e;
+  act_index[a] = g - P.base[c];
+  act_b[a] = P.b[c];
+}
+
+static int canonical_active(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
+                            int64_t rows_total, cudaStream_t st) {
+  int64_t* act_row = reinterpret_cast<int64_t*>(ws + w.act_row);
+  int bits = 1;
+  while (bits < 63 && (int64_t(1) << bits) < rows_total) ++bits;
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, temp, act_row, act_row, A, 0, bits, st);
+  char* buf = nullptr;
+  const size_t keys_bytes = ((size_t)A * 8 + 255) & ~size_t(255);
+  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&buf), keys_bytes + temp, st);
+  if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(search shard sort)");
+  int64_t* sorted = reinterpret_cast<int64_t*>(buf);
+  e = cub::DeviceRadixSort::SortKeys(buf + keys_bytes, temp, act_row, sorted, A, 0, bits, st);
+  if (e == cudaSuccess) {
+    act_from_rows_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(
+        A, P, sorted, act_row, reinterpret_cast<int64_t*>(ws + w.act_index),
+        reinterpret_cast<int64_t*>(ws + w.act_b));
+    e = cudaGetLastError();
+  }
+  scratch_free(buf, st);
+  return e == cudaSuccess ? AFFT_OK : cuda_status(e, "search shard active-list sort");
+}
+
+// est -> scan -> (exchange) -> reduce + LS fit.  With a shard of world W > 1 this rank
+// scans the chunks ch = rank (mod W) of every active node, the other slots hold
+// (+inf, INT32_MAX), and the caller's exchange replaces every slot by its minimum over
+// the ranks (score and t independently: exactly one rank holds a real value per slot),
+// after which the reduction and fit are the single-rank ones — identical results.
 static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
-                      const double* residual, cudaStream_t st) {
+                      const double* residual, cudaStream_t st,
+                      const AfftSearchShard* shard = nullptr, int64_t rows_total = 0) {
   if (A == 0) return AFFT_OK;
+  const int rank = shard && shard->world > 1 ? shard->rank : 0;
+  const int world = shard && shard->world > 1 ? shard->world : 1;
+  if (world > 1) {  // every rank must list the active nodes in the same order
+    const int rc = canonical_active(P, w, ws, A, rows_total, st);
+    if (rc) return rc;
+  }
   const int64_t* act_row = reinterpret_cast<const int64_t*>(ws + w.act_row);
   const int64_t* act_index = reinterpret_cast<const int64_t*>(ws + w.act_index);
   const int64_t* act_b = reinterpret_cast<const int64_t*>(ws + w.act_b);
@@ -727,16 +789,32 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(A, P.c, P.m, act_row, residual,
                                                                 P.R, P, est);
   AFFT_CHECK_LAUNCH("noisy_est_kernel");
-  for (int a0 = 0; a0 < A; a0 += 65535) {
+  double* part_s = reinterpret_cast<double*>(ws + w.part_s);
+  int32_t* part_t = reinterpret_cast<int32_t*>(ws + w.part_t);
+  const int64_t nparts = (int64_t)A * w.chunks;
+  if (world > 1)
+    part_fill_kernel<<<(unsigned)((nparts + 255) / 256), 256, 0, st>>>(nparts, part_s, part_t);
+  const int mine = (w.chunks - rank + world - 1) / world;
+  for (int a0 = 0; a0 < A && mine > 0; a0 += 65535) {
     const int cnt = std::min(65535, A - a0);
-    dim3 grid((unsigned)w.chunks, (unsigned)cnt);
+    dim3 grid((unsigned)mine, (unsigned)cnt);
     auto kfn = P.n < (int64_t(1) << 31) ? noisy_search_kernel<true> : noisy_search_kernel<false>;
     kfn<<<grid, kSearchThreads, 0, st>>>(
         P.n, P.c, act_index + a0, act_b + a0, est + (int64_t)a0 * P.c, w.chunks,
-        reinterpret_cast<double*>(ws + w.part_s) + (int64_t)a0 * w.chunks,
-        reinterpret_cast<int32_t*>(ws + w.part_t) + (int64_t)a0 * w.chunks);
+        part_s + (int64_t)a0 * w.chunks, part_t + (int64_t)a0 * w.chunks, rank, world);
   }
   AFFT_CHECK_LAUNCH("noisy_search_kernel");
+  if (world > 1) {
+    if (!shard->exchange) {
+      set_error("search shard without an exchange callback");
+      return AFFT_EINVAL;
+    }
+    const int rc = shard->exchange(shard->ctx, part_s, part_t, nparts, st);
+    if (rc) {
+      set_error("search shard exchange failed (%d)", rc);
+      return AFFT_ECUDA;
+    }
+  }
   noisy_finalize_kernel<<<(unsigned)((A * 32 + 255) / 256), 256, 0, st>>>(
       A, w.chunks, reinterpret_cast<const double*>(ws + w.part_s),
       reinterpret_cast<const int32_t*>(ws + w.part_t), act_row, act_index, act_b, residual, P,
@@ -876,6 +954,23 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
                                double* rec_val, int32_t rec_cap, int32_t* rec_count,
                                int32_t* rounds, int32_t* unresolved, void* workspace,
                                size_t workspace_bytes, void* stream) {
+  return afft_peel_noisy_sharded(n, batch, factors, ncycles, shifts, nshift, c, m, weights,
+                                 residual, state, node_f0, node_val, t0, t1, max_rounds, rec_pos,
+                                 rec_val, rec_cap, rec_count, rounds, unresolved, workspace,
+                                 workspace_bytes, stream, nullptr);
+}
+
+extern "C" int afft_peel_noisy_sharded(
+    int64_t n, int64_t batch, const int64_t* factors, int32_t ncycles, const int64_t* shifts,
+    int32_t nshift, int32_t c, int32_t m, const double* weights, double* residual, int8_t* state,
+    int64_t* node_f0, double* node_val, const double* t0, const double* t1, int32_t max_rounds,
+    int64_t* rec_pos, double* rec_val, int32_t rec_cap, int32_t* rec_count, int32_t* rounds,
+    int32_t* unresolved, void* workspace, size_t workspace_bytes, void* stream,
+    const AfftSearchShard* shard) {
+  if (shard && (shard->world < 1 || shard->rank < 0 || shard->rank >= shard->world)) {
+    set_error("afft_peel_noisy_sharded: rank %d of %d", shard->rank, shard->world);
+    return AFFT_EINVAL;
+  }
   if (batch == 0) return AFFT_OK;
   if (!residual || !state || !node_f0 || !node_val || !t0 || !t1 || !rec_pos || !rec_val ||
       !rec_count || !rounds || !unresolved || !weights || !shifts || max_rounds < 0) {
@@ -947,7 +1042,7 @@ extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors,
       return cuda_status(e, "afft_peel_noisy round sync");
     }
     const int A = host[0];
-    if ((rc = run_search(*P, w, ws, A, residual, st))) {
+    if ((rc = run_search(*P, w, ws, A, residual, st, shard, total))) {
       if (hscratch) scratch_free(hscratch, st);
       return rc;
     }

@@ -9,6 +9,8 @@ round run in csrc/rffast.cu.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -171,9 +173,33 @@ class NoisyDecode:
     unresolved: torch.Tensor
 
 
+def _shard_struct(shard, ws: torch.Tensor):
+    """AfftSearchShard whose exchange callback runs shard.reduce_min on views of the
+    workspace tensor (the partial arrays live inside it)."""
+    if shard is None or shard.world == 1:
+        return None, None
+    base = ws.data_ptr()
+    errors = []
+
+    def exchange(ctx, ps, pt, count, stream):
+        try:
+            scores = ws[ps - base: ps - base + 8 * count].view(torch.float64)
+            cands = ws[pt - base: pt - base + 4 * count].view(torch.int32)
+            shard.reduce_min(scores, cands)
+            return 0
+        except Exception as exc:  # noqa: BLE001 - reported to the C caller as a status
+            errors.append(exc)
+            return 1
+
+    cb = _lib.EXCHANGE_FN(exchange)
+    st = _lib.SearchShardC(shard.rank, shard.world, cb, None)
+    return st, (cb, errors)
+
+
 def peel_noisy_device(n, factors, search, residual, state, node_f0, node_val, t0, t1,
-                      max_rounds, rec_pos, rec_val, rec_count) -> NoisyDecode:
-    """afft_peel_noisy on device tensors shaped [batch, nodes, R] / [batch, nodes]."""
+                      max_rounds, rec_pos, rec_val, rec_count, shard=None) -> NoisyDecode:
+    """afft_peel_noisy on device tensors shaped [batch, nodes, R] / [batch, nodes];
+    with a shard.SearchShard the singleton search is split over its ranks."""
     batch = int(residual.shape[0])
     dev = residual.device
     fb, nc = _lib.host_i64(factors)
@@ -181,16 +207,18 @@ def peel_noisy_device(n, factors, search, residual, state, node_f0, node_val, t0
     ws = _workspace(n, batch, factors, search.c, search.m, dev)
     rounds = torch.zeros(batch, dtype=torch.int32, device=dev)
     unresolved = torch.zeros(batch, dtype=torch.int32, device=dev)
-    _lib.check(
-        _lib.load().afft_peel_noisy(
-            n, batch, fb, nc, sb, ns, search.c, search.m, wb, residual.data_ptr(),
-            state.data_ptr(), node_f0.data_ptr(), node_val.data_ptr(), t0.data_ptr(),
-            t1.data_ptr(), int(max_rounds), rec_pos.data_ptr(), rec_val.data_ptr(),
-            int(rec_pos.shape[-1]), rec_count.data_ptr(), rounds.data_ptr(),
-            unresolved.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream_ptr(),
-        ),
-        "peel_decode(noisy)",
+    sh, keep = _shard_struct(shard, ws)
+    rc = _lib.load().afft_peel_noisy_sharded(
+        n, batch, fb, nc, sb, ns, search.c, search.m, wb, residual.data_ptr(),
+        state.data_ptr(), node_f0.data_ptr(), node_val.data_ptr(), t0.data_ptr(),
+        t1.data_ptr(), int(max_rounds), rec_pos.data_ptr(), rec_val.data_ptr(),
+        int(rec_pos.shape[-1]), rec_count.data_ptr(), rounds.data_ptr(),
+        unresolved.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream_ptr(),
+        ctypes.byref(sh) if sh is not None else None,
     )
+    if keep is not None and keep[1]:
+        raise RuntimeError(f"search shard exchange failed: {keep[1][0]!r}") from keep[1][0]
+    _lib.check(rc, "peel_decode(noisy)")
     return NoisyDecode(rec_pos, rec_val, rec_count, rounds, unresolved)
 
 
@@ -265,9 +293,12 @@ class RffastBatchResult:
         return SparseSpectrum(self.n, {int(f): complex(v) for f, v in zip(pos, val)})
 
 
-def rffast_batch(x, k: int, factors, search, max_rounds: int | None = None) -> RffastBatchResult:
+def rffast_batch(x, k: int, factors, search, max_rounds: int | None = None, *,
+                 shard=None) -> RffastBatchResult:
     """R-FFAST over a (batch, n) block: graph build at the c*m search shifts,
-    median-energy thresholds, noisy peeling and top-k truncation, all on the device."""
+    median-energy thresholds, noisy peeling and top-k truncation, all on the device.
+    ``shard`` (a shard.SearchShard) splits the singleton search of this same batch
+    over several ranks (one huge signal on several GPUs); results are unchanged."""
     xd = _device.as_device_batch(x)
     batch, n = int(xd.shape[0]), int(xd.shape[1])
     dev = xd.device
@@ -294,7 +325,7 @@ def rffast_batch(x, k: int, factors, search, max_rounds: int | None = None) -> R
     rec_count = torch.zeros(batch, dtype=torch.int32, device=dev)
     mr = int(max_rounds) if max_rounds else k + 4
     out = peel_noisy_device(n, factors, search, nodes, state, f0, val, t0, t1, mr, rec_pos,
-                            rec_val, rec_count)
+                            rec_val, rec_count, shard=shard)
     kk = max(int(k), 0)
     opos = torch.empty((batch, kk), dtype=torch.int64, device=dev)
     oval = torch.empty((batch, kk), dtype=torch.complex128, device=dev)

@@ -1,4 +1,5 @@
-"""Signal-parallel sharding across ranks.
+"""Signal-parallel sharding across ranks, and the one-huge-signal
+R-FFAST split (the §8(e) stretch row, `SearchShard`).
 
 Every algorithm on the path is independent per signal, so a batch is split into
 contiguous per-rank slices with no data-path collective; the only exchange is
@@ -49,3 +50,32 @@ def max_over_ranks(values: list[float], device, group=None) -> list[float]:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return [float(v) for v in t.tolist()]
+
+
+class SearchShard:
+    """Split of one R-FFAST decode's singleton search over `world` ranks (SURVEY §8(e),
+    stretch row: "node x candidate-range split of the singleton search, MINLOC
+    all-reduce per peeling round").
+
+    Every rank builds the same graph and runs the same peeling rounds; rank r scans
+    the candidate chunks ch = r (mod world) of every active node, and once per round
+    `reduce_min(scores, cands)` must make both device tensors (float64 / int32, the
+    per-(node, chunk) partial minima, unscanned slots +inf / INT32_MAX) their
+    element-wise minimum over the ranks, in place.  Exactly one rank holds a real
+    value per slot, so MIN over each array is the MINLOC; results equal the
+    single-rank decode bit for bit.
+    """
+
+    def __init__(self, rank: int, world: int, reduce_min):
+        if world < 1 or not 0 <= rank < world:
+            raise ValueError(f"bad rank {rank} / world {world}")
+        self.rank, self.world, self.reduce_min = int(rank), int(world), reduce_min
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "SearchShard":
+        """NCCL (or gloo) all-reduce MIN over a torch.distributed group."""
+        def reduce_min(scores: torch.Tensor, cands: torch.Tensor) -> None:
+            dist.all_reduce(scores, op=dist.ReduceOp.MIN, group=group)
+            dist.all_reduce(cands, op=dist.ReduceOp.MIN, group=group)
+
+        return cls(dist.get_rank(group), dist.get_world_size(group), reduce_min)

@@ -67,3 +67,42 @@ def test_gather_slots_world2():
         assert gv == [[float(v) for v in row] for row in gp]
         assert gc == [1] * 5 + [2] * 5
         assert t == [1.0, 10.0]
+
+
+def _min_worker(rank, world, port, q):
+    import numpy as np
+
+    from paper_2011_05749_b200.shard import SearchShard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sh = SearchShard.from_process_group()
+    # slot i belongs to rank i % world; the others hold (+inf, INT32_MAX)
+    count = 7
+    scores = torch.full((count,), float("inf"), dtype=torch.float64)
+    cands = torch.full((count,), 2**31 - 1, dtype=torch.int32)
+    for i in range(rank, count, world):
+        scores[i] = 0.5 * i + 0.25
+        cands[i] = 100 + i
+    sh.reduce_min(scores, cands)
+    q.put((rank, sh.rank, sh.world, scores.tolist(), cands.tolist()))
+    dist.destroy_process_group()
+
+
+def test_search_shard_exchange_world2():
+    """SearchShard.from_process_group: the per-round partial exchange (two all-reduce
+    MIN, NCCL on GPUs) leaves every rank with the owner's value in every slot."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_min_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, r2, w2, scores, cands in got:
+        assert (r2, w2) == (rank, 2)
+        assert scores == [0.5 * i + 0.25 for i in range(7)]
+        assert cands == [100 + i for i in range(7)]
