@@ -9,6 +9,7 @@
 // reciprocal — to a caller-strided output, so the same kernel produces the
 // FilteredSpectrum layout [s][t][i] and the peeling-node layout [s][g][t].
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -106,6 +107,7 @@ struct GStockParams {
   int R;
   int64_t Ns;
   int cnt;
+  int perm;       // gfft_reg_kernel: tile -> chunk order (0 identity, 1 odd multiplier, 2 stride)
   DftPlan plan;
   int64_t tau[AFFT_MAX_SHIFTS];
 };
@@ -274,6 +276,188 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
   }
 }
 
+// Power-of-two radix R = A * B (A = 2^LA, B = 2^LB <= 16) with the DFT in registers:
+// the same pass as gstockham_kernel (same tile of kCnt = 2048 / R butterflies, same
+// input rows and output placement), restructured so that each point crosses shared
+// memory once instead of ~5 times and the inter-pass twiddles come from two table
+// reads per sub-sequence instead of one or two scattered reads per point (the smem
+// Stockham version saturated the L1 data pipe with bank conflicts and twiddle
+// gathers at 17% of HBM bandwidth, profiles/r01_k2_ncu.md).
+//   r = n1 + A n2,  q = qb + B qa:
+//   stage A, item (jj, n1): v[n2] = in[row r] * w_b^(k r tstep); DFT_B over n2;
+//                           U[jj][n1][qb] = w_R^(n1 qb) * that  (smem, stride R + 1)
+//   stage B, item (jj, qb): V[qb + B qa] = DFT_A over n1 of U[jj][n1][qb]  -> HBM
+// Global loads go straight to registers (all 16 per thread issued before use);
+// lanes run along jj so every row segment (kCnt contiguous points, >= 128 B) is
+// one coalesced request; the first pass (N_s = 1, outputs of a butterfly are
+// contiguous) runs stage B along qb instead.
+constexpr int kGfftThreads = 128;
+
+template <int LA, int LB>
+__global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
+    const __grid_constant__ GStockParams p) {
+  constexpr int A = 1 << LA, B = 1 << LB, LGR = LA + LB, R = A * B;
+  constexpr int kCnt = kGStockPoints / R, kLgCnt = 11 - LGR;
+  constexpr int LD = R + 1;
+  constexpr int IA = kCnt * A / kGfftThreads;  // stage-A items per thread
+  constexpr int IB = kCnt * B / kGfftThreads;  // stage-B items per thread
+  static_assert(IA * kGfftThreads == kCnt * A && IB * kGfftThreads == kCnt * B, "tile shape");
+  static_assert(IA * B == 16 && IB * A == 16, "16 points per thread per stage");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cd* twR = reinterpret_cast<cd*>(smem_raw);
+  cd* U = twR + R;
+  const int tid = threadIdx.x;
+  build_twiddles(twR, R, tid, kGfftThreads);
+  const int64_t nb = p.b / R;
+  const int64_t nchunks = nb >> kLgCnt;
+  const int64_t ntiles = p.batch * p.nshift * nchunks;
+  const int64_t tstep = p.b / (p.Ns * R);
+  const bool pow2ns = (p.Ns & (p.Ns - 1)) == 0;  // N_s = product of earlier radices
+  const bool first = p.in == nullptr;
+  const bool c64 = first && p.dtype == AFFT_C64;
+  const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
+  const double inv_b = 1.0 / (double)p.b;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int64_t chunk = tile % nchunks;
+    if (p.perm == 1)  // nchunks a power of two: an odd multiplier is a bijection
+      chunk = (chunk * 0x9E3779B1LL) & (nchunks - 1);
+    else if (p.perm == 2 && nchunks >= 4096 && (nchunks & 63) == 0)
+      chunk = (chunk & 63) * (nchunks >> 6) + (chunk >> 6);
+    const int64_t st_ = tile / nchunks;
+    const int t = (int)(st_ % p.nshift);
+    const int64_t s = st_ / p.nshift;
+    const int64_t j0 = chunk << kLgCnt;
+    const int64_t k0 = pow2ns ? (j0 & (p.Ns - 1)) : j0 % p.Ns;
+    // k = (j0 + jj) mod N_s
+    auto kmod = [&](int jj) -> int64_t {
+      if (pow2ns) return (j0 + jj) & (p.Ns - 1);
+      int64_t k = k0 + jj;
+      while (k >= p.Ns) k -= p.Ns;
+      return k;
+    };
+    const int64_t seq = s * p.nshift + t;
+    const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
+    const int64_t tau = first ? (p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n)
+                                               : p.tau[t])
+                              : 0;
+    // ---- stage A: loads (all issued first), twiddles, DFT_B, w_R, to smem
+    // (one branch around whole unrolled loops: with the dtype test per load, each c64
+    // load was converted right after issue and the 16 loads ran one latency apart)
+    cd v[IA][B];
+    if (c64) {
+      float2 raw[IA][B];
+#pragma unroll
+      for (int i = 0; i < IA; ++i) {
+        const int w = tid + i * kGfftThreads;
+        const int jj = w & (kCnt - 1), n1 = w >> kLgCnt;
+#pragma unroll
+        for (int n2 = 0; n2 < B; ++n2) {
+          int64_t idx = (j0 + jj + (int64_t)(n1 + A * n2) * nb) * p.L - tau;
+          if (idx < 0) idx += p.n;
+          raw[i][n2] = __ldg(reinterpret_cast<const float2*>(xs) + idx);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < IA; ++i)
+#pragma unroll
+        for (int n2 = 0; n2 < B; ++n2) v[i][n2] = cd{(double)raw[i][n2].x, (double)raw[i][n2].y};
+    } else {
+      const double2* base = first ? reinterpret_cast<const double2*>(xs)
+                                  : reinterpret_cast<const double2*>(p.in + seq * p.b);
+      const int64_t L = first ? p.L : 1;
+      const int64_t off = first ? tau : 0;
+      double2 raw[IA][B];
+#pragma unroll
+      for (int i = 0; i < IA; ++i) {
+        const int w = tid + i * kGfftThreads;
+        const int jj = w & (kCnt - 1), n1 = w >> kLgCnt;
+#pragma unroll
+        for (int n2 = 0; n2 < B; ++n2) {
+          int64_t idx = (j0 + jj + (int64_t)(n1 + A * n2) * nb) * L - off;
+          if (idx < 0) idx += p.n;
+          raw[i][n2] = __ldcs(base + idx);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < IA; ++i)
+#pragma unroll
+        for (int n2 = 0; n2 < B; ++n2) v[i][n2] = cd{raw[i][n2].x, raw[i][n2].y};
+    }
+    __syncthreads();  // the previous tile's stage B has finished reading U
+#pragma unroll
+    for (int i = 0; i < IA; ++i) {
+      const int w = tid + i * kGfftThreads;
+      const int jj = w & (kCnt - 1), n1 = w >> kLgCnt;
+      if (p.Ns > 1) {
+        // w_b^(k r tstep) for r = n1 + A n2: base w_b^(k n1 tstep), step w_b^(k A tstep)
+        const int64_t kt = kmod(jj) * tstep;
+        if (kt) {
+          cd cur = tw_b(p.tlo, p.thi, kt * n1);
+          const cd step = tw_b(p.tlo, p.thi, kt * A);
+#pragma unroll
+          for (int n2 = 0; n2 < B; ++n2) {
+            if (n1 || n2) v[i][n2] = cmul(v[i][n2], cur);
+            if (n2 + 1 < B) cur = cmul(cur, step);
+          }
+        }
+      }
+      dft_reg<B>(v[i]);
+      cd* u = U + jj * LD + n1 * B;
+#pragma unroll
+      for (int qb = 0; qb < B; ++qb) u[qb] = (n1 && qb) ? cmul(v[i][qb], twR[n1 * qb]) : v[i][qb];
+    }
+    __syncthreads();
+    // ---- stage B: DFT_A over n1, outputs q = qb + B qa
+    double* out = p.out ? p.out + 2 * (s * p.out_signal_stride + p.out_offset +
+                                       t * p.out_shift_stride)
+                        : nullptr;
+    cd* tmp = p.tmp ? p.tmp + seq * p.b : nullptr;
+#pragma unroll
+    for (int i = 0; i < IB; ++i) {
+      const int w = tid + i * kGfftThreads;
+      int jj, qb;
+      if (p.Ns == 1) {
+        qb = w & (B - 1);
+        jj = w >> LB;
+      } else {
+        jj = w & (kCnt - 1);
+        qb = w >> kLgCnt;
+      }
+      cd a[A];
+      const cd* u = U + jj * LD + qb;
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) a[n1] = u[n1 * B];
+      dft_reg<A>(a);
+      const int64_t j = j0 + jj;
+      const int64_t k = kmod(jj);
+      const int64_t base = (j - k) * R + k;
+#pragma unroll
+      for (int qa = 0; qa < A; ++qa) {
+        const int64_t dst = base + (int64_t)(qb + B * qa) * p.Ns;
+        if (tmp) {
+          __stcs(reinterpret_cast<double2*>(tmp + dst), make_double2(a[qa].re, a[qa].im));
+        } else {  // complex128 output: 16-B aligned pairs
+          const cd wv = cscale(a[qa], inv_b);
+          *reinterpret_cast<double2*>(out + 2 * dst * p.out_bin_stride) = make_double2(wv.re, wv.im);
+        }
+      }
+    }
+  }
+}
+
+static const void* gfft_reg_fn(int lgr) {
+  switch (lgr) {
+    case 2: return (const void*)gfft_reg_kernel<1, 1>;
+    case 3: return (const void*)gfft_reg_kernel<2, 1>;
+    case 4: return (const void*)gfft_reg_kernel<2, 2>;
+    case 5: return (const void*)gfft_reg_kernel<3, 2>;
+    case 6: return (const void*)gfft_reg_kernel<3, 3>;
+    case 7: return (const void*)gfft_reg_kernel<4, 3>;
+    case 8: return (const void*)gfft_reg_kernel<4, 4>;
+    default: return nullptr;
+  }
+}
+
 static const void* const* gstockham_fixed_table() {
   static const void* const t[9] = {
       nullptr,
@@ -310,7 +494,23 @@ static bool plan_radices(int64_t b, std::vector<int>* radices) {
   }
   std::sort(groups.rbegin(), groups.rend());
   radices->assign(groups.begin(), groups.end());
+  if ((b & (b - 1)) == 0 && b >= 16) {  // powers of two: the same pass count, balanced
+    int lg = 0;
+    while ((int64_t(1) << lg) < b) ++lg;
+    const int P = (lg + 7) / 8;
+    radices->clear();
+    for (int i = 0; i < P; ++i) radices->push_back(1 << (lg / P + (i < lg % P ? 1 : 0)));
+  }
   return true;
+}
+
+// AFFT_FFT_SMEM=1 selects the smem Stockham pass for power-of-two radices (A/B runs).
+static bool fft_smem_path() {
+  static const bool v = [] {
+    const char* e = getenv("AFFT_FFT_SMEM");
+    return e && e[0] == '1';
+  }();
+  return v;
 }
 
 static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
@@ -383,11 +583,23 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
       g.cnt = kGStockPoints / R;
     }
     const void* kfn = lgr < 0 ? (const void*)gstockham_kernel<-1> : gstockham_fixed_table()[lgr];
-    const size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
+    size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
+    int threads = kGStockThreads;
+    if (lgr >= 2 && !fft_smem_path()) {  // register-resident pass
+      kfn = gfft_reg_fn(lgr);
+      const int64_t nch = (b / R) / g.cnt;
+      static const int perm_env = [] {
+        const char* v = getenv("AFFT_TILE_PERM");
+        return v ? atoi(v) : 0;
+      }();
+      g.perm = (nch & (nch - 1)) == 0 ? perm_env : 0;
+      smem = (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
+      threads = kGfftThreads;
+    }
     e = ensure_smem(kfn, (int)smem);
     int occ = 0;
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kGStockThreads, smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, threads, smem);
     if (e != cudaSuccess || occ < 1) {
       rc = cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "large-b DFT pass");
       break;
@@ -395,7 +607,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     const int64_t tiles = (int64_t)seqs * ((b / R + g.cnt - 1) / g.cnt);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * occ);
     void* args[] = {&g};
-    e = cudaLaunchKernel(kfn, dim3(grid), dim3(kGStockThreads), args, smem, stream);
+    e = cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, stream);
     if (e != cudaSuccess) {
       rc = cuda_status(e, "large-b DFT launch");
       break;
@@ -403,7 +615,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     Ns *= R;
   }
   scratch_free(scratch, stream);
-  if (!rc) AFFT_CHECK_LAUNCH("gstockham_kernel");
+  if (!rc) AFFT_CHECK_LAUNCH("large-b DFT pass");
   return rc;
 }
 

@@ -247,6 +247,9 @@ struct AliasCosets {
 // All b buckets: energy[i] = sum_t |y_tau_t[i]|^2 (the w_n^(i tau) factor has modulus 1,
 // so shifts with equal tau mod L contribute equal terms); vals0 (optional) = the
 // tau = 0 values sum_l Y[i + l b].
+// LM >= L: the register footprint follows L (at LM = 32 the kernel holds 158
+// registers, one CTA per SM, which left the L = 2 layer latency-bound at 1.1 TB/s).
+template <int LM>
 __global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y, int64_t b, int L,
                                                         const __grid_constant__ AliasCosets cs,
                                                         double* __restrict__ energy,
@@ -256,14 +259,14 @@ __global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b) return;
-  cd y[kAliasMaxL];
+  cd y[LM];
 #pragma unroll
-  for (int l = 0; l < kAliasMaxL; ++l)
+  for (int l = 0; l < LM; ++l)
     if (l < L) y[l] = Y[i + (int64_t)l * b];
   if (vals0) {
     cd acc = y[0];
 #pragma unroll
-    for (int l = 1; l < kAliasMaxL; ++l)
+    for (int l = 1; l < LM; ++l)
       if (l < L) acc = cadd(acc, y[l]);
     vals0[i] = acc;
   }
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y
       cd acc = y[0];
       int m = 0;
 #pragma unroll
-      for (int l = 1; l < kAliasMaxL; ++l) {
+      for (int l = 1; l < LM; ++l) {
         if (l < L) {
           m += cs.r[u];
           if (m >= L) m -= L;
@@ -421,8 +424,18 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
       }
       ++cs.mult[u];
     }
-    alias_all_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
-        Y, b, (int)L, cs, energy, reinterpret_cast<cd*>(values0));
+    const unsigned grid = (unsigned)((b + 255) / 256);
+    cd* v0 = reinterpret_cast<cd*>(values0);
+    if (L <= 2)
+      alias_all_kernel<2><<<grid, 256, 0, st>>>(Y, b, (int)L, cs, energy, v0);
+    else if (L <= 4)
+      alias_all_kernel<4><<<grid, 256, 0, st>>>(Y, b, (int)L, cs, energy, v0);
+    else if (L <= 8)
+      alias_all_kernel<8><<<grid, 256, 0, st>>>(Y, b, (int)L, cs, energy, v0);
+    else if (L <= 16)
+      alias_all_kernel<16><<<grid, 256, 0, st>>>(Y, b, (int)L, cs, energy, v0);
+    else
+      alias_all_kernel<kAliasMaxL><<<grid, 256, 0, st>>>(Y, b, (int)L, cs, energy, v0);
   }
   AFFT_CHECK_LAUNCH("afft_alias_rows");
   return AFFT_OK;
