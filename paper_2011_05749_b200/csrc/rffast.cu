@@ -103,10 +103,56 @@ __device__ __forceinline__ int noisy_cycle(const NoisyPlan& P, int g) {
 
 // -------------------------------------------------------------- candidate scan
 
-// One CTA scores kChunk consecutive candidates t of one active node.
-// Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
+// Score of candidate cand = (index + b*t) mod n (already reduced: r = cand), summed
+// in stride order exactly as the reference does; stops (returns > bound) once the
+// partial sum exceeds bound: every term is >= 0, so such a candidate is strictly
+// worse than the candidate that set bound and can be neither the minimum nor a tie.
+// target = RN(RN(-2 pi r) / n) by Markstein's sequence with the correctly rounded
+// reciprocal: q0 = RN(x inv), rem = x - q0 n (exact, fma), q = RN(q0 + rem inv).
+// Bit-identical to the IEEE quotient for every r in [0, n) at n <= 2^28 and a
+// 2^28-point sweep at n = 3e9 (tools/div_check.cu), up to the sign of a zero at r = 0.
 // k32: n < 2^31, so the doubled residue 2r < 2^32 fits in 32 bits (the 64-bit
 // doubling-and-reduce was ~15% of the kernel's instructions; the kernel is issue-bound).
+template <bool k32>
+__device__ __forceinline__ double cand_score(
+    typename std::conditional<k32, uint32_t, int64_t>::type r,
+    typename std::conditional<k32, uint32_t, int64_t>::type nn, const double* s_est, int c,
+    double dn, double inv, double bound) {
+  double sc = 0.0;
+  for (int j = 0; j < c; ++j) {
+    const double x = __dmul_rn(-kTwoPi, (double)r);
+    const double q0 = __dmul_rn(x, inv);
+    // (r = 0 gives +0.0 here where x / n is -0.0; est - tgt differs only in the sign
+    // of a zero, which the + pi inside wrap_phase erases — the score is bit-identical)
+    const double tgt = __fma_rn(__fma_rn(-q0, dn, x), inv, q0);
+    const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
+    sc = __dadd_rn(sc, __dmul_rn(wv, wv));
+    if (sc > bound) return sc;
+    r <<= 1;
+    if (r >= nn) r -= nn;
+  }
+  return sc;
+}
+
+// Pruning bound: the full score of the candidate nearest the stride-0 estimate.
+template <bool k32>
+__device__ __forceinline__ double search_bound(int64_t n, int64_t b, int64_t L, int64_t idx,
+                                               const double* s_est, int c, double inv) {
+  using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
+  const double dn = (double)n;
+  const double fe = (-s_est[0] * dn) / kTwoPi;
+  double dd = (fe - (double)idx) / (double)b;
+  int64_t th = (int64_t)floor(dd + 0.5);
+  th %= L;
+  if (th < 0) th += L;
+  double bound = cand_score<k32>((rt)(idx + b * th), (rt)n, s_est, c, dn, inv,
+                                 __longlong_as_double(0x7ff0000000000000LL));
+  if (!(bound == bound)) bound = __longlong_as_double(0x7ff0000000000000LL);  // NaN: no pruning
+  return bound;
+}
+
+// One CTA scores kChunk consecutive candidates t of one active node.
+// Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
 template <bool k32>
 __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
     int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
@@ -124,48 +170,15 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
   __syncthreads();
   const int64_t idx = act_index[a];
   const double dn = (double)n;
-  // score of candidate t, summed in stride order exactly as the reference does;
-  // stops (returns > bound) once the partial sum exceeds bound: every term is
-  // >= 0, so such a candidate is strictly worse than the candidate that set bound
-  // and can be neither the minimum nor a tie.
-  // target = RN(RN(-2 pi r) / n) by Markstein's sequence with the correctly rounded
-  // reciprocal: q0 = RN(x inv), rem = x - q0 n (exact, fma), q = RN(q0 + rem inv).
-  // Bit-identical to the IEEE quotient for every r in [0, n) at n <= 2^28 and a
-  // 2^28-point sweep at n = 3e9 (tools/div_check.cu), up to the sign of a zero at r = 0.
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
-  const rt nn = (rt)n;
-  auto score = [&](int64_t t, double bound) -> double {
-    rt r = (rt)(idx + b * t);  // cand = (index + b*t) mod n, already < n
-    double sc = 0.0;
-    for (int j = 0; j < c; ++j) {
-      const double x = __dmul_rn(-kTwoPi, (double)r);
-      const double q0 = __dmul_rn(x, inv);
-      // (r = 0 gives +0.0 here where x / n is -0.0; est - tgt differs only in the sign
-      // of a zero, which the + pi inside wrap_phase erases — the score is bit-identical)
-      const double tgt = __fma_rn(__fma_rn(-q0, dn, x), inv, q0);
-      const double wv = wrap_phase(__dsub_rn(s_est[j], tgt));
-      sc = __dadd_rn(sc, __dmul_rn(wv, wv));
-      if (sc > bound) return sc;
-      r <<= 1;
-      if (r >= nn) r -= nn;
-    }
-    return sc;
-  };
   double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   int32_t bt = INT32_MAX;
   if (t0 < L) {
-    // pruning bound: the full score of the candidate nearest the stride-0 estimate
-    const double fe = (-s_est[0] * dn) / kTwoPi;
-    double dd = (fe - (double)idx) / (double)b;
-    int64_t th = (int64_t)floor(dd + 0.5);
-    th %= L;
-    if (th < 0) th += L;
-    double bound = score(th, __longlong_as_double(0x7ff0000000000000LL));
-    if (!(bound == bound)) bound = __longlong_as_double(0x7ff0000000000000LL);  // NaN: no pruning
+    double bound = search_bound<k32>(n, b, L, idx, s_est, c, inv);
     const int64_t t1 = min(L, t0 + (int64_t)kChunk);
     for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads) {
-      const double sc = score(t, bound);
+      const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
       if (sc > bound) continue;  // pruned / worse than a candidate that is scored in full
       if (sc < best) {
         best = sc;
@@ -200,6 +213,56 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
     }
     part_score[(int64_t)a * chunks + chunk] = b0;
     part_t[(int64_t)a * chunks + chunk] = t0w;
+  }
+}
+
+// Short candidate lists (L = n / b <= kWarpSearchMaxL, DSFFT's deep layers): one warp
+// per node, same scores, same bound, same (min score, smallest t) result as the CTA
+// kernel's single chunk — a 256-thread CTA per node left most threads idle there.
+constexpr int kWarpSearchMaxL = 1024;
+constexpr int kWarpSearchWarps = 8;
+template <bool k32>
+__global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kernel(
+    int64_t n, int c, int A, const int64_t* __restrict__ act_index,
+    const int64_t* __restrict__ act_b, const double* __restrict__ est,
+    double* __restrict__ part_score, int32_t* __restrict__ part_t) {
+  __shared__ double s_est_all[kWarpSearchWarps][kMaxStrides];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = blockIdx.x * kWarpSearchWarps + wl;
+  if (a >= A) return;  // whole warps only
+  double* s_est = s_est_all[wl];
+  for (int j = lane; j < c; j += 32) s_est[j] = est[(int64_t)a * c + j];
+  __syncwarp();
+  const int64_t b = act_b[a];
+  const int64_t L = n / b;
+  const int64_t idx = act_index[a];
+  const double dn = (double)n;
+  const double inv = 1.0 / dn;
+  using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
+  double best = __longlong_as_double(0x7ff0000000000000LL);
+  int32_t bt = INT32_MAX;
+  double bound = search_bound<k32>(n, b, L, idx, s_est, c, inv);
+  for (int64_t t = lane; t < L; t += 32) {
+    const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
+    if (sc > bound) continue;
+    if (sc < best) {
+      best = sc;
+      bt = (int32_t)t;
+    }
+    if (sc < bound) bound = sc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ob < best || (ob == best && ot < bt)) {
+      best = ob;
+      bt = ot;
+    }
+  }
+  if (lane == 0) {
+    part_score[a] = best;
+    part_t[a] = bt;
   }
 }
 
@@ -692,6 +755,7 @@ struct NoisyWs {
   size_t est, act_row, act_index, act_b, part_s, part_t, f0, val, res, dirty, done, counters,
       total;
   int chunks;
+  int64_t Lmax;  // largest candidate count n / b over the cycles
 };
 
 static NoisyWs noisy_ws(const NoisyPlan& P, int64_t rows) {
@@ -699,6 +763,7 @@ static NoisyWs noisy_ws(const NoisyPlan& P, int64_t rows) {
   int64_t bmin = P.b[0];
   for (int k = 1; k < P.ncycles; ++k) bmin = std::min(bmin, P.b[k]);
   const int64_t Lmax = P.n / bmin;
+  w.Lmax = Lmax;
   w.chunks = (int)((Lmax + kChunk - 1) / kChunk);
   size_t o = 0;
   w.est = o;       o = al256(o + (size_t)rows * P.c * 8);
@@ -795,6 +860,12 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   if (world > 1)
     part_fill_kernel<<<(unsigned)((nparts + 255) / 256), 256, 0, st>>>(nparts, part_s, part_t);
   const int mine = (w.chunks - rank + world - 1) / world;
+  if (world == 1 && w.Lmax <= kWarpSearchMaxL) {  // one chunk: part slot a = node a
+    auto kfn = P.n < (int64_t(1) << 31) ? noisy_search_warp_kernel<true>
+                                        : noisy_search_warp_kernel<false>;
+    kfn<<<(unsigned)((A + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
+          st>>>(P.n, P.c, A, act_index, act_b, est, part_s, part_t);
+  } else
   for (int a0 = 0; a0 < A && mine > 0; a0 += 65535) {
     const int cnt = std::min(65535, A - a0);
     dim3 grid((unsigned)mine, (unsigned)cnt);
