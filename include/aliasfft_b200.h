@@ -329,11 +329,11 @@ int afft_bucketize_rows(const void* x, int dtype, int64_t n, int64_t b,
 
 /*
  * The same rows from the signal's resident spectrum Y = fft(x)/n (complex128 [n],
- * e.g. afft_bucketize with b = n, tau = 0), for small n/b <= 32, by the alias identity
+ * e.g. afft_bucketize with b = n, tau = 0), by the alias identity
  *   bucketize(x, b, tau)[i] = w_n^(i tau) * sum_{l < n/b} Y[i + l b] * w_(n/b)^(l tau)
- * (equal to afft_bucketize_rows up to rounding).  energy [b] and values0 [b] (the
- * tau = 0 values of every bucket) may be NULL.  Replaces dsfft.py:88-95, 159-160 at
- * the deepest layers.
+ * (equal to afft_bucketize_rows up to rounding).  Rows need n/b <= 256; energy [b]
+ * and values0 [b] (the tau = 0 values of every bucket, may be NULL) need n/b <= 32
+ * (AFFT_EUNSUPPORTED otherwise).  Replaces dsfft.py:88-95, 159-160 at the deep layers.
  */
 int afft_alias_rows(const double* spectrum, int64_t n, int64_t b, const int64_t* shifts /* host */,
                     int32_t nshift, const int64_t* bucket_idx, int64_t nrows, double* rows,

@@ -210,29 +210,33 @@ __device__ __forceinline__ cd root_pi(int64_t m, int64_t q) {  // exp(-2 pi i m 
 }
 
 // rows[r][t] for selected buckets: one warp per row, lanes over the L spectrum
-// terms (load) and then over the shifts (sum).
+// terms (load) and then over the shifts (sum).  L <= kAliasRowsMaxL; dynamic shared
+// memory holds the L roots and each warp's L spectrum terms.
+constexpr int kAliasRowsMaxL = 256;
+
 __global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_kernel(
     const cd* __restrict__ Y, int64_t n, int64_t b, int L, const __grid_constant__ AliasShifts sh,
     const int64_t* __restrict__ idx, int64_t nrows, cd* __restrict__ rows) {
-  __shared__ cd rootL[kAliasMaxL];
-  __shared__ cd ys[kAliasWarps][kAliasMaxL];
+  extern __shared__ cd alias_smem[];
+  cd* rootL = alias_smem;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x < L) rootL[threadIdx.x] = root_pi(threadIdx.x, L);
+  cd* ys = alias_smem + L + w * L;
+  for (int j = threadIdx.x; j < L; j += blockDim.x) rootL[j] = root_pi(j, L);
   __syncthreads();
   const int64_t r = (int64_t)blockIdx.x * kAliasWarps + w;
   if (r >= nrows) return;
   const int64_t i = idx[r];
-  if (lane < L) ys[w][lane] = Y[i + (int64_t)lane * b];
+  for (int l = lane; l < L; l += 32) ys[l] = Y[i + (int64_t)l * b];
   __syncwarp();
   for (int t = lane; t < sh.nshift; t += 32) {
     const int64_t tau = sh.tau[t];
     const int rl = (int)(tau % L);
-    cd acc = ys[w][0];
+    cd acc = ys[0];
     int m = 0;
     for (int l = 1; l < L; ++l) {
       m += rl;
       if (m >= L) m -= L;
-      acc = cadd(acc, cmul(ys[w][l], rootL[m]));
+      acc = cadd(acc, cmul(ys[l], rootL[m]));
     }
     rows[r * sh.nshift + t] = cmul(acc, root_pi(mulmod(i, tau, n), n));
   }
@@ -398,8 +402,9 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
     return AFFT_EINVAL;
   }
   const int64_t L = n / b;
-  if (L > kAliasMaxL) {
-    set_error("afft_alias_rows: n/b = %lld above %d", (long long)L, kAliasMaxL);
+  if (L > kAliasRowsMaxL || ((energy || values0) && L > kAliasMaxL)) {
+    set_error("afft_alias_rows: n/b = %lld above %d (rows) / %d (energies, values)",
+              (long long)L, kAliasRowsMaxL, kAliasMaxL);
     return AFFT_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -408,8 +413,10 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
     AliasShifts sh;
     sh.nshift = nshift;
     for (int t = 0; t < nshift; ++t) sh.tau[t] = host_pymod(shifts[t], n);
-    alias_rows_kernel<<<(unsigned)((nrows + kAliasWarps - 1) / kAliasWarps), kAliasWarps * 32, 0,
-                        st>>>(Y, n, b, (int)L, sh, bucket_idx, nrows, reinterpret_cast<cd*>(rows));
+    const size_t smem = (size_t)(1 + kAliasWarps) * L * sizeof(cd);
+    alias_rows_kernel<<<(unsigned)((nrows + kAliasWarps - 1) / kAliasWarps), kAliasWarps * 32,
+                        smem, st>>>(Y, n, b, (int)L, sh, bucket_idx, nrows,
+                                    reinterpret_cast<cd*>(rows));
   }
   if (energy || values0) {
     AliasCosets cs;

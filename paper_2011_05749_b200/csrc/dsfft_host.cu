@@ -24,7 +24,10 @@
 // Host inputs that must come from numpy's PCG64 (the search-plan anchors and the
 // DT3 random shifts for every possible stop depth) are drawn by the Python caller.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -54,21 +57,19 @@ __global__ void dsfft_unquiet_kernel(const int64_t* __restrict__ act, int64_t m,
   if (i < m) quiet[act[i]] = 0;
 }
 
-// max of v[0..n) (all >= 0) into *out, one CTA.
+// max of v[0..n) (all >= 0) into *out (zeroed by the caller): fmax per thread and
+// warp, then an integer atomicMax on the bit pattern (non-negative doubles order
+// like their bits).  NaNs are ignored, as fmax does.
 __global__ void __launch_bounds__(1024) dsfft_max_kernel(const double* __restrict__ v, int64_t n,
                                                          double* __restrict__ out) {
-  __shared__ double part[32];
   double m = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, v[i]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, v[i]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, part[w]);
-    *out = r;
-  }
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(m));
 }
 
 // sum |Y|^2 for the floor bound (order irrelevant: a bound with a wide margin)
@@ -116,12 +117,84 @@ struct DBuf {
   }
 };
 
+// AFFT_DSFFT_PROFILE=1: host time spent waiting in read-backs vs issuing work
+struct HostProf {
+  bool on = std::getenv("AFFT_DSFFT_PROFILE") != nullptr;
+  double wait_s = 0.0;
+  int syncs = 0;
+};
+thread_local HostProf g_prof;
+
+struct Marks {
+  double last = 0.0, last_wait = 0.0;
+  struct Acc {
+    const char* what;
+    double total, wait;
+    int n;
+  };
+  std::vector<Acc> acc;
+  void mark(const char* what, double t, double wait) {
+    Acc* a = nullptr;
+    for (auto& x : acc)
+      if (x.what == what) a = &x;
+    if (!a) {
+      acc.push_back({what, 0.0, 0.0, 0});
+      a = &acc.back();
+    }
+    a->total += t - last;
+    a->wait += wait - last_wait;
+    ++a->n;
+    last = t;
+    last_wait = wait;
+  }
+};
+thread_local Marks g_marks;
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#define PMARK(what)                                  \
+  do {                                               \
+    if (g_prof.on) g_marks.mark(what, now_s(), g_prof.wait_s); \
+  } while (0)
+
+// Per-thread pinned staging for read-backs (a pageable D2H copy costs a bounce).
+struct PinnedStage {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~PinnedStage() {
+    if (p) cudaFreeHost(p);
+  }
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      size_t c = 4096;
+      while (c < bytes) c <<= 1;
+      if (cudaMallocHost(&p, c) != cudaSuccess) return nullptr;
+      cap = c;
+    }
+    return p;
+  }
+};
+thread_local PinnedStage g_stage;
+
 template <class T>
 int d2h(std::vector<T>& h, const void* d, size_t count, cudaStream_t st) {
   h.resize(count);
   if (!count) return AFFT_OK;
-  cudaError_t e = cudaMemcpyAsync(h.data(), d, count * sizeof(T), cudaMemcpyDeviceToHost, st);
+  const double t0 = g_prof.on ? now_s() : 0.0;
+  const size_t bytes = count * sizeof(T);
+  void* stage = g_stage.get(bytes);
+  cudaError_t e = cudaMemcpyAsync(stage ? stage : (void*)h.data(), d, bytes,
+                                  cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && stage) std::memcpy(h.data(), stage, bytes);
+  if (g_prof.on) {
+    g_prof.wait_s += now_s() - t0;
+    ++g_prof.syncs;
+  }
   return e == cudaSuccess ? AFFT_OK : cuda_status(e, "dsfft read-back");
 }
 
@@ -152,24 +225,52 @@ void swap_layers(Layer& a, Layer& b) {
 }
 
 // Python dict insertion semantics for the entries: a new key appends, a repeated
-// key keeps its position and takes the new value.
+// key keeps its position and takes the new value.  Open addressing over int64 keys
+// (frequencies, >= 0), table reused across layers: clear() resets only the slots in use.
 struct Entries {
   std::vector<int64_t> f;
   std::vector<cd> v;
-  std::unordered_map<int64_t, size_t> at;
+  std::vector<int64_t> slot_key;  // -1 = empty
+  std::vector<int32_t> slot_pos;
+  size_t mask = 0;
+  std::vector<size_t> used;  // occupied slots (a probe chain must not be cut while clearing)
   void clear() {
+    for (size_t h : used) slot_key[h] = -1;
+    used.clear();
     f.clear();
     v.clear();
-    at.clear();
   }
-  void put(int64_t key, cd val) {
-    auto it = at.find(key);
-    if (it == at.end()) {
-      at.emplace(key, f.size());
+  size_t find(int64_t key) const {  // the key's slot, or the empty slot where it belongs
+    size_t h = (size_t)((uint64_t)key * 0x9E3779B97F4A7C15ull >> 20) & mask;
+    while (slot_key[h] != -1 && slot_key[h] != key) h = (h + 1) & mask;
+    return h;
+  }
+  void grow(size_t need) {
+    if (!slot_key.empty() && 2 * need <= slot_key.size()) return;
+    size_t cap = 1024;
+    while (cap < 2 * need) cap <<= 1;
+    slot_key.assign(cap, -1);
+    slot_pos.assign(cap, 0);
+    mask = cap - 1;
+    used.clear();
+    for (size_t i = 0; i < f.size(); ++i) {
+      const size_t h = find(f[i]);
+      slot_key[h] = f[i];
+      slot_pos[h] = (int32_t)i;
+      used.push_back(h);
+    }
+  }
+  void reserve(size_t extra) { grow(f.size() + extra); }
+  void put(int64_t key, cd val) {  // callers reserve() first
+    const size_t h = find(key);
+    if (slot_key[h] == -1) {
+      slot_key[h] = key;
+      slot_pos[h] = (int32_t)f.size();
+      used.push_back(h);
       f.push_back(key);
       v.push_back(val);
     } else {
-      v[it->second] = val;
+      v[slot_pos[h]] = val;
     }
   }
 };
@@ -202,9 +303,44 @@ struct Dsfft {
   DBuf Y;             // resident spectrum fft(x)/n (lazy)
   double normY = -1;  // ||Y||^2 (lazy)
 
-  static constexpr int64_t kAliasMaxL = 32;
+  static constexpr int64_t kAliasMaxL = 32;       // rows + energies + values from Y
+  static constexpr int64_t kAliasRowsMaxL = 256;  // rows alone from Y
 
   bool alias_ok(int64_t b) const { return n / b <= kAliasMaxL; }
+
+  // Rows from the resident spectrum instead of min(#shifts, L) size-b DFTs over the
+  // signal: worth it once Y exists (A*L*R products against ~min(R, L)*b*log b), and
+  // worth computing Y for at L <= 64, where one layer's DFTs cost a full transform.
+  bool alias_rows_ok(int64_t b) const {
+    const int64_t L = n / b;
+    return L <= kAliasMaxL || (L <= kAliasRowsMaxL && (Y.p || L <= 64));
+  }
+
+  // ||Y||^2 for the noisy floor bound: from Y when resident, else by Parseval from x
+  // (sum |x|^2 / n); only ever compared against a bound with a wide margin.
+  int norm_y() {
+    if (normY >= 0) return AFFT_OK;
+    if (Y.p) {
+      DBuf s;
+      RC(s.alloc(8, st, "dsfft norm"));
+      CK(cudaMemsetAsync(s.p, 0, 8, st));
+      dsfft_norm2_kernel<<<148 * 4, 1024, 0, st>>>(Y.as<cd>(), n, s.as<double>());
+      std::vector<double> h;
+      RC(d2h(h, s.p, 1, st));
+      normY = h[0];
+      return AFFT_OK;
+    }
+    const int nparts = afft_sumsq_parts(n, dtype);
+    DBuf parts;
+    RC(parts.alloc((size_t)std::max(nparts, 1) * 8, st, "dsfft partials"));
+    RC(afft_sumsq(x, dtype, n, 1, n, parts.as<double>(), st));
+    std::vector<double> h;
+    RC(d2h(h, parts.p, (size_t)nparts, st));
+    double sum = 0.0;
+    for (double v : h) sum += v;
+    normY = sum / (double)n;
+    return AFFT_OK;
+  }
 
   int spectrum() {
     if (Y.p) return AFFT_OK;
@@ -226,6 +362,7 @@ struct Dsfft {
   }
 
   int active(const DBuf& vals, int64_t count, double thr, const int64_t* map, Layer& out) {
+    PMARK("layer values");
     RC(out.active.alloc((size_t)std::max<int64_t>(count, 1) * 8, st, "dsfft active"));
     DBuf cnt;
     RC(cnt.alloc(4, st, "dsfft count"));
@@ -234,6 +371,7 @@ struct Dsfft {
     std::vector<int32_t> h;
     RC(d2h(h, cnt.p, 1, st));
     out.m = h[0];
+    PMARK("active set");
     return AFFT_OK;
   }
 
@@ -287,7 +425,7 @@ struct Dsfft {
            DBuf& out, double* energy) {
     const int ns = (int)shifts.size();
     RC(out.alloc((size_t)std::max<int64_t>(count, 1) * ns * 16, st, "dsfft rows"));
-    if (alias_ok(b)) {
+    if (alias_ok(b) || (!energy && alias_rows_ok(b))) {
       RC(spectrum());
       return afft_alias_rows(Y.as<double>(), n, b, shifts.data(), ns, count ? idx : nullptr, count,
                              out.as<double>(), energy, nullptr, st);
@@ -296,21 +434,46 @@ struct Dsfft {
                                out.as<double>(), energy, st);
   }
 
+  // One device block per classification, read back in one copy:
+  // f0 [A] int64 | value [A] c128 | bucket [A] int64 | state [A] int8.
+  struct Pack {
+    DBuf buf;
+    int64_t A = 0;
+    size_t of = 0, ov = 0, oa = 0, os = 0, bytes = 0;
+    int64_t* f0() const { return reinterpret_cast<int64_t*>(buf.as<char>() + of); }
+    double* val() const { return reinterpret_cast<double*>(buf.as<char>() + ov); }
+    int8_t* state() const { return reinterpret_cast<int8_t*>(buf.as<char>() + os); }
+  };
+
+  int make_pack(const Layer& L, Pack& pk) {
+    const int64_t A = L.m;
+    pk.A = A;
+    if (!A) return AFFT_OK;
+    pk.of = 0;
+    pk.ov = (size_t)A * 8;
+    pk.oa = pk.ov + (size_t)A * 16;
+    pk.os = pk.oa + (size_t)A * 8;
+    pk.bytes = pk.os + (size_t)A;
+    RC(pk.buf.alloc(pk.bytes, st, "dsfft result pack"));
+    char* p = pk.buf.as<char>();
+    CK(cudaMemcpyAsync(p + pk.oa, L.active.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(p + pk.of, 0xff, (size_t)A * 8, st));  // f0 = -1
+    CK(cudaMemsetAsync(p + pk.ov, 0, (size_t)A * 16, st));
+    return AFFT_OK;
+  }
+
   // _classify_active: entries (ascending bucket order) and multiton buckets
   int classify(const Layer& L, Entries& E, std::vector<int64_t>& multi) {
     E.clear();
     multi.clear();
     const int64_t b = 1LL << L.depth;
     const int64_t A = L.m;
-    DBuf st8, f0, val, rowsb;
-    if (A) {
-      RC(st8.alloc((size_t)A, st, "dsfft states"));
-      RC(f0.alloc((size_t)A * 8, st, "dsfft f0"));
-      RC(val.alloc((size_t)A * 16, st, "dsfft values"));
-    }
+    Pack pk;
+    DBuf rowsb;
+    RC(make_pack(L, pk));
     if (P.mode == 0) {
       tr.add(5, L.depth, 3, 0);  // ledger: shifts 0, 1, 2
-      if (A == 0) return finish_classify(L, E, multi, st8, f0, val);
+      if (A == 0) return finish_classify(L, E, multi, pk);
       const std::vector<int64_t> shifts = {0, 1, 2};
       RC(rows(b, shifts, L.active.as<int64_t>(), A, rowsb, nullptr));
       // exact_thresholds (peeling.py:316-318)
@@ -322,11 +485,9 @@ struct Dsfft {
       RC(afft_exact_thresholds(parts.as<double>(), nparts, n, 1, eps.as<double>(), st));
       std::vector<double> he;
       RC(d2h(he, eps.p, 1, st));
-      CK(cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st));  // -1
-      CK(cudaMemsetAsync(val.p, 0, (size_t)A * 16, st));
       RC(afft_classify_exact(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, he[0], he[0],
-                             st8.as<int8_t>(), f0.as<int64_t>(), val.as<double>(), st));
-      return finish_classify(L, E, multi, st8, f0, val);
+                             pk.state(), pk.f0(), pk.val(), st));
+      return finish_classify(L, E, multi, pk);
     }
     // noisy: the search plan of dsfft.py:142-150 (anchors drawn by the caller)
     std::vector<int64_t> shifts;
@@ -336,29 +497,27 @@ struct Dsfft {
     tr.add(5, L.depth, R, 1);  // ledger: the plan shifts
     const double base = noise_std / std::sqrt((double)b) * std::sqrt((double)R);
     bool skip = false;
-    if (noise_std > 0.0 && alias_ok(b)) {
-      if (normY < 0) {
-        RC(spectrum());
-        DBuf s;
-        RC(s.alloc(8, st, "dsfft norm"));
-        CK(cudaMemsetAsync(s.p, 0, 8, st));
-        dsfft_norm2_kernel<<<148 * 4, 1024, 0, st>>>(Y.as<cd>(), n, s.as<double>());
-        std::vector<double> h;
-        RC(d2h(h, s.p, 1, st));
-        normY = h[0];
-      }
-      skip = 1e-8 * std::sqrt((double)R * (double)(n / b) * normY) < 1.5 * base;
+    if (noise_std > 0.0) {
+      // floor = 1e-8 sqrt(max_i energy_i) <= 1e-8 sqrt(R L ||Y||^2) (Cauchy-Schwarz on
+      // the alias sums): when that bound is below 1.5 base the floor cannot matter and
+      // the all-bucket energy pass is skipped (1.0001: rounding of the norm itself)
+      RC(norm_y());
+      skip = 1e-8 * std::sqrt((double)R * (double)(n / b) * normY * 1.0001) < 1.5 * base;
     }
     DBuf energy;
     if (!skip) RC(energy.alloc((size_t)b * 8, st, "dsfft energies"));
+    PMARK("classify setup");
     RC(rows(b, shifts, L.active.as<int64_t>(), A, rowsb, skip ? nullptr : energy.as<double>()));
+    PMARK("classify rows");
     double t0 = 0.0, t1 = 0.0;
     if (noise_std > 0.0) {
       double floor = 0.0;
       if (!skip) {
         DBuf mx;
         RC(mx.alloc(8, st, "dsfft max"));
-        dsfft_max_kernel<<<1, 1024, 0, st>>>(energy.as<double>(), b, mx.as<double>());
+        CK(cudaMemsetAsync(mx.p, 0, 8, st));
+        const unsigned grid = (unsigned)std::min<int64_t>(148 * 2, (b + 1023) / 1024);
+        dsfft_max_kernel<<<grid, 1024, 0, st>>>(energy.as<double>(), b, mx.as<double>());
         std::vector<double> h;
         RC(d2h(h, mx.p, 1, st));
         floor = 1e-8 * std::sqrt(h[0]);
@@ -366,54 +525,47 @@ struct Dsfft {
       t0 = std::max(1.5 * base, floor);
       t1 = std::max(2.5 * base, floor);
     } else {
-      DBuf quiet, d0, d1;
+      DBuf quiet, d0;
       RC(quiet.alloc((size_t)b, st, "dsfft quiet mask"));
-      RC(d0.alloc(8, st, "dsfft t0"));
-      RC(d1.alloc(8, st, "dsfft t1"));
+      RC(d0.alloc(16, st, "dsfft t0 t1"));
       dsfft_quiet_kernel<<<148 * 4, 256, 0, st>>>(b, nullptr, 0, quiet.as<uint8_t>());
       if (A)
         dsfft_unquiet_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(
             L.active.as<int64_t>(), A, quiet.as<uint8_t>());
       RC(afft_robust_thresholds(energy.as<double>(), quiet.as<uint8_t>(), b, 1, R, d0.as<double>(),
-                                d1.as<double>(), st));
-      std::vector<double> h0, h1;
-      RC(d2h(h0, d0.p, 1, st));
-      RC(d2h(h1, d1.p, 1, st));
-      t0 = h0[0];
-      t1 = h1[0];
+                                d0.as<double>() + 1, st));
+      std::vector<double> h;
+      RC(d2h(h, d0.p, 2, st));
+      t0 = h[0];
+      t1 = h[1];
     }
-    if (A == 0) return finish_classify(L, E, multi, st8, f0, val);
-    CK(cudaMemsetAsync(f0.p, 0xff, (size_t)A * 8, st));
-    CK(cudaMemsetAsync(val.p, 0, (size_t)A * 16, st));
+    PMARK("classify thresholds");
+    if (A == 0) return finish_classify(L, E, multi, pk);
     DBuf rn, ws;
     RC(rn.alloc((size_t)A * 8, st, "dsfft resnorm"));
     const size_t need = afft_singleton_workspace_size(n, A, b, P.c, P.m);
     RC(ws.alloc(need, st, "dsfft search workspace"));
     RC(afft_classify_noisy(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, shifts.data(), R,
-                           P.c, P.m, P.weights, t0, t1, st8.as<int8_t>(), f0.as<int64_t>(),
-                           val.as<double>(), rn.as<double>(), ws.p, need, st));
-    return finish_classify(L, E, multi, st8, f0, val);
+                           P.c, P.m, P.weights, t0, t1, pk.state(), pk.f0(), pk.val(),
+                           rn.as<double>(), ws.p, need, st));
+    PMARK("classify noisy");
+    const int rcf = finish_classify(L, E, multi, pk);
+    PMARK("classify finish");
+    return rcf;
   }
 
-  int finish_classify(const Layer& L, Entries& E, std::vector<int64_t>& multi,
-                      const DBuf& st8, const DBuf& f0, const DBuf& val) {
-    const int64_t A = L.m;
+  int finish_classify(const Layer& L, Entries& E, std::vector<int64_t>& multi, const Pack& pk) {
+    const int64_t A = pk.A;
     if (A) {
-      // one read-back: pack f0 | value | bucket | state on the device first
-      DBuf pack;
-      const size_t of = 0, ov = (size_t)A * 8, oa = ov + (size_t)A * 16, os = oa + (size_t)A * 8;
-      RC(pack.alloc(os + (size_t)A, st, "dsfft result pack"));
-      char* pk = pack.as<char>();
-      CK(cudaMemcpyAsync(pk + of, f0.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(pk + ov, val.p, (size_t)A * 16, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(pk + oa, L.active.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(pk + os, st8.p, (size_t)A, cudaMemcpyDeviceToDevice, st));
       std::vector<char> h;
-      RC(d2h(h, pk, os + (size_t)A, st));
-      const int64_t* hf = reinterpret_cast<const int64_t*>(h.data() + of);
-      const cd* hv = reinterpret_cast<const cd*>(h.data() + ov);
-      const int64_t* ha = reinterpret_cast<const int64_t*>(h.data() + oa);
-      const int8_t* hs = reinterpret_cast<const int8_t*>(h.data() + os);
+      PMARK("classify pack");
+      RC(d2h(h, pk.buf.p, pk.bytes, st));
+      PMARK("classify read-back");
+      const int64_t* hf = reinterpret_cast<const int64_t*>(h.data() + pk.of);
+      const cd* hv = reinterpret_cast<const cd*>(h.data() + pk.ov);
+      const int64_t* ha = reinterpret_cast<const int64_t*>(h.data() + pk.oa);
+      const int8_t* hs = reinterpret_cast<const int8_t*>(h.data() + pk.os);
+      E.reserve((size_t)A);
       for (int64_t i = 0; i < A; ++i) {
         if (hs[i] == AFFT_SINGLE_TON) {  // ascending bucket order, as the reference inserts
           E.put(hf[i], hv[i]);
@@ -468,6 +620,7 @@ struct Dsfft {
     const int64_t* hp = reinterpret_cast<const int64_t*>(h.data());
     const cd* hv = reinterpret_cast<const cd*>(h.data() + ov);
     const int32_t* hc = reinterpret_cast<const int32_t*>(h.data() + oc);
+    E.reserve((size_t)nm * a_m);
     for (int64_t r = 0; r < nm; ++r)
       for (int j = 0; j < hc[r]; ++j) E.put(hp[r * a_m + j], hv[r * a_m + j]);  // .update()
     return AFFT_OK;
@@ -497,20 +650,27 @@ struct Dsfft {
     while ((1LL << depth) < k) ++depth;  // ceil(log2 k), k >= 1
     depth = std::min(depth, max_depth);
     Layer layer, next;
+    PMARK("start");
     RC(initial(depth, layer));
+    PMARK("initial");
     while ((double)layer.m < P.theta * k && layer.depth < max_depth) {
       RC(expand(layer, next));
       swap_layers(layer, next);
+      PMARK("expand");
     }
     std::vector<int64_t> multi;
     RC(classify(layer, E, multi));
     while (P.mode != 0 && !multi.empty() && layer.depth < max_depth) {
+      PMARK("loop");
       RC(expand(layer, next));
       swap_layers(layer, next);
+      PMARK("expand");
       RC(classify(layer, E, multi));
     }
     const int64_t remaining = (int64_t)k - (int64_t)E.f.size();
+    PMARK("loop");
     if (!multi.empty() && remaining > 0) RC(resolve(layer.depth, multi, remaining, E));
+    PMARK("resolve");
     return AFFT_OK;
   }
 };
@@ -534,7 +694,20 @@ extern "C" int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k,
   }
   Entries E;
   Dsfft D{x, dtype, n, k, *params, (cudaStream_t)stream, Tracer{trace, trace_capacity}};
+  g_prof.wait_s = 0.0;
+  g_prof.syncs = 0;
+  const double t0 = g_prof.on ? now_s() : 0.0;
+  g_marks.acc.clear();
+  g_marks.last = t0;
+  g_marks.last_wait = 0.0;
   const int rc = D.run(E);
+  if (g_prof.on)
+    std::fprintf(stderr, "afft_dsfft: %.3f ms total, %.3f ms waiting in %d read-backs\n",
+                 (now_s() - t0) * 1e3, g_prof.wait_s * 1e3, g_prof.syncs);
+  if (g_prof.on)
+    for (auto& a : g_marks.acc)
+      std::fprintf(stderr, "  %-22s x%-3d %.3f ms, host %.3f ms\n", a.what, a.n, a.total * 1e3,
+                   (a.total - a.wait) * 1e3);
   const std::vector<int64_t>& ef = E.f;
   const std::vector<cd>& ev = E.v;
   if (trace_len) *trace_len = D.tr.len;

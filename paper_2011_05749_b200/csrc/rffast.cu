@@ -281,6 +281,15 @@ __global__ void noisy_est_kernel(int A, int c, int m, const int64_t* __restrict_
 // Reduce the chunk partials, then the least-squares fit (peeling.py:247-250):
 // x = a^H y / a^H a with a_r = exp(-2j*pi*((tau_r*f0) mod n)/n), resnorm = ||a x - y||.
 // One warp per active node.
+__device__ __forceinline__ double node_norm(const cd* y, int R);
+
+// decide != null: also classify_noisy's decision for nodes searched unconditionally
+// (peeling.py:257-267): ZERO_TON if ||y|| <= t0, else SINGLE_TON iff resnorm <= t1.
+struct NoisyDecide {
+  int8_t* state;
+  double t0, t1;
+};
+
 __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restrict__ part_score,
                                       const int32_t* __restrict__ part_t,
                                       const int64_t* __restrict__ act_row,
@@ -289,7 +298,7 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
                                       const double* __restrict__ residual,
                                       const __grid_constant__ NoisyPlan P,
                                       int64_t* __restrict__ out_f0, double* __restrict__ out_val,
-                                      double* __restrict__ out_res) {
+                                      double* __restrict__ out_res, NoisyDecide decide) {
   const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (a >= A) return;
@@ -343,7 +352,12 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
   if (lane == 0) {
     out_f0[a] = f0;
     reinterpret_cast<cd*>(out_val)[a] = x;
-    out_res[a] = sqrt(rs);
+    const double resn = sqrt(rs);
+    out_res[a] = resn;
+    if (decide.state)
+      decide.state[a] = node_norm(y, P.R) <= decide.t0 ? AFFT_ZERO_TON
+                        : resn <= decide.t1            ? AFFT_SINGLE_TON
+                                                       : AFFT_MULTI_TON;
   }
 }
 
@@ -836,9 +850,17 @@ static int canonical_active(const NoisyPlan& P, const NoisyWs& w, char* ws, int 
 // (+inf, INT32_MAX), and the caller's exchange replaces every slot by its minimum over
 // the ranks (score and t independently: exactly one rank holds a real value per slot),
 // after which the reduction and fit are the single-rank ones — identical results.
+struct SearchOut {  // null members: the workspace slots
+  int64_t* f0 = nullptr;
+  double* val = nullptr;
+  double* res = nullptr;
+  NoisyDecide decide = {nullptr, 0.0, 0.0};
+};
+
 static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
                       const double* residual, cudaStream_t st,
-                      const AfftSearchShard* shard = nullptr, int64_t rows_total = 0) {
+                      const AfftSearchShard* shard = nullptr, int64_t rows_total = 0,
+                      const SearchOut& out = SearchOut()) {
   if (A == 0) return AFFT_OK;
   const int rank = shard && shard->world > 1 ? shard->rank : 0;
   const int world = shard && shard->world > 1 ? shard->world : 1;
@@ -889,8 +911,9 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   noisy_finalize_kernel<<<(unsigned)((A * 32 + 255) / 256), 256, 0, st>>>(
       A, w.chunks, reinterpret_cast<const double*>(ws + w.part_s),
       reinterpret_cast<const int32_t*>(ws + w.part_t), act_row, act_index, act_b, residual, P,
-      reinterpret_cast<int64_t*>(ws + w.f0), reinterpret_cast<double*>(ws + w.val),
-      reinterpret_cast<double*>(ws + w.res));
+      out.f0 ? out.f0 : reinterpret_cast<int64_t*>(ws + w.f0),
+      out.val ? out.val : reinterpret_cast<double*>(ws + w.val),
+      out.res ? out.res : reinterpret_cast<double*>(ws + w.res), out.decide);
   AFFT_CHECK_LAUNCH("noisy_finalize_kernel");
   return AFFT_OK;
 }
@@ -975,14 +998,12 @@ __global__ void search_list_kernel(int64_t count, int64_t b, const int64_t* __re
     bs[i] = b;
   }
 }
-}  // namespace afft
 
-extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t* index,
-                                           int64_t count, int64_t b, int64_t n,
-                                           const int64_t* shifts, int32_t nshift, int32_t c,
-                                           int32_t m, const double* weights, int64_t* f0,
-                                           double* val, double* resnorm, void* workspace,
-                                           size_t workspace_bytes, void* stream) {
+static int singleton_search(const double* residual, const int64_t* index, int64_t count,
+                            int64_t b, int64_t n, const int64_t* shifts, int32_t nshift, int32_t c,
+                            int32_t m, const double* weights, int64_t* f0, double* val,
+                            double* resnorm, void* workspace, size_t workspace_bytes,
+                            cudaStream_t st, NoisyDecide decide) {
   if (count == 0) return AFFT_OK;
   if (!residual || !index || !f0 || !val || !resnorm || !shifts || !weights || b < 1 ||
       n % b) {
@@ -1000,21 +1021,33 @@ extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t
     set_error("afft_singleton_search_noisy: workspace of %zu bytes needed", w.total);
     return AFFT_ENOMEM;
   }
-  cudaStream_t st = (cudaStream_t)stream;
   char* ws = reinterpret_cast<char*>(workspace);
   // active list = the given nodes, rows 0..count-1 of `residual` (filled on the device:
   // no host staging, no synchronisation)
   search_list_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(
       count, b, index, reinterpret_cast<int64_t*>(ws + w.act_row),
       reinterpret_cast<int64_t*>(ws + w.act_index), reinterpret_cast<int64_t*>(ws + w.act_b));
-  rc = run_search(*P, w, ws, (int)count, residual, st);
-  if (!rc) {
-    cudaMemcpyAsync(f0, ws + w.f0, count * 8, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(val, ws + w.val, count * 16, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(resnorm, ws + w.res, count * 8, cudaMemcpyDeviceToDevice, st);
-    AFFT_CHECK_LAUNCH("singleton_search_noisy");
-  }
+  SearchOut out;  // the fit writes straight into the caller's arrays
+  out.f0 = f0;
+  out.val = val;
+  out.res = resnorm;
+  out.decide = decide;
+  rc = run_search(*P, w, ws, (int)count, residual, st, nullptr, 0, out);
+  if (!rc) AFFT_CHECK_LAUNCH("singleton_search_noisy");
   return rc;
+}
+
+}  // namespace afft
+
+extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t* index,
+                                           int64_t count, int64_t b, int64_t n,
+                                           const int64_t* shifts, int32_t nshift, int32_t c,
+                                           int32_t m, const double* weights, int64_t* f0,
+                                           double* val, double* resnorm, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  return singleton_search(residual, index, count, b, n, shifts, nshift, c, m, weights, f0, val,
+                          resnorm, workspace, workspace_bytes, (cudaStream_t)stream,
+                          NoisyDecide{nullptr, 0.0, 0.0});
 }
 
 extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors, int32_t ncycles,
@@ -1140,20 +1173,6 @@ extern "C" int afft_peel_noisy_sharded(
   return AFFT_OK;
 }
 
-namespace afft {
-// classify_noisy's decision for nodes searched unconditionally (per-node API):
-// ZERO_TON if ||residual|| <= t0, else SINGLE_TON iff resnorm <= t1.
-__global__ void noisy_decide_kernel(int64_t count, int R, const double* __restrict__ residual,
-                                    double t0, double t1, const double* __restrict__ res,
-                                    int8_t* __restrict__ state) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  if (node_norm(reinterpret_cast<const cd*>(residual) + i * R, R) <= t0)
-    state[i] = AFFT_ZERO_TON;
-  else
-    state[i] = res[i] <= t1 ? AFFT_SINGLE_TON : AFFT_MULTI_TON;
-}
-}  // namespace afft
 
 extern "C" int afft_classify_noisy(const double* residual, const int64_t* index, int64_t count,
                                    int64_t b, int64_t n, const int64_t* shifts, int32_t nshift,
@@ -1166,14 +1185,10 @@ extern "C" int afft_classify_noisy(const double* residual, const int64_t* index,
     set_error("afft_classify_noisy: bad arguments");
     return AFFT_EINVAL;
   }
-  int rc = afft_singleton_search_noisy(residual, index, count, b, n, shifts, nshift, c, m,
-                                       weights, f0, val, resnorm, workspace, workspace_bytes,
-                                       stream);
-  if (rc) return rc;
-  noisy_decide_kernel<<<(unsigned)((count + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-      count, nshift, residual, t0, t1, resnorm, state);
-  AFFT_CHECK_LAUNCH("noisy_decide_kernel");
-  return AFFT_OK;
+  // search + fit + the decision of peeling.py:257-267, all in the finalize kernel
+  return singleton_search(residual, index, count, b, n, shifts, nshift, c, m, weights, f0, val,
+                          resnorm, workspace, workspace_bytes, (cudaStream_t)stream,
+                          NoisyDecide{state, t0, t1});
 }
 
 namespace afft {

@@ -14,6 +14,7 @@ ledger, and keeps the reference's layer-level API (initial_layer / expand_layer)
 from __future__ import annotations
 
 import ctypes
+import functools
 import warnings
 from dataclasses import dataclass, field
 
@@ -126,8 +127,10 @@ def _expand(xd, prev: _DevLayer, thr, ledger) -> _DevLayer:
     return _DevLayer(depth, _active(vals, thr), vals)
 
 
+@functools.lru_cache(maxsize=256)
 def _search_plan(n: int, seed: int) -> SearchPlan:
-    """The noisy plan of _classify_active (dsfft.py:142-150)."""
+    """The noisy plan of _classify_active (dsfft.py:142-150).  Deterministic in
+    (n, seed), so cached: a batch decoded with one seed draws it once."""
     c = int(np.ceil(np.log2(n)))
     m = max(2, int(np.ceil(np.log2(n) ** (1.0 / 3.0))))
     rng = np.random.default_rng(seed)
@@ -137,7 +140,14 @@ def _search_plan(n: int, seed: int) -> SearchPlan:
 
 def _dt3_shift_table(n: int, config: DsfftConfig):
     """The DT3 fallback's random shifts (dsfft.py:207-212) for every possible stop depth d:
-    p = max(12, ceil(a_m log10 max(n/2^d, 10))) draws of default_rng(seed).choice."""
+    p = max(12, ceil(a_m log10 max(n/2^d, 10))) draws of default_rng(seed).choice.
+    Cached on (n, a_m, seed); the arrays are read-only."""
+    return _dt3_shift_table_cached(n, int(config.a_m), int(config.seed))
+
+
+@functools.lru_cache(maxsize=256)
+def _dt3_shift_table_cached(n: int, a_m: int, seed: int):
+    config = DsfftConfig(a_m=a_m, seed=seed)
     max_depth = n.bit_length() - 1
     offs, flat = [0], []
     for d in range(max_depth + 1):
@@ -151,7 +161,10 @@ def _dt3_shift_table(n: int, config: DsfftConfig):
         except ValueError:  # not reachable as a stop depth (too few samples)
             pass
         offs.append(len(flat))
-    return np.asarray(flat, dtype=np.int64), np.asarray(offs, dtype=np.int32)
+    flat, offs = np.asarray(flat, dtype=np.int64), np.asarray(offs, dtype=np.int32)
+    flat.setflags(write=False)
+    offs.setflags(write=False)
+    return flat, offs
 
 
 def _replay(trace_rec, n, config, plan, dt_table, ledger, trace):
