@@ -35,7 +35,7 @@ namespace afft {
 constexpr int kMaxStrides = 40;
 constexpr int kMaxRounds = 16;  // rounds per stride (m)
 constexpr int kSearchThreads = 256;
-constexpr int kCandPerThread = 16;
+constexpr int kCandPerThread = 64;  // 16 -> 64: fewer first candidates scored against the seed bound
 constexpr int kChunk = kSearchThreads * kCandPerThread;
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
@@ -151,13 +151,31 @@ __device__ __forceinline__ double search_bound(int64_t n, int64_t b, int64_t L, 
   return bound;
 }
 
+// Per-node pruning bound shared by every CTA scanning the node: the bit pattern of
+// the lowest full score seen so far (scores are >= +0, so they order like their bits;
+// the all-ones pattern, a negative NaN, is the "+inf" the est kernel initialises).
+// A candidate is dropped only once its partial sum exceeds a score some candidate
+// actually has, so the minimum and every tie with it are still scored in full: the
+// (min score, smallest t) result is the same whatever order CTAs run in.  A multiton
+// node's minimum sits far below the typical score (~27 strides x pi^2/3), and one
+// thread's own best of 16 candidates left it ~2.5x as many strides per candidate.
+__device__ __forceinline__ double shared_bound(const unsigned long long* g) {
+  const unsigned long long v = *reinterpret_cast<const volatile unsigned long long*>(g);
+  return v >= 0x7ff0000000000000ull ? __longlong_as_double(0x7ff0000000000000LL)
+                                    : __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ void lower_bound_to(unsigned long long* g, double sc) {
+  atomicMin(g, (unsigned long long)__double_as_longlong(sc));
+}
+
 // One CTA scores kChunk consecutive candidates t of one active node.
 // Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
 template <bool k32>
-__global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
+__global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
     int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
     const double* __restrict__ est, int chunks, double* __restrict__ part_score,
-    int32_t* __restrict__ part_t, int chunk_rank, int chunk_world) {
+    int32_t* __restrict__ part_t, int chunk_rank, int chunk_world,
+    unsigned long long* __restrict__ node_bound) {
   __shared__ double s_est[kMaxStrides];
   __shared__ double w_score[kSearchThreads / 32];
   __shared__ int32_t w_t[kSearchThreads / 32];
@@ -175,16 +193,22 @@ __global__ void __launch_bounds__(kSearchThreads) noisy_search_kernel(
   double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
   int32_t bt = INT32_MAX;
   if (t0 < L) {
+    unsigned long long* gb = node_bound + a;
     double bound = search_bound<k32>(n, b, L, idx, s_est, c, inv);
+    if (threadIdx.x == 0) lower_bound_to(gb, bound);
     const int64_t t1 = min(L, t0 + (int64_t)kChunk);
     for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads) {
+      bound = fmin(bound, shared_bound(gb));
       const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
       if (sc > bound) continue;  // pruned / worse than a candidate that is scored in full
       if (sc < best) {
         best = sc;
         bt = (int32_t)t;
       }
-      if (sc < bound) bound = sc;
+      if (sc < bound) {
+        bound = sc;
+        lower_bound_to(gb, sc);
+      }
     }
   }
   // block argmin, ties -> smaller t
@@ -242,14 +266,21 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
   double best = __longlong_as_double(0x7ff0000000000000LL);
   int32_t bt = INT32_MAX;
   double bound = search_bound<k32>(n, b, L, idx, s_est, c, inv);
-  for (int64_t t = lane; t < L; t += 32) {
-    const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
-    if (sc > bound) continue;
-    if (sc < best) {
-      best = sc;
-      bt = (int32_t)t;
+  // the warp shares its pruning bound after every 32 candidates (see shared_bound)
+  for (int64_t tb = 0; tb < L; tb += 32) {
+    const int64_t t = tb + lane;
+    if (t < L) {
+      const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
+      if (sc <= bound) {
+        if (sc < best) {
+          best = sc;
+          bt = (int32_t)t;
+        }
+        bound = sc;
+      }
     }
-    if (sc < bound) bound = sc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bound = fmin(bound, __shfl_xor_sync(0xffffffffu, bound, o));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -269,11 +300,13 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
 // Phase estimates of the active nodes (one thread per (node, stride)).
 __global__ void noisy_est_kernel(int A, int c, int m, const int64_t* __restrict__ act_row,
                                  const double* __restrict__ residual, int R,
-                                 const __grid_constant__ NoisyPlan P, double* __restrict__ est) {
+                                 const __grid_constant__ NoisyPlan P, double* __restrict__ est,
+                                 unsigned long long* __restrict__ node_bound) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)A * c) return;
   const int64_t a = e / c;
   const int j = (int)(e - a * c);
+  if (j == 0 && node_bound) node_bound[a] = ~0ull;  // "+inf" for the search kernel
   const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * R + (int64_t)j * m;
   est[e] = stride_estimate(y, m, P.w);
 }
@@ -767,7 +800,7 @@ static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct NoisyWs {
   size_t est, act_row, act_index, act_b, part_s, part_t, f0, val, res, dirty, done, counters,
-      total;
+      bound, total;
   int chunks;
   int64_t Lmax;  // largest candidate count n / b over the cycles
 };
@@ -792,6 +825,7 @@ static NoisyWs noisy_ws(const NoisyPlan& P, int64_t rows) {
   w.dirty = o;     o = al256(o + (size_t)rows);
   w.done = o;      o = al256(o + (size_t)rows * 4);
   w.counters = o;  o = al256(o + 64);
+  w.bound = o;     o = al256(o + (size_t)rows * 8);
   w.total = o;
   return w;
 }
@@ -873,8 +907,9 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   const int64_t* act_b = reinterpret_cast<const int64_t*>(ws + w.act_b);
   double* est = reinterpret_cast<double*>(ws + w.est);
   const int64_t ne = (int64_t)A * P.c;
+  unsigned long long* node_bound = reinterpret_cast<unsigned long long*>(ws + w.bound);
   noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(A, P.c, P.m, act_row, residual,
-                                                                P.R, P, est);
+                                                                P.R, P, est, node_bound);
   AFFT_CHECK_LAUNCH("noisy_est_kernel");
   double* part_s = reinterpret_cast<double*>(ws + w.part_s);
   int32_t* part_t = reinterpret_cast<int32_t*>(ws + w.part_t);
@@ -887,14 +922,17 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
                                         : noisy_search_warp_kernel<false>;
     kfn<<<(unsigned)((A + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
           st>>>(P.n, P.c, A, act_index, act_b, est, part_s, part_t);
-  } else
-  for (int a0 = 0; a0 < A && mine > 0; a0 += 65535) {
-    const int cnt = std::min(65535, A - a0);
-    dim3 grid((unsigned)mine, (unsigned)cnt);
-    auto kfn = P.n < (int64_t(1) << 31) ? noisy_search_kernel<true> : noisy_search_kernel<false>;
-    kfn<<<grid, kSearchThreads, 0, st>>>(
-        P.n, P.c, act_index + a0, act_b + a0, est + (int64_t)a0 * P.c, w.chunks,
-        part_s + (int64_t)a0 * w.chunks, part_t + (int64_t)a0 * w.chunks, rank, world);
+  } else {
+    for (int a0 = 0; a0 < A && mine > 0; a0 += 65535) {
+      const int cnt = std::min(65535, A - a0);
+      dim3 grid((unsigned)mine, (unsigned)cnt);
+      auto kfn =
+          P.n < (int64_t(1) << 31) ? noisy_search_kernel<true> : noisy_search_kernel<false>;
+      kfn<<<grid, kSearchThreads, 0, st>>>(
+          P.n, P.c, act_index + a0, act_b + a0, est + (int64_t)a0 * P.c, w.chunks,
+          part_s + (int64_t)a0 * w.chunks, part_t + (int64_t)a0 * w.chunks, rank, world,
+          node_bound + a0);
+    }
   }
   AFFT_CHECK_LAUNCH("noisy_search_kernel");
   if (world > 1) {
