@@ -168,6 +168,51 @@ __device__ __forceinline__ void lower_bound_to(unsigned long long* g, double sc)
   atomicMin(g, (unsigned long long)__double_as_longlong(sc));
 }
 
+// Fixed-point pre-filter of the candidate scan.  A candidate's phase at stride j is
+// frac(2^j r / n) turns, r = idx + b t; as a 64-bit fraction G(t) = A0 + t S with
+// A0 = floor(idx 2^64 / n) and S = floor((2^64 - 1) / L) (error <= L + 1 units of
+// 2^-64), and stride j's phase is the top 32 bits of G << j (one funnel shift).
+// est_j - target = E_j + phase_j in 32-bit turns wraps by itself; x = that >> 17 is
+// the wrapped difference in units of 2^-15 turn, and sum x^2 (uint32) is compared
+// against the pruning bound converted to those units plus a margin covering every
+// approximation: per term |x'^2 - d^2| <= 2 * 0.5 * e + e^2 turns^2 with
+// e <= 2^-15 + 2^-31 + (L + 1) 2^(j - 64) (the last <= 2^-20 where this is used).
+// A candidate whose approximate partial sum exceeds that limit has an exact partial
+// sum above the bound, so it is dropped exactly as cand_score would drop it; every
+// other candidate is then scored exactly.  Integer work only: ~6 instructions per
+// stride against ~18 (9 FP64) for the exact score.
+struct ApproxScan {
+  bool on;
+  uint64_t A0, S;
+  double margin;  // radians^2
+};
+constexpr double kApproxUnit2 = 3.6767e-08;  // (2 pi 2^-15)^2 rad^2 per x^2 unit, rounded down
+
+// The limit in x^2 units, or 0 when it is >= 2^31 (bound above ~79 rad^2: no
+// pre-filter, since the uint32 sum must stay below 2^32 = limit + one term <= 2^28).
+__device__ __forceinline__ uint32_t approx_limit(double bound, double margin) {
+  const double lim = (bound + margin) / kApproxUnit2;
+  return lim < 2147483648.0 ? (uint32_t)lim : 0u;
+}
+
+// true: pruned (the approximate partial sum passed lim)
+__device__ __forceinline__ bool approx_pruned(uint64_t G, const uint32_t* E, int c, uint32_t lim) {
+  const uint32_t hi = (uint32_t)(G >> 32), lo = (uint32_t)G;
+  uint32_t sum = 0;
+  const int c1 = c < 32 ? c : 32;
+  for (int j = 0; j < c1; ++j) {
+    const int32_t x = (int32_t)(E[j] + __funnelshift_l(lo, hi, j)) >> 17;
+    sum += (uint32_t)(x * x);
+    if (sum > lim) return true;
+  }
+  for (int j = 32; j < c; ++j) {
+    const int32_t x = (int32_t)(E[j] + (lo << (j - 32))) >> 17;
+    sum += (uint32_t)(x * x);
+    if (sum > lim) return true;
+  }
+  return false;
+}
+
 // One CTA scores kChunk consecutive candidates t of one active node.
 // Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
 template <bool k32>
@@ -177,6 +222,8 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
     int32_t* __restrict__ part_t, int chunk_rank, int chunk_world,
     unsigned long long* __restrict__ node_bound) {
   __shared__ double s_est[kMaxStrides];
+  __shared__ uint32_t s_e32[kMaxStrides];
+  __shared__ int s_nan;
   __shared__ double w_score[kSearchThreads / 32];
   __shared__ int32_t w_t[kSearchThreads / 32];
   const int a = blockIdx.y;
@@ -184,9 +231,31 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t t0 = (int64_t)chunk * kChunk;
-  if (threadIdx.x < c) s_est[threadIdx.x] = est[(int64_t)a * c + threadIdx.x];
+  if (threadIdx.x == 0) s_nan = 0;
+  __syncthreads();
+  if (threadIdx.x < c) {
+    const double e = est[(int64_t)a * c + threadIdx.x];
+    s_est[threadIdx.x] = e;
+    double u = e * 0.15915494309189535;  // turns (any rounding is inside the margin)
+    u -= floor(u);
+    s_e32[threadIdx.x] = (uint32_t)(uint64_t)(u * 4294967296.0);
+    if (!(e == e) || isinf(e)) s_nan = 1;
+  }
   __syncthreads();
   const int64_t idx = act_index[a];
+  ApproxScan ap;
+  ap.on = !s_nan && (uint64_t)n < (1ull << 32) &&
+          (double)(L + 1) * ldexp(1.0, c - 1) <= ldexp(1.0, 44);
+  if (ap.on) {
+    const uint64_t un = (uint64_t)n, num = (uint64_t)idx << 32;
+    const uint64_t q1 = num / un, r1 = num - q1 * un;
+    ap.A0 = (q1 << 32) | ((r1 << 32) / un);
+    ap.S = ~0ull / (uint64_t)L;
+    // e <= 2^-15 + 2^-31 + 2^-20 turns per term: (2 pi)^2 (e + e^2) rad^2, c terms,
+    // plus the uint32 limit's truncation (one unit)
+    const double e = 3.0517578125e-05 + 4.6566128730773926e-10 + 9.5367431640625e-07;
+    ap.margin = (double)c * 39.47841760435743 * (e + e * e) + 2.0 * kApproxUnit2;
+  }
   const double dn = (double)n;
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
@@ -199,6 +268,10 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
     const int64_t t1 = min(L, t0 + (int64_t)kChunk);
     for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads) {
       bound = fmin(bound, shared_bound(gb));
+      if (ap.on) {
+        const uint32_t lim = approx_limit(bound, ap.margin);
+        if (lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, s_e32, c, lim)) continue;
+      }
       const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
       if (sc > bound) continue;  // pruned / worse than a candidate that is scored in full
       if (sc < best) {
@@ -251,15 +324,37 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
     const int64_t* __restrict__ act_b, const double* __restrict__ est,
     double* __restrict__ part_score, int32_t* __restrict__ part_t) {
   __shared__ double s_est_all[kWarpSearchWarps][kMaxStrides];
+  __shared__ uint32_t s_e32_all[kWarpSearchWarps][kMaxStrides];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int a = blockIdx.x * kWarpSearchWarps + wl;
   if (a >= A) return;  // whole warps only
   double* s_est = s_est_all[wl];
-  for (int j = lane; j < c; j += 32) s_est[j] = est[(int64_t)a * c + j];
+  uint32_t* s_e32 = s_e32_all[wl];
+  bool bad = false;
+  for (int j = lane; j < c; j += 32) {
+    const double e = est[(int64_t)a * c + j];
+    s_est[j] = e;
+    double u = e * 0.15915494309189535;
+    u -= floor(u);
+    s_e32[j] = (uint32_t)(uint64_t)(u * 4294967296.0);
+    bad |= !(e == e) || isinf(e);
+  }
+  bad = __any_sync(0xffffffffu, bad);
   __syncwarp();
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t idx = act_index[a];
+  ApproxScan ap;  // the CTA kernel's pre-filter (see approx_pruned)
+  ap.on = !bad && (uint64_t)n < (1ull << 32) &&
+          (double)(L + 1) * ldexp(1.0, c - 1) <= ldexp(1.0, 44);
+  if (ap.on) {
+    const uint64_t un = (uint64_t)n, num = (uint64_t)idx << 32;
+    const uint64_t q1 = num / un, r1 = num - q1 * un;
+    ap.A0 = (q1 << 32) | ((r1 << 32) / un);
+    ap.S = ~0ull / (uint64_t)L;
+    const double e = 3.0517578125e-05 + 4.6566128730773926e-10 + 9.5367431640625e-07;
+    ap.margin = (double)c * 39.47841760435743 * (e + e * e) + 2.0 * kApproxUnit2;
+  }
   const double dn = (double)n;
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
@@ -269,7 +364,9 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
   // the warp shares its pruning bound after every 32 candidates (see shared_bound)
   for (int64_t tb = 0; tb < L; tb += 32) {
     const int64_t t = tb + lane;
-    if (t < L) {
+    uint32_t lim = 0;
+    if (ap.on) lim = approx_limit(bound, ap.margin);
+    if (t < L && !(lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, s_e32, c, lim))) {
       const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
       if (sc <= bound) {
         if (sc < best) {

@@ -149,3 +149,45 @@ def test_config3_vs_reference(variant):
     x = generate_test_case(case["n"], case["k"], case["snr"], case["seed"]).signal
     res = rffast_batch(torch.from_numpy(x).cuda()[None, :], case["k"], case["factors"], sp)
     _check_run(case, res)
+
+
+def test_batched_search_prefilter_vs_oracle():
+    """The search kernel prunes with a shared per-node bound and a fixed-point
+    pre-filter (rffast.cu: shared_bound, approx_pruned); both must leave the argmin
+    untouched.  Many nodes at once (so CTAs of one node race on the bound), mixed
+    singleton / multiton / noise-only residuals, against the oracle's exhaustive scan."""
+    from oracle import rffast as orf
+    from paper_2011_05749_b200 import _device, _lib, plan_cycles
+    from paper_2011_05749_b200.rffast import _node_workspace, _search_args
+
+    n, b = 255 * 256 * 257, 255
+    _, plan = plan_cycles(n, 8, "noisy", seed=5)
+    c, m, shifts = plan.c, plan.m, np.asarray(plan.shifts, dtype=np.int64)
+    rng = np.random.default_rng(2024)
+    rows, idx = [], []
+    for i in range(48):
+        index = int(rng.integers(0, b))
+        tones = int(rng.integers(0, 4))  # 0: noise only, 1: singleton, 2-3: multiton
+        f = index + b * rng.integers(0, n // b, size=tones)
+        v = np.exp(2j * np.pi * rng.random(tones))
+        y = (v[None, :] * np.exp(-2j * np.pi * ((shifts[:, None] * f[None, :]) % n) / n)).sum(1)
+        y = y + (0.05 + 0.3 * rng.random()) * (rng.normal(size=y.size) + 1j * rng.normal(size=y.size))
+        rows.append(y)
+        idx.append(index)
+    dev = _device.require_cuda()
+    res = torch.from_numpy(np.ascontiguousarray(np.stack(rows))).to(dev)
+    ix = torch.tensor(idx, dtype=torch.int64, device=dev)
+    cnt = len(idx)
+    f0 = torch.empty(cnt, dtype=torch.int64, device=dev)
+    val = torch.empty(cnt, dtype=torch.complex128, device=dev)
+    rn = torch.empty(cnt, dtype=torch.float64, device=dev)
+    ws = _node_workspace(n, cnt, b, c, m, dev)
+    sb, ns, wb = _search_args(plan)
+    _lib.check(_lib.load().afft_singleton_search_noisy(
+        res.data_ptr(), ix.data_ptr(), cnt, b, n, sb, ns, c, m, wb, f0.data_ptr(),
+        val.data_ptr(), rn.data_ptr(), ws.data_ptr(), ws.numel(), _device.stream_ptr()),
+        "singleton_search_noisy")
+    got = f0.cpu().numpy()
+    for i in range(cnt):
+        want, _, _ = orf.search(rows[i], idx[i], b, n, c, m, plan.weights, shifts)
+        assert int(got[i]) == want, (i, int(got[i]), want)
