@@ -159,10 +159,15 @@ __device__ __forceinline__ double search_bound(int64_t n, int64_t b, int64_t L, 
 // (min score, smallest t) result is the same whatever order CTAs run in.  A multiton
 // node's minimum sits far below the typical score (~27 strides x pi^2/3), and one
 // thread's own best of 16 candidates left it ~2.5x as many strides per candidate.
-__device__ __forceinline__ double shared_bound(const unsigned long long* g) {
-  const unsigned long long v = *reinterpret_cast<const volatile unsigned long long*>(g);
+__device__ __forceinline__ unsigned long long load_bound_bits(const unsigned long long* g) {
+  return *reinterpret_cast<const volatile unsigned long long*>(g);
+}
+__device__ __forceinline__ double bound_of_bits(unsigned long long v) {
   return v >= 0x7ff0000000000000ull ? __longlong_as_double(0x7ff0000000000000LL)
                                     : __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ double shared_bound(const unsigned long long* g) {
+  return bound_of_bits(load_bound_bits(g));
 }
 __device__ __forceinline__ void lower_bound_to(unsigned long long* g, double sc) {
   atomicMin(g, (unsigned long long)__double_as_longlong(sc));
@@ -172,27 +177,57 @@ __device__ __forceinline__ void lower_bound_to(unsigned long long* g, double sc)
 // frac(2^j r / n) turns, r = idx + b t; as a 64-bit fraction G(t) = A0 + t S with
 // A0 = floor(idx 2^64 / n) and S = floor((2^64 - 1) / L) (error <= L + 1 units of
 // 2^-64), and stride j's phase is the top 32 bits of G << j (one funnel shift).
-// est_j - target = E_j + phase_j in 32-bit turns wraps by itself; x = that >> 17 is
-// the wrapped difference in units of 2^-15 turn, and sum x^2 (uint32) is compared
-// against the pruning bound converted to those units plus a margin covering every
-// approximation: per term |x'^2 - d^2| <= 2 * 0.5 * e + e^2 turns^2 with
-// e <= 2^-15 + 2^-31 + (L + 1) 2^(j - 64) (the last <= 2^-20 where this is used).
-// A candidate whose approximate partial sum exceeds that limit has an exact partial
-// sum above the bound, so it is dropped exactly as cand_score would drop it; every
-// other candidate is then scored exactly.  Integer work only: ~6 instructions per
-// stride against ~18 (9 FP64) for the exact score.
+// est_j - target = E_j + phase_j in 32-bit turns wraps by itself; x = that >> 18 is
+// the wrapped difference in units of 2^-14 turn, and sum x^2 (uint32, every term
+// <= 2^26) is compared against the pruning bound converted to those units plus a
+// margin covering every approximation: per term |x'^2 - d^2| <= 2 * 0.5 * e + e^2
+// turns^2 with e <= 2^-14 + 2^-31 + (L + 1) 2^(j - 64) (the last <= 2^-20 where this
+// is used).  A candidate whose approximate partial sum exceeds that limit has an
+// exact partial sum above the bound, so it is dropped exactly as cand_score would
+// drop it; every other candidate is then scored exactly.  Integer work only, four
+// strides per limit test: ~6 instructions per stride against ~18 (9 FP64).
 struct ApproxScan {
   bool on;
   uint64_t A0, S;
   double margin;  // radians^2
 };
-constexpr double kApproxUnit2 = 3.6767e-08;  // (2 pi 2^-15)^2 rad^2 per x^2 unit, rounded down
+constexpr double kApproxUnit2 = 1.4706e-07;  // (2 pi 2^-14)^2 rad^2 per x^2 unit, rounded down
 
-// The limit in x^2 units, or 0 when it is >= 2^31 (bound above ~79 rad^2: no
-// pre-filter, since the uint32 sum must stay below 2^32 = limit + one term <= 2^28).
+// The limit in x^2 units (the sum may pass it by four terms: < 2^31 + 2^28 < 2^32),
+// or 0 when the bound is beyond any score (no pre-filter).
 __device__ __forceinline__ uint32_t approx_limit(double bound, double margin) {
   const double lim = (bound + margin) / kApproxUnit2;
   return lim < 2147483648.0 ? (uint32_t)lim : 0u;
+}
+
+__device__ __forceinline__ uint32_t approx_term(uint32_t e, uint32_t phase) {
+  const int32_t x = (int32_t)(e + phase) >> 18;
+  return (uint32_t)(x * x);
+}
+
+// Per-node set-up.  Phase error per term at stride j (turns): e_j = 2^-14 (the >> 18)
+// + 2^-31 (E_j rounding, the top-32-bit truncation) + (L + 1) 2^(j - 64) (G(t)); the
+// margin is (2 pi)^2 sum_j (e_j + e_j^2) rad^2 plus two limit units.  Off for NaN /
+// infinite estimates (the exact path handles them), n >= 2^32, or e_j > 2^-12.
+__device__ __forceinline__ ApproxScan make_approx(int64_t n, int64_t L, int64_t idx, int c,
+                                                  bool finite) {
+  ApproxScan ap;
+  const double drift = (double)(L + 1) * 5.421010862427522e-20;  // (L + 1) 2^-64
+  const double emax = 6.103515625e-05 + 4.6566128730773926e-10 + drift * ldexp(1.0, c - 1);
+  ap.on = finite && (uint64_t)n < (1ull << 32) && emax <= 2.44140625e-04;
+  ap.A0 = ap.S = 0;
+  ap.margin = 0.0;
+  if (ap.on) {
+    const uint64_t un = (uint64_t)n, num = (uint64_t)idx << 32;
+    const uint64_t q1 = num / un, r1 = num - q1 * un;
+    ap.A0 = (q1 << 32) | ((r1 << 32) / un);
+    ap.S = ~0ull / (uint64_t)L;
+    const double esum = (double)c * (6.103515625e-05 + 4.6566128730773926e-10) +
+                        drift * (ldexp(1.0, c) - 1.0);
+    ap.margin = 39.47841760435743 * (esum + (double)c * emax * emax) * 1.000001 +
+                2.0 * kApproxUnit2;
+  }
+  return ap;
 }
 
 // true: pruned (the approximate partial sum passed lim)
@@ -200,17 +235,17 @@ __device__ __forceinline__ bool approx_pruned(uint64_t G, const uint32_t* E, int
   const uint32_t hi = (uint32_t)(G >> 32), lo = (uint32_t)G;
   uint32_t sum = 0;
   const int c1 = c < 32 ? c : 32;
-  for (int j = 0; j < c1; ++j) {
-    const int32_t x = (int32_t)(E[j] + __funnelshift_l(lo, hi, j)) >> 17;
-    sum += (uint32_t)(x * x);
+  int j = 0;
+  for (; j + 4 <= c1; j += 4) {
+    sum += approx_term(E[j], __funnelshift_l(lo, hi, j)) +
+           approx_term(E[j + 1], __funnelshift_l(lo, hi, j + 1)) +
+           approx_term(E[j + 2], __funnelshift_l(lo, hi, j + 2)) +
+           approx_term(E[j + 3], __funnelshift_l(lo, hi, j + 3));
     if (sum > lim) return true;
   }
-  for (int j = 32; j < c; ++j) {
-    const int32_t x = (int32_t)(E[j] + (lo << (j - 32))) >> 17;
-    sum += (uint32_t)(x * x);
-    if (sum > lim) return true;
-  }
-  return false;
+  for (; j < c1; ++j) sum += approx_term(E[j], __funnelshift_l(lo, hi, j));
+  for (; j < c; ++j) sum += approx_term(E[j], lo << (j - 32));
+  return sum > lim;
 }
 
 // One CTA scores kChunk consecutive candidates t of one active node.
@@ -224,6 +259,7 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   __shared__ double s_est[kMaxStrides];
   __shared__ uint32_t s_e32[kMaxStrides];
   __shared__ int s_nan;
+  __shared__ unsigned long long s_bound;
   __shared__ double w_score[kSearchThreads / 32];
   __shared__ int32_t w_t[kSearchThreads / 32];
   const int a = blockIdx.y;
@@ -231,7 +267,10 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t t0 = (int64_t)chunk * kChunk;
-  if (threadIdx.x == 0) s_nan = 0;
+  if (threadIdx.x == 0) {
+    s_nan = 0;
+    s_bound = load_bound_bits(node_bound + a);
+  }
   __syncthreads();
   if (threadIdx.x < c) {
     const double e = est[(int64_t)a * c + threadIdx.x];
@@ -243,19 +282,7 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   }
   __syncthreads();
   const int64_t idx = act_index[a];
-  ApproxScan ap;
-  ap.on = !s_nan && (uint64_t)n < (1ull << 32) &&
-          (double)(L + 1) * ldexp(1.0, c - 1) <= ldexp(1.0, 44);
-  if (ap.on) {
-    const uint64_t un = (uint64_t)n, num = (uint64_t)idx << 32;
-    const uint64_t q1 = num / un, r1 = num - q1 * un;
-    ap.A0 = (q1 << 32) | ((r1 << 32) / un);
-    ap.S = ~0ull / (uint64_t)L;
-    // e <= 2^-15 + 2^-31 + 2^-20 turns per term: (2 pi)^2 (e + e^2) rad^2, c terms,
-    // plus the uint32 limit's truncation (one unit)
-    const double e = 3.0517578125e-05 + 4.6566128730773926e-10 + 9.5367431640625e-07;
-    ap.margin = (double)c * 39.47841760435743 * (e + e * e) + 2.0 * kApproxUnit2;
-  }
+  const ApproxScan ap = make_approx(n, L, idx, c, !s_nan);
   const double dn = (double)n;
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
@@ -263,11 +290,22 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   int32_t bt = INT32_MAX;
   if (t0 < L) {
     unsigned long long* gb = node_bound + a;
-    double bound = search_bound<k32>(n, b, L, idx, s_est, c, inv);
-    if (threadIdx.x == 0) lower_bound_to(gb, bound);
+    double bound = bound_of_bits(s_bound);  // seeded by noisy_seed_kernel
     const int64_t t1 = min(L, t0 + (int64_t)kChunk);
-    for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads) {
-      bound = fmin(bound, shared_bound(gb));
+    // Two levels: the CTA's own bound in shared memory, read before every candidate,
+    // and the node's global bound, folded into it every 4 candidates from a load
+    // issued 4 candidates earlier (a global load waited on before every candidate was
+    // 2/3 of the kernel's stall samples).  Any value read is some candidate's real
+    // score, so a stale one only prunes less.
+    volatile unsigned long long* vs_bound = &s_bound;
+    unsigned long long pending = load_bound_bits(gb);
+    int k = 0;
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads, ++k) {
+      if ((k & 3) == 3) {
+        atomicMin(&s_bound, pending);
+        pending = load_bound_bits(gb);
+      }
+      bound = fmin(bound, bound_of_bits(*vs_bound));
       if (ap.on) {
         const uint32_t lim = approx_limit(bound, ap.margin);
         if (lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, s_e32, c, lim)) continue;
@@ -280,6 +318,7 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
       }
       if (sc < bound) {
         bound = sc;
+        atomicMin(&s_bound, (unsigned long long)__double_as_longlong(sc));
         lower_bound_to(gb, sc);
       }
     }
@@ -313,6 +352,23 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   }
 }
 
+// The shared bound's seed, once per node (computing it in every CTA, by every thread,
+// was most of the CTA kernel's instructions): the full score of the candidate nearest
+// the stride-0 estimate.
+template <bool k32>
+__global__ void noisy_seed_kernel(int64_t n, int c, int A, const int64_t* __restrict__ act_index,
+                                  const int64_t* __restrict__ act_b,
+                                  const double* __restrict__ est,
+                                  unsigned long long* __restrict__ node_bound) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const int64_t b = act_b[a];
+  const double bound =
+      search_bound<k32>(n, b, n / b, act_index[a], est + (int64_t)a * c, c, 1.0 / (double)n);
+  if (bound < __longlong_as_double(0x7ff0000000000000LL))
+    node_bound[a] = (unsigned long long)__double_as_longlong(bound);
+}
+
 // Short candidate lists (L = n / b <= kWarpSearchMaxL, DSFFT's deep layers): one warp
 // per node, same scores, same bound, same (min score, smallest t) result as the CTA
 // kernel's single chunk — a 256-thread CTA per node left most threads idle there.
@@ -344,17 +400,7 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t idx = act_index[a];
-  ApproxScan ap;  // the CTA kernel's pre-filter (see approx_pruned)
-  ap.on = !bad && (uint64_t)n < (1ull << 32) &&
-          (double)(L + 1) * ldexp(1.0, c - 1) <= ldexp(1.0, 44);
-  if (ap.on) {
-    const uint64_t un = (uint64_t)n, num = (uint64_t)idx << 32;
-    const uint64_t q1 = num / un, r1 = num - q1 * un;
-    ap.A0 = (q1 << 32) | ((r1 << 32) / un);
-    ap.S = ~0ull / (uint64_t)L;
-    const double e = 3.0517578125e-05 + 4.6566128730773926e-10 + 9.5367431640625e-07;
-    ap.margin = (double)c * 39.47841760435743 * (e + e * e) + 2.0 * kApproxUnit2;
-  }
+  const ApproxScan ap = make_approx(n, L, idx, c, !bad);  // see approx_pruned
   const double dn = (double)n;
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
@@ -1020,6 +1066,11 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
     kfn<<<(unsigned)((A + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
           st>>>(P.n, P.c, A, act_index, act_b, est, part_s, part_t);
   } else {
+    if (mine > 0) {
+      auto sfn = P.n < (int64_t(1) << 31) ? noisy_seed_kernel<true> : noisy_seed_kernel<false>;
+      sfn<<<(unsigned)((A + 127) / 128), 128, 0, st>>>(P.n, P.c, A, act_index, act_b, est,
+                                                         node_bound);
+    }
     for (int a0 = 0; a0 < A && mine > 0; a0 += 65535) {
       const int cnt = std::min(65535, A - a0);
       dim3 grid((unsigned)mine, (unsigned)cnt);
