@@ -144,6 +144,58 @@ __device__ __forceinline__ void out_generic(const cd* src, cd* dst, const cd* tw
   dst[(j / Ns) * Ns * R + jm + q * Ns] = acc;
 }
 
+// Odd prime radix R >= 11 by the symmetric (Goertzel-pair) form: with
+// s_r = x_r + x_{R-r} and d_r = x_r - x_{R-r} (r = 1..h, h = (R-1)/2),
+//   X[q]   = x_0 + sum_r s_r cos(2 pi r q / R) - i d_r sin(2 pi r q / R)
+//   X[R-q] = x_0 + sum_r s_r cos(2 pi r q / R) + i d_r sin(2 pi r q / R),
+// so one work item produces two outputs from h iterations of 4 real FMAs, against
+// 2 (R - 1) complex multiply-adds for the two outputs of the direct sum.
+// Pass 1 (one thread per butterfly): inter-stage twiddles, then the pairs in place.
+__device__ __forceinline__ void sym_prep(cd* src, const cd* tw, int n, int R, int nb, int Ns,
+                                         int j) {
+  const int jm = j % Ns;
+  const int tstep = n / (Ns * R);
+  const int h = (R - 1) >> 1;
+  for (int r = 1; r <= h; ++r) {
+    cd a = src[j + r * nb], c = src[j + (R - r) * nb];
+    if (jm) {
+      a = cmul(a, tw[jm * r * tstep]);
+      c = cmul(c, tw[jm * (R - r) * tstep]);
+    }
+    src[j + r * nb] = cadd(a, c);
+    src[j + (R - r) * nb] = csub(a, c);
+  }
+}
+// Pass 2: outputs q and R - q of butterfly j (q = 0: X[0] alone).
+__device__ __forceinline__ void sym_out(const cd* src, cd* dst, const cd* tw, int n, int R,
+                                        int nb, int Ns, int j, int q) {
+  const int jm = j % Ns;
+  const int wstep = n / R;
+  const int h = (R - 1) >> 1;
+  const int base = (j / Ns) * Ns * R + jm;
+  const cd x0 = src[j];
+  if (q == 0) {
+    cd acc = x0;
+    for (int r = 1; r <= h; ++r) acc = cadd(acc, src[j + r * nb]);
+    dst[base] = acc;
+    return;
+  }
+  double are = 0.0, aim = 0.0, bre = 0.0, bim = 0.0;
+  int e = 0;  // (r q) mod R
+  for (int r = 1; r <= h; ++r) {
+    e += q;
+    if (e >= R) e -= R;
+    const cd w = tw[e * wstep];  // exp(-2 pi i e / R): cos = w.re, sin = -w.im
+    const cd sr = src[j + r * nb], dr = src[j + (R - r) * nb];
+    are = __fma_rn(sr.re, w.re, are);
+    aim = __fma_rn(sr.im, w.re, aim);
+    bre = __fma_rn(-dr.im, w.im, bre);  // d.im * sin
+    bim = __fma_rn(dr.re, w.im, bim);   // -d.re * sin
+  }
+  dst[base + q * Ns] = cd{x0.re + are + bre, x0.im + aim + bim};
+  dst[base + (R - q) * Ns] = cd{x0.re + are - bre, x0.im + aim - bim};
+}
+
 // cos(pi m / 8) for m = 0..15 as correctly rounded literals; sin(pi m / 8) =
 // cos16(m + 12).  A selection chain (not a table) so that the unrolled callers'
 // constant m folds to immediates.
@@ -325,6 +377,22 @@ __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const 
         }
         break;
       default: {
+        if (R & 1) {  // odd prime: symmetric pairs
+          for (int w = tid; w < total; w += nthreads) {
+            const int seq = w / nb, j = w - seq * nb;
+            sym_prep(a + (size_t)seq * ld, tw, n, R, nb, Ns, j);
+          }
+          __syncthreads();
+          const int hq = ((R - 1) >> 1) + 1;  // q = 0..h
+          const int outs = total * hq;
+          for (int w = tid; w < outs; w += nthreads) {
+            const int bw = w / hq;
+            const int q = w - bw * hq;
+            const int seq = bw / nb, j = bw - seq * nb;
+            sym_out(a + (size_t)seq * ld, b + (size_t)seq * ld, tw, n, R, nb, Ns, j, q);
+          }
+          break;
+        }
         for (int w = tid; w < total; w += nthreads) {
           const int seq = w / nb, j = w - seq * nb;
           scale_generic(a + (size_t)seq * ld, tw, n, R, nb, Ns, j);
