@@ -22,6 +22,11 @@ void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
 // stream-ordered scratch from the library's memory pool (kept across calls)
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
+// Pinned host staging from a process-wide pool: buffers are never freed (cudaFreeHost
+// synchronises the whole device, which a thread-local buffer's destructor did at every
+// worker-thread exit), and are reused across threads.  pinned_release returns one.
+void* pinned_acquire(size_t bytes, size_t* capacity);
+void pinned_release(void* p, size_t capacity);
 cudaError_t scratch_free(void* p, cudaStream_t stream);
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (never lowers it:
 // the attribute is process-wide, so concurrent callers on other streams/threads that

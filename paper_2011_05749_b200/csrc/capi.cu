@@ -46,6 +46,34 @@ static cudaMemPool_t library_pool() {
   return g_pools[dev];
 }
 
+static std::mutex g_pin_mu;
+static std::multimap<size_t, void*> g_pin_free;  // capacity -> buffer
+
+void* pinned_acquire(size_t bytes, size_t* capacity) {
+  {
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end()) {
+      void* p = it->second;
+      *capacity = it->first;
+      g_pin_free.erase(it);
+      return p;
+    }
+  }
+  size_t cap = 4096;
+  while (cap < bytes) cap <<= 1;
+  void* p = nullptr;
+  if (cudaMallocHost(&p, cap) != cudaSuccess) return nullptr;
+  *capacity = cap;
+  return p;
+}
+
+void pinned_release(void* p, size_t capacity) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  g_pin_free.emplace(capacity, p);
+}
+
 cudaError_t ensure_smem(const void* func, size_t bytes) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, size_t> granted;

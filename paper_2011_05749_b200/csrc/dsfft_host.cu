@@ -158,39 +158,19 @@ double now_s() {
     if (g_prof.on) g_marks.mark(what, now_s(), g_prof.wait_s); \
   } while (0)
 
-// Per-thread pinned staging for read-backs (a pageable D2H copy costs a bounce).
-struct PinnedStage {
-  void* p = nullptr;
-  size_t cap = 0;
-  ~PinnedStage() {
-    if (p) cudaFreeHost(p);
-  }
-  void* get(size_t bytes) {
-    if (bytes > cap) {
-      if (p) cudaFreeHost(p);
-      p = nullptr;
-      cap = 0;
-      size_t c = 4096;
-      while (c < bytes) c <<= 1;
-      if (cudaMallocHost(&p, c) != cudaSuccess) return nullptr;
-      cap = c;
-    }
-    return p;
-  }
-};
-thread_local PinnedStage g_stage;
-
 template <class T>
 int d2h(std::vector<T>& h, const void* d, size_t count, cudaStream_t st) {
   h.resize(count);
   if (!count) return AFFT_OK;
   const double t0 = g_prof.on ? now_s() : 0.0;
   const size_t bytes = count * sizeof(T);
-  void* stage = g_stage.get(bytes);
+  size_t cap = 0;
+  void* stage = pinned_acquire(bytes, &cap);  // a pageable D2H copy costs a bounce
   cudaError_t e = cudaMemcpyAsync(stage ? stage : (void*)h.data(), d, bytes,
                                   cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess && stage) std::memcpy(h.data(), stage, bytes);
+  pinned_release(stage, cap);
   if (g_prof.on) {
     g_prof.wait_s += now_s() - t0;
     ++g_prof.syncs;

@@ -1104,13 +1104,12 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   return AFFT_OK;
 }
 
-static int32_t* pinned_counter() {
-  static thread_local int32_t* h = nullptr;
-  if (!h) {
-    if (cudaMallocHost(&h, 64) != cudaSuccess) h = nullptr;
-  }
-  return h;
-}
+// Two pinned int32 read-back slots for one decode, from the library's pinned pool.
+struct PinnedCounter {
+  size_t cap = 0;
+  int32_t* h = static_cast<int32_t*>(pinned_acquire(64, &cap));
+  ~PinnedCounter() { pinned_release(h, cap); }
+};
 
 }  // namespace afft
 
@@ -1289,7 +1288,8 @@ extern "C" int afft_peel_noisy_sharded(
   int8_t* dirty = reinterpret_cast<int8_t*>(ws + w.dirty);
   int32_t* done = reinterpret_cast<int32_t*>(ws + w.done);
   int32_t* counters = reinterpret_cast<int32_t*>(ws + w.counters);
-  int32_t* host = pinned_counter();
+  PinnedCounter pc;
+  int32_t* host = pc.h;
   if (!host) {
     set_error("afft_peel_noisy: cannot allocate a pinned host counter");
     return AFFT_ENOMEM;

@@ -263,16 +263,33 @@ def dsfft(x, k: int, config: DsfftConfig | None = None,
     return SparseSpectrum(n, dict(zip(pos[order].tolist(), val[order].tolist())))
 
 
+_POOL_LOCK = __import__("threading").Lock()
+_POOLS: dict = {}
+
+
+def _worker_pool(workers: int, device):
+    """A persistent thread pool per (size, device) whose threads keep their own CUDA
+    stream: a worker's first decode pays the thread's and stream's set-up (measured
+    ~2x a warm decode), so pools are not torn down between calls."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    key = (workers, str(device))
+    with _POOL_LOCK:
+        pool = _POOLS.get(key)
+        if pool is None:
+            pool = ThreadPoolExecutor(max_workers=workers, thread_name_prefix="afft-dsfft")
+            _POOLS[key] = pool
+    return pool
+
+
 def dsfft_batch(xs, k: int, configs, streams: int = 4) -> list[SparseSpectrum]:
     """DSFFT over several signals, in input order.  Each signal's layer loop is
     data-dependent (one read-back per layer), so one signal alone leaves the GPU idle
     during its read-backs; with streams > 1 signals run on worker threads, each with
     its own CUDA stream (the library is reentrant per stream and the native loop runs
     without the GIL), overlapping one signal's read-backs with another's kernels.
-    Measured at config 4, 8 signals (tools/dsfft_streams.py): 1 stream 69 signals/s,
-    4 streams 117, 8 streams 137; results identical to the sequential run."""
+    Results are identical to the sequential run (tools/dsfft_streams.py)."""
     import threading
-    from concurrent.futures import ThreadPoolExecutor
 
     xd = _device.as_device_batch(xs)
     count = int(xd.shape[0])
@@ -281,24 +298,33 @@ def dsfft_batch(xs, k: int, configs, streams: int = 4) -> list[SparseSpectrum]:
     if workers == 1:
         return [dsfft(xd[i], k, cfgs[i]) for i in range(count)]
     main = torch.cuda.current_stream(xd.device)
-    local = threading.local()
-    made: list = []
+    ready = torch.cuda.Event()
+    ready.record(main)  # the batch was produced on the caller's stream
+    done = []
     lock = threading.Lock()
+    local = _worker_local
 
     def work(i):
-        if not hasattr(local, "stream"):
-            local.stream = torch.cuda.Stream(device=xd.device)
-            local.stream.wait_stream(main)  # the batch was produced on the caller's stream
-            with lock:
-                made.append(local.stream)
-        with torch.cuda.stream(local.stream):
-            return dsfft(xd[i], k, cfgs[i])
+        st = getattr(local, "stream", None)
+        if st is None or st.device != xd.device:
+            st = local.stream = torch.cuda.Stream(device=xd.device)
+        st.wait_event(ready)
+        with torch.cuda.stream(st):
+            out = dsfft(xd[i], k, cfgs[i])
+            ev = torch.cuda.Event()
+            ev.record(st)
+        with lock:
+            done.append(ev)
+        return out
 
-    with ThreadPoolExecutor(max_workers=workers) as ex:
-        out = list(ex.map(work, range(count)))
-    for st in made:
-        main.wait_stream(st)
+    out = list(_worker_pool(workers, xd.device).map(work, range(count)))
+    for ev in done:
+        main.wait_event(ev)
     return out
+
+
+_worker_local = __import__("threading").local()
+
 
 def _to_tree_layer(layer: _DevLayer) -> TreeLayer:
     if layer.cand is None:
