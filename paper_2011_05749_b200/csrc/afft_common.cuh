@@ -26,6 +26,9 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
 // synchronises the whole device, which a thread-local buffer's destructor did at every
 // worker-thread exit), and are reused across threads.  pinned_release returns one.
 void* pinned_acquire(size_t bytes, size_t* capacity);
+// dsfft.cu: a full layer's active set straight from the resident spectrum (n/b <= 32).
+int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64_t* out, int cap,
+                 int32_t* count, cudaStream_t st);
 void pinned_release(void* p, size_t capacity);
 cudaError_t scratch_free(void* p, cudaStream_t stream);
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (never lowers it:

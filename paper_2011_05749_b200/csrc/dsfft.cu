@@ -19,6 +19,8 @@
 #include <map>
 #include <vector>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "afft_common.cuh"
 
 extern "C" int afft_bucketize(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
@@ -292,6 +294,112 @@ __global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y
     }
     energy[i] = e;
   }
+}
+
+// Full deep layer straight to its active set, in one pass over the resident spectrum:
+// the tau = 0 value of bucket i is sum_l Y[i + l b], summed in the order
+// alias_all_kernel uses (so |v| and the decision are bit-identical to values + 
+// afft_active_indices), tested against thr, and never written.  Each CTA compacts its
+// active buckets (ascending within the CTA) and reserves a segment of `out` with one
+// atomic, only when it has any; sort_active_kernel then puts the list in ascending
+// order.  Against values + count + scan + write, this reads Y once and the values never.
+template <int LM>
+__global__ void __launch_bounds__(256) alias_active_kernel(const cd* __restrict__ Y, int64_t b,
+                                                           int L, double thr,
+                                                           int64_t* __restrict__ out, int cap,
+                                                           int32_t* __restrict__ count) {
+  __shared__ int warp_cnt[8];
+  __shared__ int base;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int f = 0;
+  if (i < b) {
+    cd y[LM];
+#pragma unroll
+    for (int l = 0; l < LM; ++l)
+      if (l < L) y[l] = Y[i + (int64_t)l * b];
+    cd acc = y[0];
+#pragma unroll
+    for (int l = 1; l < LM; ++l)
+      if (l < L) acc = cadd(acc, y[l]);
+    f = cabs_(acc) > thr;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, f);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) warp_cnt[w] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int k = 0; k < 8; ++k) {
+      const int c = warp_cnt[k];
+      warp_cnt[k] = run;
+      run += c;
+    }
+    base = run ? atomicAdd(count, run) : 0;
+  }
+  __syncthreads();
+  if (f) {
+    const int at = base + warp_cnt[w] + __popc(m & ((1u << lane) - 1u));
+    if (at < cap) out[at] = i;
+  }
+}
+
+// Ascending order of the active list: one CTA, cub's block radix sort over the
+// bucket indices as 32-bit keys (b <= 2^31), 16 per thread, bits [0, log2 b) only.
+// (A bitonic sort of the ~5,000 entries of config 4's deep layers took 87 us.)
+constexpr int kActiveSortThreads = 1024, kActiveSortItems = 16;
+constexpr int kActiveSortCap = kActiveSortThreads * kActiveSortItems;
+using ActiveSort = cub::BlockRadixSort<uint32_t, kActiveSortThreads, kActiveSortItems>;
+__global__ void __launch_bounds__(kActiveSortThreads) sort_active_kernel(
+    int64_t* __restrict__ list, const int32_t* __restrict__ count, int end_bit) {
+  extern __shared__ __align__(16) unsigned char sort_smem[];
+  auto& temp = *reinterpret_cast<typename ActiveSort::TempStorage*>(sort_smem);
+  const int m = *count;
+  if (m <= 1 || m > kActiveSortCap) return;
+  uint32_t keys[kActiveSortItems];
+#pragma unroll
+  for (int k = 0; k < kActiveSortItems; ++k) {
+    const int i = threadIdx.x * kActiveSortItems + k;
+    keys[k] = i < m ? (uint32_t)list[i] : 0xffffffffu;
+  }
+  ActiveSort(temp).Sort(keys, 0, end_bit);
+#pragma unroll
+  for (int k = 0; k < kActiveSortItems; ++k) {
+    const int i = threadIdx.x * kActiveSortItems + k;
+    if (i < m) list[i] = keys[k];
+  }
+}
+
+// Launches alias_active_kernel + sort_active_kernel; *count (device, zeroed here) is the
+// full active count, the list holds it only if it is <= min(cap, kActiveSortCap).
+int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64_t* out, int cap,
+                 int32_t* count, cudaStream_t st) {
+  const int64_t L = n / b;
+  if (L > kAliasMaxL || b < 1 || n % b) {
+    set_error("alias_active: n/b = %lld", (long long)L);
+    return AFFT_EUNSUPPORTED;
+  }
+  cudaError_t e = cudaMemsetAsync(count, 0, 4, st);
+  if (e != cudaSuccess) return cuda_status(e, "alias_active count");
+  const cd* Y = reinterpret_cast<const cd*>(spectrum);
+  const unsigned grid = (unsigned)((b + 255) / 256);
+  if (L <= 2)
+    alias_active_kernel<2><<<grid, 256, 0, st>>>(Y, b, (int)L, thr, out, cap, count);
+  else if (L <= 4)
+    alias_active_kernel<4><<<grid, 256, 0, st>>>(Y, b, (int)L, thr, out, cap, count);
+  else if (L <= 8)
+    alias_active_kernel<8><<<grid, 256, 0, st>>>(Y, b, (int)L, thr, out, cap, count);
+  else if (L <= 16)
+    alias_active_kernel<16><<<grid, 256, 0, st>>>(Y, b, (int)L, thr, out, cap, count);
+  else
+    alias_active_kernel<kAliasMaxL><<<grid, 256, 0, st>>>(Y, b, (int)L, thr, out, cap, count);
+  const size_t smem = sizeof(typename ActiveSort::TempStorage);
+  e = ensure_smem((const void*)sort_active_kernel, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(sort_active)");
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) < b) ++end_bit;
+  sort_active_kernel<<<1, kActiveSortThreads, smem, st>>>(out, count, end_bit);
+  AFFT_CHECK_LAUNCH("alias_active");
+  return AFFT_OK;
 }
 
 }  // namespace afft

@@ -394,7 +394,24 @@ struct Dsfft {
       tr.add(2, depth, out.m, nc);
       return AFFT_OK;
     }
-    DBuf vals;
+    if (alias_ok(b)) {  // deep layer: active set in one pass over Y, values never stored
+      RC(spectrum());
+      const int cap = (int)std::min<int64_t>(b, 16384);  // alias_active's sort capacity
+      RC(out.active.alloc((size_t)cap * 8, st, "dsfft active"));
+      DBuf cnt;
+      RC(cnt.alloc(4, st, "dsfft count"));
+      RC(alias_active(Y.as<double>(), n, b, thr, out.active.as<int64_t>(), cap,
+                      cnt.as<int32_t>(), st));
+      std::vector<int32_t> h;
+      RC(d2h(h, cnt.p, 1, st));
+      if (h[0] <= cap) {
+        out.m = h[0];
+        PMARK("active set");
+        tr.add(2, depth, out.m, -1);
+        return AFFT_OK;
+      }
+    }
+    DBuf vals;  // shallow layers, or more active buckets than the one-CTA sort holds
     RC(full_values(b, vals));
     RC(active(vals, b, thr, nullptr, out));
     tr.add(2, depth, out.m, -1);
