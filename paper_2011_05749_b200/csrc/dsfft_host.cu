@@ -396,7 +396,13 @@ struct Dsfft {
     }
     if (alias_ok(b)) {  // deep layer: active set in one pass over Y, values never stored
       RC(spectrum());
-      const int cap = (int)std::min<int64_t>(b, 16384);  // alias_active's sort capacity
+      // alias_active's sort capacity; AFFT_ACTIVE_SORT_CAP lowers it (tests force the
+      // fallback path with it)
+      static const int64_t cap_env = [] {
+        const char* v = std::getenv("AFFT_ACTIVE_SORT_CAP");
+        return v ? std::max<int64_t>(1, std::atoll(v)) : int64_t(16384);
+      }();
+      const int cap = (int)std::min<int64_t>(b, std::min<int64_t>(16384, cap_env));
       RC(out.active.alloc((size_t)cap * 8, st, "dsfft active"));
       DBuf cnt;
       RC(cnt.alloc(4, st, "dsfft count"));
