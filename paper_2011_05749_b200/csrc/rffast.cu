@@ -752,19 +752,31 @@ __global__ void robust_thresholds_kernel(int count, int pow2, const double* __re
   const int64_t s = blockIdx.x;
   const double* E = energy + s * (int64_t)count;
   const uint8_t* M = mask ? mask + s * (int64_t)count : nullptr;
+  // the reference set and max(initial=0.0) in parallel: the set's order is irrelevant
+  // (it is sorted next), and fmax is order-independent (a serial thread-0 loop over
+  // the global energies was most of this kernel's 50 us per signal)
+  __shared__ double w_max[32];
+  if (threadIdx.x == 0) m_count = 0;
+  __syncthreads();
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const double e = E[i];
+    mx = fmax(mx, e);
+    if (!M || M[i]) v[atomicAdd(&m_count, 1)] = e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) w_max[threadIdx.x >> 5] = mx;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int cnt = 0;
-    double mx = 0.0;  // scale.max(initial=0.0)
-    for (int i = 0; i < count; ++i) {
-      mx = fmax(mx, E[i]);
-      if (!M || M[i]) v[cnt++] = E[i];
-    }
-    if (M && cnt == 0) {  // empty reference set: fall back to all energies
-      for (int i = 0; i < count; ++i) v[i] = E[i];
-      cnt = count;
-    }
-    m_count = cnt;
-    m_max = mx;
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, w_max[w]);
+    m_max = r;
+  }
+  if (M && m_count == 0) {  // empty reference set: fall back to all energies
+    for (int i = threadIdx.x; i < count; i += blockDim.x) v[i] = E[i];
+    __syncthreads();
+    if (threadIdx.x == 0) m_count = count;
   }
   __syncthreads();
   const int cnt = m_count;
