@@ -166,34 +166,53 @@ __device__ __forceinline__ void sym_prep(cd* src, const cd* tw, int n, int R, in
     src[j + (R - r) * nb] = csub(a, c);
   }
 }
-// Pass 2: outputs q and R - q of butterfly j (q = 0: X[0] alone).
+// Pass 2: outputs q and R - q of butterfly j for kSymQ consecutive q = q0 .. (q = 0:
+// X[0] alone), sharing each loaded s_r, d_r across the kSymQ pairs (the one-pair
+// version spent most of its time on shared-memory loads).  Per output the arithmetic
+// is the same FMA chain over ascending r as one pair alone.
+constexpr int kSymQ = 2;
 __device__ __forceinline__ void sym_out(const cd* src, cd* dst, const cd* tw, int n, int R,
-                                        int nb, int Ns, int j, int q) {
+                                        int nb, int Ns, int j, int q0) {
   const int jm = j % Ns;
   const int wstep = n / R;
   const int h = (R - 1) >> 1;
   const int base = (j / Ns) * Ns * R + jm;
   const cd x0 = src[j];
-  if (q == 0) {
-    cd acc = x0;
-    for (int r = 1; r <= h; ++r) acc = cadd(acc, src[j + r * nb]);
-    dst[base] = acc;
-    return;
+  double are[kSymQ], aim[kSymQ], bre[kSymQ], bim[kSymQ];
+  int e[kSymQ];
+  cd acc0 = x0;  // X[0] when q0 == 0
+#pragma unroll
+  for (int u = 0; u < kSymQ; ++u) {
+    are[u] = aim[u] = bre[u] = bim[u] = 0.0;
+    e[u] = 0;
   }
-  double are = 0.0, aim = 0.0, bre = 0.0, bim = 0.0;
-  int e = 0;  // (r q) mod R
   for (int r = 1; r <= h; ++r) {
-    e += q;
-    if (e >= R) e -= R;
-    const cd w = tw[e * wstep];  // exp(-2 pi i e / R): cos = w.re, sin = -w.im
     const cd sr = src[j + r * nb], dr = src[j + (R - r) * nb];
-    are = __fma_rn(sr.re, w.re, are);
-    aim = __fma_rn(sr.im, w.re, aim);
-    bre = __fma_rn(-dr.im, w.im, bre);  // d.im * sin
-    bim = __fma_rn(dr.re, w.im, bim);   // -d.re * sin
+    if (q0 == 0) acc0 = cadd(acc0, sr);
+#pragma unroll
+    for (int u = 0; u < kSymQ; ++u) {
+      const int q = q0 + u;
+      if (q == 0 || q > h) continue;
+      e[u] += q;
+      if (e[u] >= R) e[u] -= R;
+      const cd w = tw[e[u] * wstep];  // exp(-2 pi i e / R): cos = w.re, sin = -w.im
+      are[u] = __fma_rn(sr.re, w.re, are[u]);
+      aim[u] = __fma_rn(sr.im, w.re, aim[u]);
+      bre[u] = __fma_rn(-dr.im, w.im, bre[u]);  // d.im * sin
+      bim[u] = __fma_rn(dr.re, w.im, bim[u]);   // -d.re * sin
+    }
   }
-  dst[base + q * Ns] = cd{x0.re + are + bre, x0.im + aim + bim};
-  dst[base + (R - q) * Ns] = cd{x0.re + are - bre, x0.im + aim - bim};
+#pragma unroll
+  for (int u = 0; u < kSymQ; ++u) {
+    const int q = q0 + u;
+    if (q > h) break;
+    if (q == 0) {
+      dst[base] = acc0;
+      continue;
+    }
+    dst[base + q * Ns] = cd{x0.re + are[u] + bre[u], x0.im + aim[u] + bim[u]};
+    dst[base + (R - q) * Ns] = cd{x0.re + are[u] - bre[u], x0.im + aim[u] - bim[u]};
+  }
 }
 
 // cos(pi m / 8) for m = 0..15 as correctly rounded literals; sin(pi m / 8) =
@@ -383,13 +402,13 @@ __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const 
             sym_prep(a + (size_t)seq * ld, tw, n, R, nb, Ns, j);
           }
           __syncthreads();
-          const int hq = ((R - 1) >> 1) + 1;  // q = 0..h
+          const int hq = ((R - 1) >> 1) / kSymQ + 1;  // groups of kSymQ q's over 0..h
           const int outs = total * hq;
           for (int w = tid; w < outs; w += nthreads) {
             const int bw = w / hq;
-            const int q = w - bw * hq;
+            const int g = w - bw * hq;
             const int seq = bw / nb, j = bw - seq * nb;
-            sym_out(a + (size_t)seq * ld, b + (size_t)seq * ld, tw, n, R, nb, Ns, j, q);
+            sym_out(a + (size_t)seq * ld, b + (size_t)seq * ld, tw, n, R, nb, Ns, j, g * kSymQ);
           }
           break;
         }

@@ -8,6 +8,7 @@ The truncated output is compared too, with the documented exception of
 |v| ties at the k-th rank.
 """
 
+import os
 import numpy as np
 import pytest
 import torch
@@ -183,3 +184,27 @@ def test_config5_full_batch_vs_oracle():
             total += 1
             good += f in truths[i] and abs(v - truths[i][f]) < 1e-4
     assert good >= 0.99 * total
+
+
+def test_bench_synthesis_matches_generate_test_case():
+    """bench.py synthesises config 5 on the device (numpy truth draws, cuFFT inverse,
+    complex64); the signals must be the reference generator's (signals.py:81-117) for
+    the same case seeds, up to complex64 rounding."""
+    import sys
+
+    from paper_2011_05749_b200 import generate_test_case
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+
+    dev = torch.device("cuda")
+    x = torch.empty((2, bench.N_SIG), dtype=torch.complex64, device=dev)
+    truths = bench.synth_signals(x, 5, dev)
+    for i in range(2):
+        seed = bench.case_seed(bench.N_SIG, bench.K, "exact", 0, 5 + i)
+        case = generate_test_case(bench.N_SIG, bench.K, "exact", seed=seed)
+        assert sorted(case.truth.entries) == truths[i][0].tolist()
+        want = case.signal.astype(np.complex64)
+        got = x[i].cpu().numpy()
+        assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
