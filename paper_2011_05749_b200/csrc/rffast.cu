@@ -95,6 +95,13 @@ __device__ __forceinline__ double stride_estimate(const cd* y, int m, const doub
   return est;
 }
 
+// f mod b for 0 <= f: 32-bit when both fit (the 64-bit remainder is a library call,
+// most of noisy_harvest_kernel's stall samples at config 3')
+__device__ __forceinline__ int64_t mod_nonneg(int64_t f, int64_t b) {
+  if (((uint64_t)f | (uint64_t)b) < (1ull << 32)) return (int64_t)((uint32_t)f % (uint32_t)b);
+  return f % b;
+}
+
 __device__ __forceinline__ int noisy_cycle(const NoisyPlan& P, int g) {
   int c = 0;
   while (g >= P.base[c + 1]) ++c;
@@ -635,7 +642,7 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
         take = 1;
         const int c = noisy_cycle(P, g);
         for (int c2 = 0; c2 < c; ++c2) {
-          const int g2 = P.base[c2] + (int)(f % P.b[c2]);
+          const int g2 = P.base[c2] + (int)mod_nonneg(f, P.b[c2]);
           if (state[so + g2] == AFFT_SINGLE_TON && node_f0[so + g2] == f) {
             take = 0;
             break;
@@ -666,13 +673,14 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
   const int F = P.ncycles;
   for (int e = tid; e < nf * F; e += nt) {
     const int i = e / F, c = e - i * F;
-    atomicAdd(&flag[P.base[c] + (int)(node_f0[so + found_g[i]] % P.b[c])], 1);
+    atomicAdd(&flag[P.base[c] + (int)mod_nonneg(node_f0[so + found_g[i]], P.b[c])], 1);
   }
   __syncthreads();
   block_exclusive_scan(flag, N, warp_tmp, &carry);
   for (int e = tid; e < nf * F; e += nt) {
     const int i = e / F, c = e - i * F;
-    const int slot = atomicAdd(&flag[P.base[c] + (int)(node_f0[so + found_g[i]] % P.b[c])], 1);
+    const int slot =
+        atomicAdd(&flag[P.base[c] + (int)mod_nonneg(node_f0[so + found_g[i]], P.b[c])], 1);
     found_res[slot] = i;
   }
   __syncthreads();
