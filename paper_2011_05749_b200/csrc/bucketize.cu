@@ -9,6 +9,8 @@
 // reciprocal — to a caller-strided output, so the same kernel produces the
 // FilteredSpectrum layout [s][t][i] and the peeling-node layout [s][g][t].
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -129,6 +131,33 @@ __global__ void twiddle_tables_kernel(int64_t b, cd* __restrict__ tlo, int nlo,
     sincospi(-2.0 * (double)k / (double)b, &sn, &cs);
     thi[i] = cd{cs, sn};
   }
+}
+
+// Twiddle tables of size b (w_b^m split as w_b^(m & 4095) * w_b^(m >> 12 << 12)),
+// built once per (device, b) and kept: the K2' passes of DSFFT's layers and config
+// 3''s cycles reuse the same few sizes on every call.  Built on the caller's stream,
+// which is then synchronised once so that any stream may read them afterwards.
+static const cd* twiddle_tables_for(int dev, int64_t b, int nlo, int nhi, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, cd*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, b});
+  if (it != cache.end()) return it->second;
+  cd* t = nullptr;
+  if (cudaMalloc(&t, (size_t)(nlo + nhi) * sizeof(cd)) != cudaSuccess) {
+    set_error("twiddle tables: cudaMalloc failed");
+    return nullptr;
+  }
+  twiddle_tables_kernel<<<(unsigned)((std::max(nlo, nhi) + 255) / 256), 256, 0, stream>>>(
+      b, t, nlo, t + nlo, nhi);
+  const cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    cuda_status(e, "twiddle tables");
+    cudaFree(t);
+    return nullptr;
+  }
+  cache.emplace(std::make_pair(dev, b), t);
+  return t;
 }
 
 __device__ __forceinline__ cd tw_b(const cd* tlo, const cd* thi, int64_t m) {
@@ -544,20 +573,37 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
   const size_t seqs = (size_t)batch * nshift;
   const size_t buf = (seqs * b * 16 + 255) / 256 * 256;
   const size_t nbufs = P >= 3 ? 2 : (P == 2 ? 1 : 0);
+  // cached tables, except under stream capture (no allocation or synchronisation
+  // allowed there): then they are built into the scratch as part of the work
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  const bool own_tables = cap != cudaStreamCaptureStatusNone;
+  const size_t tbytes = own_tables ? (size_t)(nlo + nhi) * 16 : 0;
   char* scratch = nullptr;
-  cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch),
-                                nbufs * buf + (size_t)(nlo + nhi) * 16, stream);
+  cudaError_t e = nbufs * buf + tbytes
+                      ? scratch_alloc(reinterpret_cast<void**>(&scratch), nbufs * buf + tbytes,
+                                      stream)
+                      : cudaSuccess;
   if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(large-b DFT)");
   cd* bufs[2] = {reinterpret_cast<cd*>(scratch), reinterpret_cast<cd*>(scratch + buf)};
-  cd* tlo = reinterpret_cast<cd*>(scratch + nbufs * buf);
-  cd* thi = tlo + nlo;
-  q.tlo = tlo;
-  q.thi = thi;
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  twiddle_tables_kernel<<<(unsigned)((std::max(nlo, nhi) + 255) / 256), 256, 0, stream>>>(
-      b, tlo, nlo, thi, nhi);
+  const cd* tables;
+  if (own_tables) {
+    cd* t = reinterpret_cast<cd*>(scratch + nbufs * buf);
+    twiddle_tables_kernel<<<(unsigned)((std::max(nlo, nhi) + 255) / 256), 256, 0, stream>>>(
+        b, t, nlo, t + nlo, nhi);
+    tables = t;
+  } else {
+    tables = twiddle_tables_for(dev, b, nlo, nhi, stream);
+  }
+  if (!tables) {
+    if (scratch) scratch_free(scratch, stream);
+    return AFFT_ECUDA;
+  }
+  q.tlo = tables;
+  q.thi = tables + nlo;
   int64_t Ns = 1;
   int rc = AFFT_OK;
   for (int s = 0; s < P && !rc; ++s) {
@@ -614,7 +660,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     }
     Ns *= R;
   }
-  scratch_free(scratch, stream);
+  if (scratch) scratch_free(scratch, stream);
   if (!rc) AFFT_CHECK_LAUNCH("large-b DFT pass");
   return rc;
 }

@@ -398,10 +398,8 @@ struct Dsfft {
       RC(spectrum());
       // alias_active's sort capacity; AFFT_ACTIVE_SORT_CAP lowers it (tests force the
       // fallback path with it)
-      static const int64_t cap_env = [] {
-        const char* v = std::getenv("AFFT_ACTIVE_SORT_CAP");
-        return v ? std::max<int64_t>(1, std::atoll(v)) : int64_t(16384);
-      }();
+      const char* cap_var = std::getenv("AFFT_ACTIVE_SORT_CAP");  // read per layer (tests)
+      const int64_t cap_env = cap_var ? std::max<int64_t>(1, std::atoll(cap_var)) : 16384;
       const int cap = (int)std::min<int64_t>(b, std::min<int64_t>(16384, cap_env));
       RC(out.active.alloc((size_t)cap * 8, st, "dsfft active"));
       DBuf cnt;

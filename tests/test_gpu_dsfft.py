@@ -87,17 +87,12 @@ def test_config4_dsfft_vs_reference(path):
     _check(case, trace, out)
 
 
-def test_dsfft_goldens_active_fallback():
+def test_dsfft_goldens_active_fallback(golden_dsfft, monkeypatch):
     """Deep full layers take their active set in one pass over the resident spectrum
     with a one-CTA sort (dsfft.cu: alias_active); above the sort's capacity the loop
     falls back to values + count / scan / write.  Forcing a capacity of 1 routes every
     deep layer through the fallback: the goldens must not change."""
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, AFFT_ACTIVE_SORT_CAP="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
-                        "tests/test_gpu_dsfft.py::test_dsfft_goldens"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    monkeypatch.setenv("AFFT_ACTIVE_SORT_CAP", "1")
+    for case in golden_dsfft["cases"]:
+        trace, out, ledger = _run(case)
+        _check(case, trace, out, ledger)
