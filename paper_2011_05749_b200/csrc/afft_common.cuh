@@ -22,6 +22,10 @@ void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
 // stream-ordered scratch from the library's memory pool (kept across calls)
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
+// Per-thread arena for scratch_alloc on `stream` between arena_begin and arena_end
+// (capi.cu); the caller must synchronise the stream before arena_end.
+cudaError_t arena_begin(size_t bytes, cudaStream_t stream);
+void arena_end();
 // Pinned host staging from a process-wide pool: buffers are never freed (cudaFreeHost
 // synchronises the whole device, which a thread-local buffer's destructor did at every
 // worker-thread exit), and are reused across threads.  pinned_release returns one.

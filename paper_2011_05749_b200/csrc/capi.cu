@@ -2,6 +2,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <vector>
 
 #include "afft_common.cuh"
 
@@ -88,13 +89,97 @@ cudaError_t ensure_smem(const void* func, size_t bytes) {
   return e;
 }
 
-cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
+// Per-thread scratch arena for one long call on one stream (the DSFFT layer loop):
+// a stack of blocks carved from one kept device buffer, so that the ~2 pool calls per
+// temporary (hundreds per decode) become pointer arithmetic.  Blocks are freed in any
+// order; the stack top drops past every freed block at the top.  Requests on another
+// stream, or that do not fit, go to the pool as usual.  Stream order makes reuse safe:
+// every block is used on the arena's stream only, and the caller synchronises that
+// stream before the arena is released (afft_dsfft ends with a read-back).
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, top = 0;
+  cudaStream_t st = nullptr;
+  bool active = false;
+  std::vector<size_t> start, end;
+  std::vector<char> freed;
+};
+static thread_local Arena g_arena;
+
+static cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t stream) {
   cudaMemPool_t pool = library_pool();
   if (!pool) return cudaMallocAsync(p, bytes, stream);
   return cudaMallocFromPoolAsync(p, bytes, pool, stream);
 }
 
-cudaError_t scratch_free(void* p, cudaStream_t stream) { return cudaFreeAsync(p, stream); }
+cudaError_t arena_begin(size_t bytes, cudaStream_t stream) {
+  Arena& A = g_arena;
+  if (A.active) return cudaSuccess;  // nested: the outer scope owns it
+  if (A.cap < bytes) {
+    if (A.base) cudaFreeAsync(A.base, stream);
+    A.base = nullptr;
+    A.cap = 0;
+    void* p = nullptr;
+    const cudaError_t e = pool_alloc(&p, bytes, stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cudaSuccess;  // no arena: every request goes to the pool
+    }
+    A.base = static_cast<char*>(p);
+    A.cap = bytes;
+  }
+  A.st = stream;
+  A.top = 0;
+  A.active = true;
+  return cudaSuccess;
+}
+
+void arena_end() {
+  Arena& A = g_arena;
+  A.active = false;
+  A.top = 0;
+  A.start.clear();
+  A.end.clear();
+  A.freed.clear();
+}
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
+  Arena& A = g_arena;
+  if (A.active && A.base && stream == A.st) {
+    const size_t off = (A.top + 255) & ~size_t(255);
+    if (off + bytes <= A.cap) {
+      A.start.push_back(off);
+      A.end.push_back(off + bytes);
+      A.freed.push_back(0);
+      A.top = off + bytes;
+      *p = A.base + off;
+      return cudaSuccess;
+    }
+  }
+  return pool_alloc(p, bytes, stream);
+}
+
+cudaError_t scratch_free(void* p, cudaStream_t stream) {
+  Arena& A = g_arena;
+  char* c = static_cast<char*>(p);
+  if (A.base && c >= A.base && c < A.base + A.cap) {
+    const size_t off = (size_t)(c - A.base);
+    for (size_t i = A.start.size(); i-- > 0;)
+      if (A.start[i] == off && !A.freed[i]) {
+        A.freed[i] = 1;
+        break;
+      }
+    while (!A.start.empty() && A.freed.back()) {
+      A.top = A.start.back();
+      A.start.pop_back();
+      A.end.pop_back();
+      A.freed.pop_back();
+    }
+    if (A.start.empty()) A.top = 0;
+    return cudaSuccess;
+  }
+  return cudaFreeAsync(p, stream);
+}
 
 }  // namespace afft
 

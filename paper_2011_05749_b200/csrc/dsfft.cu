@@ -350,11 +350,11 @@ constexpr int kActiveSortThreads = 1024, kActiveSortItems = 16;
 constexpr int kActiveSortCap = kActiveSortThreads * kActiveSortItems;
 using ActiveSort = cub::BlockRadixSort<uint32_t, kActiveSortThreads, kActiveSortItems>;
 __global__ void __launch_bounds__(kActiveSortThreads) sort_active_kernel(
-    int64_t* __restrict__ list, const int32_t* __restrict__ count, int end_bit) {
+    int64_t* __restrict__ list, const int32_t* __restrict__ count, int cap, int end_bit) {
   extern __shared__ __align__(16) unsigned char sort_smem[];
   auto& temp = *reinterpret_cast<typename ActiveSort::TempStorage*>(sort_smem);
   const int m = *count;
-  if (m <= 1 || m > kActiveSortCap) return;
+  if (m <= 1 || m > cap || m > kActiveSortCap) return;  // over capacity: the list is partial
   uint32_t keys[kActiveSortItems];
 #pragma unroll
   for (int k = 0; k < kActiveSortItems; ++k) {
@@ -397,7 +397,7 @@ int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(sort_active)");
   int end_bit = 1;
   while ((int64_t(1) << end_bit) < b) ++end_bit;
-  sort_active_kernel<<<1, kActiveSortThreads, smem, st>>>(out, count, end_bit);
+  sort_active_kernel<<<1, kActiveSortThreads, smem, st>>>(out, count, cap, end_bit);
   AFFT_CHECK_LAUNCH("alias_active");
   return AFFT_OK;
 }

@@ -694,6 +694,16 @@ extern "C" int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k,
     return AFFT_EINVAL;
   }
   Entries E;
+  // the layer loop's temporaries come from a per-thread arena (capi.cu): the spectrum,
+  // two signal-sized DFT buffers and the per-layer blocks fit in 3 n complex128 + 64 MB
+  arena_begin((size_t)n * 48 + ((size_t)64 << 20), (cudaStream_t)stream);
+  struct ArenaGuard {
+    cudaStream_t st;
+    ~ArenaGuard() {  // an early error return may leave work queued on the arena
+      cudaStreamSynchronize(st);
+      arena_end();
+    }
+  } arena_guard{(cudaStream_t)stream};
   Dsfft D{x, dtype, n, k, *params, (cudaStream_t)stream, Tracer{trace, trace_capacity}};
   g_prof.wait_s = 0.0;
   g_prof.syncs = 0;
