@@ -137,6 +137,26 @@ __device__ __noinline__ int moment_coeffs_call(const la::c2* row, int a_m, int a
   return dt::moment_coeffs(M, a, out) ? 1 : 0;
 }
 
+// The moment coefficients of every bucket, one thread per bucket (oneshot.py:143-160):
+// ok[e] = 1 solved, 0 empty bucket, -1 non-finite (None).  Done by lane 0 of the
+// locate warp, the small SVD solve left 31 lanes idle for ~22% of that kernel's time.
+__global__ void dt2_coeffs_kernel(int64_t total, int R, int a_m, const double* __restrict__ meas,
+                                  const int32_t* __restrict__ counts, int a_cap,
+                                  la::c2* __restrict__ coeffs, int8_t* __restrict__ ok) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int a = counts[e];
+  if (a_cap > 0 && a > a_cap) a = a_cap;
+  if (a <= 0) {
+    ok[e] = 0;
+    return;
+  }
+  la::c2 c[dt::kMaxAm];
+  const int r = moment_coeffs_call(reinterpret_cast<const la::c2*>(meas) + e * R, a_m, a, c);
+  for (int k = 0; k < a; ++k) coeffs[e * dt::kMaxAm + k] = c[k];
+  ok[e] = r ? 1 : -1;
+}
+
 // w_L^j = exp(-2 pi i j / L), j < L: the grid-candidate roots shared by every bucket.
 __global__ void roots_kernel(int64_t L, la::c2* __restrict__ roots) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -153,32 +173,24 @@ constexpr int kDt2LocateThreads = 256;
 __global__ void __launch_bounds__(kDt2LocateThreads, 3) dt2_locate_warp_kernel(
     int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
     const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
-    int64_t b, int64_t n, const la::c2* __restrict__ rootsL, int64_t* __restrict__ cands,
-    int32_t* __restrict__ ncand) {
+    int64_t b, int64_t n, const la::c2* __restrict__ rootsL, const la::c2* __restrict__ coef_all,
+    const int8_t* __restrict__ coef_ok, int64_t* __restrict__ cands, int32_t* __restrict__ ncand) {
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (e >= total) return;
   int a = counts[e];
   if (a_cap > 0 && a > a_cap) a = a_cap;
-  if (a <= 0) {
-    if (lane == 0) ncand[e] = 0;
+  const int ok = coef_ok[e];  // dt2_coeffs_kernel
+  if (ok <= 0) {
+    if (lane == 0) ncand[e] = ok;  // 0 empty, -1 None
     return;
   }
   const int64_t s = e / nrows;
   const int64_t bucket = bucket_ids ? bucket_ids[e] : e - s * nrows;
   la::c2 coeffs[dt::kMaxAm];
-  int ok = 0;
-  if (lane == 0) ok = moment_coeffs_call(reinterpret_cast<const la::c2*>(meas) + e * R, a_m, a,
-                                         coeffs);
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (!ok) {
-    if (lane == 0) ncand[e] = -1;
-    return;
-  }
-  for (int k = 0; k < a; ++k) {
-    coeffs[k].re = __shfl_sync(0xffffffffu, coeffs[k].re, 0);
-    coeffs[k].im = __shfl_sync(0xffffffffu, coeffs[k].im, 0);
-  }
+#pragma unroll
+  for (int k = 0; k < dt::kMaxAm; ++k)
+    if (k < a) coeffs[k] = coef_all[e * dt::kMaxAm + k];
   const int64_t step = n / b;
   const int take = (int64_t)a < step ? a : (int)step;
   constexpr int64_t kNone = INT64_MAX;
@@ -513,18 +525,27 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
   int64_t* cands = nullptr;
   const int64_t L = n / b;
   const size_t cbytes = ((size_t)total * (dt::kMaxAm * 8 + 4) + 255) / 256 * 256;
-  const size_t rbytes = variant == dt::VAR_DT2 ? (size_t)L * 16 : 0;
+  // dt2: the grid roots, then the per-bucket coefficients and their status
+  const size_t kbytes = ((size_t)total * dt::kMaxAm * 16 + 255) / 256 * 256;
+  const size_t rbytes = variant == dt::VAR_DT2 ? ((size_t)L * 16 + 255) / 256 * 256 + kbytes +
+                                                     (size_t)total
+                                               : 0;
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands), cbytes + rbytes, st);
   if (e != cudaSuccess) return cuda_status(e, "scratch (dt candidates)");
   int32_t* ncand = reinterpret_cast<int32_t*>(cands + total * dt::kMaxAm);
   if (variant == dt::VAR_DT2) {
-    la::c2* roots = reinterpret_cast<la::c2*>(reinterpret_cast<char*>(cands) + cbytes);
+    char* base = reinterpret_cast<char*>(cands) + cbytes;
+    la::c2* roots = reinterpret_cast<la::c2*>(base);
+    la::c2* coef = reinterpret_cast<la::c2*>(base + ((size_t)L * 16 + 255) / 256 * 256);
+    int8_t* cok = reinterpret_cast<int8_t*>(reinterpret_cast<char*>(coef) + kbytes);
     roots_kernel<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(L, roots);
+    dt2_coeffs_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(
+        total, 3 * a_m + p, a_m, rows, counts, a_cap, coef, cok);
     const int64_t threads = total * 32;
     dt2_locate_warp_kernel<<<(unsigned)((threads + kDt2LocateThreads - 1) / kDt2LocateThreads),
                              kDt2LocateThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
                                                          counts, bucket_ids, a_cap, b, n, roots,
-                                                         cands, ncand);
+                                                         coef, cok, cands, ncand);
   } else {
     dt_locate_rows_kernel<<<(unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads),
                             kDtSolveThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
