@@ -152,7 +152,7 @@ __device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int la
 // least-squares problem the solution is unique, so this agrees with the SVD
 // form to rounding; when the R diagonal spans more than 1e7 (possible rank
 // deficiency, where numpy's eps cutoff could bite) the Jacobi form decides.
-__device__ inline double warp_refit_qr(WarpPursuit& S, int P, int cnt, int lane) {
+__device__ __noinline__ double warp_refit_qr(WarpPursuit& S, int P, int cnt, int lane) {
   c2 w[kCols];
 #pragma unroll
   for (int c = 0; c < kCols; ++c) w[c] = (c < cnt && lane < P) ? S.A[S.sup[c]][lane] : la::C(0.0);
