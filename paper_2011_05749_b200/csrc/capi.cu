@@ -90,21 +90,27 @@ cudaError_t ensure_smem(const void* func, size_t bytes) {
 }
 
 // Per-thread scratch arena for one long call on one stream (the DSFFT layer loop):
-// a stack of blocks carved from one kept device buffer, so that the ~2 pool calls per
+// a stack of blocks carved from one device buffer, so that the ~2 pool calls per
 // temporary (hundreds per decode) become pointer arithmetic.  Blocks are freed in any
 // order; the stack top drops past every freed block at the top.  Requests on another
 // stream, or that do not fit, go to the pool as usual.  Stream order makes reuse safe:
 // every block is used on the arena's stream only, and the caller synchronises that
-// stream before the arena is released (afft_dsfft ends with a read-back).
+// stream before the arena is released (afft_dsfft ends with a read-back).  The buffer
+// itself is borrowed from a process-wide free list per device for the duration of the
+// call and returned by arena_end, so no thread keeps device memory after its call and a
+// thread that moves to another device never reuses the first device's buffer.
 struct Arena {
   char* base = nullptr;
   size_t cap = 0, top = 0;
+  int dev = -1;
   cudaStream_t st = nullptr;
   bool active = false;
   std::vector<size_t> start, end;
   std::vector<char> freed;
 };
 static thread_local Arena g_arena;
+static std::mutex g_arena_mu;
+static std::multimap<size_t, char*> g_arena_free[64];  // per device: capacity -> buffer
 
 static cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t stream) {
   cudaMemPool_t pool = library_pool();
@@ -115,19 +121,38 @@ static cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t stream) {
 cudaError_t arena_begin(size_t bytes, cudaStream_t stream) {
   Arena& A = g_arena;
   if (A.active) return cudaSuccess;  // nested: the outer scope owns it
-  if (A.cap < bytes) {
-    if (A.base) cudaFreeAsync(A.base, stream);
-    A.base = nullptr;
-    A.cap = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return cudaSuccess;  // no arena: every request goes to the pool
+  }
+  {
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    auto& fl = g_arena_free[dev];
+    auto it = fl.lower_bound(bytes);
+    if (it != fl.end()) {
+      A.base = it->second;
+      A.cap = it->first;
+      fl.erase(it);
+    } else if (!fl.empty()) {
+      // every cached buffer is too small: drop the largest (idle: its last user
+      // synchronised its stream before releasing it) to make room for a bigger one
+      auto last = std::prev(fl.end());
+      cudaFreeAsync(last->second, stream);
+      fl.erase(last);
+    }
+  }
+  if (!A.base) {
     void* p = nullptr;
     const cudaError_t e = pool_alloc(&p, bytes, stream);
     if (e != cudaSuccess) {
       cudaGetLastError();
-      return cudaSuccess;  // no arena: every request goes to the pool
+      return cudaSuccess;
     }
     A.base = static_cast<char*>(p);
     A.cap = bytes;
   }
+  A.dev = dev;
   A.st = stream;
   A.top = 0;
   A.active = true;
@@ -136,6 +161,13 @@ cudaError_t arena_begin(size_t bytes, cudaStream_t stream) {
 
 void arena_end() {
   Arena& A = g_arena;
+  if (A.base) {
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    g_arena_free[A.dev].emplace(A.cap, A.base);
+  }
+  A.base = nullptr;
+  A.cap = 0;
+  A.dev = -1;
   A.active = false;
   A.top = 0;
   A.start.clear();

@@ -661,6 +661,7 @@ static int num_sms() {
 
 // Auxiliary stream and events for the pipelined FFAST path, one set per device.
 struct AuxStreams {
+  std::mutex enqueue;  // held for a whole fork/chunk/join sequence (shared events)
   cudaStream_t aux = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t chunk[64] = {};
@@ -684,6 +685,15 @@ static int aux_streams(AuxStreams** out) {
   }
   *out = &a;
   return AFFT_OK;
+}
+
+// Split-stream mode (4) runs up to kMaxParts CTAs per signal; its partial sums and
+// per-signal tickets share the pre-pass partials block, so that block holds
+// batch * max(nparts, kMaxParts) doubles plus batch tickets.
+constexpr int kMaxParts = 16;
+
+static size_t fused_partials_bytes(int64_t batch, int nparts) {
+  return al256((size_t)batch * std::max(nparts, kMaxParts) * 8 + (size_t)batch * 4);
 }
 
 struct FfastWs {
@@ -815,7 +825,7 @@ extern "C" size_t afft_ffast_workspace_size(int64_t n, int dtype, int64_t batch,
   if (setup_graph(&G, n, factors, ncycles, (int)std::max<int64_t>(nodes, 1))) return 0;
   size_t total = 0, off = 0;
   if (fused_smem(G, true, &total, &off))  // fused path: partials + eps of the norm pre-pass
-    return al256((size_t)batch * afft_sumsq_parts(n, dtype) * 8) + al256((size_t)batch * 8);
+    return fused_partials_bytes(batch, afft_sumsq_parts(n, dtype)) + al256((size_t)batch * 8);
   const size_t bytes = peel_layout(G.nodes, ncycles, G.hmask + 1, false).total;
   return ffast_ws(n, dtype, batch, nodes, bytes > kSmemLimit ? bytes : 0).total;
 }
@@ -902,14 +912,14 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     double* partials = nullptr;
     double* epsbuf = nullptr;
     if (mode) {
-      const size_t need = al256((size_t)batch * nparts * 8) + al256((size_t)batch * 8);
+      const size_t pbytes = fused_partials_bytes(batch, nparts);
+      const size_t need = pbytes + al256((size_t)batch * 8);
       if (!workspace || workspace_bytes < need) {
         set_error("afft_ffast: workspace of %zu bytes needed, %zu given", need, workspace_bytes);
         return AFFT_ENOMEM;
       }
       partials = reinterpret_cast<double*>(workspace);
-      epsbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) +
-                                         al256((size_t)batch * nparts * 8));
+      epsbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(workspace) + pbytes);
     }
     {
       cudaError_t e = ensure_smem((const void*)ffast_fused_kernel, (int)smem);
@@ -920,6 +930,9 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     if (mode == 2) {
       AuxStreams* A = nullptr;
       if ((rc = aux_streams(&A))) return rc;
+      // the aux stream and its events are shared by every caller on this device: no
+      // other thread may re-record an event between our record and the matching wait
+      std::lock_guard<std::mutex> lock(A->enqueue);
       const int64_t esz = dtype == AFFT_C64 ? 8 : 16;
       int64_t nchunks = std::min<int64_t>(32, std::max<int64_t>(2, batch / 256));
       const int64_t csz = (batch + nchunks - 1) / nchunks;
@@ -973,7 +986,7 @@ extern "C" int afft_ffast(const void* x, int dtype, int64_t n, int64_t batch, in
     if (mode == 4) {
       const char* pe = getenv("AFFT_FFAST_PARTS");
       const int64_t want = (21LL * sms + batch / 2) / std::max<int64_t>(batch, 1);
-      const int parts = pe ? std::max(1, std::min(16, atoi(pe)))
+      const int parts = pe ? std::max(1, std::min(kMaxParts, atoi(pe)))
                            : (int)std::max<int64_t>(2, std::min<int64_t>(12, want));
       double* part_sums = partials;                               // batch * parts
       unsigned* tickets = reinterpret_cast<unsigned*>(part_sums + batch * parts);  // batch

@@ -52,6 +52,38 @@ def test_misaligned_complex64_rows():
             assert list(res.full_spectrum(i).entries) == list(o["recovered"])
 
 
+@pytest.mark.parametrize("parts", ["", "12", "16"])
+def test_split_streams_small_norm_parts(parts):
+    """Mode 4 with fewer norm-pass parts than CTAs per signal (c128 n = 32,760 gives
+    nparts = 8 while mode 4 runs up to 12, or 16 by override): its partial sums and
+    tickets must stay inside the workspace afft_ffast_workspace_size reports.  The
+    workspace is followed by a guard band that must come back untouched."""
+    import os
+
+    from paper_2011_05749_b200 import _lib, ffast_batch
+    from paper_2011_05749_b200.batch import ffast_workspace_bytes
+
+    n, k, f, batch = 32760, 8, [13, 35, 72], 64
+    lib = _lib.load()
+    assert 2 <= int(lib.afft_sumsq_parts(n, _lib.AFFT_C128)) <= 12
+    xs = _signals(n, k, batch, seed0=40)
+    need = ffast_workspace_bytes(n, _lib.AFFT_C128, batch, f)
+    buf = torch.full((need + 4096,), 0xA5, dtype=torch.uint8, device="cuda")
+    os.environ["AFFT_FFAST_MODE"] = "4"
+    if parts:
+        os.environ["AFFT_FFAST_PARTS"] = parts
+    try:
+        res = ffast_batch(torch.from_numpy(xs).cuda(), k, f, workspace=buf[:need])
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("AFFT_FFAST_MODE", None)
+        os.environ.pop("AFFT_FFAST_PARTS", None)
+    assert bool((buf[need:] == 0xA5).all()), "mode 4 wrote past its workspace"
+    for i in range(batch):
+        _, o = of.ffast(xs[i], k, f)
+        assert list(res.full_spectrum(i).entries) == list(o["recovered"])
+
+
 def test_empty_and_k0():
     from paper_2011_05749_b200 import ffast, ffast_batch
 
