@@ -840,7 +840,7 @@ def run_configs(dev, args):
     seeds = [case_seed(n, k, 20.0, 0, i) for i in range(S)]
     plans = [plan_cycles(n, k, "noisy", seed=s) for s in seeds]
     for name, factors in (("c3", [511, 512, 513]), ("c3auto", list(plans[0][0].factors))):
-        searches = plans[0][1]  # one search plan (signal 0's anchors) for the batch
+        searches = [p[1] for p in plans]  # each signal's own anchors (peeling.py:163-164)
         res = rffast_batch(x, k, factors, searches)
         ms = _timed(lambda: rffast_batch(x, k, factors, searches), reps)
         cnt = res.count.cpu().numpy()

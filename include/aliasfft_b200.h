@@ -232,9 +232,12 @@ int afft_classify_noisy(const double* residual, const int64_t* index, int64_t co
 /*
  * peel_decode, noisy mode (peeling.py:270-313 with classify_noisy 253-267) over a
  * batch of graphs in node layout residual[s][g][c*m]: rounds of
- * prep -> exhaustive search -> fit -> harvest/subtract on the device; the host
- * only reads one counter per round to stop.  t0/t1 [batch] per-signal gates.
- * State/f0/val/rec_* as in afft_peel_exact.  Synchronises.
+ * prep -> exhaustive search -> fit -> harvest/subtract on the device, the round loop
+ * itself a CUDA-graph WHILE node whose condition the last kernel of each round sets
+ * (no host round-trip; stream-ordered).  t0/t1 [batch] per-signal gates.
+ * State/f0/val/rec_* as in afft_peel_exact.  The sharded variant (one signal's search
+ * split over ranks) exchanges partials through the host callback once per round and
+ * synchronises.
  */
 int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors /* host */, int32_t ncycles,
                     const int64_t* shifts /* host */, int32_t nshift, int32_t c, int32_t m,
@@ -243,6 +246,28 @@ int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors /* host */,
                     int32_t max_rounds, int64_t* rec_pos, double* rec_val, int32_t rec_cap,
                     int32_t* rec_count, int32_t* rounds, int32_t* unresolved, void* workspace,
                     size_t workspace_bytes, void* stream);
+
+/*
+ * r_ffast (peeling.py:361-386) over a batch, one stream-ordered enqueue: build_graph
+ * at each signal's own search shifts (SearchPlan.shifts = anchors[j] + 2^j t,
+ * peeling.py:60-62; anchors [batch][c] host, row stride anchor_stride, 0 = one set for
+ * every signal) -> node energies -> robust_thresholds (peeling.py:335-358) -> noisy
+ * peel_decode with max_rounds (0: k + 4, peeling.py:384) -> truncate_spectrum.
+ * weights (host, m - 1) = kay_weights(m).  Outputs (device): out_* [batch][k]
+ * truncated, all_* [batch][sum factors] the pre-truncation spectrum in insertion
+ * order, rounds / unresolved / t0 / t1 [batch].  Workspace: afft_rffast_workspace_size.
+ * Replaces the reference's per-signal r_ffast call (peeling.py:361) and its
+ * build_graph / noisy_thresholds / peel_decode sequence.
+ */
+size_t afft_rffast_workspace_size(int64_t n, int64_t batch, const int64_t* factors /* host */,
+                                  int32_t ncycles, int32_t c, int32_t m);
+int afft_rffast(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                const int64_t* factors /* host */, int32_t ncycles,
+                const int64_t* anchors /* host */, int64_t anchor_stride, int32_t c, int32_t m,
+                const double* weights /* host */, int32_t k, int32_t max_rounds, int64_t* out_pos,
+                double* out_val, int32_t* out_count, int64_t* all_pos, double* all_val,
+                int32_t* all_count, int32_t* rounds, int32_t* unresolved, double* t0, double* t1,
+                void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ smallnum */
 /*

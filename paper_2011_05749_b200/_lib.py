@@ -69,6 +69,10 @@ SIGNATURES = {
     "afft_peel_noisy_sharded": (
         _INT, [_I64, _I64, _P, _I32, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _I32, _P,
                _P, _I32, _P, _P, _P, _P, _SZ, _P, _P]),
+    "afft_rffast_workspace_size": (_SZ, [_I64, _I64, _P, _I32, _I32, _I32]),
+    "afft_rffast": (
+        _INT, [_P, _INT, _I64, _I64, _I64, _P, _I32, _P, _I64, _I32, _I32, _P, _I32, _I32, _P, _P,
+               _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "afft_small_la": (_INT, [_I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P]),
     "afft_bucketize_table": (_INT, [_P, _INT, _I64, _I64, _I64, _I64, _P, _I32, _P, _I64, _I64,
                                     _I64, _P]),

@@ -34,6 +34,10 @@ void* pinned_acquire(size_t bytes, size_t* capacity);
 int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64_t* out, int cap,
                  int32_t* count, cudaStream_t st);
 void pinned_release(void* p, size_t capacity);
+// bucketize.cu: build_graph with per-signal raw shifts (device [batch][nshift]).
+int build_graph_table(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                      const int64_t* factors, int32_t ncycles, const int64_t* shift_table,
+                      int32_t nshift, double* nodes, cudaStream_t stream);
 cudaError_t scratch_free(void* p, cudaStream_t stream);
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (never lowers it:
 // the attribute is process-wide, so concurrent callers on other streams/threads that

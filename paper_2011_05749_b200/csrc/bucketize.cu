@@ -791,6 +791,27 @@ extern "C" int afft_build_graph(const void* x, int dtype, int64_t n, int64_t bat
                            total * nshift, 1, nshift, (cudaStream_t)stream);
 }
 
+namespace afft {
+// build_graph (peeling.py:169-178) with per-signal shifts: shift_table is a device
+// [batch][nshift] array of raw shifts (reduced on the device).
+int build_graph_table(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                      const int64_t* factors, int32_t ncycles, const int64_t* shift_table,
+                      int32_t nshift, double* nodes, cudaStream_t stream) {
+  if (ncycles < 1 || ncycles > AFFT_MAX_CYCLES || !factors) {
+    set_error("number of cycles %d outside 1..%d", ncycles, AFFT_MAX_CYCLES);
+    return AFFT_EUNSUPPORTED;
+  }
+  int64_t offs[AFFT_MAX_CYCLES];
+  int64_t total = 0;
+  for (int c = 0; c < ncycles; ++c) {
+    offs[c] = total * nshift;
+    total += factors[c];
+  }
+  return launch_gather_dft(x, dtype, n, batch, ld, factors, ncycles, offs, nullptr, nshift, nodes,
+                           total * nshift, 1, nshift, stream, shift_table);
+}
+}  // namespace afft
+
 extern "C" int afft_bucketize_table(const void* x, int dtype, int64_t n, int64_t batch,
                                     int64_t ld, int64_t b, const int64_t* shift_table,
                                     int32_t nshift, double* out, int64_t out_signal_stride,

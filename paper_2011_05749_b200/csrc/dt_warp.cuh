@@ -10,6 +10,10 @@
 //
 // Same algorithm and tie rules as dt::estimate_values / la::lstsq; only the
 // summation order of the row reductions differs (ulp-level).
+//
+// Group width W: 32 lanes per bucket, or 16 when p <= 16 (BASELINE's p = 15): two
+// buckets share a warp, every row reduction is one butterfly level shorter, and the
+// two halves run independently (their shuffles and syncs name only their own lanes).
 #pragma once
 
 #include "oneshot_core.cuh"
@@ -20,10 +24,11 @@ namespace dtw {
 using la::c2;
 constexpr int kCols = 2 * dt::kMaxAm;  // merged support <= 2 * want <= 8
 
+template <int W>
 struct WarpPursuit {
-  c2 A[dt::kMaxFreqs][32];  // atom k, row i
-  c2 y[32];
-  c2 r[32];
+  c2 A[dt::kMaxFreqs][W];  // atom k, row i
+  c2 y[W];
+  c2 r[W];
   c2 V[kCols][kCols];       // V[row j][col c]
   c2 x[kCols];              // refit solution
   c2 best_coef[dt::kMaxAm];
@@ -40,23 +45,33 @@ struct WarpPursuit {
   int F;
 };
 
+// the calling group's lane mask (its W lanes of the warp)
+template <int W>
+__device__ __forceinline__ unsigned gmask() {
+  return W == 32 ? 0xffffffffu : ((0xffffffffu >> (32 - W)) << (threadIdx.x & (32 - W)));
+}
+
+template <int W>
 __device__ __forceinline__ double wsum(double v) {
+  const unsigned m = gmask<W>();
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
   return v;
 }
 
 // ||v|| over rows < P as vnorm does (real and imaginary squares summed apart).
+template <int W>
 __device__ __forceinline__ double warp_vnorm(c2 v, int P, int lane) {
   const bool on = lane < P;
-  const double sr = wsum(on ? v.re * v.re : 0.0);
-  const double si = wsum(on ? v.im * v.im : 0.0);
+  const double sr = wsum<W>(on ? v.re * v.re : 0.0);
+  const double si = wsum<W>(on ? v.im * v.im : 0.0);
   return sqrt(sr + si);
 }
 
 // refit (oneshot.py:229-232): x = lstsq(A[:, sup], y) with numpy's cutoff; returns
 // ||y - A_s x||.  S.sup[0..cnt) are atom indices; the solution lands in S.x.
-__device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int lane) {
+template <int W>
+__device__ __noinline__ double warp_refit(WarpPursuit<W>& S, int P, int cnt, int lane) {
   c2 w[kCols], v[kCols];
 #pragma unroll
   for (int c = 0; c < kCols; ++c) {
@@ -71,10 +86,10 @@ __device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int la
 #pragma unroll
       for (int q = p + 1; q < kCols; ++q) {
         if (q >= cnt) continue;
-        const double alpha = wsum(la::abs2(w[p]));
-        const double beta = wsum(la::abs2(w[q]));
+        const double alpha = wsum<W>(la::abs2(w[p]));
+        const double beta = wsum<W>(la::abs2(w[q]));
         const c2 gl = la::cmulc(w[p], w[q]);
-        const c2 gamma = la::C(wsum(gl.re), wsum(gl.im));
+        const c2 gamma = la::C(wsum<W>(gl.re), wsum<W>(gl.im));
         const double g = la::cabs(gamma);
         if (g == 0.0 || g <= la::kEps * sqrt(alpha * beta)) continue;
         rotated = true;
@@ -101,16 +116,16 @@ __device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int la
 #pragma unroll
   for (int c = 0; c < kCols; ++c) {
     if (c >= cnt) break;
-    const double s2 = wsum(la::abs2(w[c]));
+    const double s2 = wsum<W>(la::abs2(w[c]));
     const c2 dl = la::cmulc(w[c], yl);
-    const c2 d = la::C(wsum(dl.re), wsum(dl.im));
+    const c2 d = la::C(wsum<W>(dl.re), wsum<W>(dl.im));
     if (lane == 0) {
       S.sig[c] = sqrt(s2);
       S.dot[c] = d;
     }
     if (lane < cnt) S.V[lane][c] = v[c];
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   if (lane == 0) {  // selection sort descending (svd_jacobi's swaps, on a permutation)
     for (int j = 0; j < cnt; ++j) S.ord[j] = j;
     for (int j = 0; j < cnt; ++j) {
@@ -127,7 +142,7 @@ __device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int la
       }
     }
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   if (lane < cnt) {  // x_j = sum_k V[j][k] (u_k^H y) / s_k, k descending, above the cutoff
     const double cutoff = la::kEps * (double)(P > cnt ? P : cnt) * S.sig[0];
     c2 xj = la::C(0.0);
@@ -139,11 +154,11 @@ __device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int la
     }
     S.x[lane] = xj;
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   c2 acc = la::C(0.0);
   if (lane < P)
     for (int c = 0; c < cnt; ++c) acc = la::add(acc, la::mul(S.A[S.sup[c]][lane], S.x[c]));
-  return warp_vnorm(la::sub(yl, acc), P, lane);
+  return warp_vnorm<W>(la::sub(yl, acc), P, lane);
 }
 
 // refit by Householder QR, lanes over rows: cnt reflector steps, each one norm
@@ -152,7 +167,8 @@ __device__ __noinline__ double warp_refit(WarpPursuit& S, int P, int cnt, int la
 // least-squares problem the solution is unique, so this agrees with the SVD
 // form to rounding; when the R diagonal spans more than 1e7 (possible rank
 // deficiency, where numpy's eps cutoff could bite) the Jacobi form decides.
-__device__ __noinline__ double warp_refit_qr(WarpPursuit& S, int P, int cnt, int lane) {
+template <int W>
+__device__ __noinline__ double warp_refit_qr(WarpPursuit<W>& S, int P, int cnt, int lane) {
   c2 w[kCols];
 #pragma unroll
   for (int c = 0; c < kCols; ++c) w[c] = (c < cnt && lane < P) ? S.A[S.sup[c]][lane] : la::C(0.0);
@@ -163,8 +179,9 @@ __device__ __noinline__ double warp_refit_qr(WarpPursuit& S, int P, int cnt, int
   for (int j = 0; j < kCols; ++j) {
     if (j >= cnt) break;
     const bool below = lane >= j && lane < P;
-    const double nx = sqrt(wsum(below ? la::abs2(w[j]) : 0.0));
-    const c2 x0 = la::C(__shfl_sync(0xffffffffu, w[j].re, j), __shfl_sync(0xffffffffu, w[j].im, j));
+    const double nx = sqrt(wsum<W>(below ? la::abs2(w[j]) : 0.0));
+    const c2 x0 = la::C(__shfl_sync(gmask<W>(), w[j].re, j, W),
+                        __shfl_sync(gmask<W>(), w[j].im, j, W));
     dmax = nx > dmax ? nx : dmax;
     dmin = nx < dmin ? nx : dmin;
     if (nx == 0.0) break;
@@ -177,24 +194,24 @@ __device__ __noinline__ double warp_refit_qr(WarpPursuit& S, int P, int cnt, int
     for (int k = j + 1; k < kCols; ++k) {
       if (k >= cnt) break;
       const c2 dl = la::cmulc(v, w[k]);
-      const c2 d = la::C(wsum(dl.re), wsum(dl.im));
+      const c2 d = la::C(wsum<W>(dl.re), wsum<W>(dl.im));
       w[k] = la::sub(w[k], la::mul(v, la::scale(d, inv)));
     }
     {
       const c2 dl = la::cmulc(v, qy);
-      const c2 d = la::C(wsum(dl.re), wsum(dl.im));
+      const c2 d = la::C(wsum<W>(dl.re), wsum<W>(dl.im));
       qy = la::sub(qy, la::mul(v, la::scale(d, inv)));
     }
     if (lane == j) w[j] = alpha;
   }
-  if (!(dmin > 1e-7 * dmax)) return warp_refit(S, P, cnt, lane);
+  if (!(dmin > 1e-7 * dmax)) return warp_refit<W>(S, P, cnt, lane);
   if (lane < cnt) {
 #pragma unroll
     for (int k = 0; k < kCols; ++k)
       if (k < cnt) S.V[lane][k] = w[k];
     S.dot[lane] = qy;
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   if (lane == 0) {  // back substitution R x = Q^H y
     for (int j = cnt - 1; j >= 0; --j) {
       c2 sacc = S.dot[j];
@@ -202,36 +219,38 @@ __device__ __noinline__ double warp_refit_qr(WarpPursuit& S, int P, int cnt, int
       S.x[j] = la::div(sacc, S.V[j][j]);
     }
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   c2 acc = la::C(0.0);
   if (lane < P)
     for (int c = 0; c < cnt; ++c) acc = la::add(acc, la::mul(S.A[S.sup[c]][lane], S.x[c]));
-  return warp_vnorm(la::sub(yl, acc), P, lane);
+  return warp_vnorm<W>(la::sub(yl, acc), P, lane);
 }
 
 // |A^H v| per atom (v in shared memory), lanes over atoms; then lane 0 picks the
 // `want` largest (stable) into out[].
-__device__ __forceinline__ void warp_top_corr(WarpPursuit& S, const c2* vec, int P, int want,
+template <int W>
+__device__ __forceinline__ void warp_top_corr(WarpPursuit<W>& S, const c2* vec, int P, int want,
                                               int* out, int lane) {
   if (lane < S.F) {
     c2 acc = la::C(0.0);
     for (int i = 0; i < P; ++i) acc = la::add(acc, la::cmulc(S.A[lane][i], vec[i]));
     S.corr[lane] = la::cabs(acc);
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   if (lane == 0) dt::top_desc(S.corr, S.F, want, out);
-  __syncwarp();
+  __syncwarp(gmask<W>());
 }
 
 // estimate_values (oneshot.py:203-257) for one bucket, called by all 32 lanes.
 // Returns the support size; lane 0 writes positions/values (stride 1).
-__device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_t* shifts, int P,
+template <int W>
+__device__ inline int warp_estimate(WarpPursuit<W>& S, const c2* rand, const int64_t* shifts, int P,
                                     const int64_t* cands, int nc, int64_t b, int64_t n,
                                     int64_t* out_pos, c2* out_val) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & (W - 1);
   const c2 yl = lane < P ? rand[lane] : la::C(0.0);
   S.y[lane] = yl;
-  const double ynorm = warp_vnorm(yl, P, lane);
+  const double ynorm = warp_vnorm<W>(yl, P, lane);
   if (nc == 0 || ynorm == 0.0) return 0;
   if (lane == 0) {
     int F = 0;
@@ -246,13 +265,13 @@ __device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_
     }
     S.F = F;
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   const int F = S.F;
   if (lane < P) {
     const int64_t sh = dt::pmod(shifts[lane], n);
     for (int k = 0; k < F; ++k) S.A[k][lane] = dt::unit_root_(sh * S.freqs[k] % n, n);
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   int want = nc;
   if (F < want) want = F;
   if (P < want) want = P;
@@ -263,7 +282,7 @@ __device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_
     S.best_sup[lane] = S.sup[lane];
     S.best_coef[lane] = S.x[lane];
   }
-  __syncwarp();
+  __syncwarp(gmask<W>());
   for (int it = 0; it < dt::kSpMaxIters; ++it) {
     if (best_res <= tol) break;
     c2 acc = la::C(0.0);
@@ -271,7 +290,7 @@ __device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_
       for (int c = 0; c < want; ++c)
         acc = la::add(acc, la::mul(S.A[S.best_sup[c]][lane], S.best_coef[c]));
     S.r[lane] = la::sub(yl, acc);
-    __syncwarp();
+    __syncwarp(gmask<W>());
     warp_top_corr(S, S.r, P, want, S.fresh, lane);
     int nm = 0;
     if (lane == 0) {  // merged = union1d(best_sup, fresh)
@@ -281,8 +300,8 @@ __device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_
       nm = dt::sort_unique(mg, nm);
       for (int i = 0; i < nm; ++i) S.sup[i] = (int)mg[i];
     }
-    nm = __shfl_sync(0xffffffffu, nm, 0);
-    __syncwarp();
+    nm = __shfl_sync(gmask<W>(), nm, 0, W);
+    __syncwarp(gmask<W>());
     warp_refit_qr(S, P, nm, lane);
     if (lane == 0) {  // keep the `want` largest |coef|, sorted by atom index
       for (int i = 0; i < nm; ++i) S.mag[i] = la::cabs(S.x[i]);
@@ -293,7 +312,7 @@ __device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_
       dt::sort_unique(pr, want);
       for (int i = 0; i < want; ++i) S.sup[i] = (int)pr[i];
     }
-    __syncwarp();
+    __syncwarp(gmask<W>());
     const double res = warp_refit_qr(S, P, want, lane);
     if (res >= best_res) break;
     best_res = res;
@@ -301,7 +320,7 @@ __device__ inline int warp_estimate(WarpPursuit& S, const c2* rand, const int64_
       S.best_sup[lane] = S.sup[lane];
       S.best_coef[lane] = S.x[lane];
     }
-    __syncwarp();
+    __syncwarp(gmask<W>());
   }
   if (lane < want) {
     out_pos[lane] = S.freqs[S.best_sup[lane]];

@@ -13,6 +13,7 @@
 //   truncate — entries in bucket order, top-k by (-|v|, f) (260-263).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "afft_common.cuh"
@@ -302,19 +303,21 @@ __global__ void __launch_bounds__(kDtSolveThreads) dt_locate_rows_kernel(
   ncand[e] = c;
 }
 
-// estimate_values for every row, one warp per row (dt_warp.cuh).  Row e belongs
-// to signal e / nrows, whose random shifts start at rshifts + signal * shift_stride.
-constexpr int kDtEstWarps = 1;
-
-__global__ void __launch_bounds__(kDtEstWarps * 32, 24) dt_estimate_warp_kernel(
+// estimate_values for every row, one group of W lanes per row (dt_warp.cuh): a full
+// warp, or half a warp when p <= 16.  Row e belongs to signal e / nrows, whose random
+// shifts start at rshifts + signal * shift_stride.  One warp per CTA.
+template <int W>
+__global__ void __launch_bounds__(32, W == 32 ? 24 : 16) dt_estimate_warp_kernel(
     int64_t total, int64_t nrows, int R, int a_m, int p, const double* __restrict__ meas,
     const int64_t* __restrict__ rshifts, int64_t shift_stride, const int64_t* __restrict__ cands,
     const int32_t* __restrict__ ncand, int64_t b, int64_t n, int out_stride,
     int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_cnt) {
-  __shared__ dtw::WarpPursuit pursuit[kDtEstWarps];
-  __shared__ int64_t cand_s[kDtEstWarps][dt::kMaxAm];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t e = (int64_t)blockIdx.x * kDtEstWarps + wid;
+  constexpr int G = 32 / W;  // rows per warp
+  __shared__ dtw::WarpPursuit<W> pursuit[G];
+  __shared__ int64_t cand_s[G][dt::kMaxAm];
+  const int g = threadIdx.x / W, lane = threadIdx.x & (W - 1);
+  const unsigned gm = dtw::gmask<W>();
+  const int64_t e = (int64_t)blockIdx.x * G + g;
   if (e >= total) return;
   int nc = 0;
   if (lane == 0) {
@@ -323,17 +326,17 @@ __global__ void __launch_bounds__(kDtEstWarps * 32, 24) dt_estimate_warp_kernel(
     int64_t c[dt::kMaxAm];
     for (int k = 0; k < nc; ++k) c[k] = cands[e * dt::kMaxAm + k];
     if (nc > 0) nc = dt::sort_unique(c, nc);
-    for (int k = 0; k < nc; ++k) cand_s[wid][k] = c[k];
+    for (int k = 0; k < nc; ++k) cand_s[g][k] = c[k];
   }
-  nc = __shfl_sync(0xffffffffu, nc, 0);
-  __syncwarp();
+  nc = __shfl_sync(gm, nc, 0, W);
+  __syncwarp(gm);
   int cnt = 0;
   if (nc > 0) {
     const int64_t s = e / nrows;
     const la::c2* row = reinterpret_cast<const la::c2*>(meas) + e * R;
-    cnt = dtw::warp_estimate(pursuit[wid], row + 3 * a_m, rshifts + s * shift_stride, p,
-                             cand_s[wid], nc, b, n, out_pos + e * out_stride,
-                             reinterpret_cast<la::c2*>(out_val) + e * out_stride);
+    cnt = dtw::warp_estimate<W>(pursuit[g], row + 3 * a_m, rshifts + s * shift_stride, p,
+                                cand_s[g], nc, b, n, out_pos + e * out_stride,
+                                reinterpret_cast<la::c2*>(out_val) + e * out_stride);
   }
   if (lane == 0) out_cnt[e] = cnt;
 }
@@ -552,10 +555,15 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
                                                       counts, bucket_ids, a_cap, variant, b, n,
                                                       cands, ncand);
   }
-  dt_estimate_warp_kernel<<<(unsigned)((total + kDtEstWarps - 1) / kDtEstWarps),
-                            kDtEstWarps * 32, 0, st>>>(total, nrows, 3 * a_m + p, a_m, p, rows,
-                                                       rand_shifts, p, cands, ncand, b, n, a_m,
-                                                       out_pos, out_val, out_cnt);
+  const char* wenv = getenv("AFFT_DT_EST_WIDTH");  // 32 forces the full-warp form
+  if (p <= 16 && !(wenv && atoi(wenv) == 32))
+    dt_estimate_warp_kernel<16><<<(unsigned)((total + 1) / 2), 32, 0, st>>>(
+        total, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, p, cands, ncand, b, n, a_m,
+        out_pos, out_val, out_cnt);
+  else
+    dt_estimate_warp_kernel<32><<<(unsigned)total, 32, 0, st>>>(
+        total, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, p, cands, ncand, b, n, a_m,
+        out_pos, out_val, out_cnt);
   scratch_free(cands, st);
   AFFT_CHECK_LAUNCH("dt_estimate_warp_kernel");
   return AFFT_OK;
@@ -678,10 +686,14 @@ extern "C" int afft_dt_estimate(const double* rows, const int64_t* rand_shifts, 
     set_error("afft_dt_estimate: bad arguments");
     return AFFT_EINVAL;
   }
-  dt_estimate_warp_kernel<<<(unsigned)((count + kDtEstWarps - 1) / kDtEstWarps),
-                            kDtEstWarps * 32, 0, (cudaStream_t)stream>>>(
-      count, count, 3 * a_m + p, a_m, p, rows, rand_shifts, 0, cands, ncand, b, n, dt::kMaxAm,
-      out_pos, out_val, out_n);
+  if (p <= 16)
+    dt_estimate_warp_kernel<16><<<(unsigned)((count + 1) / 2), 32, 0, (cudaStream_t)stream>>>(
+        count, count, 3 * a_m + p, a_m, p, rows, rand_shifts, 0, cands, ncand, b, n,
+        dt::kMaxAm, out_pos, out_val, out_n);
+  else
+    dt_estimate_warp_kernel<32><<<(unsigned)count, 32, 0, (cudaStream_t)stream>>>(
+        count, count, 3 * a_m + p, a_m, p, rows, rand_shifts, 0, cands, ncand, b, n,
+        dt::kMaxAm, out_pos, out_val, out_n);
   AFFT_CHECK_LAUNCH("dt_estimate_warp_kernel");
   return AFFT_OK;
 }

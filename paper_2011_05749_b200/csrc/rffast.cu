@@ -51,7 +51,14 @@ struct NoisyPlan {
   int32_t base[AFFT_MAX_CYCLES + 1];
   double w[kMaxRounds];          // Kay weights (m - 1 entries)
   int64_t tau[AFFT_MAX_SHIFTS];  // shifts reduced mod n
+  // optional per-signal shifts: device [signals][R], reduced mod n (R-FFAST batches whose
+  // signals carry their own search anchors, peeling.py:163-164); null: tau for all
+  const int64_t* tau_tab;
 };
+
+__device__ __forceinline__ int64_t plan_tau(const NoisyPlan& P, int64_t s, int r) {
+  return P.tau_tab ? P.tau_tab[s * P.R + r] : P.tau[r];
+}
 
 // numpy: np.remainder(p + pi, 2pi) - pi.  The common ranges need no sign-of-zero fix:
 // x >= 0 there and x - k 2pi is exact (Sterbenz), so a zero result is +0 already.
@@ -255,41 +262,47 @@ __device__ __forceinline__ bool approx_pruned(uint64_t G, const uint32_t* E, int
   return sum > lim;
 }
 
-// One CTA scores kChunk consecutive candidates t of one active node.
-// Active node a: residue `index[a]` of cycle size `bsz[a]`, estimates est[a][0..c).
+// Shared state of one CTA's chunk scan.
+struct ScanSmem {
+  double est[kMaxStrides];
+  uint32_t e32[kMaxStrides];
+  int nan;
+  unsigned long long bound;
+  double w_score[kSearchThreads / 32];
+  int32_t w_t[kSearchThreads / 32];
+};
+
+// One CTA scores kChunk consecutive candidates t (chunk `chunk`) of active node a:
+// residue `act_index[a]` of cycle size `act_b[a]`, estimates est[a][0..c).  Leaves the
+// chunk's (min score, smallest t) in part_score / part_t [a][chunk].  Ends with a
+// barrier, so a persistent CTA may reuse `sm` for its next chunk.
 template <bool k32>
-__global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
-    int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
-    const double* __restrict__ est, int chunks, double* __restrict__ part_score,
-    int32_t* __restrict__ part_t, int chunk_rank, int chunk_world,
-    unsigned long long* __restrict__ node_bound) {
-  __shared__ double s_est[kMaxStrides];
-  __shared__ uint32_t s_e32[kMaxStrides];
-  __shared__ int s_nan;
-  __shared__ unsigned long long s_bound;
-  __shared__ double w_score[kSearchThreads / 32];
-  __shared__ int32_t w_t[kSearchThreads / 32];
-  const int a = blockIdx.y;
-  const int chunk = chunk_rank + (int)blockIdx.x * chunk_world;  // this rank's chunks
+__device__ __forceinline__ void scan_chunk(ScanSmem& sm, int64_t n, int c, int a, int chunk,
+                                           const int64_t* __restrict__ act_index,
+                                           const int64_t* __restrict__ act_b,
+                                           const double* __restrict__ est, int chunks,
+                                           double* __restrict__ part_score,
+                                           int32_t* __restrict__ part_t,
+                                           unsigned long long* __restrict__ node_bound) {
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t t0 = (int64_t)chunk * kChunk;
   if (threadIdx.x == 0) {
-    s_nan = 0;
-    s_bound = load_bound_bits(node_bound + a);
+    sm.nan = 0;
+    sm.bound = load_bound_bits(node_bound + a);
   }
   __syncthreads();
   if (threadIdx.x < c) {
     const double e = est[(int64_t)a * c + threadIdx.x];
-    s_est[threadIdx.x] = e;
+    sm.est[threadIdx.x] = e;
     double u = e * 0.15915494309189535;  // turns (any rounding is inside the margin)
     u -= floor(u);
-    s_e32[threadIdx.x] = (uint32_t)(uint64_t)(u * 4294967296.0);
-    if (!(e == e) || isinf(e)) s_nan = 1;
+    sm.e32[threadIdx.x] = (uint32_t)(uint64_t)(u * 4294967296.0);
+    if (!(e == e) || isinf(e)) sm.nan = 1;
   }
   __syncthreads();
   const int64_t idx = act_index[a];
-  const ApproxScan ap = make_approx(n, L, idx, c, !s_nan);
+  const ApproxScan ap = make_approx(n, L, idx, c, !sm.nan);
   const double dn = (double)n;
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
@@ -297,27 +310,27 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
   int32_t bt = INT32_MAX;
   if (t0 < L) {
     unsigned long long* gb = node_bound + a;
-    double bound = bound_of_bits(s_bound);  // seeded by noisy_seed_kernel
+    double bound = bound_of_bits(sm.bound);  // seeded by noisy_seed_kernel
     const int64_t t1 = min(L, t0 + (int64_t)kChunk);
     // Two levels: the CTA's own bound in shared memory, read before every candidate,
     // and the node's global bound, folded into it every 4 candidates from a load
     // issued 4 candidates earlier (a global load waited on before every candidate was
     // 2/3 of the kernel's stall samples).  Any value read is some candidate's real
     // score, so a stale one only prunes less.
-    volatile unsigned long long* vs_bound = &s_bound;
+    volatile unsigned long long* vs_bound = &sm.bound;
     unsigned long long pending = load_bound_bits(gb);
     int k = 0;
     for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads, ++k) {
       if ((k & 3) == 3) {
-        atomicMin(&s_bound, pending);
+        atomicMin(&sm.bound, pending);
         pending = load_bound_bits(gb);
       }
       bound = fmin(bound, bound_of_bits(*vs_bound));
       if (ap.on) {
         const uint32_t lim = approx_limit(bound, ap.margin);
-        if (lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, s_e32, c, lim)) continue;
+        if (lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, sm.e32, c, lim)) continue;
       }
-      const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
+      const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, sm.est, c, dn, inv, bound);
       if (sc > bound) continue;  // pruned / worse than a candidate that is scored in full
       if (sc < best) {
         best = sc;
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
       }
       if (sc < bound) {
         bound = sc;
-        atomicMin(&s_bound, (unsigned long long)__double_as_longlong(sc));
+        atomicMin(&sm.bound, (unsigned long long)__double_as_longlong(sc));
         lower_bound_to(gb, sc);
       }
     }
@@ -341,21 +354,58 @@ __global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
     }
   }
   if ((threadIdx.x & 31) == 0) {
-    w_score[threadIdx.x >> 5] = best;
-    w_t[threadIdx.x >> 5] = bt;
+    sm.w_score[threadIdx.x >> 5] = best;
+    sm.w_t[threadIdx.x >> 5] = bt;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double b0 = w_score[0];
-    int32_t t0w = w_t[0];
+    double b0 = sm.w_score[0];
+    int32_t t0w = sm.w_t[0];
     for (int w = 1; w < kSearchThreads / 32; ++w) {
-      if (w_score[w] < b0 || (w_score[w] == b0 && w_t[w] < t0w)) {
-        b0 = w_score[w];
-        t0w = w_t[w];
+      if (sm.w_score[w] < b0 || (sm.w_score[w] == b0 && sm.w_t[w] < t0w)) {
+        b0 = sm.w_score[w];
+        t0w = sm.w_t[w];
       }
     }
     part_score[(int64_t)a * chunks + chunk] = b0;
     part_t[(int64_t)a * chunks + chunk] = t0w;
+  }
+  __syncthreads();
+}
+
+// Grid (this rank's chunks, active nodes): one chunk per CTA.
+template <bool k32>
+__global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_kernel(
+    int64_t n, int c, const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
+    const double* __restrict__ est, int chunks, double* __restrict__ part_score,
+    int32_t* __restrict__ part_t, int chunk_rank, int chunk_world,
+    unsigned long long* __restrict__ node_bound) {
+  __shared__ ScanSmem sm;
+  const int a = blockIdx.y;
+  const int chunk = chunk_rank + (int)blockIdx.x * chunk_world;  // this rank's chunks
+  scan_chunk<k32>(sm, n, c, a, chunk, act_index, act_b, est, chunks, part_score, part_t,
+                  node_bound);
+}
+
+// Device-resident rounds: the active count is only known on the device, so a
+// persistent grid (a few CTAs per SM) pulls (node, chunk) items from a ticket counter,
+// node-major, until all A * chunks are scanned.  Same per-chunk results as above.
+template <bool k32>
+__global__ void __launch_bounds__(kSearchThreads, 8) noisy_search_persistent_kernel(
+    int64_t n, int c, const int32_t* __restrict__ A_dev, const int64_t* __restrict__ act_index,
+    const int64_t* __restrict__ act_b, const double* __restrict__ est, int chunks,
+    double* __restrict__ part_score, int32_t* __restrict__ part_t,
+    unsigned long long* __restrict__ node_bound, int32_t* __restrict__ ticket) {
+  __shared__ ScanSmem sm;
+  __shared__ int item;
+  const int64_t total = (int64_t)(*A_dev) * chunks;
+  for (;;) {
+    if (threadIdx.x == 0) item = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int it = item;
+    if (it >= total) break;
+    scan_chunk<k32>(sm, n, c, it / chunks, it % chunks, act_index, act_b, est, chunks,
+                    part_score, part_t, node_bound);
   }
 }
 
@@ -366,7 +416,9 @@ template <bool k32>
 __global__ void noisy_seed_kernel(int64_t n, int c, int A, const int64_t* __restrict__ act_index,
                                   const int64_t* __restrict__ act_b,
                                   const double* __restrict__ est,
-                                  unsigned long long* __restrict__ node_bound) {
+                                  unsigned long long* __restrict__ node_bound,
+                                  const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= A) return;
   const int64_t b = act_b[a];
@@ -385,7 +437,9 @@ template <bool k32>
 __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kernel(
     int64_t n, int c, int A, const int64_t* __restrict__ act_index,
     const int64_t* __restrict__ act_b, const double* __restrict__ est,
-    double* __restrict__ part_score, int32_t* __restrict__ part_t) {
+    double* __restrict__ part_score, int32_t* __restrict__ part_t,
+    const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
   __shared__ double s_est_all[kWarpSearchWarps][kMaxStrides];
   __shared__ uint32_t s_e32_all[kWarpSearchWarps][kMaxStrides];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -448,10 +502,14 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
 }
 
 // Phase estimates of the active nodes (one thread per (node, stride)).
+// A_dev (device-resident rounds): the active count as the prep kernel left it; the
+// grid then covers the largest possible list and the excess threads exit.
 __global__ void noisy_est_kernel(int A, int c, int m, const int64_t* __restrict__ act_row,
                                  const double* __restrict__ residual, int R,
                                  const __grid_constant__ NoisyPlan P, double* __restrict__ est,
-                                 unsigned long long* __restrict__ node_bound) {
+                                 unsigned long long* __restrict__ node_bound,
+                                 const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)A * c) return;
   const int64_t a = e / c;
@@ -481,7 +539,9 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
                                       const double* __restrict__ residual,
                                       const __grid_constant__ NoisyPlan P,
                                       int64_t* __restrict__ out_f0, double* __restrict__ out_val,
-                                      double* __restrict__ out_res, NoisyDecide decide) {
+                                      double* __restrict__ out_res, NoisyDecide decide,
+                                      const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
   const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (a >= A) return;
@@ -508,10 +568,11 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
   const int64_t n = P.n;
   const int64_t f0 = (act_index[a] + act_b[a] * (int64_t)bt) % n;
   const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * P.R;
+  const int64_t sig = P.tau_tab ? act_row[a] / P.nodes : 0;
   // a^H y and a^H a
   double nre = 0.0, nim = 0.0, den = 0.0;
   for (int r = lane; r < P.R; r += 32) {
-    const cd at = unit_root(mulmod(P.tau[r], f0, n), n);
+    const cd at = unit_root(mulmod(plan_tau(P, sig, r), f0, n), n);
     const cd yv = y[r];
     nre += at.re * yv.re + at.im * yv.im;
     nim += at.re * yv.im - at.im * yv.re;
@@ -526,7 +587,7 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
   const cd x = cd{nre / den, nim / den};
   double rs = 0.0;
   for (int r = lane; r < P.R; r += 32) {
-    const cd at = unit_root(mulmod(P.tau[r], f0, n), n);
+    const cd at = unit_root(mulmod(plan_tau(P, sig, r), f0, n), n);
     const cd d = csub(cmul(at, x), y[r]);
     rs += d.re * d.re + d.im * d.im;
   }
@@ -587,7 +648,9 @@ __global__ void noisy_apply_kernel(int A, const __grid_constant__ NoisyPlan P,
                                    const int64_t* __restrict__ f0s, const double* __restrict__ vals,
                                    const double* __restrict__ res, const double* __restrict__ t1,
                                    int8_t* __restrict__ state, int8_t* __restrict__ dirty,
-                                   int64_t* __restrict__ node_f0, double* __restrict__ node_val) {
+                                   int64_t* __restrict__ node_f0, double* __restrict__ node_val,
+                                   const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= A) return;
   const int64_t e = act_row[a];
@@ -708,7 +771,7 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
         const int i = found_res[a2];
         const int64_t f = node_f0[so + found_g[i]];
         const cd v = reinterpret_cast<const cd*>(node_val)[so + found_g[i]];
-        acc = csub(acc, cmul(v, unit_root(mulmod(P.tau[r], f, P.n), P.n)));
+        acc = csub(acc, cmul(v, unit_root(mulmod(plan_tau(P, s, r), f, P.n), P.n)));
       }
       y[r] = acc;
     }
@@ -1084,12 +1147,12 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
     auto kfn = P.n < (int64_t(1) << 31) ? noisy_search_warp_kernel<true>
                                         : noisy_search_warp_kernel<false>;
     kfn<<<(unsigned)((A + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
-          st>>>(P.n, P.c, A, act_index, act_b, est, part_s, part_t);
+          st>>>(P.n, P.c, A, act_index, act_b, est, part_s, part_t, nullptr);
   } else {
     if (mine > 0) {
       auto sfn = P.n < (int64_t(1) << 31) ? noisy_seed_kernel<true> : noisy_seed_kernel<false>;
       sfn<<<(unsigned)((A + 127) / 128), 128, 0, st>>>(P.n, P.c, A, act_index, act_b, est,
-                                                         node_bound);
+                                                         node_bound, nullptr);
     }
     for (int a0 = 0; a0 < A && mine > 0; a0 += 65535) {
       const int cnt = std::min(65535, A - a0);
@@ -1121,6 +1184,159 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
       out.val ? out.val : reinterpret_cast<double*>(ws + w.val),
       out.res ? out.res : reinterpret_cast<double*>(ws + w.res), out.decide);
   AFFT_CHECK_LAUNCH("noisy_finalize_kernel");
+  return AFFT_OK;
+}
+
+// ------------------------------------------------------------ device-resident rounds
+//
+// peel_decode's loop (peeling.py:283-313) without host round-trips: one round's
+// kernels (prep -> est -> seed + search -> finalize -> apply -> harvest -> control)
+// are captured once into the body of a CUDA-graph WHILE node; the control kernel sets
+// the node's condition from the round's harvest count and the round budget, so the
+// whole decode is one graph launch.  Launch shapes cannot depend on the active count
+// (it lives on the device): list-sized kernels get the largest possible grid and read
+// the count, and the candidate scan is a persistent grid pulling (node, chunk) items.
+// counters[0] active count, [1] tones harvested this round, [2] scan ticket, [3] rounds run.
+__global__ void noisy_round_control_kernel(cudaGraphConditionalHandle handle,
+                                           int32_t* __restrict__ counters, int max_rounds) {
+  const int it = counters[3] + 1;
+  counters[3] = it;
+  const bool more = counters[1] != 0 && it < max_rounds;
+  counters[0] = 0;
+  counters[1] = 0;
+  counters[2] = 0;
+  cudaGraphSetConditional(handle, more ? 1u : 0u);
+}
+
+static int device_sms() {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  return v;
+}
+
+// Enqueue one round's kernels on the capturing stream `cs`.
+static int enqueue_round(const NoisyPlan& P, const NoisyWs& w, char* ws, int64_t batch,
+                         double* residual, int8_t* state, int8_t* dirty, int32_t* done,
+                         int64_t* node_f0, double* node_val, const double* t0, const double* t1,
+                         int64_t* rec_pos, double* rec_val, int32_t rec_cap, int32_t* rec_count,
+                         int32_t* rounds, int32_t* counters, char* hscratch, size_t hbytes,
+                         size_t hsmem, cudaGraphConditionalHandle handle, int max_rounds,
+                         cudaStream_t cs) {
+  const int64_t rows = batch * P.nodes;  // the largest possible active list
+  int64_t* act_row = reinterpret_cast<int64_t*>(ws + w.act_row);
+  int64_t* act_index = reinterpret_cast<int64_t*>(ws + w.act_index);
+  int64_t* act_b = reinterpret_cast<int64_t*>(ws + w.act_b);
+  double* est = reinterpret_cast<double*>(ws + w.est);
+  double* part_s = reinterpret_cast<double*>(ws + w.part_s);
+  int32_t* part_t = reinterpret_cast<int32_t*>(ws + w.part_t);
+  unsigned long long* node_bound = reinterpret_cast<unsigned long long*>(ws + w.bound);
+  int64_t* f0s = reinterpret_cast<int64_t*>(ws + w.f0);
+  double* vals = reinterpret_cast<double*>(ws + w.val);
+  double* res = reinterpret_cast<double*>(ws + w.res);
+  const int32_t* A_dev = counters;
+  const bool k32 = P.n < (int64_t(1) << 31);
+  noisy_prep_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, cs>>>(
+      batch, P, residual, state, dirty, done, t0, counters, act_row, act_index, act_b);
+  AFFT_CHECK_LAUNCH("noisy_prep_kernel");
+  const int64_t ne = rows * P.c;
+  noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, cs>>>(0, P.c, P.m, act_row, residual,
+                                                                P.R, P, est, node_bound, A_dev);
+  AFFT_CHECK_LAUNCH("noisy_est_kernel");
+  if (w.Lmax <= kWarpSearchMaxL) {  // one chunk per node: part slot a = node a
+    auto kfn = k32 ? noisy_search_warp_kernel<true> : noisy_search_warp_kernel<false>;
+    kfn<<<(unsigned)((rows + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
+          cs>>>(P.n, P.c, 0, act_index, act_b, est, part_s, part_t, A_dev);
+  } else {
+    auto sfn = k32 ? noisy_seed_kernel<true> : noisy_seed_kernel<false>;
+    sfn<<<(unsigned)((rows + 127) / 128), 128, 0, cs>>>(P.n, P.c, 0, act_index, act_b, est,
+                                                        node_bound, A_dev);
+    auto kfn = k32 ? noisy_search_persistent_kernel<true> : noisy_search_persistent_kernel<false>;
+    kfn<<<(unsigned)(device_sms() * 8), kSearchThreads, 0, cs>>>(
+        P.n, P.c, A_dev, act_index, act_b, est, w.chunks, part_s, part_t, node_bound,
+        counters + 2);
+  }
+  AFFT_CHECK_LAUNCH("noisy_search_persistent_kernel");
+  noisy_finalize_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, cs>>>(
+      0, w.chunks, part_s, part_t, act_row, act_index, act_b, residual, P, f0s, vals, res,
+      NoisyDecide{nullptr, 0.0, 0.0}, A_dev);
+  AFFT_CHECK_LAUNCH("noisy_finalize_kernel");
+  noisy_apply_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, cs>>>(
+      0, P, act_row, f0s, vals, res, t1, state, dirty, node_f0, node_val, A_dev);
+  AFFT_CHECK_LAUNCH("noisy_apply_kernel");
+  noisy_harvest_kernel<<<(unsigned)batch, 1024, hsmem, cs>>>(
+      P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap, rec_count,
+      rounds, counters + 1, hscratch, hbytes);
+  AFFT_CHECK_LAUNCH("noisy_harvest_kernel");
+  noisy_round_control_kernel<<<1, 1, 0, cs>>>(handle, counters, max_rounds);
+  AFFT_CHECK_LAUNCH("noisy_round_control_kernel");
+  return AFFT_OK;
+}
+
+// A capture stream per thread: capture must not touch the caller's stream (it may
+// hold pending work), and the graph is launched on the caller's stream afterwards.
+static cudaStream_t capture_stream() {
+  thread_local cudaStream_t cs = nullptr;
+  thread_local int cs_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!cs || cs_dev != dev) {
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    cs_dev = dev;
+  }
+  return cs;
+}
+
+// The whole round loop as one graph launch on `st` (see above).
+static int peel_rounds_graph(const NoisyPlan& P, const NoisyWs& w, char* ws, int64_t batch,
+                             double* residual, int8_t* state, int8_t* dirty, int32_t* done,
+                             int64_t* node_f0, double* node_val, const double* t0,
+                             const double* t1, int32_t max_rounds, int64_t* rec_pos,
+                             double* rec_val, int32_t rec_cap, int32_t* rec_count,
+                             int32_t* rounds, int32_t* counters, char* hscratch, size_t hbytes,
+                             size_t hsmem, cudaStream_t st) {
+  if (max_rounds <= 0) return AFFT_OK;
+  cudaError_t e = cudaMemsetAsync(counters, 0, 16, st);
+  if (e != cudaSuccess) return cuda_status(e, "afft_peel_noisy counters");
+  cudaStream_t cs = capture_stream();
+  if (!cs) return cuda_status(cudaGetLastError(), "capture stream");
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  int rc = AFFT_OK;
+  do {
+    if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) break;
+    cudaGraphConditionalHandle h;
+    if ((e = cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault)) !=
+        cudaSuccess)
+      break;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &np)) != cudaSuccess) break;
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+      break;
+    rc = enqueue_round(P, w, ws, batch, residual, state, dirty, done, node_f0, node_val, t0, t1,
+                       rec_pos, rec_val, rec_cap, rec_count, rounds, counters, hscratch, hbytes,
+                       hsmem, h, max_rounds, cs);
+    cudaGraph_t captured = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(cs, &captured);
+    if (rc) break;
+    if ((e = e2) != cudaSuccess) break;
+    if ((e = cudaGraphInstantiate(&ex, g, 0)) != cudaSuccess) break;
+    e = cudaGraphLaunch(ex, st);
+  } while (false);
+  if (ex) cudaGraphExecDestroy(ex);  // safe: destruction waits for nothing, launch is queued
+  if (g) cudaGraphDestroy(g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_status(e, "afft_peel_noisy round graph");
   return AFFT_OK;
 }
 
@@ -1255,6 +1471,15 @@ extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t
                           NoisyDecide{nullptr, 0.0, 0.0});
 }
 
+namespace afft {
+static int peel_noisy_core(NoisyPlan* P, int64_t batch, double* residual, int8_t* state,
+                           int64_t* node_f0, double* node_val, const double* t0,
+                           const double* t1, int32_t max_rounds, int64_t* rec_pos,
+                           double* rec_val, int32_t rec_cap, int32_t* rec_count, int32_t* rounds,
+                           int32_t* unresolved, void* workspace, size_t workspace_bytes,
+                           void* stream, const AfftSearchShard* shard);
+}  // namespace afft
+
 extern "C" int afft_peel_noisy(int64_t n, int64_t batch, const int64_t* factors, int32_t ncycles,
                                const int64_t* shifts, int32_t nshift, int32_t c, int32_t m,
                                const double* weights, double* residual, int8_t* state,
@@ -1292,6 +1517,19 @@ extern "C" int afft_peel_noisy_sharded(
   if (rc) {
     return rc;
   }
+  return peel_noisy_core(P, batch, residual, state, node_f0, node_val, t0, t1, max_rounds,
+                         rec_pos, rec_val, rec_cap, rec_count, rounds, unresolved, workspace,
+                         workspace_bytes, stream, shard);
+}
+
+namespace afft {
+static int peel_noisy_core(NoisyPlan* P, int64_t batch, double* residual, int8_t* state,
+                           int64_t* node_f0, double* node_val, const double* t0,
+                           const double* t1, int32_t max_rounds, int64_t* rec_pos,
+                           double* rec_val, int32_t rec_cap, int32_t* rec_count, int32_t* rounds,
+                           int32_t* unresolved, void* workspace, size_t workspace_bytes,
+                           void* stream, const AfftSearchShard* shard) {
+  int rc = AFFT_OK;
   const int N = P->nodes;
   const NoisyWs w = noisy_ws(*P, batch * N);
   if (!workspace || workspace_bytes < w.total) {
@@ -1339,6 +1577,17 @@ extern "C" int afft_peel_noisy_sharded(
     }
   }
   const int64_t total = batch * N;
+  if (!shard || shard->world <= 1) {
+    rc = peel_rounds_graph(*P, w, ws, batch, residual, state, dirty, done, node_f0, node_val, t0,
+                           t1, max_rounds, rec_pos, rec_val, rec_cap, rec_count, rounds, counters,
+                           hscratch, hbytes, hsmem, st);
+    if (!rc) {
+      count_multi_kernel<<<(unsigned)batch, 256, 0, st>>>(batch, N, state, unresolved);
+      rc = cudaGetLastError() == cudaSuccess ? AFFT_OK : AFFT_ECUDA;
+    }
+    if (hscratch) scratch_free(hscratch, st);
+    return rc;
+  }
   for (int it = 0; it < max_rounds; ++it) {
     cudaMemsetAsync(counters, 0, 8, st);
     noisy_prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
@@ -1378,6 +1627,7 @@ extern "C" int afft_peel_noisy_sharded(
   AFFT_CHECK_LAUNCH("count_multi_kernel");
   return AFFT_OK;
 }
+}  // namespace afft
 
 
 extern "C" int afft_classify_noisy(const double* residual, const int64_t* index, int64_t count,
@@ -1449,4 +1699,139 @@ extern "C" size_t afft_singleton_workspace_size(int64_t n, int64_t count, int64_
   double wts[kMaxRounds] = {0};
   if (make_noisy_plan(P.get(), n, &b, 1, zeros.data(), c * m, c, m, wts, 1)) return 0;
   return noisy_ws(*P, count).total;
+}
+
+// ------------------------------------------------------------------ afft_rffast
+//
+// r_ffast's body (peeling.py:361-386) for a batch, one enqueue: graph build at every
+// signal's own search shifts (r_j + 2^j t from its anchors, peeling.py:60-62) ->
+// node energies -> robust thresholds (peeling.py:335-358) -> device-resident noisy
+// peeling (peeling.py:270-313) -> top-k truncation (oneshot.py:260-263).
+
+namespace afft {
+struct RffastWs {
+  size_t nodes, tau_raw, tau_red, energy, state, f0, val, peel, total;
+};
+
+static RffastWs rffast_ws(const NoisyPlan& P, int64_t batch) {
+  RffastWs r;
+  const int64_t rows = batch * P.nodes;
+  size_t o = 0;
+  r.nodes = o;   o = al256(o + (size_t)rows * P.R * 16);
+  r.tau_raw = o; o = al256(o + (size_t)batch * P.R * 8);
+  r.tau_red = o; o = al256(o + (size_t)batch * P.R * 8);
+  r.energy = o;  o = al256(o + (size_t)rows * 8);
+  r.state = o;   o = al256(o + (size_t)rows);
+  r.f0 = o;      o = al256(o + (size_t)rows * 8);
+  r.val = o;     o = al256(o + (size_t)rows * 16);
+  r.peel = o;    o = al256(o + noisy_ws(P, rows).total);
+  r.total = o;
+  return r;
+}
+
+__global__ void rffast_init_kernel(int64_t rows, int8_t* __restrict__ state,
+                                   int64_t* __restrict__ f0, double* __restrict__ val,
+                                   int64_t batch, int32_t* __restrict__ rec_count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) {
+    state[i] = AFFT_UNKNOWN;
+    f0[i] = -1;
+    reinterpret_cast<cd*>(val)[i] = cd{0.0, 0.0};
+  }
+  if (i < batch) rec_count[i] = 0;
+}
+
+static int rffast_plan(NoisyPlan* P, int64_t n, const int64_t* factors, int32_t ncycles,
+                       int32_t c, int32_t m, const double* weights) {
+  if (c < 1 || c > kMaxStrides || m < 2 || m > kMaxRounds) {
+    set_error("search plan c=%d m=%d unsupported", c, m);
+    return AFFT_EUNSUPPORTED;
+  }
+  std::vector<int64_t> zeros((size_t)c * m, 0);
+  int64_t nodes = 0;
+  for (int k = 0; k < ncycles && factors; ++k) nodes += factors[k];
+  return make_noisy_plan(P, n, factors, ncycles, zeros.data(), c * m, c, m, weights,
+                         (int)std::min<int64_t>(nodes, INT32_MAX));
+}
+}  // namespace afft
+
+extern "C" size_t afft_rffast_workspace_size(int64_t n, int64_t batch, const int64_t* factors,
+                                             int32_t ncycles, int32_t c, int32_t m) {
+  std::unique_ptr<NoisyPlan> P(new NoisyPlan());
+  double wts[kMaxRounds] = {0};
+  if (!factors || rffast_plan(P.get(), n, factors, ncycles, c, m, wts)) return 0;
+  return rffast_ws(*P, std::max<int64_t>(batch, 1)).total;
+}
+
+extern "C" int afft_rffast(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                           const int64_t* factors, int32_t ncycles, const int64_t* anchors,
+                           int64_t anchor_stride, int32_t c, int32_t m, const double* weights,
+                           int32_t k, int32_t max_rounds, int64_t* out_pos, double* out_val,
+                           int32_t* out_count, int64_t* all_pos, double* all_val,
+                           int32_t* all_count, int32_t* rounds, int32_t* unresolved, double* t0,
+                           double* t1, void* workspace, size_t workspace_bytes, void* stream) {
+  if (batch == 0) return AFFT_OK;
+  if (!x || !factors || !anchors || !weights || (k > 0 && (!out_pos || !out_val)) ||
+      !out_count || !all_pos || !all_val || !all_count || !rounds || !unresolved || !t0 || !t1 ||
+      k < 0 || batch < 0 || ld < n || anchor_stride < 0 ||
+      (dtype != AFFT_C64 && dtype != AFFT_C128)) {
+    set_error("afft_rffast: bad arguments");
+    return AFFT_EINVAL;
+  }
+  std::unique_ptr<NoisyPlan> P_owner(new NoisyPlan());
+  NoisyPlan* P = P_owner.get();
+  int rc = rffast_plan(P, n, factors, ncycles, c, m, weights);
+  if (rc) return rc;
+  const RffastWs w = rffast_ws(*P, batch);
+  if (!workspace || workspace_bytes < w.total) {
+    set_error("afft_rffast: workspace of %zu bytes needed, %zu given", w.total, workspace_bytes);
+    return AFFT_ENOMEM;
+  }
+  if ((int64_t)batch * P->nodes > INT32_MAX) {
+    set_error("afft_rffast: batch * nodes exceeds 2^31");
+    return AFFT_EUNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = reinterpret_cast<char*>(workspace);
+  const int R = P->R, N = P->nodes;
+  const int64_t rows = batch * N;
+  // per-signal shifts r_j + 2^j t (SearchPlan.shifts, peeling.py:60-62): raw for the
+  // gather, reduced for the peel; staged from pageable memory (the copy returns once
+  // staged, so the vectors may go out of scope)
+  std::vector<int64_t> raw((size_t)batch * R), red((size_t)batch * R);
+  for (int64_t s = 0; s < batch; ++s)
+    for (int j = 0; j < c; ++j)
+      for (int t = 0; t < m; ++t) {
+        const int64_t v = anchors[s * anchor_stride + j] + (int64_t(1) << j) * t;
+        raw[(size_t)s * R + j * m + t] = v;
+        red[(size_t)s * R + j * m + t] = host_pymod(v, n);
+      }
+  for (int r = 0; r < R; ++r) P->tau[r] = red[r];
+  int64_t* tau_raw = reinterpret_cast<int64_t*>(ws + w.tau_raw);
+  int64_t* tau_red = reinterpret_cast<int64_t*>(ws + w.tau_red);
+  cudaError_t e = cudaMemcpyAsync(tau_raw, raw.data(), raw.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(tau_red, red.data(), red.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e, "afft_rffast shift tables");
+  P->tau_tab = tau_red;
+  double* nodes = reinterpret_cast<double*>(ws + w.nodes);
+  if ((rc = build_graph_table(x, dtype, n, batch, ld, factors, ncycles, tau_raw, R, nodes, st)))
+    return rc;
+  double* energy = reinterpret_cast<double*>(ws + w.energy);
+  node_energy_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(rows, R, nodes, energy);
+  AFFT_CHECK_LAUNCH("node_energy_kernel");
+  if ((rc = afft_robust_thresholds(energy, nullptr, N, batch, R, t0, t1, st))) return rc;
+  int8_t* state = reinterpret_cast<int8_t*>(ws + w.state);
+  int64_t* f0 = reinterpret_cast<int64_t*>(ws + w.f0);
+  double* val = reinterpret_cast<double*>(ws + w.val);
+  rffast_init_kernel<<<(unsigned)((std::max<int64_t>(rows, batch) + 255) / 256), 256, 0, st>>>(
+      rows, state, f0, val, batch, all_count);
+  AFFT_CHECK_LAUNCH("rffast_init_kernel");
+  const int mr = max_rounds > 0 ? max_rounds : k + 4;
+  if ((rc = peel_noisy_core(P, batch, nodes, state, f0, val, t0, t1, mr, all_pos, all_val, N,
+                            all_count, rounds, unresolved, ws + w.peel,
+                            w.total - w.peel, stream, nullptr)))
+    return rc;
+  return afft_truncate(all_pos, all_val, all_count, N, batch, k, out_pos, out_val, out_count,
+                       stream);
 }

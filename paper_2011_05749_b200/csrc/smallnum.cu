@@ -1,7 +1,8 @@
 // smallnum API (smallnum.py:54-142) on the device: one matrix per call, one
 // thread, built from the same smallla.cuh templates the per-bucket solvers use.
-// Shapes are capped at the hot path's sizes (tall side <= 32, short side <= 8);
-// larger inputs are rejected with AFFT_EUNSUPPORTED (the reference caps at 64).
+// Shapes up to the hot path's sizes (tall side <= 32, short side <= 8) run one
+// thread; larger ones, up to the reference's 64 x 64 cap, go to the CTA-cooperative
+// solvers of smallnum_cta.cu.
 #include <cstring>
 
 #include "afft_common.cuh"
@@ -186,6 +187,13 @@ __global__ void small_api_kernel(int op, int m, int n, const double* __restrict_
 
 }  // namespace afft
 
+namespace afft {
+// smallnum_cta.cu: one CTA per call for shapes beyond the per-thread templates (<= 64)
+int small_la_cta(int op, int m, int n, const double* a, const double* b, int rank,
+                 double* out_u, double* out_s, double* out_v, double* out_x, int* out_i,
+                 cudaStream_t st);
+}  // namespace afft
+
 using namespace afft;
 
 extern "C" int afft_small_la(int32_t op, int32_t m, int32_t n, const double* a, const double* b,
@@ -205,6 +213,12 @@ extern "C" int afft_small_la(int32_t op, int32_t m, int32_t n, const double* a, 
     case OP_PENCIL: ok = m == n && m <= kC && rank >= 1 && rank < m && out_x && out_i; break;
     default: ok = false;
   }
+  if (!ok && op != OP_ROOTS && hi <= 64 && (op != OP_LSTSQ || (m >= n && b && out_x && out_s && out_i)) &&
+      (op != OP_EIGVALS || (m == n && out_x && out_i)) &&
+      (op != OP_PENCIL || (m == n && rank >= 1 && rank < m && out_x && out_i)) &&
+      (op != OP_SVD || (out_u && out_s && out_v)))
+    return small_la_cta(op, m, n, a, b, rank, out_u, out_s, out_v, out_x, out_i,
+                        (cudaStream_t)stream);
   if (!ok) {
     set_error("afft_small_la: op %d unsupported for a %d x %d matrix (device caps %d x %d)", op,
               m, n, kR, kC);

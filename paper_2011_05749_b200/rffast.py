@@ -297,18 +297,79 @@ def rffast_batch(x, k: int, factors, search, max_rounds: int | None = None, *,
                  shard=None) -> RffastBatchResult:
     """R-FFAST over a (batch, n) block: graph build at the c*m search shifts,
     median-energy thresholds, noisy peeling and top-k truncation, all on the device.
-    ``shard`` (a shard.SearchShard) splits the singleton search of this same batch
-    over several ranks (one huge signal on several GPUs); results are unchanged."""
+
+    ``search`` is one SearchPlan for every signal or a list with one per signal (the
+    reference draws each signal's anchors from its own seed, peeling.py:163-164).
+    Unsharded, the whole decode is one stream-ordered afft_rffast enqueue (the
+    peeling rounds run as a device-side graph loop).  ``shard`` (a shard.SearchShard)
+    splits the singleton search of this same batch over several ranks (one huge
+    signal on several GPUs; one shared plan); results are unchanged."""
     xd = _device.as_device_batch(x)
     batch, n = int(xd.shape[0]), int(xd.shape[1])
     dev = xd.device
     factors = [int(b) for b in factors]
-    shifts = search.shifts
-    R = len(shifts)
-    N = sum(factors)
+    plans = list(search) if isinstance(search, (list, tuple)) else [search] * max(batch, 1)
+    if len(plans) != max(batch, 1):
+        raise ValueError(f"{len(plans)} search plans for {batch} signals")
+    c, m = plans[0].c, plans[0].m
+    if any(p.c != c or p.m != m for p in plans):
+        raise ValueError("every signal's search plan must share c and m")
     for b in factors:
         if b < 1 or n % b:
             raise ValueError(f"bucket count {b} does not divide signal size {n}")
+    if shard is not None and shard.world > 1:
+        if any(list(p.anchors) != list(plans[0].anchors) for p in plans):
+            raise ValueError("a sharded search needs one search plan for the batch")
+        return _rffast_batch_sharded(xd, k, factors, plans[0], max_rounds, shard)
+    N = sum(factors)
+    kk = max(int(k), 0)
+    lib = _lib.load()
+    fb, nc = _lib.host_i64(factors)
+    need = int(lib.afft_rffast_workspace_size(n, batch, fb, nc, c, m))
+    if need == 0:
+        _lib.check(_lib.AFFT_EUNSUPPORTED, "r_ffast plan")
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    same = all(p is plans[0] for p in plans)
+    anchors = np.asarray([list(p.anchors) for p in (plans[:1] if same else plans)],
+                         dtype=np.int64)
+    if anchors.shape[1] != c:
+        raise ValueError("search plan anchors must number c")
+    ab = anchors.ctypes.data_as(ctypes.c_void_p)
+    wb = _lib.host_f64(np.asarray(plans[0].weights, dtype=np.float64).tolist())
+    out = RffastBatchResult(
+        n, k,
+        pos=torch.empty((batch, kk), dtype=torch.int64, device=dev),
+        val=torch.empty((batch, kk), dtype=torch.complex128, device=dev),
+        count=torch.empty(batch, dtype=torch.int32, device=dev),
+        all_pos=torch.empty((batch, N), dtype=torch.int64, device=dev),
+        all_val=torch.empty((batch, N), dtype=torch.complex128, device=dev),
+        all_count=torch.empty(batch, dtype=torch.int32, device=dev),
+        rounds=torch.empty(batch, dtype=torch.int32, device=dev),
+        unresolved=torch.empty(batch, dtype=torch.int32, device=dev),
+        t0=torch.empty(batch, dtype=torch.float64, device=dev),
+        t1=torch.empty(batch, dtype=torch.float64, device=dev),
+    )
+    if batch == 0:
+        return out
+    ld = int(xd.stride(0)) if batch > 1 else n
+    mr = int(max_rounds) if max_rounds else kk + 4
+    _lib.check(lib.afft_rffast(
+        xd.data_ptr(), _device.dtype_code(xd), n, batch, ld, fb, nc, ab, 0 if same else c, c, m,
+        wb, kk, mr, out.pos.data_ptr(), out.val.data_ptr(), out.count.data_ptr(),
+        out.all_pos.data_ptr(), out.all_val.data_ptr(), out.all_count.data_ptr(),
+        out.rounds.data_ptr(), out.unresolved.data_ptr(), out.t0.data_ptr(), out.t1.data_ptr(),
+        ws.data_ptr(), ws.numel(), _device.stream_ptr()), "r_ffast")
+    return out
+
+
+def _rffast_batch_sharded(xd, k, factors, search, max_rounds, shard) -> RffastBatchResult:
+    """The sequence with a split singleton search: graph build, thresholds, then
+    afft_peel_noisy_sharded (one partial exchange per round through the shard)."""
+    batch, n = int(xd.shape[0]), int(xd.shape[1])
+    dev = xd.device
+    shifts = search.shifts
+    R = len(shifts)
+    N = sum(factors)
     nodes = torch.empty((batch, N, R), dtype=torch.complex128, device=dev)
     fb, nc = _lib.host_i64(factors)
     sb, ns = _lib.host_i64(shifts)

@@ -63,8 +63,10 @@ def child(name):
     elif name in ("c3", "c3auto"):
         n, k = 511 * 512 * 513, 1000
         x, _ = bench.synth_batch(n, k, 20.0, list(range(S)), torch.complex128, dev, chunk=2)
-        plan, search = plan_cycles(n, k, "noisy", seed=bench.case_seed(n, k, 20.0, 0, 0))
-        factors = [511, 512, 513] if name == "c3" else list(plan.factors)
+        plans = [plan_cycles(n, k, "noisy", seed=bench.case_seed(n, k, 20.0, 0, i))
+                 for i in range(S)]
+        search = [p[1] for p in plans]
+        factors = [511, 512, 513] if name == "c3" else list(plans[0][0].factors)
 
         def call():
             rffast_batch(x, k, factors, search)
