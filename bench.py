@@ -406,7 +406,7 @@ def run_ours(args, world, rank, local):
 
     total = args.signals
     if total % world:
-        raise SystemExit("--signals must be a multiple of the rank count (equal result slots)")
+        raise SystemExit("--total-signals must be a multiple of the rank count (equal result slots)")
     first, stop = shard_range(total, rank, world)
     per = stop - first
 
@@ -991,6 +991,49 @@ def _ref_step_worker(wid, per_step, steps, barrier, q, use_port):
         q.put(f"{type(exc).__name__}: {exc}")
 
 
+# ============================================================================ dry run
+
+
+def run_dry(args, world, rank):
+    """The multi-rank plumbing without a GPU (tests/test_bench_launcher.py): gloo
+    process group, the same signal sharding, result-slot all-gather and max-over-ranks
+    timing as run_ours, over stand-in result slots (slot values derived from the global
+    signal index, so the gathered order is checkable).  No decode runs; the line says
+    so with "dry_run": true."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_05749_b200.shard import gather_slots, max_over_ranks, shard_range
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    total = args.signals
+    if total % world:
+        raise SystemExit("--total-signals must be a multiple of the rank count (equal result slots)")
+    first, stop = shard_range(total, rank, world)
+    per = stop - first
+    idx = torch.arange(first, stop, dtype=torch.int64)
+    pos = idx[:, None] * 1000 + torch.arange(K, dtype=torch.int64)[None, :]
+    val = torch.complex(idx[:, None].double().expand(per, K), torch.zeros(per, K, dtype=torch.float64))
+    cnt = torch.full((per,), K, dtype=torch.int32)
+    t0 = time.perf_counter()
+    gp, gv, gc = gather_slots(pos, val, cnt) if world > 1 else (pos, val, cnt)
+    ms = (time.perf_counter() - t0) * 1e3
+    ok = (gp.shape[0] == total and bool((gp[:, 0] == torch.arange(total) * 1000).all())
+          and bool((gv[:, 0].real == torch.arange(total).double()).all())
+          and int(gc.sum()) == total * K)
+    (ms_max,) = max_over_ranks([ms], torch.device("cpu"))
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "config": config_dict(world, total),
+            "checks": {"gathered_slots_in_rank_order": ok, "signals_per_rank": per},
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ============================================================================ entry
 
 
@@ -1003,6 +1046,7 @@ def relaunch_under_torchrun(args_list, n):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
@@ -1018,7 +1062,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--signals", type=int, default=TOTAL_SIGNALS)
+    ap.add_argument("--total-signals", dest="signals", type=int, default=TOTAL_SIGNALS)
     ap.add_argument("--e2e-signals", type=int, default=256)
     ap.add_argument("--no-configs", action="store_true", help="skip configs 1-4 at N=1")
     ap.add_argument("--quick", action="store_true",
@@ -1027,6 +1071,8 @@ def main(argv=None):
                     help="only time the reference on this host for these configs "
                          "(comma list) and write --ref-cpu-out")
     ap.add_argument("--ref-cpu-out", default=os.path.join(ROOT, "profiles", "r02_ref_cpu.json"))
+    ap.add_argument("--dry-run", action="store_true",
+                    help="exercise the launcher / sharding / gather plumbing on CPU (gloo)")
     argv = sys.argv[1:] if argv is None else argv
     args = ap.parse_args(argv)
     if args.warmup < 3:
@@ -1052,7 +1098,9 @@ def main(argv=None):
     if world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         return 2
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args, world, rank)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)
