@@ -388,6 +388,19 @@ def synth_batch(n, k, snr, trials, dtype, dev, chunk=8):
     return x, truths
 
 
+def synth_signals(x, first_trial: int, dev, chunk: int = 32):
+    """Fill a preallocated [count, N] config-5 batch with trials first_trial.. (tools/)."""
+    truths = []
+    for c0 in range(0, x.shape[0], chunk):
+        c1 = min(x.shape[0], c0 + chunk)
+        xs, tr = synth_batch(N_SIG, K, "exact", list(range(first_trial + c0, first_trial + c1)),
+                             x.dtype, dev, chunk=chunk)
+        x[c0:c1] = xs
+        truths += tr
+        del xs
+    return truths
+
+
 # ============================================================================ our arm
 
 

@@ -402,6 +402,207 @@ int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64
   return AFFT_OK;
 }
 
+// ---------------------------------------------------------------- all deep layers
+//
+// Every full deep layer (L = n/b <= 32: depths dmin = log2(n) - log2(Lmax) .. log2 n)
+// in ONE pass over the resident spectrum, instead of one pass + a one-CTA sort per
+// layer.  Thread i0 < bmin loads its Lmax aliases y[l] = Y[i0 + l bmin]; layer j
+// (b_j = bmin 2^j, L_j = Lmax >> j) holds the buckets i0 + m bmin, m < 2^j, whose tau = 0
+// value is sum_{l < L_j} Y[i + l b_j] = sum_l y[m + l 2^j] — summed in l order as
+// alias_active_kernel does, so the decisions |v| > thr_j are bit-identical to it.  The
+// warp's flags for one (layer, m) are one 32-bit word of the layer's bitmap (lanes
+// hold consecutive i0); a count / scan / write pass then turns the bitmaps into
+// ascending active lists, all layers at once.
+constexpr int kDeepMaxLayers = 8;
+struct DeepLayers {
+  int nl;                          // layers: j = 0 .. nl - 1
+  double thr[kDeepMaxLayers];      // activity threshold of layer j
+  int64_t word_off[kDeepMaxLayers + 1];   // bitmap words before layer j
+  int64_t chunk_off[kDeepMaxLayers + 1];  // count chunks before layer j
+};
+constexpr int kDeepChunkWords = 2048;  // words per count / write CTA (256 threads x 8)
+
+template <int LM, int LOG2LM>
+__global__ void __launch_bounds__(128) deep_flags_kernel(const cd* __restrict__ Y, int64_t bmin,
+                                                         const __grid_constant__ DeepLayers D,
+                                                         uint32_t* __restrict__ words) {
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool on = i0 < bmin;
+  cd y[LM];
+#pragma unroll
+  for (int l = 0; l < LM; ++l) y[l] = on ? Y[i0 + (int64_t)l * bmin] : cd{0.0, 0.0};
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j <= LOG2LM; ++j) {  // layer j: b = bmin 2^j, L = LM >> j
+    if (j >= D.nl) break;
+#pragma unroll
+    for (int m = 0; m < (1 << j); ++m) {
+      cd acc = y[m];
+#pragma unroll
+      for (int l = 1; l < (LM >> j); ++l) acc = cadd(acc, y[m + (l << j)]);
+      // |v| > thr decided on |v|^2 against thr^2 with a 1e-14 guard band (|v|^2 in double
+      // is within 3 ulp, hypot within 1): only values inside the band take hypot, so
+      // every decision equals hypot(v) > thr (alias_active_kernel's test)
+      const double sq = acc.re * acc.re + acc.im * acc.im;
+      const double t2 = D.thr[j] * D.thr[j];
+      const bool f = sq > t2 * (1.0 + 1e-14) ? true
+                     : sq < t2 * (1.0 - 1e-14) ? false
+                                               : cabs_(acc) > D.thr[j];
+      const unsigned flags = __ballot_sync(0xffffffffu, on && f);
+      if (lane == 0 && on)
+        words[D.word_off[j] + (i0 >> 5) + (int64_t)m * (bmin >> 5)] = flags;
+    }
+  }
+}
+
+// popcounts of kDeepChunkWords words per CTA; chunks never straddle two layers
+__global__ void __launch_bounds__(256) deep_count_kernel(const uint32_t* __restrict__ words,
+                                                         const __grid_constant__ DeepLayers D,
+                                                         int32_t* __restrict__ chunk_cnt) {
+  const int64_t c = blockIdx.x;
+  int j = 0;
+  while (j + 1 < D.nl && c >= D.chunk_off[j + 1]) ++j;
+  const int64_t w0 = D.word_off[j] + (c - D.chunk_off[j]) * kDeepChunkWords;
+  const int64_t w1 = min(D.word_off[j + 1], w0 + kDeepChunkWords);
+  int cnt = 0;
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) cnt += __popc(words[w]);
+  __shared__ int part[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < 8; ++k) t += part[k];
+    chunk_cnt[c] = t;
+  }
+}
+
+// exclusive scan of the chunk counts within each layer (one CTA), layer totals out
+__global__ void deep_scan_kernel(int32_t* __restrict__ chunk_cnt,
+                                 const __grid_constant__ DeepLayers D,
+                                 int32_t* __restrict__ layer_count) {
+  for (int j = threadIdx.x; j < D.nl; j += blockDim.x) {
+    int run = 0;
+    for (int64_t c = D.chunk_off[j]; c < D.chunk_off[j + 1]; ++c) {
+      const int v = chunk_cnt[c];
+      chunk_cnt[c] = run;
+      run += v;
+    }
+    layer_count[j] = run;
+  }
+}
+
+// ascending bucket indices of every layer: list j at out + j * cap (first cap kept)
+__global__ void __launch_bounds__(256) deep_write_kernel(const uint32_t* __restrict__ words,
+                                                         const __grid_constant__ DeepLayers D,
+                                                         const int32_t* __restrict__ chunk_base,
+                                                         int64_t* __restrict__ out, int cap) {
+  const int64_t c = blockIdx.x;
+  int j = 0;
+  while (j + 1 < D.nl && c >= D.chunk_off[j + 1]) ++j;
+  const int64_t lw0 = (c - D.chunk_off[j]) * kDeepChunkWords;  // first word within the layer
+  const int64_t w0 = D.word_off[j] + lw0;
+  const int64_t nw = min(D.word_off[j + 1] - w0, (int64_t)kDeepChunkWords);
+  constexpr int PER = kDeepChunkWords / 256;  // contiguous words per thread
+  uint32_t wv[PER];
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int64_t w = (int64_t)threadIdx.x * PER + k;
+    wv[k] = w < nw ? words[w0 + w] : 0u;
+    cnt += __popc(wv[k]);
+  }
+  // block exclusive scan of cnt
+  __shared__ int warp_tot[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yv = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += yv;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  int woff = 0;
+  for (int k = 0; k < wid; ++k) woff += warp_tot[k];
+  int at = chunk_base[c] + woff + x - cnt;
+  int64_t* lst = out + (int64_t)j * cap;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    uint32_t v = wv[k];
+    const int64_t bit0 = (lw0 + (int64_t)threadIdx.x * PER + k) * 32;
+    while (v) {
+      const int t = __ffs(v) - 1;
+      v &= v - 1;
+      if (at < cap) lst[at] = bit0 + t;
+      ++at;
+    }
+  }
+}
+
+// Active lists of the full deep layers b = bmin, 2 bmin, ..., n (nl layers, thr[j] for
+// b = bmin << j) from the resident spectrum: lists [nl][cap] ascending (device),
+// counts [nl] (device; a count above cap means the list is partial).
+int deep_active_all(const double* spectrum, int64_t n, int64_t bmin, int nl, const double* thr,
+                    int64_t* out, int cap, int32_t* counts, void* scratch, size_t scratch_bytes,
+                    cudaStream_t st) {
+  const int64_t Lmax = n / bmin;
+  if (nl < 1 || nl > kDeepMaxLayers || Lmax > kAliasMaxL || (Lmax >> (nl - 1)) < 1 ||
+      bmin % 32 || n % bmin || (Lmax & (Lmax - 1))) {
+    set_error("deep_active_all: unsupported layers (n=%lld, bmin=%lld, nl=%d)", (long long)n,
+              (long long)bmin, nl);
+    return AFFT_EUNSUPPORTED;
+  }
+  DeepLayers D;
+  memset(&D, 0, sizeof(D));
+  D.nl = nl;
+  for (int j = 0; j < nl; ++j) {
+    D.thr[j] = thr[j];
+    const int64_t nw = (bmin << j) / 32;
+    D.word_off[j + 1] = D.word_off[j] + nw;
+    D.chunk_off[j + 1] = D.chunk_off[j] + (nw + kDeepChunkWords - 1) / kDeepChunkWords;
+  }
+  const size_t words_bytes = ((size_t)D.word_off[nl] * 4 + 255) & ~size_t(255);
+  const size_t need = words_bytes + (size_t)D.chunk_off[nl] * 4;
+  if (!scratch || scratch_bytes < need) {
+    set_error("deep_active_all: scratch of %zu bytes needed", need);
+    return AFFT_ENOMEM;
+  }
+  uint32_t* words = reinterpret_cast<uint32_t*>(scratch);
+  int32_t* chunk = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + words_bytes);
+  const cd* Y = reinterpret_cast<const cd*>(spectrum);
+  const unsigned grid = (unsigned)((bmin + 127) / 128);
+  switch (Lmax) {
+    case 1: deep_flags_kernel<1, 0><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    case 2: deep_flags_kernel<2, 1><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    case 4: deep_flags_kernel<4, 2><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    case 8: deep_flags_kernel<8, 3><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    case 16: deep_flags_kernel<16, 4><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    case 32: deep_flags_kernel<32, 5><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    default:
+      set_error("deep_active_all: n/bmin = %lld is not a power of two <= 32", (long long)Lmax);
+      return AFFT_EUNSUPPORTED;
+  }
+  AFFT_CHECK_LAUNCH("deep_flags_kernel");
+  const unsigned chunks = (unsigned)D.chunk_off[nl];
+  deep_count_kernel<<<chunks, 256, 0, st>>>(words, D, chunk);
+  deep_scan_kernel<<<1, 32, 0, st>>>(chunk, D, counts);
+  deep_write_kernel<<<chunks, 256, 0, st>>>(words, D, chunk, out, cap);
+  AFFT_CHECK_LAUNCH("deep_write_kernel");
+  return AFFT_OK;
+}
+
+size_t deep_active_scratch(int64_t n, int64_t bmin, int nl) {
+  int64_t words = 0, chunks = 0;
+  for (int j = 0; j < nl; ++j) {
+    const int64_t nw = (bmin << j) / 32;
+    words += nw;
+    chunks += (nw + kDeepChunkWords - 1) / kDeepChunkWords;
+  }
+  return (((size_t)words * 4 + 255) & ~size_t(255)) + (size_t)chunks * 4;
+}
+
 }  // namespace afft
 
 using namespace afft;

@@ -283,6 +283,13 @@ struct Dsfft {
   DBuf Y;             // resident spectrum fft(x)/n (lazy)
   double normY = -1;  // ||Y||^2 (lazy)
 
+  // Full deep layers (L <= 32) from one pass over Y for all of them (deep_active_all),
+  // made at the first such expansion: per-layer lists + counts, read back once.
+  bool deep_done = false;
+  int deep_d0 = 0, deep_nl = 0, deep_cap = 0;
+  DBuf deep_lists;
+  std::vector<int32_t> deep_counts;
+
   static constexpr int64_t kAliasMaxL = 32;       // rows + energies + values from Y
   static constexpr int64_t kAliasRowsMaxL = 256;  // rows alone from Y
 
@@ -291,9 +298,14 @@ struct Dsfft {
   // Rows from the resident spectrum instead of min(#shifts, L) size-b DFTs over the
   // signal: worth it once Y exists (A*L*R products against ~min(R, L)*b*log b), and
   // worth computing Y for at L <= 64, where one layer's DFTs cost a full transform.
+  // AFFT_DSFFT_Y_L: the largest L at which rows alone justify computing Y (default 64)
+  int64_t y_rows_l = [] {
+    const char* e = std::getenv("AFFT_DSFFT_Y_L");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : 64;
+  }();
   bool alias_rows_ok(int64_t b) const {
     const int64_t L = n / b;
-    return L <= kAliasMaxL || (L <= kAliasRowsMaxL && (Y.p || L <= 64));
+    return L <= kAliasMaxL || (L <= kAliasRowsMaxL && (Y.p || L <= y_rows_l));
   }
 
   // ||Y||^2 for the noisy floor bound: from Y when resident, else by Parseval from x
@@ -401,6 +413,19 @@ struct Dsfft {
       const char* cap_var = std::getenv("AFFT_ACTIVE_SORT_CAP");  // read per layer (tests)
       const int64_t cap_env = cap_var ? std::max<int64_t>(1, std::atoll(cap_var)) : 16384;
       const int cap = (int)std::min<int64_t>(b, std::min<int64_t>(16384, cap_env));
+      if (!deep_done && !std::getenv("AFFT_DSFFT_DEEP_PER_LAYER")) RC(deep_all(depth, cap));
+      if (deep_done && depth >= deep_d0 && depth < deep_d0 + deep_nl &&
+          deep_counts[depth - deep_d0] <= std::min(cap, deep_cap)) {
+        const int j = depth - deep_d0;
+        out.m = deep_counts[j];
+        RC(out.active.alloc((size_t)std::max<int64_t>(out.m, 1) * 8, st, "dsfft active"));
+        if (out.m)
+          CK(cudaMemcpyAsync(out.active.p, deep_lists.as<int64_t>() + (int64_t)j * deep_cap,
+                             (size_t)out.m * 8, cudaMemcpyDeviceToDevice, st));
+        PMARK("active set");
+        tr.add(2, depth, out.m, -1);
+        return AFFT_OK;
+      }
       RC(out.active.alloc((size_t)cap * 8, st, "dsfft active"));
       DBuf cnt;
       RC(cnt.alloc(4, st, "dsfft count"));
@@ -419,6 +444,28 @@ struct Dsfft {
     RC(full_values(b, vals));
     RC(active(vals, b, thr, nullptr, out));
     tr.add(2, depth, out.m, -1);
+    return AFFT_OK;
+  }
+
+  // The active lists of every full deep layer from `depth` to the bottom, one pass.
+  int deep_all(int depth, int cap) {
+    deep_done = true;  // attempted: a failure below leaves the per-layer path
+    const int nl = max_depth - depth + 1;
+    const int64_t bmin = 1LL << depth;
+    if (nl < 1 || nl > 8 || bmin % 32) return AFFT_OK;
+    std::vector<double> thr((size_t)nl);
+    for (int j = 0; j < nl; ++j) thr[j] = threshold(depth + j);
+    DBuf counts, scratch;
+    RC(deep_lists.alloc((size_t)nl * cap * 8, st, "dsfft deep lists"));
+    RC(counts.alloc((size_t)nl * 4, st, "dsfft deep counts"));
+    const size_t sb = deep_active_scratch(n, bmin, nl);
+    RC(scratch.alloc(sb, st, "dsfft deep scratch"));
+    RC(deep_active_all(Y.as<double>(), n, bmin, nl, thr.data(), deep_lists.as<int64_t>(), cap,
+                       counts.as<int32_t>(), scratch.p, sb, st));
+    RC(d2h(deep_counts, counts.p, (size_t)nl, st));
+    deep_d0 = depth;
+    deep_nl = nl;
+    deep_cap = cap;
     return AFFT_OK;
   }
 

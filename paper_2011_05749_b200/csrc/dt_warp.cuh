@@ -29,7 +29,9 @@ struct WarpPursuit {
   c2 A[dt::kMaxFreqs][W];  // atom k, row i
   c2 y[W];
   c2 r[W];
-  c2 V[kCols][kCols];       // V[row j][col c]
+  c2 V[kCols][kCols];       // V[row j][col c]; the Jacobi refit keeps V's column c, row
+                            // `lane`, at V[c][lane] while it rotates
+  c2 Wk[kCols][W];          // refit working columns (column c, row `lane`)
   c2 x[kCols];              // refit solution
   c2 best_coef[dt::kMaxAm];
   c2 dot[kCols];
@@ -70,25 +72,29 @@ __device__ __forceinline__ double warp_vnorm(c2 v, int P, int lane) {
 
 // refit (oneshot.py:229-232): x = lstsq(A[:, sup], y) with numpy's cutoff; returns
 // ||y - A_s x||.  S.sup[0..cnt) are atom indices; the solution lands in S.x.
+// Working columns live in shared memory (S.Wk[c][row], V column c at S.V[c][row]) and
+// the loops stay rolled: the unrolled register form was ~40k SASS instructions per
+// kernel and ncu charged 68% of the stall samples to instruction fetch.
 template <int W>
 __device__ __noinline__ double warp_refit(WarpPursuit<W>& S, int P, int cnt, int lane) {
-  c2 w[kCols], v[kCols];
-#pragma unroll
-  for (int c = 0; c < kCols; ++c) {
-    w[c] = (c < cnt && lane < P) ? S.A[S.sup[c]][lane] : la::C(0.0);
-    v[c] = la::C(lane == c ? 1.0 : 0.0);  // row `lane` of V (lanes < cnt)
+  const unsigned gm = gmask<W>();
+  for (int c = 0; c < cnt; ++c) {
+    S.Wk[c][lane] = lane < P ? S.A[S.sup[c]][lane] : la::C(0.0);
+    if (lane < cnt) S.V[c][lane] = la::C(lane == c ? 1.0 : 0.0);
   }
   const c2 yl = lane < P ? S.y[lane] : la::C(0.0);
+  __syncwarp(gm);
+#pragma unroll 1
   for (int sweep = 0; sweep < 60; ++sweep) {
     bool rotated = false;
-#pragma unroll
-    for (int p = 0; p < kCols - 1; ++p) {
-#pragma unroll
-      for (int q = p + 1; q < kCols; ++q) {
-        if (q >= cnt) continue;
-        const double alpha = wsum<W>(la::abs2(w[p]));
-        const double beta = wsum<W>(la::abs2(w[q]));
-        const c2 gl = la::cmulc(w[p], w[q]);
+#pragma unroll 1
+    for (int p = 0; p < cnt - 1; ++p) {
+#pragma unroll 1
+      for (int q = p + 1; q < cnt; ++q) {
+        const c2 wp = S.Wk[p][lane], wq = S.Wk[q][lane];
+        const double alpha = wsum<W>(la::abs2(wp));
+        const double beta = wsum<W>(la::abs2(wq));
+        const c2 gl = la::cmulc(wp, wq);
         const c2 gamma = la::C(wsum<W>(gl.re), wsum<W>(gl.im));
         const double g = la::cabs(gamma);
         if (g == 0.0 || g <= la::kEps * sqrt(alpha * beta)) continue;
@@ -99,33 +105,33 @@ __device__ __noinline__ double warp_refit(WarpPursuit<W>& S, int P, int cnt, int
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
         {
-          const c2 ap = w[p], aq = la::cmulc(ph, w[q]);
-          w[p] = la::sub(la::scale(ap, cs), la::scale(aq, sn));
-          w[q] = la::add(la::scale(ap, sn), la::scale(aq, cs));
+          const c2 aq = la::cmulc(ph, wq);
+          S.Wk[p][lane] = la::sub(la::scale(wp, cs), la::scale(aq, sn));
+          S.Wk[q][lane] = la::add(la::scale(wp, sn), la::scale(aq, cs));
         }
-        {
-          const c2 vp = v[p], vq = la::cmulc(ph, v[q]);
-          v[p] = la::sub(la::scale(vp, cs), la::scale(vq, sn));
-          v[q] = la::add(la::scale(vp, sn), la::scale(vq, cs));
+        if (lane < cnt) {
+          const c2 vp = S.V[p][lane], vq = la::cmulc(ph, S.V[q][lane]);
+          S.V[p][lane] = la::sub(la::scale(vp, cs), la::scale(vq, sn));
+          S.V[q][lane] = la::add(la::scale(vp, sn), la::scale(vq, cs));
         }
+        __syncwarp(gm);
       }
     }
     if (!rotated) break;
   }
-  // singular values, u_k^H y numerators, V rows to shared memory
-#pragma unroll
-  for (int c = 0; c < kCols; ++c) {
-    if (c >= cnt) break;
-    const double s2 = wsum<W>(la::abs2(w[c]));
-    const c2 dl = la::cmulc(w[c], yl);
+  // singular values and u_k^H y numerators (lane 0), V rows for the solution
+#pragma unroll 1
+  for (int c = 0; c < cnt; ++c) {
+    const c2 wc = S.Wk[c][lane];
+    const double s2 = wsum<W>(la::abs2(wc));
+    const c2 dl = la::cmulc(wc, yl);
     const c2 d = la::C(wsum<W>(dl.re), wsum<W>(dl.im));
     if (lane == 0) {
       S.sig[c] = sqrt(s2);
       S.dot[c] = d;
     }
-    if (lane < cnt) S.V[lane][c] = v[c];
   }
-  __syncwarp(gmask<W>());
+  __syncwarp(gm);
   if (lane == 0) {  // selection sort descending (svd_jacobi's swaps, on a permutation)
     for (int j = 0; j < cnt; ++j) S.ord[j] = j;
     for (int j = 0; j < cnt; ++j) {
@@ -142,7 +148,7 @@ __device__ __noinline__ double warp_refit(WarpPursuit<W>& S, int P, int cnt, int
       }
     }
   }
-  __syncwarp(gmask<W>());
+  __syncwarp(gm);
   if (lane < cnt) {  // x_j = sum_k V[j][k] (u_k^H y) / s_k, k descending, above the cutoff
     const double cutoff = la::kEps * (double)(P > cnt ? P : cnt) * S.sig[0];
     c2 xj = la::C(0.0);
@@ -150,11 +156,11 @@ __device__ __noinline__ double warp_refit(WarpPursuit<W>& S, int P, int cnt, int
       if (!(S.sig[r] > cutoff)) continue;
       const int k = S.ord[r];
       const c2 coef = la::scale(S.dot[k], 1.0 / (S.sig[r] * S.sig[r]));
-      xj = la::add(xj, la::mul(S.V[lane][k], coef));
+      xj = la::add(xj, la::mul(S.V[k][lane], coef));
     }
     S.x[lane] = xj;
   }
-  __syncwarp(gmask<W>());
+  __syncwarp(gm);
   c2 acc = la::C(0.0);
   if (lane < P)
     for (int c = 0; c < cnt; ++c) acc = la::add(acc, la::mul(S.A[S.sup[c]][lane], S.x[c]));
@@ -167,59 +173,56 @@ __device__ __noinline__ double warp_refit(WarpPursuit<W>& S, int P, int cnt, int
 // least-squares problem the solution is unique, so this agrees with the SVD
 // form to rounding; when the R diagonal spans more than 1e7 (possible rank
 // deficiency, where numpy's eps cutoff could bite) the Jacobi form decides.
+// R ends up in S.Wk: R[j][k] = S.Wk[k][j] for j <= k.
 template <int W>
 __device__ __noinline__ double warp_refit_qr(WarpPursuit<W>& S, int P, int cnt, int lane) {
-  c2 w[kCols];
-#pragma unroll
-  for (int c = 0; c < kCols; ++c) w[c] = (c < cnt && lane < P) ? S.A[S.sup[c]][lane] : la::C(0.0);
+  const unsigned gm = gmask<W>();
+  for (int c = 0; c < cnt; ++c) S.Wk[c][lane] = lane < P ? S.A[S.sup[c]][lane] : la::C(0.0);
   const c2 yl = lane < P ? S.y[lane] : la::C(0.0);
   c2 qy = yl;
   double dmax = 0.0, dmin = 1e300;
-#pragma unroll
-  for (int j = 0; j < kCols; ++j) {
-    if (j >= cnt) break;
+  __syncwarp(gm);
+#pragma unroll 1
+  for (int j = 0; j < cnt; ++j) {
     const bool below = lane >= j && lane < P;
-    const double nx = sqrt(wsum<W>(below ? la::abs2(w[j]) : 0.0));
-    const c2 x0 = la::C(__shfl_sync(gmask<W>(), w[j].re, j, W),
-                        __shfl_sync(gmask<W>(), w[j].im, j, W));
+    const c2 wj = S.Wk[j][lane];
+    const double nx = sqrt(wsum<W>(below ? la::abs2(wj) : 0.0));
+    const c2 x0 = S.Wk[j][j];
     dmax = nx > dmax ? nx : dmax;
     dmin = nx < dmin ? nx : dmin;
     if (nx == 0.0) break;
     const double a0 = la::cabs(x0);
     const c2 ph = a0 > 0.0 ? la::C(x0.re / a0, x0.im / a0) : la::C(1.0);
     const c2 alpha = la::C(-ph.re * nx, -ph.im * nx);
-    const c2 v = lane == j ? la::sub(x0, alpha) : (below ? w[j] : la::C(0.0));
+    const c2 v = lane == j ? la::sub(x0, alpha) : (below ? wj : la::C(0.0));
     const double inv = 2.0 / (2.0 * nx * (nx + a0));  // 2 / v^H v
-#pragma unroll
-    for (int k = j + 1; k < kCols; ++k) {
-      if (k >= cnt) break;
-      const c2 dl = la::cmulc(v, w[k]);
+#pragma unroll 1
+    for (int k = j + 1; k < cnt; ++k) {
+      const c2 wk = S.Wk[k][lane];
+      const c2 dl = la::cmulc(v, wk);
       const c2 d = la::C(wsum<W>(dl.re), wsum<W>(dl.im));
-      w[k] = la::sub(w[k], la::mul(v, la::scale(d, inv)));
+      S.Wk[k][lane] = la::sub(wk, la::mul(v, la::scale(d, inv)));
     }
     {
       const c2 dl = la::cmulc(v, qy);
       const c2 d = la::C(wsum<W>(dl.re), wsum<W>(dl.im));
       qy = la::sub(qy, la::mul(v, la::scale(d, inv)));
     }
-    if (lane == j) w[j] = alpha;
+    __syncwarp(gm);
+    if (lane == j) S.Wk[j][lane] = alpha;
+    __syncwarp(gm);
   }
   if (!(dmin > 1e-7 * dmax)) return warp_refit<W>(S, P, cnt, lane);
-  if (lane < cnt) {
-#pragma unroll
-    for (int k = 0; k < kCols; ++k)
-      if (k < cnt) S.V[lane][k] = w[k];
-    S.dot[lane] = qy;
-  }
-  __syncwarp(gmask<W>());
+  if (lane < cnt) S.dot[lane] = qy;
+  __syncwarp(gm);
   if (lane == 0) {  // back substitution R x = Q^H y
     for (int j = cnt - 1; j >= 0; --j) {
       c2 sacc = S.dot[j];
-      for (int k = j + 1; k < cnt; ++k) sacc = la::sub(sacc, la::mul(S.V[j][k], S.x[k]));
-      S.x[j] = la::div(sacc, S.V[j][j]);
+      for (int k = j + 1; k < cnt; ++k) sacc = la::sub(sacc, la::mul(S.Wk[k][j], S.x[k]));
+      S.x[j] = la::div(sacc, S.Wk[j][j]);
     }
   }
-  __syncwarp(gmask<W>());
+  __syncwarp(gm);
   c2 acc = la::C(0.0);
   if (lane < P)
     for (int c = 0; c < cnt; ++c) acc = la::add(acc, la::mul(S.A[S.sup[c]][lane], S.x[c]));

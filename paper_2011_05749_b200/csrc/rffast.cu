@@ -20,6 +20,7 @@
 // candidate.  Only atan2 differs from glibc, by <= 2 ulp in the estimates.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <type_traits>
@@ -54,7 +55,19 @@ struct NoisyPlan {
   // optional per-signal shifts: device [signals][R], reduced mod n (R-FFAST batches whose
   // signals carry their own search anchors, peeling.py:163-164); null: tau for all
   const int64_t* tau_tab;
+  uint64_t nmagic;  // floor((2^64 - 1) / n): Barrett reduction for tau * f mod n
 };
+
+// (a * b) mod P.n for 0 <= a, b < n <= 2e9 (a * b < 2^62): Barrett with the plan's
+// magic, exact after at most two corrections — the int64 '%' it replaces compiled to
+// a ~70-instruction division routine (13% of noisy_finalize_kernel's instructions).
+__device__ __forceinline__ int64_t plan_mulmod(const NoisyPlan& P, int64_t a, int64_t b) {
+  const uint64_t p = (uint64_t)(a * b);
+  const uint64_t q = __umul64hi(p, P.nmagic);
+  uint64_t r = p - q * (uint64_t)P.n;
+  while (r >= (uint64_t)P.n) r -= (uint64_t)P.n;
+  return (int64_t)r;
+}
 
 __device__ __forceinline__ int64_t plan_tau(const NoisyPlan& P, int64_t s, int r) {
   return P.tau_tab ? P.tau_tab[s * P.R + r] : P.tau[r];
@@ -542,8 +555,13 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
                                       double* __restrict__ out_res, NoisyDecide decide,
                                       const int32_t* __restrict__ A_dev = nullptr) {
   if (A_dev) A = *A_dev;
+  // classify's zero-ton gate needs ||y||: the squares land in shared memory while the
+  // rows are loaded, and lane 0 sums them in node_norm's order (not 2 x R dependent
+  // global loads on one lane — 30% of this kernel's instructions and its latency chain)
+  constexpr int kNormRows = 128;
+  __shared__ double nsq[8][2][kNormRows];  // blockDim 256
   const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wl = (threadIdx.x >> 5) & 7;
   if (a >= A) return;
   double best = __longlong_as_double(0x7ff0000000000000LL);
   int32_t bt = INT32_MAX;
@@ -566,14 +584,26 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
   }
   if (bt == INT32_MAX) bt = 0;  // all-NaN scores: numpy argmin would return the first NaN
   const int64_t n = P.n;
-  const int64_t f0 = (act_index[a] + act_b[a] * (int64_t)bt) % n;
+  // index < b and t < n / b, so the candidate is already reduced (no '% n')
+  const int64_t f0 = act_index[a] + act_b[a] * (int64_t)bt;
   const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * P.R;
   const int64_t sig = P.tau_tab ? act_row[a] / P.nodes : 0;
-  // a^H y and a^H a
+  // a^H y and a^H a; each lane's atoms kept for the residual (one sincos per row)
+  constexpr int kAtomRegs = 4;  // rows lane, lane + 32, ... cached up to R = 128
+  cd atc[kAtomRegs];
   double nre = 0.0, nim = 0.0, den = 0.0;
-  for (int r = lane; r < P.R; r += 32) {
-    const cd at = unit_root(mulmod(plan_tau(P, sig, r), f0, n), n);
+#pragma unroll
+  for (int q = 0; q < kAtomRegs; ++q) atc[q] = cd{0.0, 0.0};
+  for (int r = lane, q = 0; r < P.R; r += 32, ++q) {
+    const cd at = unit_root(plan_mulmod(P, plan_tau(P, sig, r), f0), n);
+#pragma unroll
+    for (int qq = 0; qq < kAtomRegs; ++qq)
+      if (qq == q) atc[qq] = at;
     const cd yv = y[r];
+    if (decide.state && P.R <= kNormRows) {
+      nsq[wl][0][r] = __dmul_rn(yv.re, yv.re);
+      nsq[wl][1][r] = __dmul_rn(yv.im, yv.im);
+    }
     nre += at.re * yv.re + at.im * yv.im;
     nim += at.re * yv.im - at.im * yv.re;
     den += at.re * at.re + at.im * at.im;
@@ -586,8 +616,11 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
   }
   const cd x = cd{nre / den, nim / den};
   double rs = 0.0;
-  for (int r = lane; r < P.R; r += 32) {
-    const cd at = unit_root(mulmod(plan_tau(P, sig, r), f0, n), n);
+  for (int r = lane, q = 0; r < P.R; r += 32, ++q) {
+    cd at = q < kAtomRegs ? cd{0.0, 0.0} : unit_root(plan_mulmod(P, plan_tau(P, sig, r), f0), n);
+#pragma unroll
+    for (int qq = 0; qq < kAtomRegs; ++qq)
+      if (qq == q) at = atc[qq];
     const cd d = csub(cmul(at, x), y[r]);
     rs += d.re * d.re + d.im * d.im;
   }
@@ -598,10 +631,24 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
     reinterpret_cast<cd*>(out_val)[a] = x;
     const double resn = sqrt(rs);
     out_res[a] = resn;
-    if (decide.state)
-      decide.state[a] = node_norm(y, P.R) <= decide.t0 ? AFFT_ZERO_TON
-                        : resn <= decide.t1            ? AFFT_SINGLE_TON
-                                                       : AFFT_MULTI_TON;
+  }
+  if (decide.state) {
+    double nrm;
+    if (P.R <= kNormRows) {
+      __syncwarp();
+      double sre = 0.0, sim = 0.0;
+      if (lane == 0) {
+        for (int r = 0; r < P.R; ++r) sre = __dadd_rn(sre, nsq[wl][0][r]);
+        for (int r = 0; r < P.R; ++r) sim = __dadd_rn(sim, nsq[wl][1][r]);
+      }
+      nrm = sqrt(__dadd_rn(sre, sim));
+    } else {
+      nrm = lane == 0 ? node_norm(y, P.R) : 0.0;
+    }
+    if (lane == 0)
+      decide.state[a] = nrm <= decide.t0 ? AFFT_ZERO_TON
+                        : out_res[a] <= decide.t1 ? AFFT_SINGLE_TON
+                                                  : AFFT_MULTI_TON;
   }
 }
 
@@ -771,7 +818,7 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
         const int i = found_res[a2];
         const int64_t f = node_f0[so + found_g[i]];
         const cd v = reinterpret_cast<const cd*>(node_val)[so + found_g[i]];
-        acc = csub(acc, cmul(v, unit_root(mulmod(plan_tau(P, s, r), f, P.n), P.n)));
+        acc = csub(acc, cmul(v, unit_root(plan_mulmod(P, plan_tau(P, s, r), f), P.n)));
       }
       y[r] = acc;
     }
@@ -1016,6 +1063,7 @@ static int make_noisy_plan(NoisyPlan* P, int64_t n, const int64_t* factors, int 
   P->nodes = (int)total;
   for (int t = 0; t < m - 1; ++t) P->w[t] = weights[t];
   for (int r = 0; r < R; ++r) P->tau[r] = host_pymod(shifts[r], n);
+  P->nmagic = ~0ull / (uint64_t)n;
   int hcap = 16;
   while (hcap < 2 * std::max(rec_cap, 1)) hcap <<= 1;
   P->hmask = hcap - 1;
@@ -1577,7 +1625,11 @@ static int peel_noisy_core(NoisyPlan* P, int64_t batch, double* residual, int8_t
     }
   }
   const int64_t total = batch * N;
-  if (!shard || shard->world <= 1) {
+  static const bool host_loop = [] {  // AFFT_PEEL_GRAPH=0: the host-synchronised loop below
+    const char* e = getenv("AFFT_PEEL_GRAPH");
+    return e && e[0] == '0';
+  }();
+  if ((!shard || shard->world <= 1) && !host_loop) {
     rc = peel_rounds_graph(*P, w, ws, batch, residual, state, dirty, done, node_f0, node_val, t0,
                            t1, max_rounds, rec_pos, rec_val, rec_cap, rec_count, rounds, counters,
                            hscratch, hbytes, hsmem, st);

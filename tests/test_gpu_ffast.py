@@ -199,12 +199,11 @@ def test_bench_synthesis_matches_generate_test_case():
     import bench
 
     dev = torch.device("cuda")
-    x = torch.empty((2, bench.N_SIG), dtype=torch.complex64, device=dev)
-    truths = bench.synth_signals(x, 5, dev)
+    x, truths = bench.synth_batch(bench.N_SIG, bench.K, "exact", [5, 6], torch.complex64, dev)
     for i in range(2):
         seed = bench.case_seed(bench.N_SIG, bench.K, "exact", 0, 5 + i)
         case = generate_test_case(bench.N_SIG, bench.K, "exact", seed=seed)
-        assert sorted(case.truth.entries) == truths[i][0].tolist()
+        assert sorted(case.truth.entries) == truths[i].tolist()
         want = case.signal.astype(np.complex64)
         got = x[i].cpu().numpy()
         assert np.max(np.abs(got - want)) <= 1e-5 * np.max(np.abs(want))
