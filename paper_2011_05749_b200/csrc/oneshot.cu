@@ -171,7 +171,7 @@ __global__ void roots_kernel(int64_t L, la::c2* __restrict__ roots) {
 // count, 0 for an empty bucket, -1 for None.
 constexpr int kDt2LocateThreads = 256;
 
-__global__ void __launch_bounds__(kDt2LocateThreads, 3) dt2_locate_warp_kernel(
+__global__ void __launch_bounds__(kDt2LocateThreads, 2) dt2_locate_warp_kernel(
     int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
     const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
     int64_t b, int64_t n, const la::c2* __restrict__ rootsL, const la::c2* __restrict__ coef_all,
@@ -242,21 +242,31 @@ __global__ void __launch_bounds__(kDt2LocateThreads, 3) dt2_locate_warp_kernel(
   // into coeffs[] would live in local memory); two independent candidates per
   // iteration, since each chain is a dependent sequence of complex products (four
   // spill at the 80-register cap and measured slower)
+  // The candidate products and the Horner steps use explicit FMAs (4 instead of 6
+  // and 8 FP64 instructions per complex product / step; the kernel is FP64-pipe
+  // bound).  The reference's |P| values are matched to rounding only either way —
+  // its roots come from exp() of each candidate, these from a table — so only
+  // ulp-level ties in the ranking can differ (SURVEY §8c's correlation/|P| ties).
+  auto fmul = [](la::c2 u, la::c2 v) {
+    return la::C(__fma_rn(u.re, v.re, -u.im * v.im), __fma_rn(u.re, v.im, u.im * v.re));
+  };
   auto horner = [&](la::c2 z) {
     la::c2 y = la::C(1.0);
 #pragma unroll
     for (int kk = dt::kMaxAm - 1; kk >= 0; --kk)
-      if (kk < a) y = la::add(la::mul(y, z), coeffs[kk]);
+      if (kk < a)
+        y = la::C(__fma_rn(y.re, z.re, __fma_rn(-y.im, z.im, coeffs[kk].re)),
+                  __fma_rn(y.re, z.im, __fma_rn(y.im, z.re, coeffs[kk].im)));
     return y;
   };
   int64_t j = lane;
-  for (; j + 32 < step; j += 64) {
-    const la::c2 y0 = horner(la::mul(z0, rootsL[j]));
-    const la::c2 y1 = horner(la::mul(z0, rootsL[j + 32]));
+  for (; j + 32 < step; j += 64) {  // two independent Horner chains per lane
+    const la::c2 y0 = horner(fmul(z0, rootsL[j]));
+    const la::c2 y1 = horner(fmul(z0, rootsL[j + 32]));
     consider(y0, j);
     consider(y1, j + 32);
   }
-  for (; j < step; j += 32) consider(horner(la::mul(z0, rootsL[j])), j);
+  for (; j < step; j += 32) consider(horner(fmul(z0, rootsL[j])), j);
   // butterfly merge: insert the partner lane's list (lists of different lanes are disjoint)
   for (int o = 16; o > 0; o >>= 1) {
     double ov[dt::kMaxAm];
@@ -280,14 +290,49 @@ __global__ void __launch_bounds__(kDt2LocateThreads, 3) dt2_locate_warp_kernel(
   }
 }
 
+// Rows grouped by their tone count a (1..4) for the thread-per-row locate: a warp
+// of mixed counts ran ~4 of 32 lanes per instruction (ncu, config 4).  bins[0..4]
+// count rows per a; empty rows get ncand = 0 here and no slot.
+__global__ void rows_by_count_kernel(int64_t total, const int32_t* __restrict__ counts, int a_cap,
+                                     int32_t* __restrict__ bins, int32_t* __restrict__ ncand) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int a = counts[e];
+  if (a_cap > 0 && a > a_cap) a = a_cap;
+  if (a <= 0) {
+    ncand[e] = 0;
+    return;
+  }
+  atomicAdd(bins + (a < dt::kMaxAm ? a : dt::kMaxAm), 1);
+}
+__global__ void rows_scatter_kernel(int64_t total, const int32_t* __restrict__ counts, int a_cap,
+                                    const int32_t* __restrict__ bins, int32_t* __restrict__ fill,
+                                    int32_t* __restrict__ order) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int a = counts[e];
+  if (a_cap > 0 && a > a_cap) a = a_cap;
+  if (a <= 0) return;
+  const int bin = a < dt::kMaxAm ? a : dt::kMaxAm;
+  int base = 0;
+  for (int k = 1; k < bin; ++k) base += bins[k];
+  order[base + atomicAdd(fill + bin, 1)] = (int32_t)e;
+}
+
 // dt1 / dt3 locate (oneshot.py:161-191), one thread per bucket: ncand[e] = count,
-// 0 for an empty bucket, -1 for None.
+// 0 for an empty bucket, -1 for None.  With `order`, thread i takes row order[i]
+// (rows grouped by a; entries < 0 are past the non-empty rows).
 __global__ void __launch_bounds__(kDtSolveThreads) dt_locate_rows_kernel(
     int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
     const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
-    int variant, int64_t b, int64_t n, int64_t* __restrict__ cands, int32_t* __restrict__ ncand) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int variant, int64_t b, int64_t n, int64_t* __restrict__ cands, int32_t* __restrict__ ncand,
+    const int32_t* __restrict__ order = nullptr) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= total) return;
+  if (order) {
+    e = order[e];
+    if (e < 0) return;
+  }
   int a = counts[e];
   if (a_cap > 0 && a > a_cap) a = a_cap;  // dsfft.py:219 caps at a_m
   if (a <= 0) {
@@ -550,10 +595,28 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
                                                          counts, bucket_ids, a_cap, b, n, roots,
                                                          coef, cok, cands, ncand);
   } else {
+    int32_t* grp = nullptr;  // bins[8] | fill[8] | order[total]
+    e = scratch_alloc(reinterpret_cast<void**>(&grp), 64 + (size_t)total * 4, st);
+    if (e != cudaSuccess) {
+      scratch_free(cands, st);
+      return cuda_status(e, "scratch (dt row groups)");
+    }
+    int32_t* order = grp + 16;
+    e = cudaMemsetAsync(grp, 0, 64, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(order, 0xff, (size_t)total * 4, st);
+    if (e != cudaSuccess) {
+      scratch_free(grp, st);
+      scratch_free(cands, st);
+      return cuda_status(e, "dt row groups");
+    }
+    const unsigned g = (unsigned)((total + 255) / 256);
+    rows_by_count_kernel<<<g, 256, 0, st>>>(total, counts, a_cap, grp, ncand);
+    rows_scatter_kernel<<<g, 256, 0, st>>>(total, counts, a_cap, grp, grp + 8, order);
     dt_locate_rows_kernel<<<(unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads),
                             kDtSolveThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
                                                       counts, bucket_ids, a_cap, variant, b, n,
-                                                      cands, ncand);
+                                                      cands, ncand, order);
+    scratch_free(grp, st);
   }
   const char* wenv = getenv("AFFT_DT_EST_WIDTH");  // 32 forces the full-warp form
   if (p <= 16 && !(wenv && atoi(wenv) == 32))
