@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_kernel(
   extern __shared__ cd alias_smem[];
   cd* rootL = alias_smem;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  cd* ys = alias_smem + L + w * L;
+  cd* ys = alias_smem + L + 2 * w * L;  // the warp's L terms + an L-entry work buffer
   for (int j = threadIdx.x; j < L; j += blockDim.x) rootL[j] = root_pi(j, L);
   __syncthreads();
   const int64_t r = (int64_t)blockIdx.x * kAliasWarps + w;
@@ -230,6 +230,32 @@ __global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_kernel(
   const int64_t i = idx[r];
   for (int l = lane; l < L; l += 32) ys[l] = Y[i + (int64_t)l * b];
   __syncwarp();
+  if ((L & (L - 1)) == 0) {
+    // every coset value Z[rl] = sum_l ys[l] w_L^(l rl) at once: a radix-2 Stockham
+    // DFT of the L aliases in the warp's two shared buffers (L log L products instead
+    // of one L-term sum per shift: 72 shifts x L at DSFFT's 72-shift plan)
+    cd* x = ys;
+    cd* z = ys + L;
+    for (int Ls = 1; Ls < L; Ls <<= 1) {
+      const int stride = L / (2 * Ls);
+      for (int k = lane; k < L / 2; k += 32) {
+        const int j = k & (Ls - 1), g = k / Ls;
+        const cd a = x[g * Ls + j];
+        const cd t = j ? cmul(x[g * Ls + j + L / 2], rootL[j * stride]) : x[g * Ls + j + L / 2];
+        z[2 * g * Ls + j] = cadd(a, t);
+        z[2 * g * Ls + j + Ls] = csub(a, t);
+      }
+      __syncwarp();
+      cd* tmp = x;
+      x = z;
+      z = tmp;
+    }
+    for (int t = lane; t < sh.nshift; t += 32) {
+      const int64_t tau = sh.tau[t];
+      rows[r * sh.nshift + t] = cmul(x[(int)(tau & (L - 1))], root_pi(mulmod(i, tau, n), n));
+    }
+    return;
+  }
   for (int t = lane; t < sh.nshift; t += 32) {
     const int64_t tau = sh.tau[t];
     const int rl = (int)(tau % L);
@@ -241,6 +267,45 @@ __global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_kernel(
       acc = cadd(acc, cmul(ys[l], rootL[m]));
     }
     rows[r * sh.nshift + t] = cmul(acc, root_pi(mulmod(i, tau, n), n));
+  }
+}
+
+// Rows for L > kAliasRowsMaxL (L a power of two): one CTA per row, the L aliases and
+// a work buffer in shared memory, the radix-2 Stockham DFT across the CTA; every
+// coset value at once (the rows of DSFFT's shallow noisy layers straight from the
+// resident spectrum instead of 72 size-b DFTs over the signal).
+__global__ void __launch_bounds__(256) alias_rows_cta_kernel(
+    const cd* __restrict__ Y, int64_t n, int64_t b, int L, const __grid_constant__ AliasShifts sh,
+    const int64_t* __restrict__ idx, int64_t nrows, cd* __restrict__ rows, bool tabled) {
+  extern __shared__ cd alias_smem[];
+  const int64_t r = blockIdx.x;
+  if (r >= nrows) return;
+  const int64_t i = idx[r];
+  cd* x = alias_smem;
+  cd* z = alias_smem + L;
+  cd* rt = tabled ? alias_smem + 2 * L : nullptr;  // w_L^j, j < L/2
+  for (int l = threadIdx.x; l < L; l += blockDim.x) x[l] = Y[i + (int64_t)l * b];
+  if (rt)
+    for (int j = threadIdx.x; j < L / 2; j += blockDim.x) rt[j] = root_pi(j, L);
+  __syncthreads();
+  for (int Ls = 1; Ls < L; Ls <<= 1) {
+    for (int k = threadIdx.x; k < L / 2; k += blockDim.x) {
+      const int j = k & (Ls - 1), g = k / Ls;
+      const cd a = x[g * Ls + j];
+      const cd u = x[g * Ls + j + L / 2];
+      const int m = j * (L / (2 * Ls));
+      const cd t = j ? cmul(u, rt ? rt[m] : root_pi(m, L)) : u;
+      z[2 * g * Ls + j] = cadd(a, t);
+      z[2 * g * Ls + j + Ls] = csub(a, t);
+    }
+    __syncthreads();
+    cd* tmp = x;
+    x = z;
+    z = tmp;
+  }
+  for (int t = threadIdx.x; t < sh.nshift; t += blockDim.x) {
+    const int64_t tau = sh.tau[t];
+    rows[r * sh.nshift + t] = cmul(x[(int)(tau & (L - 1))], root_pi(mulmod(i, tau, n), n));
   }
 }
 
@@ -479,18 +544,30 @@ __global__ void __launch_bounds__(256) deep_count_kernel(const uint32_t* __restr
 }
 
 // exclusive scan of the chunk counts within each layer (one CTA), layer totals out
+// one warp per layer: lanes take contiguous runs of chunks, a warp scan joins them
 __global__ void deep_scan_kernel(int32_t* __restrict__ chunk_cnt,
                                  const __grid_constant__ DeepLayers D,
                                  int32_t* __restrict__ layer_count) {
-  for (int j = threadIdx.x; j < D.nl; j += blockDim.x) {
-    int run = 0;
-    for (int64_t c = D.chunk_off[j]; c < D.chunk_off[j + 1]; ++c) {
-      const int v = chunk_cnt[c];
-      chunk_cnt[c] = run;
-      run += v;
-    }
-    layer_count[j] = run;
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (j >= D.nl) return;
+  const int64_t c0 = D.chunk_off[j], nc = D.chunk_off[j + 1] - c0;
+  const int64_t per = (nc + 31) / 32;
+  const int64_t lo = c0 + min(nc, lane * per), hi = c0 + min(nc, (lane + 1) * per);
+  int local = 0;
+  for (int64_t c = lo; c < hi; ++c) local += chunk_cnt[c];
+  int x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  int run = x - local;
+  for (int64_t c = lo; c < hi; ++c) {
+    const int v = chunk_cnt[c];
+    chunk_cnt[c] = run;
+    run += v;
+  }
+  if (lane == 31) layer_count[j] = x;
 }
 
 // ascending bucket indices of every layer: list j at out + j * cap (first cap kept)
@@ -587,7 +664,7 @@ int deep_active_all(const double* spectrum, int64_t n, int64_t bmin, int nl, con
   AFFT_CHECK_LAUNCH("deep_flags_kernel");
   const unsigned chunks = (unsigned)D.chunk_off[nl];
   deep_count_kernel<<<chunks, 256, 0, st>>>(words, D, chunk);
-  deep_scan_kernel<<<1, 32, 0, st>>>(chunk, D, counts);
+  deep_scan_kernel<<<1, 32 * kDeepMaxLayers, 0, st>>>(chunk, D, counts);
   deep_write_kernel<<<chunks, 256, 0, st>>>(words, D, chunk, out, cap);
   AFFT_CHECK_LAUNCH("deep_write_kernel");
   return AFFT_OK;
@@ -711,7 +788,9 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
     return AFFT_EINVAL;
   }
   const int64_t L = n / b;
-  if (L > kAliasRowsMaxL || ((energy || values0) && L > kAliasMaxL)) {
+  const bool pow2L = (L & (L - 1)) == 0;
+  if ((L > kAliasRowsMaxL && !(pow2L && !energy && !values0 && L <= (1 << 14))) ||
+      ((energy || values0) && L > kAliasMaxL)) {
     set_error("afft_alias_rows: n/b = %lld above %d (rows) / %d (energies, values)",
               (long long)L, kAliasRowsMaxL, kAliasMaxL);
     return AFFT_EUNSUPPORTED;
@@ -722,10 +801,21 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
     AliasShifts sh;
     sh.nshift = nshift;
     for (int t = 0; t < nshift; ++t) sh.tau[t] = host_pymod(shifts[t], n);
-    const size_t smem = (size_t)(1 + kAliasWarps) * L * sizeof(cd);
-    alias_rows_kernel<<<(unsigned)((nrows + kAliasWarps - 1) / kAliasWarps), kAliasWarps * 32,
-                        smem, st>>>(Y, n, b, (int)L, sh, bucket_idx, nrows,
-                                    reinterpret_cast<cd*>(rows));
+    if (L > kAliasRowsMaxL) {  // one CTA per row, 2 L entries of shared memory
+      const bool tabled = L <= 4096;  // the root table fits beside the two buffers
+      const size_t smem = (size_t)(tabled ? 2 * L + L / 2 : 2 * L) * sizeof(cd);
+      cudaError_t e = ensure_smem((const void*)alias_rows_cta_kernel, smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(alias_rows_cta)");
+      alias_rows_cta_kernel<<<(unsigned)nrows, 256, smem, st>>>(
+          Y, n, b, (int)L, sh, bucket_idx, nrows, reinterpret_cast<cd*>(rows), tabled);
+    } else {
+      const size_t smem = (size_t)(1 + 2 * kAliasWarps) * L * sizeof(cd);
+      cudaError_t e = ensure_smem((const void*)alias_rows_kernel, smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(alias_rows)");
+      alias_rows_kernel<<<(unsigned)((nrows + kAliasWarps - 1) / kAliasWarps),
+                          kAliasWarps * 32, smem, st>>>(Y, n, b, (int)L, sh, bucket_idx, nrows,
+                                                        reinterpret_cast<cd*>(rows));
+    }
   }
   if (energy || values0) {
     AliasCosets cs;

@@ -298,14 +298,20 @@ struct Dsfft {
   // Rows from the resident spectrum instead of min(#shifts, L) size-b DFTs over the
   // signal: worth it once Y exists (A*L*R products against ~min(R, L)*b*log b), and
   // worth computing Y for at L <= 64, where one layer's DFTs cost a full transform.
-  // AFFT_DSFFT_Y_L: the largest L at which rows alone justify computing Y (default 64)
+  // AFFT_DSFFT_Y_L: the largest L at which rows alone justify computing Y (default 64).
+  // Rows from Y cost one L-strided gather per active bucket (a sector per alias): at
+  // config 4, L = 2048 / 1024 / 512 took 258 / 121 / 71 us against 20 / 41 / 61 us for
+  // the coset DFTs over the signal, so shallow layers keep the DFTs (ncu launch lists).
   int64_t y_rows_l = [] {
     const char* e = std::getenv("AFFT_DSFFT_Y_L");
     return e ? std::max<int64_t>(1, std::atoll(e)) : 64;
   }();
   bool alias_rows_ok(int64_t b) const {
     const int64_t L = n / b;
-    return L <= kAliasMaxL || (L <= kAliasRowsMaxL && (Y.p || L <= y_rows_l));
+    if (L <= kAliasMaxL) return true;
+    if (L <= kAliasRowsMaxL) return Y.p || L <= y_rows_l;
+    // larger L: one CTA per row (L <= 2^14), only when asked for (AFFT_DSFFT_Y_L)
+    return L <= (1 << 14) && L <= y_rows_l;
   }
 
   // ||Y||^2 for the noisy floor bound: from Y when resident, else by Parseval from x

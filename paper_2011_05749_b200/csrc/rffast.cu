@@ -445,6 +445,14 @@ __global__ void noisy_seed_kernel(int64_t n, int c, int A, const int64_t* __rest
 // per node, same scores, same bound, same (min score, smallest t) result as the CTA
 // kernel's single chunk — a 256-thread CTA per node left most threads idle there.
 constexpr int kWarpSearchMaxL = 1024;
+// the candidate count up to which the warp kernel scans (AFFT_WARP_SEARCH_MAXL, diagnostic)
+static int64_t warp_search_maxl() {
+  static const int64_t v = [] {
+    const char* e = getenv("AFFT_WARP_SEARCH_MAXL");
+    return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)kWarpSearchMaxL;
+  }();
+  return v;
+}
 constexpr int kWarpSearchWarps = 8;
 template <bool k32>
 __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kernel(
@@ -1191,7 +1199,7 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   if (world > 1)
     part_fill_kernel<<<(unsigned)((nparts + 255) / 256), 256, 0, st>>>(nparts, part_s, part_t);
   const int mine = (w.chunks - rank + world - 1) / world;
-  if (world == 1 && w.Lmax <= kWarpSearchMaxL) {  // one chunk: part slot a = node a
+  if (world == 1 && w.Lmax <= warp_search_maxl()) {  // one chunk: part slot a = node a
     auto kfn = P.n < (int64_t(1) << 31) ? noisy_search_warp_kernel<true>
                                         : noisy_search_warp_kernel<false>;
     kfn<<<(unsigned)((A + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
@@ -1294,7 +1302,7 @@ static int enqueue_round(const NoisyPlan& P, const NoisyWs& w, char* ws, int64_t
   noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, cs>>>(0, P.c, P.m, act_row, residual,
                                                                 P.R, P, est, node_bound, A_dev);
   AFFT_CHECK_LAUNCH("noisy_est_kernel");
-  if (w.Lmax <= kWarpSearchMaxL) {  // one chunk per node: part slot a = node a
+  if (w.Lmax <= warp_search_maxl()) {  // one chunk per node: part slot a = node a
     auto kfn = k32 ? noisy_search_warp_kernel<true> : noisy_search_warp_kernel<false>;
     kfn<<<(unsigned)((rows + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
           cs>>>(P.n, P.c, 0, act_index, act_b, est, part_s, part_t, A_dev);
