@@ -474,6 +474,206 @@ __global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
   }
 }
 
+// ---- the same pass with its row loads on the TMA engine (bulk async copies into a
+// double-buffered shared-memory stage, completion on an mbarrier): a persistent CTA
+// issues tile k+1's R row segments before computing tile k, so loads overlap the
+// DFT work instead of alternating with it per CTA.  Used when every row segment is
+// contiguous in memory: every pass after the first, and a first pass over a plain
+// (L = 1, tau = 0) signal — the DSFFT spectrum and the dense transform.  Same
+// arithmetic as gfft_reg_kernel (bit-identical outputs).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int LA, int LB>
+__global__ void __launch_bounds__(kGfftThreads) gfft_tma_kernel(
+    const __grid_constant__ GStockParams p) {
+  constexpr int A = 1 << LA, B = 1 << LB, LGR = LA + LB, R = A * B;
+  constexpr int kCnt = kGStockPoints / R, kLgCnt = 11 - LGR;
+  constexpr int LD = R + 1;
+  constexpr int IA = kCnt * A / kGfftThreads;
+  constexpr int IB = kCnt * B / kGfftThreads;
+  static_assert(IA * B == 16 && IB * A == 16, "16 points per thread per stage");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const bool first = p.in == nullptr;
+  const bool c64 = first && p.dtype == AFFT_C64;
+  const int esz = c64 ? 8 : 16;
+  const uint32_t seg = (uint32_t)(kCnt * esz);            // bytes per row segment
+  const size_t stage_bytes = (size_t)R * kCnt * 16;          // sized for c128
+  unsigned char* stage[2] = {smem_raw, smem_raw + stage_bytes};
+  cd* twR = reinterpret_cast<cd*>(smem_raw + 2 * stage_bytes);
+  cd* U = twR + R;
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  build_twiddles(twR, R, tid, kGfftThreads);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nb = p.b / R;
+  const int64_t nchunks = nb >> kLgCnt;
+  const int64_t ntiles = p.batch * p.nshift * nchunks;
+  const int64_t tstep = p.b / (p.Ns * R);
+  const bool pow2ns = (p.Ns & (p.Ns - 1)) == 0;
+  const double inv_b = 1.0 / (double)p.b;
+  const int64_t in_esz = first ? esz : 16;
+  // row segments of one tile -> stage[buf]: warp 0's lanes issue R / 32 bulk copies each
+  auto issue = [&](int64_t tile, int buf) {
+    if (tid >= 32) return;
+    const int64_t chunk = tile % nchunks;
+    const int64_t st_ = tile / nchunks;
+    const int t = (int)(st_ % p.nshift);
+    const int64_t s = st_ / p.nshift;
+    const int64_t seq = s * p.nshift + t;
+    const char* base = first ? reinterpret_cast<const char*>(p.x) + s * p.ld * in_esz
+                             : reinterpret_cast<const char*>(p.in + seq * p.b);
+    const int64_t j0 = chunk << kLgCnt;
+    // the previous reads of this buffer (generic proxy) before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tid == 0) mbar_arrive_expect_tx(&bar[buf], (uint32_t)R * seg);
+    __syncwarp();
+    for (int r = tid; r < R; r += 32)
+      bulk_load(stage[buf] + (size_t)r * seg, base + (j0 + (int64_t)r * nb) * in_esz, seg,
+                &bar[buf]);
+  };
+  uint32_t phase[2] = {0u, 0u};
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, 0);
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) issue(next, buf ^ 1);  // its buffer was released at the end of it-1
+    const int64_t chunk = tile % nchunks;
+    const int64_t st_ = tile / nchunks;
+    const int t = (int)(st_ % p.nshift);
+    const int64_t s = st_ / p.nshift;
+    const int64_t j0 = chunk << kLgCnt;
+    const int64_t k0 = pow2ns ? (j0 & (p.Ns - 1)) : j0 % p.Ns;
+    auto kmod = [&](int jj) -> int64_t {
+      if (pow2ns) return (j0 + jj) & (p.Ns - 1);
+      int64_t k = k0 + jj;
+      while (k >= p.Ns) k -= p.Ns;
+      return k;
+    };
+    const int64_t seq = s * p.nshift + t;
+    mbar_wait(&bar[buf], phase[buf]);
+    phase[buf] ^= 1u;
+    // ---- stage A from the staged rows
+    cd v[IA][B];
+#pragma unroll
+    for (int i = 0; i < IA; ++i) {
+      const int w = tid + i * kGfftThreads;
+      const int jj = w & (kCnt - 1), n1 = w >> kLgCnt;
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) {
+        const int r = n1 + A * n2;
+        if (c64) {
+          const float2 f = reinterpret_cast<const float2*>(stage[buf])[r * kCnt + jj];
+          v[i][n2] = cd{(double)f.x, (double)f.y};
+        } else {
+          const double2 d = reinterpret_cast<const double2*>(stage[buf])[r * kCnt + jj];
+          v[i][n2] = cd{d.x, d.y};
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < IA; ++i) {
+      const int w = tid + i * kGfftThreads;
+      const int jj = w & (kCnt - 1), n1 = w >> kLgCnt;
+      if (p.Ns > 1) {
+        const int64_t kt = kmod(jj) * tstep;
+        if (kt) {
+          cd cur = tw_b(p.tlo, p.thi, kt * n1);
+          const cd step = tw_b(p.tlo, p.thi, kt * A);
+#pragma unroll
+          for (int n2 = 0; n2 < B; ++n2) {
+            if (n1 || n2) v[i][n2] = cmul(v[i][n2], cur);
+            if (n2 + 1 < B) cur = cmul(cur, step);
+          }
+        }
+      }
+      dft_reg<B>(v[i]);
+      cd* u = U + jj * LD + n1 * B;
+#pragma unroll
+      for (int qb = 0; qb < B; ++qb) u[qb] = (n1 && qb) ? cmul(v[i][qb], twR[n1 * qb]) : v[i][qb];
+    }
+    __syncthreads();
+    // ---- stage B: DFT_A over n1, outputs q = qb + B qa
+    double* out = p.out ? p.out + 2 * (s * p.out_signal_stride + p.out_offset +
+                                       t * p.out_shift_stride)
+                        : nullptr;
+    cd* tmp = p.tmp ? p.tmp + seq * p.b : nullptr;
+#pragma unroll
+    for (int i = 0; i < IB; ++i) {
+      const int w = tid + i * kGfftThreads;
+      int jj, qb;
+      if (p.Ns == 1) {
+        qb = w & (B - 1);
+        jj = w >> LB;
+      } else {
+        jj = w & (kCnt - 1);
+        qb = w >> kLgCnt;
+      }
+      cd a[A];
+      const cd* u = U + jj * LD + qb;
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) a[n1] = u[n1 * B];
+      dft_reg<A>(a);
+      const int64_t j = j0 + jj;
+      const int64_t k = kmod(jj);
+      const int64_t base = (j - k) * R + k;
+#pragma unroll
+      for (int qa = 0; qa < A; ++qa) {
+        const int64_t dst = base + (int64_t)(qb + B * qa) * p.Ns;
+        if (tmp) {
+          __stcs(reinterpret_cast<double2*>(tmp + dst), make_double2(a[qa].re, a[qa].im));
+        } else {
+          const cd wv = cscale(a[qa], inv_b);
+          *reinterpret_cast<double2*>(out + 2 * dst * p.out_bin_stride) = make_double2(wv.re, wv.im);
+        }
+      }
+    }
+    __syncthreads();  // U and this tile's stage are free again
+  }
+}
+
+static const void* gfft_tma_fn(int lgr) {
+  switch (lgr) {
+    case 4: return (const void*)gfft_tma_kernel<2, 2>;
+    case 5: return (const void*)gfft_tma_kernel<3, 2>;
+    case 6: return (const void*)gfft_tma_kernel<3, 3>;
+    case 7: return (const void*)gfft_tma_kernel<4, 3>;
+    case 8: return (const void*)gfft_tma_kernel<4, 4>;
+    default: return nullptr;
+  }
+}
+
 static const void* gfft_reg_fn(int lgr) {
   switch (lgr) {
     case 2: return (const void*)gfft_reg_kernel<1, 1>;
@@ -631,7 +831,20 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     const void* kfn = lgr < 0 ? (const void*)gstockham_kernel<-1> : gstockham_fixed_table()[lgr];
     size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
     int threads = kGStockThreads;
-    if (lgr >= 2 && !fft_smem_path()) {  // register-resident pass
+    // TMA-staged register pass when every row segment is contiguous and 16-B aligned
+    const bool contiguous = s > 0 || (q.L == 1 && nshift == 1 && q.tau[0] == 0 && !shift_table &&
+                                      (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                                      (batch == 1 || (ld * (dtype == AFFT_C64 ? 8 : 16)) % 16 == 0));
+    static const bool tma_env = [] {
+      const char* v = getenv("AFFT_FFT_TMA");
+      return !(v && v[0] == '0');
+    }();
+    if (lgr >= 4 && !fft_smem_path() && contiguous && tma_env) {
+      kfn = gfft_tma_fn(lgr);
+      g.perm = 0;
+      smem = 2 * (size_t)R * g.cnt * 16 + (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
+      threads = kGfftThreads;
+    } else if (lgr >= 2 && !fft_smem_path()) {  // register-resident pass
       kfn = gfft_reg_fn(lgr);
       const int64_t nch = (b / R) / g.cnt;
       static const int perm_env = [] {

@@ -3,7 +3,7 @@
 //
 // Everything is register/local-memory resident and runs in one thread; matrices
 // are at most kLaMaxRows x kLaMaxCols.  Written host+device so the same source is
-// unit-tested on the CPU against numpy (tests/test_smallla_host.py).
+// unit-tested on the CPU against numpy (tests/test_dt_core_host.py via tests/native/).
 //   svd_jacobi   one-sided (Hestenes) Jacobi SVD: accurate small singular values,
 //                which the sFFT-DT vote quantises at 1e-12 (oneshot.py:136);
 //   lstsq        SVD least squares with numpy's lstsq cutoff eps*max(m,n)*smax

@@ -3,8 +3,9 @@
 Drop-in for /root/reference/pkg/src/aliasfft/oneshot.py.  The configuration and
 the seeded random-shift draw (``rng.choice(n, p, replace=False)``, 93-94) stay
 on the host; measurement collection, the Hankel-SVD vote, localisation (roots /
-grid enumeration / matrix pencil) and subspace pursuit run in csrc/oneshot.cu,
-one thread per bucket for the per-bucket solves.
+grid enumeration / matrix pencil) and subspace pursuit run in csrc/oneshot.cu:
+dt2's grid scan and the pursuit one warp (or half-warp, p <= 16) per bucket, the
+dt1/dt3 roots one thread per bucket over rows grouped by tone count.
 """
 
 from __future__ import annotations
