@@ -414,6 +414,11 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        # NCCL's communicator INIT lines (nranks per comm) on stderr, also when the
+        # driver launches torchrun itself
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2011_05749_b200.shard import gather_slots, max_over_ranks, shard_range
 
