@@ -835,9 +835,12 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     const bool contiguous = s > 0 || (q.L == 1 && nshift == 1 && q.tau[0] == 0 && !shift_table &&
                                       (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
                                       (batch == 1 || (ld * (dtype == AFFT_C64 ? 8 : 16)) % 16 == 0));
+    // opt-in: with 128-byte row segments (256 bulk requests per 32 KB tile) the TMA
+    // form measured 0.97 ms against 0.34 ms for the register-load form on a 2^24 c128
+    // transform (tools/k2_time.py, identical outputs); the requests are too small
     static const bool tma_env = [] {
       const char* v = getenv("AFFT_FFT_TMA");
-      return !(v && v[0] == '0');
+      return v && v[0] == '1';
     }();
     if (lgr >= 4 && !fft_smem_path() && contiguous && tma_env) {
       kfn = gfft_tma_fn(lgr);

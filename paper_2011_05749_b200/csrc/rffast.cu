@@ -482,13 +482,18 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
   const int64_t b = act_b[a];
   const int64_t L = n / b;
   const int64_t idx = act_index[a];
-  const ApproxScan ap = make_approx(n, L, idx, c, !bad);  // see approx_pruned
+  // one candidate per lane (L <= 32, DSFFT's deep layers): no pruning bound to seed
+  // and no pre-filter to set up — both cost a candidate's worth of dependent work and
+  // could only save part of one score; every candidate is scored in full instead
+  const bool single = L <= 32;
+  const ApproxScan ap = make_approx(n, L, idx, c, !bad && !single);  // see approx_pruned
   const double dn = (double)n;
   const double inv = 1.0 / dn;
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
   double best = __longlong_as_double(0x7ff0000000000000LL);
   int32_t bt = INT32_MAX;
-  double bound = search_bound<k32>(n, b, L, idx, s_est, c, inv);
+  double bound = single ? __longlong_as_double(0x7ff0000000000000LL)
+                        : search_bound<k32>(n, b, L, idx, s_est, c, inv);
   // the warp shares its pruning bound after every 32 candidates (see shared_bound)
   for (int64_t tb = 0; tb < L; tb += 32) {
     const int64_t t = tb + lane;
