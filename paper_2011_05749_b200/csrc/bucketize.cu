@@ -15,6 +15,9 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "afft_common.cuh"
 #include "gather_dft.cuh"
 
@@ -511,7 +514,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 
 template <int LA, int LB>
 __global__ void __launch_bounds__(kGfftThreads) gfft_tma_kernel(
-    const __grid_constant__ GStockParams p) {
+    const __grid_constant__ GStockParams p, const __grid_constant__ CUtensorMap tmap,
+    int use_tmap) {
   constexpr int A = 1 << LA, B = 1 << LB, LGR = LA + LB, R = A * B;
   constexpr int kCnt = kGStockPoints / R, kLgCnt = 11 - LGR;
   constexpr int LD = R + 1;
@@ -524,8 +528,12 @@ __global__ void __launch_bounds__(kGfftThreads) gfft_tma_kernel(
   const int esz = c64 ? 8 : 16;
   const uint32_t seg = (uint32_t)(kCnt * esz);            // bytes per row segment
   const size_t stage_bytes = (size_t)R * kCnt * 16;          // sized for c128
-  unsigned char* stage[2] = {smem_raw, smem_raw + stage_bytes};
-  cd* twR = reinterpret_cast<cd*>(smem_raw + 2 * stage_bytes);
+  // TMA destinations must be 128-byte aligned: the dynamic region follows the static
+  // one, so align by hand (the launch adds 128 bytes)
+  unsigned char* sm0 = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  unsigned char* stage[2] = {sm0, sm0 + stage_bytes};
+  cd* twR = reinterpret_cast<cd*>(sm0 + 2 * stage_bytes);
   cd* U = twR + R;
   __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x;
@@ -556,6 +564,19 @@ __global__ void __launch_bounds__(kGfftThreads) gfft_tma_kernel(
     const int64_t j0 = chunk << kLgCnt;
     // the previous reads of this buffer (generic proxy) before the async-proxy writes
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (use_tmap) {  // one tensor request: box [1 seq][R rows][kCnt points]
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&bar[buf], (uint32_t)R * seg);
+        const int c0 = (int)(j0 * 2), c2 = (int)seq;
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(stage[buf])),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(c0), "r"(0), "r"(c2),
+            "r"(smem_u32(&bar[buf]))
+            : "memory");
+      }
+      return;
+    }
     if (tid == 0) mbar_arrive_expect_tx(&bar[buf], (uint32_t)R * seg);
     __syncwarp();
     for (int r = tid; r < R; r += 32)
@@ -663,6 +684,15 @@ __global__ void __launch_bounds__(kGfftThreads) gfft_tma_kernel(
   }
 }
 
+// AFFT_FFT_TMAP=1: the staged pass with one TMA tensor request per tile (UTMALDG)
+static bool tmap_env() {
+  static const bool v = [] {
+    const char* e = getenv("AFFT_FFT_TMAP");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 static const void* gfft_tma_fn(int lgr) {
   switch (lgr) {
     case 4: return (const void*)gfft_tma_kernel<2, 2>;
@@ -740,6 +770,43 @@ static bool fft_smem_path() {
     return e && e[0] == '1';
   }();
   return v;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// The input of one register pass as a 3-D tensor of scalars: [seq][R rows][2 nb] with
+// row stride nb points and sequence stride `seq_stride_bytes`; box [1][R][2 kCnt].
+static bool encode_pass_map(CUtensorMap* m, const void* base, bool f32, int64_t nb, int R,
+                            int kCnt, int64_t nseq, int64_t seq_stride_bytes) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int64_t esz = f32 ? 8 : 16;  // bytes per complex point
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || seq_stride_bytes % 16 || (nb * esz) % 16 ||
+      2 * nb > (int64_t(1) << 32) || nseq > (int64_t(1) << 32) || R > 256 || 2 * kCnt > 256)
+    return false;
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * nb), (cuuint64_t)R, (cuuint64_t)nseq};
+  cuuint64_t strides[2] = {(cuuint64_t)(nb * esz), (cuuint64_t)seq_stride_bytes};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * kCnt), (cuuint32_t)R, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                         3, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
@@ -842,11 +909,20 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
       const char* v = getenv("AFFT_FFT_TMA");
       return v && v[0] == '1';
     }();
-    if (lgr >= 4 && !fft_smem_path() && contiguous && tma_env) {
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    int use_tmap = 0;
+    if (lgr >= 4 && !fft_smem_path() && contiguous && (tma_env || tmap_env())) {
       kfn = gfft_tma_fn(lgr);
       g.perm = 0;
-      smem = 2 * (size_t)R * g.cnt * 16 + (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
+      smem = 128 + 2 * (size_t)R * g.cnt * 16 + (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
       threads = kGfftThreads;
+      if (tmap_env()) {
+        const bool f32 = s == 0 && dtype == AFFT_C64;
+        const void* base = s == 0 ? x : (const void*)g.in;
+        const int64_t sstride = s == 0 ? ld * (dtype == AFFT_C64 ? 8 : 16) : b * 16;
+        use_tmap = encode_pass_map(&tmap, base, f32, b / R, R, g.cnt, (int64_t)seqs, sstride) ? 1 : 0;
+      }
     } else if (lgr >= 2 && !fft_smem_path()) {  // register-resident pass
       kfn = gfft_reg_fn(lgr);
       const int64_t nch = (b / R) / g.cnt;
@@ -868,8 +944,11 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     }
     const int64_t tiles = (int64_t)seqs * ((b / R + g.cnt - 1) / g.cnt);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * occ);
-    void* args[] = {&g};
-    e = cudaLaunchKernel(kfn, dim3(grid), dim3(threads), args, smem, stream);
+    void* args_reg[] = {&g};
+    void* args_tma[] = {&g, &tmap, &use_tmap};
+    const bool tma_kernel = kfn == gfft_tma_fn(lgr) && lgr >= 4;
+    e = cudaLaunchKernel(kfn, dim3(grid), dim3(threads), tma_kernel ? args_tma : args_reg, smem,
+                         stream);
     if (e != cudaSuccess) {
       rc = cuda_status(e, "large-b DFT launch");
       break;
