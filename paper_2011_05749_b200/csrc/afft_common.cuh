@@ -39,6 +39,12 @@ int deep_active_all(const double* spectrum, int64_t n, int64_t bmin, int nl, con
                     int64_t* out, int cap, int32_t* counts, void* scratch, size_t scratch_bytes,
                     cudaStream_t st);
 size_t deep_active_scratch(int64_t n, int64_t bmin, int nl);
+// dsfft.cu: every full layer from depth d0 to d0 + nl - 1 (n a power of two, 2^d0 >= 32):
+// deep ones from the spectrum, shallower ones by summing children; one pass + one count.
+int full_active_all(const double* spectrum, int64_t n, int d0, int nl, const double* thr,
+                    int64_t* out, int cap, int32_t* counts, void* scratch, size_t scratch_bytes,
+                    cudaStream_t st);
+size_t full_active_scratch(int64_t n, int d0, int nl);
 // bucketize.cu: build_graph with per-signal raw shifts (device [batch][nshift]).
 int build_graph_table(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                       const int64_t* factors, int32_t ncycles, const int64_t* shift_table,

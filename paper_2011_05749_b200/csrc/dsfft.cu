@@ -478,7 +478,7 @@ int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64
 // warp's flags for one (layer, m) are one 32-bit word of the layer's bitmap (lanes
 // hold consecutive i0); a count / scan / write pass then turns the bitmaps into
 // ascending active lists, all layers at once.
-constexpr int kDeepMaxLayers = 8;
+constexpr int kDeepMaxLayers = 16;
 struct DeepLayers {
   int nl;                          // layers: j = 0 .. nl - 1
   double thr[kDeepMaxLayers];      // activity threshold of layer j
@@ -490,7 +490,8 @@ constexpr int kDeepChunkWords = 2048;  // words per count / write CTA (256 threa
 template <int LM, int LOG2LM>
 __global__ void __launch_bounds__(128) deep_flags_kernel(const cd* __restrict__ Y, int64_t bmin,
                                                          const __grid_constant__ DeepLayers D,
-                                                         uint32_t* __restrict__ words) {
+                                                         int jd, uint32_t* __restrict__ words,
+                                                         cd* __restrict__ v_out) {
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool on = i0 < bmin;
   cd y[LM];
@@ -499,23 +500,25 @@ __global__ void __launch_bounds__(128) deep_flags_kernel(const cd* __restrict__ 
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j <= LOG2LM; ++j) {  // layer j: b = bmin 2^j, L = LM >> j
-    if (j >= D.nl) break;
+    if (jd + j >= D.nl) break;
 #pragma unroll
     for (int m = 0; m < (1 << j); ++m) {
       cd acc = y[m];
 #pragma unroll
       for (int l = 1; l < (LM >> j); ++l) acc = cadd(acc, y[m + (l << j)]);
+      if (j == 0 && v_out && on) v_out[i0] = acc;  // the shallowest deep layer's values
       // |v| > thr decided on |v|^2 against thr^2 with a 1e-14 guard band (|v|^2 in double
       // is within 3 ulp, hypot within 1): only values inside the band take hypot, so
       // every decision equals hypot(v) > thr (alias_active_kernel's test)
       const double sq = acc.re * acc.re + acc.im * acc.im;
-      const double t2 = D.thr[j] * D.thr[j];
+      const double thr = D.thr[jd + j];
+      const double t2 = thr * thr;
       const bool f = sq > t2 * (1.0 + 1e-14) ? true
                      : sq < t2 * (1.0 - 1e-14) ? false
-                                               : cabs_(acc) > D.thr[j];
+                                               : cabs_(acc) > thr;
       const unsigned flags = __ballot_sync(0xffffffffu, on && f);
       if (lane == 0 && on)
-        words[D.word_off[j] + (i0 >> 5) + (int64_t)m * (bmin >> 5)] = flags;
+        words[D.word_off[jd + j] + (i0 >> 5) + (int64_t)m * (bmin >> 5)] = flags;
     }
   }
 }
@@ -618,50 +621,102 @@ __global__ void __launch_bounds__(256) deep_write_kernel(const uint32_t* __restr
   }
 }
 
-// Active lists of the full deep layers b = bmin, 2 bmin, ..., n (nl layers, thr[j] for
-// b = bmin << j) from the resident spectrum: lists [nl][cap] ascending (device),
-// counts [nl] (device; a count above cap means the list is partial).
-int deep_active_all(const double* spectrum, int64_t n, int64_t bmin, int nl, const double* thr,
+// One shallower full layer from the next one: parent = sum of its two children
+// (v_d[i] = v_{d+1}[i] + v_{d+1}[i + 2^d], the identity behind expand_layer's
+// "children {i, i + 2^(d-1)}", dsfft.py:82-115), flags into the layer's bitmap.
+__global__ void __launch_bounds__(256) tree_level_kernel(const cd* __restrict__ vin, int64_t b,
+                                                         double thr, cd* __restrict__ vout,
+                                                         uint32_t* __restrict__ words) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool on = i < b;
+  cd v = cd{0.0, 0.0};
+  if (on) {
+    v = cadd(vin[i], vin[i + b]);
+    vout[i] = v;
+  }
+  const double sq = v.re * v.re + v.im * v.im, t2 = thr * thr;
+  const bool f = on && (sq > t2 * (1.0 + 1e-14) ? true
+                        : sq < t2 * (1.0 - 1e-14) ? false
+                                                  : cabs_(v) > thr);
+  const unsigned flags = __ballot_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && on) words[i >> 5] = flags;
+}
+
+static void full_layers_layout(int64_t n, int d0, int nl, DeepLayers* D, int* jd, size_t* words_b,
+                               size_t* chunks_b, size_t* vbuf_b) {
+  memset(D, 0, sizeof(*D));
+  D->nl = nl;
+  int log2n = 0;
+  while ((int64_t(1) << log2n) < n) ++log2n;
+  const int dd = std::max(d0, log2n - 5);  // first layer with n/b <= 32
+  *jd = dd - d0;
+  for (int j = 0; j < nl; ++j) {
+    const int64_t nw = (int64_t(1) << (d0 + j)) / 32;
+    D->word_off[j + 1] = D->word_off[j] + nw;
+    D->chunk_off[j + 1] = D->chunk_off[j] + (nw + kDeepChunkWords - 1) / kDeepChunkWords;
+  }
+  *words_b = ((size_t)D->word_off[nl] * 4 + 255) & ~size_t(255);
+  *chunks_b = ((size_t)D->chunk_off[nl] * 4 + 255) & ~size_t(255);
+  size_t v = 0;  // values of layers 0 .. jd (the shallow ones and the first deep one)
+  for (int j = 0; j <= *jd && *jd > 0; ++j) v += ((size_t)16 << (d0 + j));
+  *vbuf_b = v;
+}
+
+// Active lists of the full layers at depths d0 .. d0 + nl - 1 (thr[j] for depth d0 + j)
+// from the resident spectrum: the layers with n/b <= 32 in one pass (deep_flags), the
+// shallower ones by summing children pairwise from there down, then one count / scan /
+// write over every layer's bitmap.  lists [nl][cap] ascending (device), counts [nl]
+// (device; a count above cap means the list is partial).
+int full_active_all(const double* spectrum, int64_t n, int d0, int nl, const double* thr,
                     int64_t* out, int cap, int32_t* counts, void* scratch, size_t scratch_bytes,
                     cudaStream_t st) {
-  const int64_t Lmax = n / bmin;
-  if (nl < 1 || nl > kDeepMaxLayers || Lmax > kAliasMaxL || (Lmax >> (nl - 1)) < 1 ||
-      bmin % 32 || n % bmin || (Lmax & (Lmax - 1))) {
-    set_error("deep_active_all: unsupported layers (n=%lld, bmin=%lld, nl=%d)", (long long)n,
-              (long long)bmin, nl);
+  DeepLayers D;
+  int jd = 0;
+  size_t wb = 0, cb = 0, vb = 0;
+  if (nl < 1 || nl > kDeepMaxLayers || (int64_t(1) << d0) < 32 || (n & (n - 1)) ||
+      (int64_t(1) << (d0 + nl - 1)) > n) {
+    set_error("full_active_all: unsupported layers (n=%lld, d0=%d, nl=%d)", (long long)n, d0, nl);
     return AFFT_EUNSUPPORTED;
   }
-  DeepLayers D;
-  memset(&D, 0, sizeof(D));
-  D.nl = nl;
-  for (int j = 0; j < nl; ++j) {
-    D.thr[j] = thr[j];
-    const int64_t nw = (bmin << j) / 32;
-    D.word_off[j + 1] = D.word_off[j] + nw;
-    D.chunk_off[j + 1] = D.chunk_off[j] + (nw + kDeepChunkWords - 1) / kDeepChunkWords;
+  full_layers_layout(n, d0, nl, &D, &jd, &wb, &cb, &vb);
+  if (jd >= nl) {
+    set_error("full_active_all: no layer with n/b <= 32 among the requested ones");
+    return AFFT_EUNSUPPORTED;
   }
-  const size_t words_bytes = ((size_t)D.word_off[nl] * 4 + 255) & ~size_t(255);
-  const size_t need = words_bytes + (size_t)D.chunk_off[nl] * 4;
-  if (!scratch || scratch_bytes < need) {
-    set_error("deep_active_all: scratch of %zu bytes needed", need);
+  for (int j = 0; j < nl; ++j) D.thr[j] = thr[j];
+  if (!scratch || scratch_bytes < wb + cb + vb) {
+    set_error("full_active_all: scratch of %zu bytes needed", wb + cb + vb);
     return AFFT_ENOMEM;
   }
   uint32_t* words = reinterpret_cast<uint32_t*>(scratch);
-  int32_t* chunk = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + words_bytes);
+  int32_t* chunk = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + wb);
+  cd* vbuf = jd > 0 ? reinterpret_cast<cd*>(reinterpret_cast<char*>(scratch) + wb + cb) : nullptr;
+  // layer j's values at vbuf + vofs[j]
+  int64_t vofs[kDeepMaxLayers + 1] = {0};
+  for (int j = 0; j < jd; ++j) vofs[j + 1] = vofs[j] + (int64_t(1) << (d0 + j));
   const cd* Y = reinterpret_cast<const cd*>(spectrum);
+  const int64_t bmin = int64_t(1) << (d0 + jd);
+  const int64_t Lmax = n / bmin;
+  cd* vdeep = vbuf ? vbuf + vofs[jd] : nullptr;
   const unsigned grid = (unsigned)((bmin + 127) / 128);
   switch (Lmax) {
-    case 1: deep_flags_kernel<1, 0><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
-    case 2: deep_flags_kernel<2, 1><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
-    case 4: deep_flags_kernel<4, 2><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
-    case 8: deep_flags_kernel<8, 3><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
-    case 16: deep_flags_kernel<16, 4><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
-    case 32: deep_flags_kernel<32, 5><<<grid, 128, 0, st>>>(Y, bmin, D, words); break;
+    case 1: deep_flags_kernel<1, 0><<<grid, 128, 0, st>>>(Y, bmin, D, jd, words, vdeep); break;
+    case 2: deep_flags_kernel<2, 1><<<grid, 128, 0, st>>>(Y, bmin, D, jd, words, vdeep); break;
+    case 4: deep_flags_kernel<4, 2><<<grid, 128, 0, st>>>(Y, bmin, D, jd, words, vdeep); break;
+    case 8: deep_flags_kernel<8, 3><<<grid, 128, 0, st>>>(Y, bmin, D, jd, words, vdeep); break;
+    case 16: deep_flags_kernel<16, 4><<<grid, 128, 0, st>>>(Y, bmin, D, jd, words, vdeep); break;
+    case 32: deep_flags_kernel<32, 5><<<grid, 128, 0, st>>>(Y, bmin, D, jd, words, vdeep); break;
     default:
-      set_error("deep_active_all: n/bmin = %lld is not a power of two <= 32", (long long)Lmax);
+      set_error("full_active_all: n/bmin = %lld is not a power of two <= 32", (long long)Lmax);
       return AFFT_EUNSUPPORTED;
   }
   AFFT_CHECK_LAUNCH("deep_flags_kernel");
+  for (int j = jd - 1; j >= 0; --j) {
+    const int64_t b = int64_t(1) << (d0 + j);
+    tree_level_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
+        vbuf + vofs[j + 1], b, thr[j], vbuf + vofs[j], words + D.word_off[j]);
+  }
+  AFFT_CHECK_LAUNCH("tree_level_kernel");
   const unsigned chunks = (unsigned)D.chunk_off[nl];
   deep_count_kernel<<<chunks, 256, 0, st>>>(words, D, chunk);
   deep_scan_kernel<<<1, 32 * kDeepMaxLayers, 0, st>>>(chunk, D, counts);
@@ -670,14 +725,32 @@ int deep_active_all(const double* spectrum, int64_t n, int64_t bmin, int nl, con
   return AFFT_OK;
 }
 
-size_t deep_active_scratch(int64_t n, int64_t bmin, int nl) {
-  int64_t words = 0, chunks = 0;
-  for (int j = 0; j < nl; ++j) {
-    const int64_t nw = (bmin << j) / 32;
-    words += nw;
-    chunks += (nw + kDeepChunkWords - 1) / kDeepChunkWords;
+size_t full_active_scratch(int64_t n, int d0, int nl) {
+  DeepLayers D;
+  int jd = 0;
+  size_t wb = 0, cb = 0, vb = 0;
+  full_layers_layout(n, d0, nl, &D, &jd, &wb, &cb, &vb);
+  return wb + cb + vb;
+}
+
+// The deep layers alone (b = bmin .. n, all with n/b <= 32).
+int deep_active_all(const double* spectrum, int64_t n, int64_t bmin, int nl, const double* thr,
+                    int64_t* out, int cap, int32_t* counts, void* scratch, size_t scratch_bytes,
+                    cudaStream_t st) {
+  int d0 = 0;
+  while ((int64_t(1) << d0) < bmin) ++d0;
+  if ((int64_t(1) << d0) != bmin || n / bmin > kAliasMaxL) {
+    set_error("deep_active_all: unsupported layers (n=%lld, bmin=%lld)", (long long)n,
+              (long long)bmin);
+    return AFFT_EUNSUPPORTED;
   }
-  return (((size_t)words * 4 + 255) & ~size_t(255)) + (size_t)chunks * 4;
+  return full_active_all(spectrum, n, d0, nl, thr, out, cap, counts, scratch, scratch_bytes, st);
+}
+
+size_t deep_active_scratch(int64_t n, int64_t bmin, int nl) {
+  int d0 = 0;
+  while ((int64_t(1) << d0) < bmin) ++d0;
+  return full_active_scratch(n, d0, nl);
 }
 
 }  // namespace afft

@@ -377,7 +377,41 @@ struct Dsfft {
     return std::max(P.activity_floor, 3.0 * noise_std / std::sqrt((double)(1LL << depth)));
   }
 
+  // AFFT_ACTIVE_SORT_CAP lowers the capacity of the one-pass active lists (tests force
+  // the per-layer fallbacks with it); read per call
+  static int active_cap(int64_t b) {
+    const char* cap_var = std::getenv("AFFT_ACTIVE_SORT_CAP");
+    const int64_t cap_env = cap_var ? std::max<int64_t>(1, std::atoll(cap_var)) : 16384;
+    return (int)std::min<int64_t>(b, std::min<int64_t>(16384, cap_env));
+  }
+
+  // A full layer's active set from the cached one-pass lists (layers_all), if held.
+  bool cached_layer(int depth, int kind, Layer& out, int* rc) {
+    *rc = AFFT_OK;
+    if (!deep_done || depth < deep_d0 || depth >= deep_d0 + deep_nl) return false;
+    const int j = depth - deep_d0;
+    if (deep_counts[j] > std::min(active_cap(1LL << depth), deep_cap)) return false;
+    out.depth = depth;
+    out.m = deep_counts[j];
+    if ((*rc = out.active.alloc((size_t)std::max<int64_t>(out.m, 1) * 8, st, "dsfft active")))
+      return true;
+    if (out.m) {
+      const cudaError_t e =
+          cudaMemcpyAsync(out.active.p, deep_lists.as<int64_t>() + (int64_t)j * deep_cap,
+                          (size_t)out.m * 8, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) {
+        *rc = cuda_status(e, "dsfft cached active list");
+        return true;
+      }
+    }
+    PMARK("active set");
+    tr.add(kind, depth, out.m, -1);
+    return true;
+  }
+
   int initial(int depth, Layer& out) {
+    int crc = AFFT_OK;
+    if (cached_layer(depth, 1, out, &crc)) return crc;
     DBuf vals;
     RC(full_values(1LL << depth, vals));
     out.depth = depth;
@@ -412,25 +446,17 @@ struct Dsfft {
       tr.add(2, depth, out.m, nc);
       return AFFT_OK;
     }
+    {
+      int crc = AFFT_OK;
+      if (cached_layer(depth, 2, out, &crc)) return crc;
+    }
     if (alias_ok(b)) {  // deep layer: active set in one pass over Y, values never stored
       RC(spectrum());
-      // alias_active's sort capacity; AFFT_ACTIVE_SORT_CAP lowers it (tests force the
-      // fallback path with it)
-      const char* cap_var = std::getenv("AFFT_ACTIVE_SORT_CAP");  // read per layer (tests)
-      const int64_t cap_env = cap_var ? std::max<int64_t>(1, std::atoll(cap_var)) : 16384;
-      const int cap = (int)std::min<int64_t>(b, std::min<int64_t>(16384, cap_env));
-      if (!deep_done && !std::getenv("AFFT_DSFFT_DEEP_PER_LAYER")) RC(deep_all(depth, cap));
-      if (deep_done && depth >= deep_d0 && depth < deep_d0 + deep_nl &&
-          deep_counts[depth - deep_d0] <= std::min(cap, deep_cap)) {
-        const int j = depth - deep_d0;
-        out.m = deep_counts[j];
-        RC(out.active.alloc((size_t)std::max<int64_t>(out.m, 1) * 8, st, "dsfft active"));
-        if (out.m)
-          CK(cudaMemcpyAsync(out.active.p, deep_lists.as<int64_t>() + (int64_t)j * deep_cap,
-                             (size_t)out.m * 8, cudaMemcpyDeviceToDevice, st));
-        PMARK("active set");
-        tr.add(2, depth, out.m, -1);
-        return AFFT_OK;
+      const int cap = active_cap(b);
+      if (!deep_done && !std::getenv("AFFT_DSFFT_DEEP_PER_LAYER")) {
+        RC(layers_all(depth, cap));
+        int crc = AFFT_OK;
+        if (cached_layer(depth, 2, out, &crc)) return crc;
       }
       RC(out.active.alloc((size_t)cap * 8, st, "dsfft active"));
       DBuf cnt;
@@ -453,20 +479,22 @@ struct Dsfft {
     return AFFT_OK;
   }
 
-  // The active lists of every full deep layer from `depth` to the bottom, one pass.
-  int deep_all(int depth, int cap) {
+  // The active lists of every full layer from `depth` to the bottom in one pass over
+  // the resident spectrum (full_active_all): the layers with n/b <= 32 directly, the
+  // shallower ones by summing children pairwise; one read-back of all the counts.
+  int layers_all(int depth, int cap) {
     deep_done = true;  // attempted: a failure below leaves the per-layer path
     const int nl = max_depth - depth + 1;
-    const int64_t bmin = 1LL << depth;
-    if (nl < 1 || nl > 8 || bmin % 32) return AFFT_OK;
+    if (nl < 1 || nl > 16 || (1LL << depth) < 32 || (n & (n - 1))) return AFFT_OK;
+    RC(spectrum());
     std::vector<double> thr((size_t)nl);
     for (int j = 0; j < nl; ++j) thr[j] = threshold(depth + j);
     DBuf counts, scratch;
-    RC(deep_lists.alloc((size_t)nl * cap * 8, st, "dsfft deep lists"));
-    RC(counts.alloc((size_t)nl * 4, st, "dsfft deep counts"));
-    const size_t sb = deep_active_scratch(n, bmin, nl);
-    RC(scratch.alloc(sb, st, "dsfft deep scratch"));
-    RC(deep_active_all(Y.as<double>(), n, bmin, nl, thr.data(), deep_lists.as<int64_t>(), cap,
+    RC(deep_lists.alloc((size_t)nl * cap * 8, st, "dsfft layer lists"));
+    RC(counts.alloc((size_t)nl * 4, st, "dsfft layer counts"));
+    const size_t sb = full_active_scratch(n, depth, nl);
+    RC(scratch.alloc(sb, st, "dsfft layer scratch"));
+    RC(full_active_all(Y.as<double>(), n, depth, nl, thr.data(), deep_lists.as<int64_t>(), cap,
                        counts.as<int32_t>(), scratch.p, sb, st));
     RC(d2h(deep_counts, counts.p, (size_t)nl, st));
     deep_d0 = depth;
@@ -705,6 +733,17 @@ struct Dsfft {
     depth = std::min(depth, max_depth);
     Layer layer, next;
     PMARK("start");
+    // noisy decodes of large signals reach the bottom layer (the re-expansion runs while
+    // multitons remain, dsfft.py:190-192), so the spectrum is computed first and every
+    // full layer's active set comes from it in one pass (AFFT_DSFFT_LAYERS_UPFRONT=0:
+    // per layer)
+    static const bool upfront = [] {
+      const char* e = std::getenv("AFFT_DSFFT_LAYERS_UPFRONT");
+      return !(e && e[0] == '0');
+    }();
+    if (upfront && P.mode != 0 && n >= (1LL << 16) && (1LL << depth) >= 32 &&
+        !std::getenv("AFFT_DSFFT_DEEP_PER_LAYER"))
+      RC(layers_all(depth, active_cap(n)));
     RC(initial(depth, layer));
     PMARK("initial");
     while ((double)layer.m < P.theta * k && layer.depth < max_depth) {
