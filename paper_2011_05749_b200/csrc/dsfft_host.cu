@@ -168,7 +168,22 @@ int d2h(std::vector<T>& h, const void* d, size_t count, cudaStream_t st) {
   void* stage = pinned_acquire(bytes, &cap);  // a pageable D2H copy costs a bounce
   cudaError_t e = cudaMemcpyAsync(stage ? stage : (void*)h.data(), d, bytes,
                                   cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) {
+    // AFFT_BLOCKING_SYNC=1: wait on a blocking-sync event (the thread sleeps) instead of
+    // the stream's spin-wait — many concurrent decodes on few host cores
+    static const bool blocking = [] {
+      const char* v = std::getenv("AFFT_BLOCKING_SYNC");
+      return v && v[0] == '1';
+    }();
+    if (blocking) {
+      thread_local cudaEvent_t ev = nullptr;
+      if (!ev) e = cudaEventCreateWithFlags(&ev, cudaEventBlockingSync | cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+      if (e == cudaSuccess) e = cudaEventSynchronize(ev);
+    } else {
+      e = cudaStreamSynchronize(st);
+    }
+  }
   if (e == cudaSuccess && stage) std::memcpy(h.data(), stage, bytes);
   pinned_release(stage, cap);
   if (g_prof.on) {
@@ -318,7 +333,7 @@ struct Dsfft {
   // (sum |x|^2 / n); only ever compared against a bound with a wide margin.
   int norm_y() {
     if (normY >= 0) return AFFT_OK;
-    if (Y.p) {
+    if (Y.p && dtype != AFFT_C64) {  // a c64 signal is half the bytes of its spectrum
       DBuf s;
       RC(s.alloc(8, st, "dsfft norm"));
       CK(cudaMemsetAsync(s.p, 0, 8, st));

@@ -171,6 +171,98 @@ __global__ void roots_kernel(int64_t L, la::c2* __restrict__ roots) {
 // count, 0 for an empty bucket, -1 for None.
 constexpr int kDt2LocateThreads = 256;
 
+// One lane's part of the dt2 grid scan for a bucket whose moment polynomial has degree
+// A, then the warp's butterfly merge: bv/bj (A valid slots, the rest +inf / none) end
+// up holding the `take` smallest (|P|, j) over all n/b candidates — the stable argsort's
+// first `take` (oneshot.py:193-198).
+template <int A>
+__device__ __forceinline__ void dt2_scan(const la::c2* __restrict__ coef, int64_t bucket,
+                                         int64_t b, int64_t n, int64_t step, int take,
+                                         const la::c2* __restrict__ rootsL, int lane, double* bv_out,
+                                         int64_t* bj_out) {
+  constexpr int64_t kNone = INT64_MAX;
+  la::c2 coeffs[A];
+#pragma unroll
+  for (int k = 0; k < A; ++k) coeffs[k] = coef[k];
+  double bv[A];
+  int64_t bj[A];
+#pragma unroll
+  for (int i = 0; i < A; ++i) {
+    bv[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    bj[i] = kNone;
+  }
+  auto insert = [&](double v, int64_t j) {
+#pragma unroll
+    for (int i = 0; i < A; ++i) {
+      const bool before = i < take && j != kNone &&
+                          (bj[i] == kNone || v < bv[i] || (v == bv[i] && j < bj[i]));
+      if (before) {
+        const double tv = bv[i];
+        const int64_t tj = bj[i];
+        bv[i] = v;
+        bj[i] = j;
+        v = tv;
+        j = tj;
+      }
+    }
+  };
+  const la::c2 z0 = dt::root_pi_(bucket, n);
+  double worst = __longlong_as_double(0x7ff0000000000000ll);
+  double worst_sq = worst;
+  bool full = false;
+  auto consider = [&](la::c2 y, int64_t j) {
+    if (full && !(la::abs2(y) <= worst_sq)) return;  // |y| > worst beyond any rounding
+    const double v = la::cabs(y);
+    if (full && !(v < worst)) return;  // j ascends within a lane: earlier j wins ties
+    insert(v, j);
+#pragma unroll
+    for (int i = 0; i < A; ++i)
+      if (i == take - 1) {
+        worst = bv[i];
+        full = bj[i] != kNone;
+      }
+    worst_sq = worst * worst * (1.0 + 1e-13);
+  };
+  // explicit FMAs: the kernel is FP64-pipe bound, and the reference's |P| is matched to
+  // rounding only either way (its roots come from exp() per candidate, these from a
+  // table), so only ulp-level ties in the ranking can differ
+  auto fmul = [](la::c2 u, la::c2 v) {
+    return la::C(__fma_rn(u.re, v.re, -u.im * v.im), __fma_rn(u.re, v.im, u.im * v.re));
+  };
+  auto horner = [&](la::c2 z) {
+    la::c2 y = la::add(z, coeffs[A - 1]);  // leading coefficient 1
+#pragma unroll
+    for (int kk = A - 2; kk >= 0; --kk)
+      y = la::C(__fma_rn(y.re, z.re, __fma_rn(-y.im, z.im, coeffs[kk].re)),
+                __fma_rn(y.re, z.im, __fma_rn(y.im, z.re, coeffs[kk].im)));
+    return y;
+  };
+  int64_t j = lane;
+  for (; j + 32 < step; j += 64) {  // two independent chains per lane
+    const la::c2 y0 = horner(fmul(z0, rootsL[j]));
+    const la::c2 y1 = horner(fmul(z0, rootsL[j + 32]));
+    consider(y0, j);
+    consider(y1, j + 32);
+  }
+  for (; j < step; j += 32) consider(horner(fmul(z0, rootsL[j])), j);
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov[A];
+    int64_t oj[A];
+#pragma unroll
+    for (int i = 0; i < A; ++i) {
+      ov[i] = __shfl_xor_sync(0xffffffffu, bv[i], o);
+      oj[i] = __shfl_xor_sync(0xffffffffu, bj[i], o);
+    }
+#pragma unroll
+    for (int i = 0; i < A; ++i) insert(ov[i], oj[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < dt::kMaxAm; ++i) {
+    bv_out[i] = i < A ? bv[i] : __longlong_as_double(0x7ff0000000000000ll);
+    bj_out[i] = i < A ? bj[i] : kNone;
+  }
+}
+
 __global__ void __launch_bounds__(kDt2LocateThreads, 2) dt2_locate_warp_kernel(
     int64_t total, int64_t nrows, int R, int a_m, const double* __restrict__ meas,
     const int32_t* __restrict__ counts, const int64_t* __restrict__ bucket_ids, int a_cap,
@@ -188,96 +280,19 @@ __global__ void __launch_bounds__(kDt2LocateThreads, 2) dt2_locate_warp_kernel(
   }
   const int64_t s = e / nrows;
   const int64_t bucket = bucket_ids ? bucket_ids[e] : e - s * nrows;
-  la::c2 coeffs[dt::kMaxAm];
-#pragma unroll
-  for (int k = 0; k < dt::kMaxAm; ++k)
-    if (k < a) coeffs[k] = coef_all[e * dt::kMaxAm + k];
   const int64_t step = n / b;
   const int take = (int64_t)a < step ? a : (int)step;
   constexpr int64_t kNone = INT64_MAX;
   double bv[dt::kMaxAm];
   int64_t bj[dt::kMaxAm];
-#pragma unroll
-  for (int i = 0; i < dt::kMaxAm; ++i) {
-    bv[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    bj[i] = kNone;
-  }
-  // insert (v, j) into the sorted (value, j) list of the first `take` slots; the
-  // displaced element carries on and the last one drops (compile-time indices only)
-  auto insert = [&](double v, int64_t j) {
-#pragma unroll
-    for (int i = 0; i < dt::kMaxAm; ++i) {
-      const bool before = i < take && j != kNone &&
-                          (bj[i] == kNone || v < bv[i] || (v == bv[i] && j < bj[i]));
-      if (before) {
-        const double tv = bv[i];
-        const int64_t tj = bj[i];
-        bv[i] = v;
-        bj[i] = j;
-        v = tv;
-        j = tj;
-      }
-    }
-  };
-  // candidate z_j = w_n^(bucket + b j) = w_n^bucket * w_L^j  (L = n/b, table roots)
-  const la::c2 z0 = dt::root_pi_(bucket, n);
-  double worst = __longlong_as_double(0x7ff0000000000000ll);  // value in slot take-1
-  double worst_sq = worst;  // worst^2 (1 + 1e-13): a safe cheap reject on |y|^2
-  bool full = false;
-  auto consider = [&](la::c2 y, int64_t j) {
-    if (full && !(la::abs2(y) <= worst_sq)) return;  // |y| > worst beyond any rounding
-    const double v = la::cabs(y);
-    // j ascends within a lane, so an equal value never displaces (earlier j wins)
-    if (full && !(v < worst)) return;
-    insert(v, j);
-#pragma unroll
-    for (int i = 0; i < dt::kMaxAm; ++i)
-      if (i == take - 1) {
-        worst = bv[i];
-        full = bj[i] != kNone;
-      }
-    worst_sq = worst * worst * (1.0 + 1e-13);
-  };
-  // Horner from the leading 1 with compile-time coefficient indices (a runtime index
-  // into coeffs[] would live in local memory); two independent candidates per
-  // iteration, since each chain is a dependent sequence of complex products (four
-  // spill at the 80-register cap and measured slower)
-  // The candidate products and the Horner steps use explicit FMAs (4 instead of 6
-  // and 8 FP64 instructions per complex product / step; the kernel is FP64-pipe
-  // bound).  The reference's |P| values are matched to rounding only either way —
-  // its roots come from exp() of each candidate, these from a table — so only
-  // ulp-level ties in the ranking can differ (SURVEY §8c's correlation/|P| ties).
-  auto fmul = [](la::c2 u, la::c2 v) {
-    return la::C(__fma_rn(u.re, v.re, -u.im * v.im), __fma_rn(u.re, v.im, u.im * v.re));
-  };
-  auto horner = [&](la::c2 z) {
-    la::c2 y = la::C(1.0);
-#pragma unroll
-    for (int kk = dt::kMaxAm - 1; kk >= 0; --kk)
-      if (kk < a)
-        y = la::C(__fma_rn(y.re, z.re, __fma_rn(-y.im, z.im, coeffs[kk].re)),
-                  __fma_rn(y.re, z.im, __fma_rn(y.im, z.re, coeffs[kk].im)));
-    return y;
-  };
-  int64_t j = lane;
-  for (; j + 32 < step; j += 64) {  // two independent Horner chains per lane
-    const la::c2 y0 = horner(fmul(z0, rootsL[j]));
-    const la::c2 y1 = horner(fmul(z0, rootsL[j + 32]));
-    consider(y0, j);
-    consider(y1, j + 32);
-  }
-  for (; j < step; j += 32) consider(horner(fmul(z0, rootsL[j])), j);
-  // butterfly merge: insert the partner lane's list (lists of different lanes are disjoint)
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov[dt::kMaxAm];
-    int64_t oj[dt::kMaxAm];
-#pragma unroll
-    for (int i = 0; i < dt::kMaxAm; ++i) {
-      ov[i] = __shfl_xor_sync(0xffffffffu, bv[i], o);
-      oj[i] = __shfl_xor_sync(0xffffffffu, bj[i], o);
-    }
-#pragma unroll
-    for (int i = 0; i < dt::kMaxAm; ++i) insert(ov[i], oj[i]);
+  // the scan with the polynomial degree a known at compile time (a is uniform in the
+  // warp): exactly a Horner steps and a top-`take` list of a slots, no predicated
+  // padding steps (the runtime-a form ran ~95 instructions per candidate pair)
+  switch (a) {
+    case 1: dt2_scan<1>(coef_all + e * dt::kMaxAm, bucket, b, n, step, take, rootsL, lane, bv, bj); break;
+    case 2: dt2_scan<2>(coef_all + e * dt::kMaxAm, bucket, b, n, step, take, rootsL, lane, bv, bj); break;
+    case 3: dt2_scan<3>(coef_all + e * dt::kMaxAm, bucket, b, n, step, take, rootsL, lane, bv, bj); break;
+    default: dt2_scan<4>(coef_all + e * dt::kMaxAm, bucket, b, n, step, take, rootsL, lane, bv, bj); break;
   }
   if (lane == 0) {
     int64_t pos[dt::kMaxAm];
@@ -356,14 +371,19 @@ __global__ void __launch_bounds__(32, W == 32 ? 24 : 16) dt_estimate_warp_kernel
     int64_t total, int64_t nrows, int R, int a_m, int p, const double* __restrict__ meas,
     const int64_t* __restrict__ rshifts, int64_t shift_stride, const int64_t* __restrict__ cands,
     const int32_t* __restrict__ ncand, int64_t b, int64_t n, int out_stride,
-    int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_cnt) {
+    int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_cnt,
+    const int32_t* __restrict__ order = nullptr) {
   constexpr int G = 32 / W;  // rows per warp
   __shared__ dtw::WarpPursuit<W> pursuit[G];
   __shared__ int64_t cand_s[G][dt::kMaxAm];
   const int g = threadIdx.x / W, lane = threadIdx.x & (W - 1);
   const unsigned gm = dtw::gmask<W>();
-  const int64_t e = (int64_t)blockIdx.x * G + g;
+  int64_t e = (int64_t)blockIdx.x * G + g;
   if (e >= total) return;
+  if (order) {  // rows grouped by a; out_cnt of the rows never listed is zeroed already
+    e = order[e];
+    if (e < 0) return;
+  }
   int nc = 0;
   if (lane == 0) {
     nc = ncand[e];
@@ -581,6 +601,29 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
   cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&cands), cbytes + rbytes, st);
   if (e != cudaSuccess) return cuda_status(e, "scratch (dt candidates)");
   int32_t* ncand = reinterpret_cast<int32_t*>(cands + total * dt::kMaxAm);
+  // rows grouped by tone count a: the thread-per-row locate runs whole warps of one a,
+  // and the pursuit's two half-warp buckets per warp usually share a (and with it
+  // their support sizes and branch structure)
+  int32_t* grp = nullptr;  // bins[8] | fill[8] | order[total]
+  e = scratch_alloc(reinterpret_cast<void**>(&grp), 64 + (size_t)total * 4, st);
+  if (e != cudaSuccess) {
+    scratch_free(cands, st);
+    return cuda_status(e, "scratch (dt row groups)");
+  }
+  int32_t* order = grp + 16;
+  e = cudaMemsetAsync(grp, 0, 64, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(order, 0xff, (size_t)total * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out_cnt, 0, (size_t)total * 4, st);
+  if (e != cudaSuccess) {
+    scratch_free(grp, st);
+    scratch_free(cands, st);
+    return cuda_status(e, "dt row groups");
+  }
+  {
+    const unsigned g = (unsigned)((total + 255) / 256);
+    rows_by_count_kernel<<<g, 256, 0, st>>>(total, counts, a_cap, grp, ncand);
+    rows_scatter_kernel<<<g, 256, 0, st>>>(total, counts, a_cap, grp, grp + 8, order);
+  }
   if (variant == dt::VAR_DT2) {
     char* base = reinterpret_cast<char*>(cands) + cbytes;
     la::c2* roots = reinterpret_cast<la::c2*>(base);
@@ -595,38 +638,21 @@ extern "C" int afft_dt_solve(const double* rows, const int64_t* rand_shifts, int
                                                          counts, bucket_ids, a_cap, b, n, roots,
                                                          coef, cok, cands, ncand);
   } else {
-    int32_t* grp = nullptr;  // bins[8] | fill[8] | order[total]
-    e = scratch_alloc(reinterpret_cast<void**>(&grp), 64 + (size_t)total * 4, st);
-    if (e != cudaSuccess) {
-      scratch_free(cands, st);
-      return cuda_status(e, "scratch (dt row groups)");
-    }
-    int32_t* order = grp + 16;
-    e = cudaMemsetAsync(grp, 0, 64, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(order, 0xff, (size_t)total * 4, st);
-    if (e != cudaSuccess) {
-      scratch_free(grp, st);
-      scratch_free(cands, st);
-      return cuda_status(e, "dt row groups");
-    }
-    const unsigned g = (unsigned)((total + 255) / 256);
-    rows_by_count_kernel<<<g, 256, 0, st>>>(total, counts, a_cap, grp, ncand);
-    rows_scatter_kernel<<<g, 256, 0, st>>>(total, counts, a_cap, grp, grp + 8, order);
     dt_locate_rows_kernel<<<(unsigned)((total + kDtSolveThreads - 1) / kDtSolveThreads),
                             kDtSolveThreads, 0, st>>>(total, nrows, 3 * a_m + p, a_m, rows,
                                                       counts, bucket_ids, a_cap, variant, b, n,
                                                       cands, ncand, order);
-    scratch_free(grp, st);
   }
   const char* wenv = getenv("AFFT_DT_EST_WIDTH");  // 32 forces the full-warp form
   if (p <= 16 && !(wenv && atoi(wenv) == 32))
     dt_estimate_warp_kernel<16><<<(unsigned)((total + 1) / 2), 32, 0, st>>>(
         total, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, p, cands, ncand, b, n, a_m,
-        out_pos, out_val, out_cnt);
+        out_pos, out_val, out_cnt, order);
   else
     dt_estimate_warp_kernel<32><<<(unsigned)total, 32, 0, st>>>(
         total, nrows, 3 * a_m + p, a_m, p, rows, rand_shifts, p, cands, ncand, b, n, a_m,
-        out_pos, out_val, out_cnt);
+        out_pos, out_val, out_cnt, order);
+  scratch_free(grp, st);
   scratch_free(cands, st);
   AFFT_CHECK_LAUNCH("dt_estimate_warp_kernel");
   return AFFT_OK;

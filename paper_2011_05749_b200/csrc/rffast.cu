@@ -444,7 +444,9 @@ __global__ void noisy_seed_kernel(int64_t n, int c, int A, const int64_t* __rest
 // Short candidate lists (L = n / b <= kWarpSearchMaxL, DSFFT's deep layers): one warp
 // per node, same scores, same bound, same (min score, smallest t) result as the CTA
 // kernel's single chunk — a 256-thread CTA per node left most threads idle there.
-constexpr int kWarpSearchMaxL = 1024;
+// 2048: DSFFT's depth-13 nodes (L = 2048) scan faster as one warp each than as one CTA
+// each behind a seed kernel (config 4: 673 -> 708 signals/s, tools/dsfft_gpu_busy.py)
+constexpr int kWarpSearchMaxL = 2048;
 // the candidate count up to which the warp kernel scans (AFFT_WARP_SEARCH_MAXL, diagnostic)
 static int64_t warp_search_maxl() {
   static const int64_t v = [] {
@@ -530,18 +532,33 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
 // Phase estimates of the active nodes (one thread per (node, stride)).
 // A_dev (device-resident rounds): the active count as the prep kernel left it; the
 // grid then covers the largest possible list and the excess threads exit.
+// fill (per-node search of one cycle size, classify_noisy): the active list is the
+// given nodes in order — row a, fill->index[a], fill->b — written here instead of by a
+// separate list kernel.
+struct EstFill {
+  const int64_t* index;
+  int64_t b;
+  int64_t *act_row, *act_index, *act_b;
+};
 __global__ void noisy_est_kernel(int A, int c, int m, const int64_t* __restrict__ act_row,
                                  const double* __restrict__ residual, int R,
                                  const __grid_constant__ NoisyPlan P, double* __restrict__ est,
                                  unsigned long long* __restrict__ node_bound,
-                                 const int32_t* __restrict__ A_dev = nullptr) {
+                                 const int32_t* __restrict__ A_dev = nullptr,
+                                 EstFill fill = EstFill{nullptr, 0, nullptr, nullptr, nullptr}) {
   if (A_dev) A = *A_dev;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)A * c) return;
   const int64_t a = e / c;
   const int j = (int)(e - a * c);
   if (j == 0 && node_bound) node_bound[a] = ~0ull;  // "+inf" for the search kernel
-  const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * R + (int64_t)j * m;
+  if (j == 0 && fill.index) {
+    fill.act_row[a] = a;
+    fill.act_index[a] = fill.index[a];
+    fill.act_b[a] = fill.b;
+  }
+  const int64_t row = fill.index ? a : act_row[a];
+  const cd* y = reinterpret_cast<const cd*>(residual) + row * R + (int64_t)j * m;
   est[e] = stride_estimate(y, m, P.w);
 }
 
@@ -1181,7 +1198,8 @@ struct SearchOut {  // null members: the workspace slots
 static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
                       const double* residual, cudaStream_t st,
                       const AfftSearchShard* shard = nullptr, int64_t rows_total = 0,
-                      const SearchOut& out = SearchOut()) {
+                      const SearchOut& out = SearchOut(), const int64_t* fill_index = nullptr,
+                      int64_t fill_b = 0) {
   if (A == 0) return AFFT_OK;
   const int rank = shard && shard->world > 1 ? shard->rank : 0;
   const int world = shard && shard->world > 1 ? shard->world : 1;
@@ -1195,8 +1213,12 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   double* est = reinterpret_cast<double*>(ws + w.est);
   const int64_t ne = (int64_t)A * P.c;
   unsigned long long* node_bound = reinterpret_cast<unsigned long long*>(ws + w.bound);
+  EstFill fill{fill_index, fill_b, const_cast<int64_t*>(act_row),
+               const_cast<int64_t*>(act_index), const_cast<int64_t*>(act_b)};
+  if (!fill_index) fill = EstFill{nullptr, 0, nullptr, nullptr, nullptr};
   noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(A, P.c, P.m, act_row, residual,
-                                                                P.R, P, est, node_bound);
+                                                                P.R, P, est, node_bound, nullptr,
+                                                                fill);
   AFFT_CHECK_LAUNCH("noisy_est_kernel");
   double* part_s = reinterpret_cast<double*>(ws + w.part_s);
   int32_t* part_t = reinterpret_cast<int32_t*>(ws + w.part_t);
@@ -1470,17 +1492,6 @@ extern "C" int afft_robust_thresholds(const double* energy, const uint8_t* mask,
 }
 
 namespace afft {
-__global__ void search_list_kernel(int64_t count, int64_t b, const int64_t* __restrict__ index,
-                                   int64_t* __restrict__ rows, int64_t* __restrict__ idx,
-                                   int64_t* __restrict__ bs) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < count) {
-    rows[i] = i;
-    idx[i] = index[i];
-    bs[i] = b;
-  }
-}
-
 static int singleton_search(const double* residual, const int64_t* index, int64_t count,
                             int64_t b, int64_t n, const int64_t* shifts, int32_t nshift, int32_t c,
                             int32_t m, const double* weights, int64_t* f0, double* val,
@@ -1504,17 +1515,14 @@ static int singleton_search(const double* residual, const int64_t* index, int64_
     return AFFT_ENOMEM;
   }
   char* ws = reinterpret_cast<char*>(workspace);
-  // active list = the given nodes, rows 0..count-1 of `residual` (filled on the device:
-  // no host staging, no synchronisation)
-  search_list_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(
-      count, b, index, reinterpret_cast<int64_t*>(ws + w.act_row),
-      reinterpret_cast<int64_t*>(ws + w.act_index), reinterpret_cast<int64_t*>(ws + w.act_b));
+  // active list = the given nodes, rows 0..count-1 of `residual`: the estimate kernel
+  // fills it on the device (no host staging, no synchronisation, no extra launch)
   SearchOut out;  // the fit writes straight into the caller's arrays
   out.f0 = f0;
   out.val = val;
   out.res = resnorm;
   out.decide = decide;
-  rc = run_search(*P, w, ws, (int)count, residual, st, nullptr, 0, out);
+  rc = run_search(*P, w, ws, (int)count, residual, st, nullptr, 0, out, index, b);
   if (!rc) AFFT_CHECK_LAUNCH("singleton_search_noisy");
   return rc;
 }
