@@ -158,9 +158,16 @@ def main():
             out = json.load(fh)
     for name in args.configs.split(","):
         cmd = ["ncu", "--profile-from-start", "off", "--clock-control", "none", "--csv",
+               "--graph-profiling", "node",
                "--metrics", ",".join(METRICS), sys.executable, os.path.abspath(__file__),
                "--child", name]
-        p = subprocess.run(cmd, capture_output=True, text=True)
+        env = dict(os.environ)
+        if name in ("c3", "c3auto"):
+            # ncu does not profile the kernels inside the R-FFAST round graph's WHILE
+            # body; the host-driven loop runs the same per-round kernels (its scan on a
+            # grid instead of the persistent ticket grid)
+            env["AFFT_PEEL_GRAPH"] = "0"
+        p = subprocess.run(cmd, capture_output=True, text=True, env=env)
         if p.returncode != 0:
             print(p.stdout[-3000:], p.stderr[-3000:], file=sys.stderr)
             raise SystemExit(f"ncu failed for {name}")
