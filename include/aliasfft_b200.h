@@ -408,6 +408,25 @@ int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k, const AfftDsfftPa
                int64_t* out_count /* host */, int32_t* trace /* host */, int32_t trace_capacity,
                int32_t* trace_len /* host */, void* stream);
 
+/*
+ * dsfft for a batch of signals (x [batch][ld], one power-of-two n) in lockstep: the
+ * spectra and every full layer's active set for all signals first, then one launch
+ * sequence per classify depth for every signal sitting there (rows of all their active
+ * buckets in one list, classify_noisy with per-row signal ids).  params [batch] (host)
+ * as for afft_dsfft.  Outputs per signal s (host): out_pos/out_val [s][capacity],
+ * out_count[s], trace [s][trace_capacity][4], trace_len[s] — identical to afft_dsfft's —
+ * and fallback[s] = 1 for a signal that left the common path (exact mode, calibration,
+ * a selective expansion, an active set beyond the one-pass lists, a classify needing
+ * the all-bucket energy pass, leftover multitons at the bottom): decode those with
+ * afft_dsfft.  Replaces the reference's per-signal dsfft loop (dsfft.py:244-267) for
+ * batches such as BASELINE config 4.  Synchronises.
+ */
+int afft_dsfft_batch(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld, int32_t k,
+                     const AfftDsfftParams* params /* host [batch] */, int64_t* out_pos /* host */,
+                     double* out_val /* host */, int64_t capacity, int64_t* out_count /* host */,
+                     int32_t* trace /* host */, int32_t trace_capacity, int32_t* trace_len /* host */,
+                     int32_t* fallback /* host */, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

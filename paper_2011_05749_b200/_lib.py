@@ -92,6 +92,8 @@ SIGNATURES = {
     "afft_selective_sums": (_INT, [_P, _INT, _I64, _I64, _P, _I64, _P, _P]),
     "afft_median": (_INT, [_P, _I32, _I64, _I64, _P, _P]),
     "afft_dsfft": (_INT, [_P, _INT, _I64, _I32, _P, _P, _P, _I64, _P, _P, _I32, _P, _P]),
+    "afft_dsfft_batch": (_INT, [_P, _INT, _I64, _I64, _I64, _I32, _P, _P, _P, _I64, _P, _P, _I32,
+                                _P, _P, _P]),
 }
 
 _lock = threading.Lock()

@@ -45,6 +45,23 @@ int full_active_all(const double* spectrum, int64_t n, int d0, int nl, const dou
                     int64_t* out, int cap, int32_t* counts, void* scratch, size_t scratch_bytes,
                     cudaStream_t st);
 size_t full_active_scratch(int64_t n, int d0, int nl);
+// rffast.cu: classify_noisy over rows of several signals (row_sig, per-signal shift
+// tables and gates on the device); workspace afft_singleton_workspace_size(n, count, b, c, m).
+int classify_noisy_multi(const double* residual, const int64_t* index, const int32_t* row_sig,
+                         int64_t count, int64_t b, int64_t n, const int64_t* tau_tab, int32_t c,
+                         int32_t m, const double* weights, const double* t0s, const double* t1s,
+                         int8_t* state, int64_t* f0, double* val, double* resnorm,
+                         void* workspace, size_t workspace_bytes, cudaStream_t st);
+// dsfft.cu: rows for (signal, bucket) pairs from per-signal coset DFTs Y [S][U][b]
+// (coset [S][nshift] which DFT serves shift t, q [S][nshift] its rotation).
+int rows_gather_multi(const double* Y, int64_t b, int U, int nshift, const int32_t* coset,
+                      const int64_t* q, const int64_t* idx, const int32_t* sig, int64_t nrows,
+                      double* rows, cudaStream_t st);
+// dsfft.cu: rows for (signal, bucket) pairs from per-signal resident spectra
+// (Y + sig * n), per-signal reduced shifts tau_tab [S][nshift]; n/b <= 256.
+int alias_rows_multi(const double* Y, int64_t n, int64_t b, const int64_t* tau_tab, int nshift,
+                     const int64_t* idx, const int32_t* sig, int64_t nrows, double* rows,
+                     cudaStream_t st);
 // bucketize.cu: build_graph with per-signal raw shifts (device [batch][nshift]).
 int build_graph_table(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                       const int64_t* factors, int32_t ncycles, const int64_t* shift_table,

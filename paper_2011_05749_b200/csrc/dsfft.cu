@@ -57,6 +57,45 @@ __global__ void rows_gather_kernel(const __grid_constant__ RowsParams p, const c
   rows[e] = cmul(y, cd{cs, sn});
 }
 
+// rows_gather_kernel for rows of several signals: row r is bucket idx[r] of signal
+// sig[r]; signal s's shift t is served by its coset DFT coset[s][t] (Y + (s U + coset) b)
+// rotated by q[s][t].
+__global__ void rows_gather_multi_kernel(const cd* __restrict__ Y, int64_t b, int U, int nshift,
+                                         const int32_t* __restrict__ coset,
+                                         const int64_t* __restrict__ q,
+                                         const int64_t* __restrict__ idx,
+                                         const int32_t* __restrict__ sig, int64_t nrows,
+                                         cd* __restrict__ rows) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nrows * nshift) return;
+  const int64_t r = e / nshift;
+  const int t = (int)(e - r * nshift);
+  const int64_t i = idx[r];
+  const int s = sig[r];
+  const int64_t qt = q[(int64_t)s * nshift + t];
+  const cd y = Y[((int64_t)s * U + coset[(int64_t)s * nshift + t]) * b + i];
+  if (qt == 0) {
+    rows[e] = y;
+    return;
+  }
+  const int64_t ph = (i * qt) % b;
+  double sn, cs;
+  sincospi(-2.0 * (double)ph / (double)b, &sn, &cs);
+  rows[e] = cmul(y, cd{cs, sn});
+}
+
+int rows_gather_multi(const double* Y, int64_t b, int U, int nshift, const int32_t* coset,
+                      const int64_t* q, const int64_t* idx, const int32_t* sig, int64_t nrows,
+                      double* rows, cudaStream_t st) {
+  if (nrows == 0) return AFFT_OK;
+  const int64_t tot = nrows * nshift;
+  rows_gather_multi_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const cd*>(Y), b, U, nshift, coset, q, idx, sig, nrows,
+      reinterpret_cast<cd*>(rows));
+  AFFT_CHECK_LAUNCH("rows_gather_multi_kernel");
+  return AFFT_OK;
+}
+
 struct Mult {
   int32_t m[AFFT_MAX_SHIFTS];
 };
@@ -268,6 +307,68 @@ __global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_kernel(
     }
     rows[r * sh.nshift + t] = cmul(acc, root_pi(mulmod(i, tau, n), n));
   }
+}
+
+// alias_rows_kernel for rows of several signals (DSFFT batches): row r is bucket idx[r]
+// of signal sig[r], whose spectrum is Y + sig n and whose reduced shifts are
+// tau_tab[sig][0..nshift); L a power of two <= kAliasRowsMaxL.
+__global__ void __launch_bounds__(kAliasWarps * 32) alias_rows_multi_kernel(
+    const cd* __restrict__ Y, int64_t n, int64_t b, int L, const int64_t* __restrict__ tau_tab,
+    int nshift, const int64_t* __restrict__ idx, const int32_t* __restrict__ sig, int64_t nrows,
+    cd* __restrict__ rows) {
+  extern __shared__ cd alias_smem[];
+  cd* rootL = alias_smem;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  cd* ys = alias_smem + L + 2 * w * L;
+  for (int j = threadIdx.x; j < L; j += blockDim.x) rootL[j] = root_pi(j, L);
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * kAliasWarps + w;
+  if (r >= nrows) return;
+  const int64_t i = idx[r];
+  const int s = sig[r];
+  const cd* Ys = Y + (int64_t)s * n;
+  for (int l = lane; l < L; l += 32) ys[l] = Ys[i + (int64_t)l * b];
+  __syncwarp();
+  cd* x = ys;
+  cd* z = ys + L;
+  for (int Ls = 1; Ls < L; Ls <<= 1) {
+    const int stride = L / (2 * Ls);
+    for (int k = lane; k < L / 2; k += 32) {
+      const int j = k & (Ls - 1), g = k / Ls;
+      const cd a = x[g * Ls + j];
+      const cd t = j ? cmul(x[g * Ls + j + L / 2], rootL[j * stride]) : x[g * Ls + j + L / 2];
+      z[2 * g * Ls + j] = cadd(a, t);
+      z[2 * g * Ls + j + Ls] = csub(a, t);
+    }
+    __syncwarp();
+    cd* tmp = x;
+    x = z;
+    z = tmp;
+  }
+  const int64_t* taus = tau_tab + (int64_t)s * nshift;
+  for (int t = lane; t < nshift; t += 32) {
+    const int64_t tau = taus[t];
+    rows[r * nshift + t] = cmul(x[(int)(tau & (L - 1))], root_pi(mulmod(i, tau, n), n));
+  }
+}
+
+int alias_rows_multi(const double* Y, int64_t n, int64_t b, const int64_t* tau_tab, int nshift,
+                     const int64_t* idx, const int32_t* sig, int64_t nrows, double* rows,
+                     cudaStream_t st) {
+  const int64_t L = n / b;
+  if (nrows == 0 || nshift == 0) return AFFT_OK;
+  if (L > kAliasRowsMaxL || (L & (L - 1)) || b < 1 || n % b) {
+    set_error("alias_rows_multi: n/b = %lld unsupported", (long long)L);
+    return AFFT_EUNSUPPORTED;
+  }
+  const size_t smem = (size_t)(1 + 2 * kAliasWarps) * L * sizeof(cd);
+  cudaError_t e = ensure_smem((const void*)alias_rows_multi_kernel, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(alias_rows_multi)");
+  alias_rows_multi_kernel<<<(unsigned)((nrows + kAliasWarps - 1) / kAliasWarps), kAliasWarps * 32,
+                            smem, st>>>(reinterpret_cast<const cd*>(Y), n, b, (int)L, tau_tab,
+                                        nshift, idx, sig, nrows, reinterpret_cast<cd*>(rows));
+  AFFT_CHECK_LAUNCH("alias_rows_multi_kernel");
+  return AFFT_OK;
 }
 
 // Rows for L > kAliasRowsMaxL (L a power of two): one CTA per row, the L aliases and

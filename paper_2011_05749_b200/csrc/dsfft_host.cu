@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -783,6 +784,328 @@ struct Dsfft {
   }
 };
 
+// ------------------------------------------------------------------ batches
+//
+// The layer loop of several signals in lockstep: one launch per step for all of them.
+// Noisy decodes of large signals follow the same path (spectrum first, every full
+// layer's active set from one pass, then classify at the stop depth and re-expand while
+// multitons remain), so a step is "classify every signal that sits at depth d": their
+// active buckets' rows in one list (alias rows from the batch's spectra, or each
+// signal's coset DFTs at shallow depths), one classify_noisy over the list with
+// per-row signal ids (search shifts and gates per signal), one read-back for all.
+// Signals that leave the common path — calibration, a selective expansion, a layer
+// whose active set overflows the one-pass lists, a classify that needs the all-bucket
+// energy pass, leftover multitons at the bottom — are flagged and the caller decodes
+// them alone (afft_dsfft); every other signal's decisions are the single-signal ones.
+struct BatchSig {
+  bool on = false, fallback = false;
+  int depth = 0;
+  int64_t m = 0;
+  double normY = 0.0;
+  std::vector<int64_t> shifts;  // raw plan shifts anchors[j] + 2^j t
+  Entries E;
+  std::vector<int64_t> multi;
+  int64_t nsingle = 0;
+  std::vector<int32_t> trace;   // [kind, depth, a, b] records
+  void add(int kind, int64_t a, int64_t b, int64_t c) {
+    trace.push_back(kind);
+    trace.push_back((int32_t)a);
+    trace.push_back((int32_t)b);
+    trace.push_back((int32_t)c);
+  }
+};
+
+// The concatenated active list of one step: member q's m[q] buckets from its cached
+// list at src[q], its signal id alongside (one launch for every member).
+constexpr int kBatchMax = 64;
+struct StepMembers {
+  int n;
+  int32_t sig[kBatchMax];
+  int64_t off[kBatchMax + 1];   // row offsets (off[n] = total)
+  const int64_t* src[kBatchMax];
+};
+__global__ void step_list_kernel(const __grid_constant__ StepMembers M, int64_t* __restrict__ idx,
+                                 int32_t* __restrict__ sig) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M.off[M.n]) return;
+  int q = 0;
+  while (i >= M.off[q + 1]) ++q;
+  idx[i] = M.src[q][i - M.off[q]];
+  sig[i] = M.sig[q];
+}
+
+// per member: singles and multitons of its rows (the trace and the loop control need
+// only the counts; entries are read back at a signal's last classify only)
+__global__ void step_count_kernel(const __grid_constant__ StepMembers M,
+                                  const int8_t* __restrict__ state, int32_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = M.off[M.n];
+  int q = 0;
+  int single = 0, multi = 0;
+  if (i < tot) {
+    while (i >= M.off[q + 1]) ++q;
+    single = state[i] == AFFT_SINGLE_TON;
+    multi = state[i] == AFFT_MULTI_TON;
+  }
+  if (single) atomicAdd(cnt + 2 * q, 1);
+  if (multi) atomicAdd(cnt + 2 * q + 1, 1);
+}
+
+static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64_t ld, int k,
+                           const AfftDsfftParams* prm, std::vector<BatchSig>& sig,
+                           cudaStream_t st) {
+  int max_depth = 0;
+  while ((2LL << max_depth) <= n) ++max_depth;
+  int d0 = 0;
+  while ((1LL << d0) < k) ++d0;
+  d0 = std::min(d0, max_depth);
+  const int nl = max_depth - d0 + 1;
+  const int c = prm[0].c, mm = prm[0].m, R = c * mm;
+  sig.assign((size_t)S, BatchSig());
+  for (int64_t s = 0; s < S; ++s) {
+    const AfftDsfftParams& P = prm[s];
+    BatchSig& g = sig[s];
+    g.on = P.mode != 0 && P.noise_std > 0.0 && P.c == c && P.m == mm && P.anchors &&
+           P.weights;
+    g.fallback = !g.on;
+    if (g.on)
+      for (int j = 0; j < c; ++j)
+        for (int t = 0; t < mm; ++t) g.shifts.push_back(P.anchors[j] + (int64_t(1) << j) * t);
+  }
+  if ((n & (n - 1)) || n < (1LL << 16) || (1LL << d0) < 32 || nl > 16 || R > AFFT_MAX_SHIFTS ||
+      R < 1 || S > kBatchMax) {
+    for (auto& g : sig) g.on = false, g.fallback = true;
+    return AFFT_OK;
+  }
+  const int cap = (int)std::min<int64_t>(16384, n);
+  // spectra of every signal and the |x|^2 partials (the floor bound), then every full
+  // layer's active list per signal, one read-back for all the counts and partials
+  DBuf Y, parts, lists, counts, scratch, taus;
+  RC(Y.alloc((size_t)S * n * 16, st, "dsfft batch spectra"));
+  const int64_t zero = 0;
+  RC(afft_bucketize(x, dtype, n, S, ld, n, &zero, 1, Y.as<double>(), n, n, 1, st));
+  const int nparts = afft_sumsq_parts(n, dtype);
+  RC(parts.alloc((size_t)S * nparts * 8, st, "dsfft batch partials"));
+  RC(afft_sumsq(x, dtype, n, S, ld, parts.as<double>(), st));
+  RC(lists.alloc((size_t)S * nl * cap * 8, st, "dsfft batch lists"));
+  RC(counts.alloc((size_t)S * nl * 4, st, "dsfft batch counts"));
+  const size_t sb = full_active_scratch(n, d0, nl);
+  RC(scratch.alloc(sb, st, "dsfft batch layer scratch"));
+  for (int64_t s = 0; s < S; ++s) {
+    if (!sig[s].on) continue;
+    std::vector<double> thr((size_t)nl);
+    for (int j = 0; j < nl; ++j)
+      thr[j] = std::max(prm[s].activity_floor,
+                        3.0 * prm[s].noise_std / std::sqrt((double)(1LL << (d0 + j))));
+    RC(full_active_all(Y.as<double>() + 2 * s * n, n, d0, nl, thr.data(),
+                       lists.as<int64_t>() + s * nl * cap, cap, counts.as<int32_t>() + s * nl,
+                       scratch.p, sb, st));
+  }
+  std::vector<int32_t> hc;
+  std::vector<double> hp;
+  RC(d2h(hc, counts.p, (size_t)S * nl, st));
+  RC(d2h(hp, parts.p, (size_t)S * nparts, st));
+  // reduced shift tables for the alias rows and the fit
+  {
+    std::vector<int64_t> tt((size_t)S * R, 0);
+    for (int64_t s = 0; s < S; ++s)
+      if (sig[s].on)
+        for (int r = 0; r < R; ++r) tt[(size_t)s * R + r] = host_pymod(sig[s].shifts[r], n);
+    RC(taus.alloc(tt.size() * 8, st, "dsfft batch shifts"));
+    CK(cudaMemcpyAsync(taus.p, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, st));
+  }
+  auto count_at = [&](int64_t s, int depth) { return (int64_t)hc[(size_t)s * nl + (depth - d0)]; };
+  // initial layer and the first expansions, from the counts (dsfft.py:258-264)
+  for (int64_t s = 0; s < S; ++s) {
+    BatchSig& g = sig[s];
+    if (!g.on) continue;
+    double sum = 0.0;
+    for (int q = 0; q < nparts; ++q) sum += hp[(size_t)s * nparts + q];
+    g.normY = sum / (double)n;
+    g.depth = d0;
+    g.m = count_at(s, d0);
+    if (g.m > cap) {
+      g.on = false, g.fallback = true;
+      continue;
+    }
+    g.add(1, d0, g.m, -1);
+    while ((double)g.m < prm[s].theta * k && g.depth < max_depth) {
+      const int next = g.depth + 1;
+      if (2 * g.m <= next || count_at(s, next) > cap) {  // selective / overflow: alone
+        g.on = false, g.fallback = true;
+        break;
+      }
+      g.m = count_at(s, next);
+      g.depth = next;
+      g.add(2, next, g.m, -1);
+    }
+  }
+  // classify steps: all signals at the smallest pending depth together
+  DBuf idx, sidx, rows, ws, gates;
+  for (;;) {
+    int depth = INT32_MAX;
+    for (auto& g : sig)
+      if (g.on) depth = std::min(depth, g.depth);
+    if (depth == INT32_MAX) break;
+    const int64_t b = 1LL << depth, L = n / b;
+    std::vector<int64_t> members, offs;
+    std::vector<double> t0s((size_t)S, 0.0), t1s((size_t)S, 0.0);
+    int64_t A = 0;
+    for (int64_t s = 0; s < S; ++s) {
+      BatchSig& g = sig[s];
+      if (!g.on || g.depth != depth) continue;
+      const double base = prm[s].noise_std / std::sqrt((double)b) * std::sqrt((double)R);
+      // the floor 1e-8 sqrt(max energy) is provably below 1.5 base (see classify)
+      if (!(1e-8 * std::sqrt((double)R * (double)L * g.normY * 1.0001) < 1.5 * base)) {
+        g.on = false, g.fallback = true;
+        continue;
+      }
+      t0s[s] = 1.5 * base;
+      t1s[s] = 2.5 * base;
+      members.push_back(s);
+      offs.push_back(A);
+      A += g.m;
+    }
+    if (members.empty()) continue;
+    StepMembers M;
+    memset(&M, 0, sizeof(M));
+    M.n = (int)members.size();
+    for (size_t q = 0; q < members.size(); ++q) {
+      M.sig[q] = (int32_t)members[q];
+      M.off[q] = offs[q];
+      M.src[q] = lists.as<int64_t>() + (members[q] * nl + (depth - d0)) * cap;
+    }
+    M.off[members.size()] = A;
+    std::vector<int32_t> hcnt((size_t)2 * members.size(), 0);
+    DBuf pk_state, pk_f0, pk_val, dcnt;
+    if (A > 0) {
+      RC(idx.alloc((size_t)A * 8, st, "dsfft batch rows index"));
+      RC(sidx.alloc((size_t)A * 4, st, "dsfft batch rows signal"));
+      step_list_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(M, idx.as<int64_t>(),
+                                                                    sidx.as<int32_t>());
+      CK(cudaGetLastError());
+      RC(rows.alloc((size_t)A * R * 16, st, "dsfft batch rows"));
+      if (L <= 256) {
+        RC(alias_rows_multi(Y.as<double>(), n, b, taus.as<int64_t>(), R, idx.as<int64_t>(),
+                            sidx.as<int32_t>(), A, rows.as<double>(), st));
+      } else {
+        // shallow layers: every member's distinct-residue coset DFTs (tau mod L) over its
+        // own signal in one batched transform, then the rows picked and rotated
+        std::vector<std::vector<int64_t>> res(S);
+        std::vector<int32_t> coset((size_t)S * R, 0);
+        std::vector<int64_t> qrot((size_t)S * R, 0);
+        int U = 1;
+        for (int64_t s2 : members) {
+          std::map<int64_t, int> seen;
+          for (int t = 0; t < R; ++t) {
+            const int64_t tm = host_pymod(sig[s2].shifts[t], n), r = tm % L;
+            auto it = seen.find(r);
+            int u;
+            if (it == seen.end()) {
+              u = (int)res[s2].size();
+              seen[r] = u;
+              res[s2].push_back(r);
+            } else {
+              u = it->second;
+            }
+            coset[(size_t)s2 * R + t] = u;
+            qrot[(size_t)s2 * R + t] = tm / L;
+          }
+          U = std::max(U, (int)res[s2].size());
+        }
+        // every signal of the batch gets U residues (non-members / padding repeat one)
+        std::vector<int64_t> table((size_t)S * U, 0);
+        for (int64_t s2 = 0; s2 < S; ++s2)
+          for (int u = 0; u < U; ++u)
+            table[(size_t)s2 * U + u] =
+                res[s2].empty() ? 0 : res[s2][std::min<size_t>((size_t)u, res[s2].size() - 1)];
+        DBuf dtab, dcos, dq, cosets;
+        RC(dtab.alloc(table.size() * 8, st, "dsfft batch residues"));
+        RC(dcos.alloc(coset.size() * 4, st, "dsfft batch coset map"));
+        RC(dq.alloc(qrot.size() * 8, st, "dsfft batch rotations"));
+        CK(cudaMemcpyAsync(dtab.p, table.data(), table.size() * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dcos.p, coset.data(), coset.size() * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dq.p, qrot.data(), qrot.size() * 8, cudaMemcpyHostToDevice, st));
+        RC(cosets.alloc((size_t)S * U * b * 16, st, "dsfft batch coset DFTs"));
+        RC(afft_bucketize_table(x, dtype, n, S, ld, b, dtab.as<int64_t>(), U, cosets.as<double>(),
+                                (int64_t)U * b, b, 1, st));
+        RC(rows_gather_multi(cosets.as<double>(), b, U, R, dcos.as<int32_t>(), dq.as<int64_t>(),
+                             idx.as<int64_t>(), sidx.as<int32_t>(), A, rows.as<double>(), st));
+      }
+      std::vector<double> gt((size_t)2 * S);
+      for (int64_t s2 = 0; s2 < S; ++s2) {
+        gt[s2] = t0s[s2];
+        gt[S + s2] = t1s[s2];
+      }
+      RC(gates.alloc(gt.size() * 8, st, "dsfft batch gates"));
+      CK(cudaMemcpyAsync(gates.p, gt.data(), gt.size() * 8, cudaMemcpyHostToDevice, st));
+      RC(pk_state.alloc((size_t)A, st, "dsfft batch states"));
+      RC(pk_f0.alloc((size_t)A * 8, st, "dsfft batch f0"));
+      RC(pk_val.alloc((size_t)A * 16, st, "dsfft batch values"));
+      DBuf rn;
+      RC(rn.alloc((size_t)A * 8, st, "dsfft batch resnorm"));
+      const size_t need = afft_singleton_workspace_size(n, A, b, c, mm);
+      RC(ws.alloc(need, st, "dsfft batch search workspace"));
+      RC(classify_noisy_multi(rows.as<double>(), idx.as<int64_t>(), sidx.as<int32_t>(), A, b, n,
+                              taus.as<int64_t>(), c, mm, prm[members[0]].weights,
+                              gates.as<double>(), gates.as<double>() + S,
+                              pk_state.as<int8_t>(), pk_f0.as<int64_t>(), pk_val.as<double>(),
+                              rn.as<double>(), ws.p, need, st));
+      RC(dcnt.alloc((size_t)2 * members.size() * 4, st, "dsfft batch step counts"));
+      CK(cudaMemsetAsync(dcnt.p, 0, (size_t)2 * members.size() * 4, st));
+      step_count_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(M, pk_state.as<int8_t>(),
+                                                                     dcnt.as<int32_t>());
+      CK(cudaGetLastError());
+      RC(d2h(hcnt, dcnt.p, (size_t)2 * members.size(), st));
+    }
+    // trace and loop control from the counts; the entries of a signal's last classify
+    std::vector<size_t> last;
+    for (size_t q = 0; q < members.size(); ++q) {
+      BatchSig& g = sig[members[q]];
+      const int64_t ns = hcnt[2 * q], nm = hcnt[2 * q + 1];
+      g.add(5, depth, R, 1);
+      g.add(3, depth, ns, nm);
+      g.E.clear();
+      g.multi.clear();
+      g.nsingle = ns;
+      if (nm > 0 && g.depth < max_depth) {  // re-expand (dsfft.py:190-192)
+        const int next = g.depth + 1;
+        if (2 * g.m <= next || count_at(members[q], next) > cap) {
+          g.on = false, g.fallback = true;
+          continue;
+        }
+        g.m = count_at(members[q], next);
+        g.depth = next;
+        g.add(2, next, g.m, -1);
+      } else {
+        g.on = false;
+        if (nm > 0 && (int64_t)k - ns > 0) {
+          g.fallback = true;  // leftover multitons: _resolve_aliased, alone
+        } else {
+          last.push_back(q);
+        }
+      }
+    }
+    if (!last.empty() && A > 0) {
+      std::vector<int8_t> hs;
+      std::vector<int64_t> hf;
+      std::vector<cd> hv;
+      RC(d2h(hs, pk_state.p, (size_t)A, st));
+      RC(d2h(hf, pk_f0.p, (size_t)A, st));
+      RC(d2h(hv, pk_val.p, (size_t)A, st));
+      for (size_t q : last) {
+        BatchSig& g = sig[members[q]];
+        g.E.reserve((size_t)g.nsingle);
+        // ascending bucket order within the member (its cached list is ascending); the
+        // singletons' f0 are distinct (f0 mod b is the bucket)
+        for (int64_t i = offs[q]; i < offs[q] + M.off[q + 1] - M.off[q]; ++i)
+          if (hs[i] == AFFT_SINGLE_TON) g.E.put(hf[i], hv[i]);
+      }
+    }
+  }
+  return AFFT_OK;
+}
+
 }  // namespace
 }  // namespace afft
 
@@ -841,4 +1164,64 @@ extern "C" int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k,
     out_val[2 * i + 1] = ev[i].im;
   }
   return AFFT_OK;
+}
+
+extern "C" int afft_dsfft_batch(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
+                                int32_t k, const AfftDsfftParams* params, int64_t* out_pos,
+                                double* out_val, int64_t capacity, int64_t* out_count,
+                                int32_t* trace, int32_t trace_capacity, int32_t* trace_len,
+                                int32_t* fallback, void* stream) {
+  if (batch == 0) return AFFT_OK;
+  if (!x || !params || !out_count || !fallback || n < 1 || k < 1 || batch < 0 || ld < n ||
+      (dtype != AFFT_C64 && dtype != AFFT_C128) || (capacity > 0 && (!out_pos || !out_val))) {
+    set_error("afft_dsfft_batch: bad arguments");
+    return AFFT_EINVAL;
+  }
+  // the batch's temporaries from one borrowed device buffer (capi.cu arena): the
+  // spectra S n complex128, coset DFTs up to S 72 n / 2^13 complex128 at the shallow
+  // layers, rows and lists; repeated calls reuse it instead of growing the pool
+  arena_begin((size_t)batch * n * 16 * 2 + ((size_t)512 << 20), (cudaStream_t)stream);
+  struct ArenaGuard {
+    cudaStream_t st;
+    ~ArenaGuard() {
+      cudaStreamSynchronize(st);
+      arena_end();
+    }
+  } arena_guard{(cudaStream_t)stream};
+  std::vector<BatchSig> sig;
+  g_prof.wait_s = 0.0;
+  g_prof.syncs = 0;
+  const double t_start = g_prof.on ? now_s() : 0.0;
+  const int rc = dsfft_batch_run(x, dtype, n, batch, ld, k, params, sig, (cudaStream_t)stream);
+  if (g_prof.on)
+    std::fprintf(stderr, "afft_dsfft_batch: %lld signals, %.3f ms total, %.3f ms waiting in %d "
+                 "read-backs\n", (long long)batch, (now_s() - t_start) * 1e3, g_prof.wait_s * 1e3,
+                 g_prof.syncs);
+  if (rc) {
+    cudaStreamSynchronize((cudaStream_t)stream);
+    return rc;
+  }
+  int over = AFFT_OK;
+  for (int64_t s = 0; s < batch; ++s) {
+    const BatchSig& g = sig[s];
+    fallback[s] = g.fallback ? 1 : 0;
+    out_count[s] = g.fallback ? 0 : (int64_t)g.E.f.size();
+    const int32_t tl = (int32_t)(g.trace.size() / 4);
+    if (trace_len) trace_len[s] = g.fallback ? 0 : tl;
+    if (g.fallback) continue;
+    if ((int64_t)g.E.f.size() > capacity) {
+      over = AFFT_ENOMEM;
+      continue;
+    }
+    for (size_t i = 0; i < g.E.f.size(); ++i) {
+      out_pos[s * capacity + (int64_t)i] = g.E.f[i];
+      out_val[2 * (s * capacity + (int64_t)i)] = g.E.v[i].re;
+      out_val[2 * (s * capacity + (int64_t)i) + 1] = g.E.v[i].im;
+    }
+    if (trace)
+      for (int32_t q = 0; q < std::min(tl, trace_capacity) * 4; ++q)
+        trace[(int64_t)s * trace_capacity * 4 + q] = g.trace[q];
+  }
+  if (over) set_error("afft_dsfft_batch: entries beyond capacity %lld", (long long)capacity);
+  return over;
 }

@@ -56,7 +56,14 @@ struct NoisyPlan {
   // signals carry their own search anchors, peeling.py:163-164); null: tau for all
   const int64_t* tau_tab;
   uint64_t nmagic;  // floor((2^64 - 1) / n): Barrett reduction for tau * f mod n
+  // optional signal of each residual row (DSFFT batches: rows of several signals in one
+  // list); null: row / nodes
+  const int32_t* row_sig;
 };
+
+__device__ __forceinline__ int64_t plan_row_signal(const NoisyPlan& P, int64_t row) {
+  return P.row_sig ? P.row_sig[row] : (P.tau_tab ? row / P.nodes : 0);
+}
 
 // (a * b) mod P.n for 0 <= a, b < n <= 2e9 (a * b < 2^62): Barrett with the plan's
 // magic, exact after at most two corrections — the int64 '%' it replaces compiled to
@@ -572,6 +579,8 @@ __device__ __forceinline__ double node_norm(const cd* y, int R);
 struct NoisyDecide {
   int8_t* state;
   double t0, t1;
+  const double* t0s;  // per-signal gates (signal of the row), overriding t0 / t1
+  const double* t1s;
 };
 
 __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restrict__ part_score,
@@ -617,7 +626,7 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
   // index < b and t < n / b, so the candidate is already reduced (no '% n')
   const int64_t f0 = act_index[a] + act_b[a] * (int64_t)bt;
   const cd* y = reinterpret_cast<const cd*>(residual) + act_row[a] * P.R;
-  const int64_t sig = P.tau_tab ? act_row[a] / P.nodes : 0;
+  const int64_t sig = plan_row_signal(P, act_row[a]);
   // a^H y and a^H a; each lane's atoms kept for the residual (one sincos per row)
   constexpr int kAtomRegs = 4;  // rows lane, lane + 32, ... cached up to R = 128
   cd atc[kAtomRegs];
@@ -676,8 +685,9 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
       nrm = lane == 0 ? node_norm(y, P.R) : 0.0;
     }
     if (lane == 0)
-      decide.state[a] = nrm <= decide.t0 ? AFFT_ZERO_TON
-                        : out_res[a] <= decide.t1 ? AFFT_SINGLE_TON
+      decide.state[a] = nrm <= (decide.t0s ? decide.t0s[sig] : decide.t0) ? AFFT_ZERO_TON
+                        : out_res[a] <= (decide.t1s ? decide.t1s[sig] : decide.t1)
+                            ? AFFT_SINGLE_TON
                                                   : AFFT_MULTI_TON;
   }
 }
@@ -1345,7 +1355,7 @@ static int enqueue_round(const NoisyPlan& P, const NoisyWs& w, char* ws, int64_t
   AFFT_CHECK_LAUNCH("noisy_search_persistent_kernel");
   noisy_finalize_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, cs>>>(
       0, w.chunks, part_s, part_t, act_row, act_index, act_b, residual, P, f0s, vals, res,
-      NoisyDecide{nullptr, 0.0, 0.0}, A_dev);
+      NoisyDecide{nullptr, 0.0, 0.0, nullptr, nullptr}, A_dev);
   AFFT_CHECK_LAUNCH("noisy_finalize_kernel");
   noisy_apply_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, cs>>>(
       0, P, act_row, f0s, vals, res, t1, state, dirty, node_f0, node_val, A_dev);
@@ -1496,7 +1506,8 @@ static int singleton_search(const double* residual, const int64_t* index, int64_
                             int64_t b, int64_t n, const int64_t* shifts, int32_t nshift, int32_t c,
                             int32_t m, const double* weights, int64_t* f0, double* val,
                             double* resnorm, void* workspace, size_t workspace_bytes,
-                            cudaStream_t st, NoisyDecide decide) {
+                            cudaStream_t st, NoisyDecide decide, const int64_t* tau_tab = nullptr,
+                            const int32_t* row_sig = nullptr) {
   if (count == 0) return AFFT_OK;
   if (!residual || !index || !f0 || !val || !resnorm || !shifts || !weights || b < 1 ||
       n % b) {
@@ -1509,6 +1520,8 @@ static int singleton_search(const double* residual, const int64_t* index, int64_
   if (rc) {
     return rc;
   }
+  P->tau_tab = tau_tab;
+  P->row_sig = row_sig;
   const NoisyWs w = noisy_ws(*P, count);
   if (!workspace || workspace_bytes < w.total) {
     set_error("afft_singleton_search_noisy: workspace of %zu bytes needed", w.total);
@@ -1527,6 +1540,25 @@ static int singleton_search(const double* residual, const int64_t* index, int64_
   return rc;
 }
 
+// classify_noisy over rows of several signals at once (DSFFT batches): row r belongs to
+// signal row_sig[r], whose reduced search shifts are tau_tab[sig][0..c*m) (device) and
+// whose gates are t0s[sig] / t1s[sig] (device).
+int classify_noisy_multi(const double* residual, const int64_t* index, const int32_t* row_sig,
+                         int64_t count, int64_t b, int64_t n, const int64_t* tau_tab, int32_t c,
+                         int32_t m, const double* weights, const double* t0s, const double* t1s,
+                         int8_t* state, int64_t* f0, double* val, double* resnorm,
+                         void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  if (count == 0) return AFFT_OK;
+  if (!row_sig || !tau_tab || !t0s || !t1s || !state) {
+    set_error("classify_noisy_multi: bad arguments");
+    return AFFT_EINVAL;
+  }
+  std::vector<int64_t> zeros((size_t)c * m, 0);
+  return singleton_search(residual, index, count, b, n, zeros.data(), c * m, c, m, weights, f0,
+                          val, resnorm, workspace, workspace_bytes, st,
+                          NoisyDecide{state, 0.0, 0.0, t0s, t1s}, tau_tab, row_sig);
+}
+
 }  // namespace afft
 
 extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t* index,
@@ -1537,7 +1569,7 @@ extern "C" int afft_singleton_search_noisy(const double* residual, const int64_t
                                            size_t workspace_bytes, void* stream) {
   return singleton_search(residual, index, count, b, n, shifts, nshift, c, m, weights, f0, val,
                           resnorm, workspace, workspace_bytes, (cudaStream_t)stream,
-                          NoisyDecide{nullptr, 0.0, 0.0});
+                          NoisyDecide{nullptr, 0.0, 0.0, nullptr, nullptr});
 }
 
 namespace afft {
@@ -1717,7 +1749,7 @@ extern "C" int afft_classify_noisy(const double* residual, const int64_t* index,
   // search + fit + the decision of peeling.py:257-267, all in the finalize kernel
   return singleton_search(residual, index, count, b, n, shifts, nshift, c, m, weights, f0, val,
                           resnorm, workspace, workspace_bytes, (cudaStream_t)stream,
-                          NoisyDecide{state, t0, t1});
+                          NoisyDecide{state, t0, t1, nullptr, nullptr});
 }
 
 namespace afft {
