@@ -389,6 +389,11 @@ int afft_median(const double* values, int32_t mode, int64_t count, int64_t batch
  * out_count set even on AFFT_ENOMEM) and a trace of [kind, depth, a, b] records:
  * 0 calibrate, 1 initial (m_d), 2 expand (m_d, candidates or -1), 3 classify
  * (#single, #multi), 4 resolve (#buckets, p), 5 classify read set (R, mode).
+ * full_classify = 0 lets a noisy decode classify only a probe set at the layers whose
+ * entries the reference discards (dsfft.py:188-192 keeps only the last classify's
+ * entries; an intermediate layer only decides whether any multi-ton remains): same
+ * output, and classify records of probe layers carry #single = -1.  1 classifies every
+ * active bucket at every layer (the reference's per-layer counts in the trace).
  */
 typedef struct {
   double theta;          /* DsfftConfig.theta (stop rule) */
@@ -401,6 +406,7 @@ typedef struct {
   const double* weights;
   const int64_t* dt_shifts;
   const int32_t* dt_shift_off; /* [log2(n) + 2] */
+  int32_t full_classify;       /* 1: every layer classified in full (exact trace counts) */
 } AfftDsfftParams;
 
 int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k, const AfftDsfftParams* params,

@@ -131,6 +131,7 @@ class DsfftParams(ctypes.Structure):
         ("weights", ctypes.c_void_p),
         ("dt_shifts", ctypes.c_void_p),
         ("dt_shift_off", ctypes.c_void_p),
+        ("full_classify", ctypes.c_int32),
     ]
 
 

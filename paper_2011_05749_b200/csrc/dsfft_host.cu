@@ -306,6 +306,34 @@ struct Dsfft {
   DBuf deep_lists;
   std::vector<int32_t> deep_counts;
 
+  // Host copies of those lists for the probe classifies (copied asynchronously right
+  // after the counts, waited for at the first probe): one pinned block, per-layer offsets.
+  void* hl_stage = nullptr;
+  size_t hl_cap = 0;
+  std::vector<size_t> hl_off;
+  cudaEvent_t hl_ev = nullptr;
+  bool hl_ready = false;
+  ~Dsfft() {
+    if (hl_ev) {
+      cudaEventSynchronize(hl_ev);  // the copy must land before the block is reused
+      cudaEventDestroy(hl_ev);
+    }
+    pinned_release(hl_stage, hl_cap);
+  }
+
+  // Probe classifies (full_classify = 0, noisy mode): an intermediate layer's entries are
+  // discarded by the reference (dsfft.py:188-192 keeps only the last classify's), so such
+  // a layer only has to show that some multi-ton remains.  It classifies the active
+  // children of the previous layer's multi-tons found so far (the first layer: its first
+  // kProbe0 active buckets); if none of them is a multi-ton, the whole layer is
+  // classified as the reference does.  The bottom layer is always classified in full.
+  // AFFT_DSFFT_PROBE0 sets the first layer's probe size (0 disables probing).
+  bool lazy = false;
+  int64_t probe0 = [] {
+    const char* e = std::getenv("AFFT_DSFFT_PROBE0");
+    return e ? std::max<int64_t>(0, std::atoll(e)) : 256;
+  }();
+
   static constexpr int64_t kAliasMaxL = 32;       // rows + energies + values from Y
   static constexpr int64_t kAliasRowsMaxL = 256;  // rows alone from Y
 
@@ -516,7 +544,35 @@ struct Dsfft {
     deep_d0 = depth;
     deep_nl = nl;
     deep_cap = cap;
+    if (lazy) {
+      hl_off.assign((size_t)nl + 1, 0);
+      for (int j = 0; j < nl; ++j)
+        hl_off[j + 1] = hl_off[j] + (size_t)std::min(deep_counts[j], cap);
+      hl_stage = pinned_acquire(std::max<size_t>(hl_off[nl], 1) * 8, &hl_cap);
+      if (hl_stage) {
+        CK(cudaEventCreateWithFlags(&hl_ev, cudaEventDisableTiming));
+        for (int j = 0; j < nl; ++j)
+          if (hl_off[j + 1] > hl_off[j])
+            CK(cudaMemcpyAsync(static_cast<int64_t*>(hl_stage) + hl_off[j],
+                               deep_lists.as<int64_t>() + (int64_t)j * cap,
+                               (hl_off[j + 1] - hl_off[j]) * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(hl_ev, st));
+      }
+    }
     return AFFT_OK;
+  }
+
+  // The host copy of a cached full layer's ascending active list (nullptr if not held).
+  const int64_t* host_list(int depth, int64_t* m) {
+    if (!hl_stage || !deep_done || depth < deep_d0 || depth >= deep_d0 + deep_nl) return nullptr;
+    const int j = depth - deep_d0;
+    if (deep_counts[j] > std::min(active_cap(1LL << depth), deep_cap)) return nullptr;
+    if (!hl_ready) {
+      if (cudaEventSynchronize(hl_ev) != cudaSuccess) return nullptr;
+      hl_ready = true;
+    }
+    *m = deep_counts[j];
+    return static_cast<const int64_t*>(hl_stage) + hl_off[j];
   }
 
   int rows(int64_t b, const std::vector<int64_t>& shifts, const int64_t* idx, int64_t count,
@@ -543,8 +599,7 @@ struct Dsfft {
     int8_t* state() const { return reinterpret_cast<int8_t*>(buf.as<char>() + os); }
   };
 
-  int make_pack(const Layer& L, Pack& pk) {
-    const int64_t A = L.m;
+  int make_pack(const int64_t* idx, int64_t A, Pack& pk) {
     pk.A = A;
     if (!A) return AFFT_OK;
     pk.of = 0;
@@ -554,7 +609,7 @@ struct Dsfft {
     pk.bytes = pk.os + (size_t)A;
     RC(pk.buf.alloc(pk.bytes, st, "dsfft result pack"));
     char* p = pk.buf.as<char>();
-    CK(cudaMemcpyAsync(p + pk.oa, L.active.p, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(p + pk.oa, idx, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemsetAsync(p + pk.of, 0xff, (size_t)A * 8, st));  // f0 = -1
     CK(cudaMemsetAsync(p + pk.ov, 0, (size_t)A * 16, st));
     return AFFT_OK;
@@ -562,18 +617,42 @@ struct Dsfft {
 
   // _classify_active: entries (ascending bucket order) and multiton buckets
   int classify(const Layer& L, Entries& E, std::vector<int64_t>& multi) {
+    bool declined = false;
+    return classify_list(L.depth, L.active.as<int64_t>(), L.m, false, E, multi, &declined);
+  }
+
+  // A probe classify of `cand` (ascending, a subset of layer `depth`'s active set): the
+  // multi-tons among them into `found`, no entries.  *declined (nothing done) when the
+  // layer's thresholds need the all-bucket energy pass or the quiet-bucket median.
+  int probe(int depth, const std::vector<int64_t>& cand, std::vector<int64_t>& found,
+            bool* declined) {
+    DBuf idx;
+    RC(idx.alloc(std::max<size_t>(cand.size(), 1) * 8, st, "dsfft probe list"));
+    if (!cand.empty())
+      CK(cudaMemcpyAsync(idx.p, cand.data(), cand.size() * 8, cudaMemcpyHostToDevice, st));
+    Entries none;
+    return classify_list(depth, idx.as<int64_t>(), (int64_t)cand.size(), true, none, found,
+                         declined);
+  }
+
+  int classify_list(int depth, const int64_t* idx, int64_t A, bool is_probe, Entries& E,
+                    std::vector<int64_t>& multi, bool* declined) {
+    *declined = false;
     E.clear();
     multi.clear();
-    const int64_t b = 1LL << L.depth;
-    const int64_t A = L.m;
+    const int64_t b = 1LL << depth;
     Pack pk;
     DBuf rowsb;
-    RC(make_pack(L, pk));
+    if (is_probe && P.mode == 0) {
+      *declined = true;
+      return AFFT_OK;
+    }
+    RC(make_pack(idx, A, pk));
     if (P.mode == 0) {
-      tr.add(5, L.depth, 3, 0);  // ledger: shifts 0, 1, 2
-      if (A == 0) return finish_classify(L, E, multi, pk);
+      tr.add(5, depth, 3, 0);  // ledger: shifts 0, 1, 2
+      if (A == 0) return finish_classify(depth, E, multi, pk, is_probe);
       const std::vector<int64_t> shifts = {0, 1, 2};
-      RC(rows(b, shifts, L.active.as<int64_t>(), A, rowsb, nullptr));
+      RC(rows(b, shifts, idx, A, rowsb, nullptr));
       // exact_thresholds (peeling.py:316-318)
       const int nparts = afft_sumsq_parts(n, dtype);
       DBuf parts, eps;
@@ -583,16 +662,15 @@ struct Dsfft {
       RC(afft_exact_thresholds(parts.as<double>(), nparts, n, 1, eps.as<double>(), st));
       std::vector<double> he;
       RC(d2h(he, eps.p, 1, st));
-      RC(afft_classify_exact(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, he[0], he[0],
+      RC(afft_classify_exact(rowsb.as<double>(), idx, A, b, n, he[0], he[0],
                              pk.state(), pk.f0(), pk.val(), st));
-      return finish_classify(L, E, multi, pk);
+      return finish_classify(depth, E, multi, pk, is_probe);
     }
     // noisy: the search plan of dsfft.py:142-150 (anchors drawn by the caller)
     std::vector<int64_t> shifts;
     for (int j = 0; j < P.c; ++j)
       for (int t = 0; t < P.m; ++t) shifts.push_back(P.anchors[j] + (int64_t(1) << j) * t);
     const int R = (int)shifts.size();
-    tr.add(5, L.depth, R, 1);  // ledger: the plan shifts
     const double base = noise_std / std::sqrt((double)b) * std::sqrt((double)R);
     bool skip = false;
     if (noise_std > 0.0) {
@@ -602,10 +680,15 @@ struct Dsfft {
       RC(norm_y());
       skip = 1e-8 * std::sqrt((double)R * (double)(n / b) * normY * 1.0001) < 1.5 * base;
     }
+    if (is_probe && !skip) {  // thresholds from every bucket: classify the layer in full
+      *declined = true;
+      return AFFT_OK;
+    }
+    tr.add(5, depth, R, 1);  // ledger: the plan shifts
     DBuf energy;
     if (!skip) RC(energy.alloc((size_t)b * 8, st, "dsfft energies"));
     PMARK("classify setup");
-    RC(rows(b, shifts, L.active.as<int64_t>(), A, rowsb, skip ? nullptr : energy.as<double>()));
+    RC(rows(b, shifts, idx, A, rowsb, skip ? nullptr : energy.as<double>()));
     PMARK("classify rows");
     double t0 = 0.0, t1 = 0.0;
     if (noise_std > 0.0) {
@@ -629,7 +712,7 @@ struct Dsfft {
       dsfft_quiet_kernel<<<148 * 4, 256, 0, st>>>(b, nullptr, 0, quiet.as<uint8_t>());
       if (A)
         dsfft_unquiet_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(
-            L.active.as<int64_t>(), A, quiet.as<uint8_t>());
+            idx, A, quiet.as<uint8_t>());
       RC(afft_robust_thresholds(energy.as<double>(), quiet.as<uint8_t>(), b, 1, R, d0.as<double>(),
                                 d0.as<double>() + 1, st));
       std::vector<double> h;
@@ -638,21 +721,22 @@ struct Dsfft {
       t1 = h[1];
     }
     PMARK("classify thresholds");
-    if (A == 0) return finish_classify(L, E, multi, pk);
+    if (A == 0) return finish_classify(depth, E, multi, pk, is_probe);
     DBuf rn, ws;
     RC(rn.alloc((size_t)A * 8, st, "dsfft resnorm"));
     const size_t need = afft_singleton_workspace_size(n, A, b, P.c, P.m);
     RC(ws.alloc(need, st, "dsfft search workspace"));
-    RC(afft_classify_noisy(rowsb.as<double>(), L.active.as<int64_t>(), A, b, n, shifts.data(), R,
+    RC(afft_classify_noisy(rowsb.as<double>(), idx, A, b, n, shifts.data(), R,
                            P.c, P.m, P.weights, t0, t1, pk.state(), pk.f0(), pk.val(),
                            rn.as<double>(), ws.p, need, st));
     PMARK("classify noisy");
-    const int rcf = finish_classify(L, E, multi, pk);
+    const int rcf = finish_classify(depth, E, multi, pk, is_probe);
     PMARK("classify finish");
     return rcf;
   }
 
-  int finish_classify(const Layer& L, Entries& E, std::vector<int64_t>& multi, const Pack& pk) {
+  int finish_classify(int depth, Entries& E, std::vector<int64_t>& multi, const Pack& pk,
+                      bool is_probe) {
     const int64_t A = pk.A;
     if (A) {
       std::vector<char> h;
@@ -666,13 +750,13 @@ struct Dsfft {
       E.reserve((size_t)A);
       for (int64_t i = 0; i < A; ++i) {
         if (hs[i] == AFFT_SINGLE_TON) {  // ascending bucket order, as the reference inserts
-          E.put(hf[i], hv[i]);
+          if (!is_probe) E.put(hf[i], hv[i]);
         } else if (hs[i] == AFFT_MULTI_TON) {
           multi.push_back(ha[i]);
         }
       }
     }
-    tr.add(3, L.depth, (int64_t)E.f.size(), (int64_t)multi.size());
+    tr.add(3, depth, is_probe ? -1 : (int64_t)E.f.size(), (int64_t)multi.size());
     return AFFT_OK;
   }
 
@@ -739,7 +823,40 @@ struct Dsfft {
     return AFFT_OK;
   }
 
+  // One classify step of the loop: a probe first where allowed (see `lazy`), the whole
+  // layer otherwise or when the probe finds no multi-ton.  `multi` holds the multi-tons
+  // found (all of them after a full classify, the probe's after a probe).
+  int classify_layer(const Layer& L, Entries& E, std::vector<int64_t>& multi, bool first) {
+    int64_t m = 0;
+    const int64_t* act = (lazy && L.depth < max_depth) ? host_list(L.depth, &m) : nullptr;
+    if (act && m > 0) {
+      std::vector<int64_t> cand;
+      if (first) {
+        cand.assign(act, act + std::min<int64_t>(m, probe0));
+      } else {  // active children {i, i + 2^(d-1)} of the multi-tons found one layer up
+        const int64_t half = 1LL << (L.depth - 1);
+        for (int pass = 0; pass < 2; ++pass)
+          for (int64_t i : multi) {
+            const int64_t c = i + (pass ? half : 0);
+            if (std::binary_search(act, act + m, c)) cand.push_back(c);
+          }
+      }
+      if (!cand.empty() && (int64_t)cand.size() < m) {
+        std::vector<int64_t> found;
+        bool declined = false;
+        RC(probe(L.depth, cand, found, &declined));
+        PMARK("probe");
+        if (!declined && !found.empty()) {
+          multi.swap(found);
+          return AFFT_OK;
+        }
+      }
+    }
+    return classify(L, E, multi);
+  }
+
   int run(Entries& E) {
+    lazy = P.mode != 0 && !P.full_classify && probe0 > 0;
     max_depth = 0;
     while ((2LL << max_depth) <= n) ++max_depth;  // n.bit_length() - 1
     noise_std = P.noise_std;
@@ -768,13 +885,13 @@ struct Dsfft {
       PMARK("expand");
     }
     std::vector<int64_t> multi;
-    RC(classify(layer, E, multi));
+    RC(classify_layer(layer, E, multi, true));
     while (P.mode != 0 && !multi.empty() && layer.depth < max_depth) {
       PMARK("loop");
       RC(expand(layer, next));
       swap_layers(layer, next);
       PMARK("expand");
-      RC(classify(layer, E, multi));
+      RC(classify_layer(layer, E, multi, false));
     }
     const int64_t remaining = (int64_t)k - (int64_t)E.f.size();
     PMARK("loop");

@@ -14,6 +14,7 @@ ledger, and keeps the reference's layer-level API (initial_layer / expand_layer)
 from __future__ import annotations
 
 import ctypes
+import os
 import functools
 import warnings
 from dataclasses import dataclass, field
@@ -220,7 +221,10 @@ def _dsfft_arrays(xd: torch.Tensor, k: int, config: DsfftConfig,
         c=int(plan.c) if noisy else 0, m=int(plan.m) if noisy else 0,
         anchors=anchors.ctypes.data, weights=weights.ctypes.data,
         dt_shifts=dt_table[0].ctypes.data if dt_table[0].size else None,
-        dt_shift_off=dt_table[1].ctypes.data)
+        dt_shift_off=dt_table[1].ctypes.data,
+        # a requested trace carries the reference's per-layer counts: classify every
+        # layer in full; otherwise intermediate layers classify probe sets (same output)
+        full_classify=int(trace is not None or os.environ.get("AFFT_DSFFT_LAZY") == "0"))
     lib = _lib.load()
     cap = max(8 * k, 1024)
     tcap = 4 * (n.bit_length() + 8)
@@ -302,7 +306,7 @@ def _dsfft_batch_native(xd: torch.Tensor, k: int, cfgs, idx: list[int]):
             activity_floor=float(c.activity_floor), c=int(plan.c), m=int(plan.m),
             anchors=anchors.ctypes.data, weights=weights.ctypes.data,
             dt_shifts=table[0].ctypes.data if table[0].size else None,
-            dt_shift_off=table[1].ctypes.data)
+            dt_shift_off=table[1].ctypes.data, full_classify=1)
     sub = xd[idx] if idx != list(range(xd.shape[0])) else xd
     sub = sub.contiguous()
     lib = _lib.load()

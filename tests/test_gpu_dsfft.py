@@ -96,3 +96,36 @@ def test_dsfft_goldens_active_fallback(golden_dsfft, monkeypatch):
     for case in golden_dsfft["cases"]:
         trace, out, ledger = _run(case)
         _check(case, trace, out, ledger)
+
+
+def _entries_lazy_and_full(case, monkeypatch, probe0=None):
+    """The native loop's entries dict with probe classifies (no trace requested) and with
+    every layer classified in full (trace requested)."""
+    from paper_2011_05749_b200 import DsfftConfig, _device
+    from paper_2011_05749_b200.dsfft import _dsfft_arrays
+
+    if probe0 is not None:
+        monkeypatch.setenv("AFFT_DSFFT_PROBE0", str(probe0))
+    xd = _device.as_device_signal(dsfft_signal(case))
+    cfg = DsfftConfig(mode=case["mode"], seed=case["seed"], noise_std=case["noise_std"])
+    lazy = _dsfft_arrays(xd, case["k"], cfg)
+    full = _dsfft_arrays(xd, case["k"], cfg, trace=[])
+    return lazy, full
+
+
+@pytest.mark.parametrize("probe0", [None, 1, 4096])
+def test_probe_classifies_change_nothing(golden_dsfft, monkeypatch, probe0):
+    """Intermediate layers' entries are discarded by the reference, so a noisy decode
+    classifies only probe sets there (the active children of the multi-tons found one
+    layer up; the first layer's first AFFT_DSFFT_PROBE0 buckets) and the whole layer only
+    when a probe finds no multi-ton.  The entries — positions in insertion order and
+    values — must be bit-identical to classifying every layer in full, for every golden
+    case and config 4's signals, whatever the first probe's size (1: the chain dies out
+    early and the full fallback runs often; 4096: the first layer in full)."""
+    cases = [c for c in golden_dsfft["cases"] if c["mode"] != "exact"]
+    cases += [json.load(open(p)) for p in C4]
+    assert cases
+    for case in cases:
+        (pl, vl), (pf, vf) = _entries_lazy_and_full(case, monkeypatch, probe0)
+        assert pl.tolist() == pf.tolist()
+        assert np.array_equal(vl, vf)
