@@ -13,6 +13,7 @@
 #include <mutex>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
@@ -325,9 +326,79 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
 // contiguous) runs stage B along qb instead.
 constexpr int kGfftThreads = 128;
 
-template <int LA, int LB>
-__global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
-    const __grid_constant__ GStockParams p) {
+// DeepFuse epilogue of the last radix-256 pass (N_s = n/256, 8 alias classes j0 + jj per
+// tile, thread (jj = tid & 7, qb = tid >> 3) holding y[qa] = Y[j + (qb + 16 qa) N_s]).
+// Depth dtop + t (dtop = log2 n - 8) has 2^t buckets r over each j, with values in the
+// tree order of dsfft.cu tree_sum: v_8(r) = Y[j + r N_s], v_t(r) = v_{t+1}(r) +
+// v_{t+1}(r + 2^t).  t >= 4: r = qb + 16 m, and r + 2^t is the same thread's m + 2^(t-4)
+// (in registers, in place); t = 3: the partner is thread qb + 8 (one value through
+// shared memory); t < 3: within warp 0.  The same sums as deep_flags_kernel and
+// tree_level_kernel, so every decision is bit-identical to the unfused path.  A tile owns
+// 8 consecutive bits (j0 % 8 == 0) of every bitmap: whole bytes, no atomics; a warp's
+// ballot holds 4 of them (lanes jj + 8 (qb & 3)).
+__device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], cd* V, int tid, int64_t j0,
+                                                   int dtop, const DeepFuse& f) {
+  const int jj = tid & 7, qb = tid >> 3, lane = tid & 31;
+  uint8_t* wb = reinterpret_cast<uint8_t*>(f.words);
+  const int64_t byte0 = j0 >> 3, rstride = int64_t(1) << (dtop - 3);
+  // |v| > thr_t: |v|^2 against the guard band, hypot only inside it (deep_flags_kernel)
+  auto put = [&](int t, int r, cd v, bool on) {
+    const double sq = v.re * v.re + v.im * v.im;
+    const bool flag = sq > f.t2hi[t] ? true : sq < f.t2lo[t] ? false : cabs_(v) > f.thr[t];
+    const unsigned bal = __ballot_sync(0xffffffffu, on && flag);
+    if (on && (lane & 7) == 0)
+      wb[f.word_off[t] * 4 + byte0 + (int64_t)r * rstride] = (uint8_t)(bal >> (lane & 24));
+  };
+  auto level = [&](auto tc) {  // compile-time M (a runtime bound left y[] in local memory)
+    constexpr int t = decltype(tc)::value, M = 1 << (t - 4);
+    if (t < 8) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) y[m] = cadd(y[m], y[m + M]);
+    }
+    if (t >= f.t_lo) {  // warp-uniform: shallower layers may not be asked for
+#pragma unroll
+      for (int m = 0; m < M; ++m) put(t, qb + 16 * m, y[m], true);
+    }
+  };
+  level(std::integral_constant<int, 8>{});
+  level(std::integral_constant<int, 7>{});
+  level(std::integral_constant<int, 6>{});
+  level(std::integral_constant<int, 5>{});
+  level(std::integral_constant<int, 4>{});
+  // V: [0, 128) v_4 by (jj, qb); then v_3 [64], v_2 [32], v_1 [16], v_0 [8]
+  __syncthreads();  // the previous tile's reads of V are done
+  V[jj * 16 + qb] = y[0];
+  __syncthreads();
+  if (tid < 64) {  // t = 3: 64 buckets, whole warps 0 and 1
+    const int r = tid >> 3;
+    const cd v = cadd(V[jj * 16 + r], V[jj * 16 + r + 8]);
+    V[128 + jj * 8 + r] = v;
+    if (3 >= f.t_lo) put(3, r, v, true);
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const cd* vin = V + 128;
+    cd* vout = V + 192;
+#pragma unroll
+    for (int t = 2; t >= 0; --t) {
+      const int items = 8 << t, r = tid >> 3;
+      const bool on = tid < items;
+      cd v = cd{0.0, 0.0};
+      if (on) {
+        v = cadd(vin[jj * (2 << t) + r], vin[jj * (2 << t) + r + (1 << t)]);
+        vout[jj * (1 << t) + r] = v;
+      }
+      __syncwarp();
+      if (t >= f.t_lo) put(t, r, v, on);
+      if (t == 0 && f.vtop && on) f.vtop[j0 + jj] = v;
+      vin = vout;
+      vout += items;
+    }
+  }
+}
+
+template <int LA, int LB, bool FUSE>
+__device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepFuse& f) {
   constexpr int A = 1 << LA, B = 1 << LB, LGR = LA + LB, R = A * B;
   constexpr int kCnt = kGStockPoints / R, kLgCnt = 11 - LGR;
   constexpr int LD = R + 1;
@@ -349,6 +420,7 @@ __global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
   const bool c64 = first && p.dtype == AFFT_C64;
   const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
   const double inv_b = 1.0 / (double)p.b;
+  double fsq = 0.0;  // FUSE: this thread's sum |Y|^2 over its tiles
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     int64_t chunk = tile % nchunks;
     if (p.perm == 1)  // nchunks a power of two: an odd multiplier is a bijection
@@ -471,10 +543,41 @@ __global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
         } else {  // complex128 output: 16-B aligned pairs
           const cd wv = cscale(a[qa], inv_b);
           *reinterpret_cast<double2*>(out + 2 * dst * p.out_bin_stride) = make_double2(wv.re, wv.im);
+          if constexpr (FUSE) {
+            a[qa] = wv;
+            fsq += wv.re * wv.re + wv.im * wv.im;
+          }
         }
+      }
+      if constexpr (FUSE) {
+        static_assert(A == 16 && B == 16 && IB == 1, "fused epilogue: the radix-256 last pass");
+        // dtop = log2(N_s): N_s = n / 256 on the last pass
+        deep_fuse_epilogue(a, U + kCnt * LD, tid, j0, 63 - __clzll((unsigned long long)p.Ns), f);
       }
     }
   }
+  if constexpr (FUSE) {
+    // sum |Y|^2 (only ever compared against a bound with a wide margin): one atomic
+    // per warp of the persistent grid (one per warp per tile serialised on the address)
+    if (f.norm2) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) fsq += __shfl_xor_sync(0xffffffffu, fsq, o);
+      if ((tid & 31) == 0) atomicAdd(f.norm2, fsq);
+    }
+  }
+}
+
+template <int LA, int LB>
+__global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
+    const __grid_constant__ GStockParams p) {
+  gfft_reg_body<LA, LB, false>(p, DeepFuse{});
+}
+
+// The last radix-256 pass of a DSFFT spectrum with the tree layers decided in its
+// epilogue (DeepFuse, afft_common.cuh).
+__global__ void __launch_bounds__(kGfftThreads, 3) gfft_flags_kernel(
+    const __grid_constant__ GStockParams p, const __grid_constant__ DeepFuse f) {
+  gfft_reg_body<4, 4, true>(p, f);
 }
 
 // ---- the same pass with its row loads on the TMA engine (bulk async copies into a
@@ -812,10 +915,17 @@ static bool encode_pass_map(CUtensorMap* m, const void* base, bool f32, int64_t 
 static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, int64_t ld,
                            int64_t b, const int64_t* shifts, int nshift, double* out,
                            int64_t out_offset, int64_t oss, int64_t osh, int64_t obin,
-                           cudaStream_t stream, const int64_t* shift_table) {
+                           cudaStream_t stream, const int64_t* shift_table,
+                           const DeepFuse* fuse = nullptr) {
   std::vector<int> radices;
   if (!plan_radices(b, &radices)) {
     set_error("bucket count %lld has a prime factor above %d", (long long)b, AFFT_MAX_SMEM_DFT);
+    return AFFT_EUNSUPPORTED;
+  }
+  // the fused epilogue needs a register-resident radix-256 last pass over full tiles
+  if (fuse && (radices.size() < 2 || radices.back() != 256 || (b / 256) % (kGStockPoints / 256) ||
+               fft_smem_path() || batch != 1 || nshift != 1 || obin != 1)) {
+    set_error("spectrum_fused: plan without a radix-256 register last pass");
     return AFFT_EUNSUPPORTED;
   }
   GStockParams q;
@@ -912,7 +1022,12 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     int use_tmap = 0;
-    if (lgr >= 4 && !fft_smem_path() && contiguous && (tma_env || tmap_env())) {
+    if (fuse && s == P - 1) {  // last pass with the DeepFuse epilogue
+      kfn = (const void*)gfft_flags_kernel;
+      g.perm = 0;
+      smem = (size_t)(R + (int64_t)g.cnt * (R + 1) + 256) * 16;  // + V (248 values)
+      threads = kGfftThreads;
+    } else if (lgr >= 4 && !fft_smem_path() && contiguous && (tma_env || tmap_env())) {
       kfn = gfft_tma_fn(lgr);
       g.perm = 0;
       smem = 128 + 2 * (size_t)R * g.cnt * 16 + (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
@@ -946,9 +1061,13 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * occ);
     void* args_reg[] = {&g};
     void* args_tma[] = {&g, &tmap, &use_tmap};
+    DeepFuse fz_arg = fuse ? *fuse : DeepFuse{};
+    void* args_fuse[] = {&g, &fz_arg};
     const bool tma_kernel = kfn == gfft_tma_fn(lgr) && lgr >= 4;
-    e = cudaLaunchKernel(kfn, dim3(grid), dim3(threads), tma_kernel ? args_tma : args_reg, smem,
-                         stream);
+    e = cudaLaunchKernel(kfn, dim3(grid), dim3(threads),
+                         tma_kernel ? args_tma
+                                    : (kfn == (const void*)gfft_flags_kernel ? args_fuse : args_reg),
+                         smem, stream);
     if (e != cudaSuccess) {
       rc = cuda_status(e, "large-b DFT launch");
       break;
@@ -1053,6 +1172,16 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
   gather_dft_kernel<<<grid, 256, smem_max, stream>>>(q);
   AFFT_CHECK_LAUNCH("gather_dft_kernel");
   return AFFT_OK;
+}
+
+int spectrum_fused(const void* x, int dtype, int64_t n, double* Y, const DeepFuse& f,
+                   cudaStream_t st) {
+  if (n < 4096 || (n & (n - 1))) {
+    set_error("spectrum_fused: n = %lld", (long long)n);
+    return AFFT_EUNSUPPORTED;
+  }
+  const int64_t zero = 0;
+  return launch_fourstep(x, dtype, n, 1, n, n, &zero, 1, Y, 0, n, n, 1, st, nullptr, &f);
 }
 
 }  // namespace afft

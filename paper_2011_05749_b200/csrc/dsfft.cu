@@ -17,6 +17,7 @@
 #include <climits>
 #include <cstring>
 #include <map>
+#include <utility>
 #include <vector>
 
 #include <cub/block/block_radix_sort.cuh>
@@ -250,6 +251,24 @@ __device__ __forceinline__ cd root_pi(int64_t m, int64_t q) {  // exp(-2 pi i m 
   return cd{cs, sn};
 }
 
+// A full layer's tau = 0 value from its aliases y[l] = Y[i + l b], l < L (L a power of
+// two <= LM), in the TREE order every path shares: T(i, d) = T(i, d+1) + T(i + 2^d, d+1)
+// with T(i, log2 n) = Y[i] (expand_layer's parent = sum of children, dsfft.py:82-115)
+// — i.e. y[l] += y[l + s] for s = L/2, ..., 1.  alias_all_kernel, alias_active_kernel,
+// deep_flags_kernel, tree_level_kernel and the spectrum's fused epilogue
+// (bucketize.cu) all produce exactly these sums, so their |v| > thr decisions agree
+// bit for bit, and a tree costs L - 1 additions for every layer below it at once.
+template <int LM>
+__device__ __forceinline__ cd tree_sum(cd (&y)[LM], int L) {
+#pragma unroll
+  for (int s = LM / 2; s >= 1; s >>= 1)
+    if (s < L) {
+#pragma unroll
+      for (int l = 0; l < s; ++l) y[l] = cadd(y[l], y[l + s]);
+    }
+  return y[0];
+}
+
 // rows[r][t] for selected buckets: one warp per row, lanes over the L spectrum
 // terms (load) and then over the shifts (sum).  L <= kAliasRowsMaxL; dynamic shared
 // memory holds the L roots and each warp's L spectrum terms.
@@ -436,11 +455,10 @@ __global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y
   for (int l = 0; l < LM; ++l)
     if (l < L) y[l] = Y[i + (int64_t)l * b];
   if (vals0) {
-    cd acc = y[0];
+    cd t[LM];
 #pragma unroll
-    for (int l = 1; l < LM; ++l)
-      if (l < L) acc = cadd(acc, y[l]);
-    vals0[i] = acc;
+    for (int l = 0; l < LM; ++l) t[l] = y[l];
+    vals0[i] = tree_sum<LM>(t, L);
   }
   if (energy) {
     double e = 0.0;
@@ -463,9 +481,9 @@ __global__ void __launch_bounds__(256) alias_all_kernel(const cd* __restrict__ Y
 }
 
 // Full deep layer straight to its active set, in one pass over the resident spectrum:
-// the tau = 0 value of bucket i is sum_l Y[i + l b], summed in the order
-// alias_all_kernel uses (so |v| and the decision are bit-identical to values + 
-// afft_active_indices), tested against thr, and never written.  Each CTA compacts its
+// the tau = 0 value of bucket i is sum_l Y[i + l b] in the tree order (tree_sum: |v| and
+// the decision are bit-identical to values + afft_active_indices), tested against thr,
+// and never written.  Each CTA compacts its
 // active buckets (ascending within the CTA) and reserves a segment of `out` with one
 // atomic, only when it has any; sort_active_kernel then puts the list in ascending
 // order.  Against values + count + scan + write, this reads Y once and the values never.
@@ -483,11 +501,7 @@ __global__ void __launch_bounds__(256) alias_active_kernel(const cd* __restrict_
 #pragma unroll
     for (int l = 0; l < LM; ++l)
       if (l < L) y[l] = Y[i + (int64_t)l * b];
-    cd acc = y[0];
-#pragma unroll
-    for (int l = 1; l < LM; ++l)
-      if (l < L) acc = cadd(acc, y[l]);
-    f = cabs_(acc) > thr;
+    f = cabs_(tree_sum<LM>(y, L)) > thr;
   }
   const unsigned m = __ballot_sync(0xffffffffu, f);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -574,8 +588,9 @@ int alias_active(const double* spectrum, int64_t n, int64_t b, double thr, int64
 // in ONE pass over the resident spectrum, instead of one pass + a one-CTA sort per
 // layer.  Thread i0 < bmin loads its Lmax aliases y[l] = Y[i0 + l bmin]; layer j
 // (b_j = bmin 2^j, L_j = Lmax >> j) holds the buckets i0 + m bmin, m < 2^j, whose tau = 0
-// value is sum_{l < L_j} Y[i + l b_j] = sum_l y[m + l 2^j] — summed in l order as
-// alias_active_kernel does, so the decisions |v| > thr_j are bit-identical to it.  The
+// value is T_j(m) = T_{j+1}(m) + T_{j+1}(m + 2^j), T_log2(Lmax)(m) = y[m] — the tree order
+// of tree_sum, computed deepest layer first in place (Lmax - 1 additions for all
+// layers), so the decisions |v| > thr_j are bit-identical to alias_active_kernel's.  The
 // warp's flags for one (layer, m) are one 32-bit word of the layer's bitmap (lanes
 // hold consecutive i0); a count / scan / write pass then turns the bitmaps into
 // ascending active lists, all layers at once.
@@ -583,10 +598,17 @@ constexpr int kDeepMaxLayers = 16;
 struct DeepLayers {
   int nl;                          // layers: j = 0 .. nl - 1
   double thr[kDeepMaxLayers];      // activity threshold of layer j
+  double t2hi[kDeepMaxLayers], t2lo[kDeepMaxLayers];  // thr^2 (1 +- 1e-14), the guard band
   int64_t word_off[kDeepMaxLayers + 1];   // bitmap words before layer j
   int64_t chunk_off[kDeepMaxLayers + 1];  // count chunks before layer j
 };
 constexpr int kDeepChunkWords = 2048;  // words per count / write CTA (256 threads x 8)
+
+// f(integral_constant<J>) for J = TOP, TOP - 1, ..., 0
+template <int TOP, class F, int... K>
+__device__ __forceinline__ void deepest_first(F& f, std::integer_sequence<int, K...>) {
+  (f(std::integral_constant<int, TOP - K>{}), ...);
+}
 
 template <int LM, int LOG2LM>
 __global__ void __launch_bounds__(128) deep_flags_kernel(const cd* __restrict__ Y, int64_t bmin,
@@ -599,29 +621,31 @@ __global__ void __launch_bounds__(128) deep_flags_kernel(const cd* __restrict__ 
 #pragma unroll
   for (int l = 0; l < LM; ++l) y[l] = on ? Y[i0 + (int64_t)l * bmin] : cd{0.0, 0.0};
   const int lane = threadIdx.x & 31;
+  // layer j: b = bmin 2^j, L = LM >> j; y[m] = T_j(m) after its additions.  Compile-time
+  // j per level (runtime loop bounds left y[] in local memory).
+  auto level = [&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    if (j < LOG2LM) {
 #pragma unroll
-  for (int j = 0; j <= LOG2LM; ++j) {  // layer j: b = bmin 2^j, L = LM >> j
-    if (jd + j >= D.nl) break;
+      for (int m = 0; m < (1 << j); ++m) y[m] = cadd(y[m], y[m + (1 << j)]);
+    }
+    if (jd + j >= D.nl) return;
 #pragma unroll
     for (int m = 0; m < (1 << j); ++m) {
-      cd acc = y[m];
-#pragma unroll
-      for (int l = 1; l < (LM >> j); ++l) acc = cadd(acc, y[m + (l << j)]);
+      const cd acc = y[m];
       if (j == 0 && v_out && on) v_out[i0] = acc;  // the shallowest deep layer's values
       // |v| > thr decided on |v|^2 against thr^2 with a 1e-14 guard band (|v|^2 in double
       // is within 3 ulp, hypot within 1): only values inside the band take hypot, so
       // every decision equals hypot(v) > thr (alias_active_kernel's test)
       const double sq = acc.re * acc.re + acc.im * acc.im;
       const double thr = D.thr[jd + j];
-      const double t2 = thr * thr;
-      const bool f = sq > t2 * (1.0 + 1e-14) ? true
-                     : sq < t2 * (1.0 - 1e-14) ? false
-                                               : cabs_(acc) > thr;
+      const bool f = sq > D.t2hi[jd + j] ? true : sq < D.t2lo[jd + j] ? false : cabs_(acc) > thr;
       const unsigned flags = __ballot_sync(0xffffffffu, on && f);
       if (lane == 0 && on)
         words[D.word_off[jd + j] + (i0 >> 5) + (int64_t)m * (bmin >> 5)] = flags;
     }
-  }
+  };
+  deepest_first<LOG2LM>(level, std::make_integer_sequence<int, LOG2LM + 1>{});
 }
 
 // popcounts of kDeepChunkWords words per CTA; chunks never straddle two layers
@@ -743,6 +767,14 @@ __global__ void __launch_bounds__(256) tree_level_kernel(const cd* __restrict__ 
   if ((threadIdx.x & 31) == 0 && on) words[i >> 5] = flags;
 }
 
+// thr and its guard band, rounded exactly as the kernels would (IEEE, no contraction)
+static void set_layer_threshold(DeepLayers* D, int j, double thr) {
+  const double t2 = thr * thr;
+  D->thr[j] = thr;
+  D->t2hi[j] = t2 * (1.0 + 1e-14);
+  D->t2lo[j] = t2 * (1.0 - 1e-14);
+}
+
 static void full_layers_layout(int64_t n, int d0, int nl, DeepLayers* D, int* jd, size_t* words_b,
                                size_t* chunks_b, size_t* vbuf_b) {
   memset(D, 0, sizeof(*D));
@@ -784,7 +816,7 @@ int full_active_all(const double* spectrum, int64_t n, int d0, int nl, const dou
     set_error("full_active_all: no layer with n/b <= 32 among the requested ones");
     return AFFT_EUNSUPPORTED;
   }
-  for (int j = 0; j < nl; ++j) D.thr[j] = thr[j];
+  for (int j = 0; j < nl; ++j) set_layer_threshold(&D, j, thr[j]);
   if (!scratch || scratch_bytes < wb + cb + vb) {
     set_error("full_active_all: scratch of %zu bytes needed", wb + cb + vb);
     return AFFT_ENOMEM;
@@ -813,6 +845,72 @@ int full_active_all(const double* spectrum, int64_t n, int d0, int nl, const dou
   }
   AFFT_CHECK_LAUNCH("deep_flags_kernel");
   for (int j = jd - 1; j >= 0; --j) {
+    const int64_t b = int64_t(1) << (d0 + j);
+    tree_level_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
+        vbuf + vofs[j + 1], b, thr[j], vbuf + vofs[j], words + D.word_off[j]);
+  }
+  AFFT_CHECK_LAUNCH("tree_level_kernel");
+  const unsigned chunks = (unsigned)D.chunk_off[nl];
+  deep_count_kernel<<<chunks, 256, 0, st>>>(words, D, chunk);
+  deep_scan_kernel<<<1, 32 * kDeepMaxLayers, 0, st>>>(chunk, D, counts);
+  deep_write_kernel<<<chunks, 256, 0, st>>>(words, D, chunk, out, cap);
+  AFFT_CHECK_LAUNCH("deep_write_kernel");
+  return AFFT_OK;
+}
+
+// full_active_all with the spectrum computed here: the last K2' pass decides every layer
+// at depths >= dtop = log2(n) - 8 in its epilogue (bucketize.cu deep_fuse_epilogue, the
+// tree_sum order, so the bitmaps are bit-identical to deep_flags_kernel's and
+// tree_level_kernel's) and leaves the depth-dtop values for the shallower layers; sum |Y|^2
+// into *norm2 (device, zeroed here).  Saves the deep_flags pass over Y (n 16 bytes).
+int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int d0, int nl,
+                          const double* thr, int64_t* out, int cap, int32_t* counts,
+                          double* norm2, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  DeepLayers D;
+  int jd = 0;
+  size_t wb = 0, cb = 0, vb = 0;
+  int log2n = 0;
+  while ((int64_t(1) << log2n) < n) ++log2n;
+  const int dtop = log2n - 8;
+  if (nl < 1 || nl > kDeepMaxLayers || (int64_t(1) << d0) < 32 || (n & (n - 1)) ||
+      d0 + nl - 1 != log2n || dtop < 12) {
+    set_error("full_active_all_fused: unsupported layers (n=%lld, d0=%d, nl=%d)", (long long)n,
+              d0, nl);
+    return AFFT_EUNSUPPORTED;
+  }
+  full_layers_layout(n, d0, nl, &D, &jd, &wb, &cb, &vb);
+  for (int j = 0; j < nl; ++j) set_layer_threshold(&D, j, thr[j]);
+  if (!scratch || scratch_bytes < wb + cb + vb) {
+    set_error("full_active_all_fused: scratch of %zu bytes needed", wb + cb + vb);
+    return AFFT_ENOMEM;
+  }
+  uint32_t* words = reinterpret_cast<uint32_t*>(scratch);
+  int32_t* chunk = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + wb);
+  cd* vbuf = jd > 0 ? reinterpret_cast<cd*>(reinterpret_cast<char*>(scratch) + wb + cb) : nullptr;
+  int64_t vofs[kDeepMaxLayers + 1] = {0};
+  for (int j = 0; j < jd; ++j) vofs[j + 1] = vofs[j] + (int64_t(1) << (d0 + j));
+  // layer j = depth d0 + j; fused depths dtop + t, t = 0..8
+  DeepFuse f;
+  memset(&f, 0, sizeof(f));
+  f.words = words;
+  f.t_lo = std::max(0, d0 - dtop);
+  for (int t = 0; t <= 8; ++t) {
+    const int j = dtop + t - d0;
+    f.word_off[t] = j >= 0 ? D.word_off[j] : 0;
+    f.thr[t] = j >= 0 ? D.thr[j] : 0.0;
+    f.t2hi[t] = j >= 0 ? D.t2hi[j] : 0.0;
+    f.t2lo[t] = j >= 0 ? D.t2lo[j] : 0.0;
+  }
+  const int jtop = dtop - d0;  // layer index of depth dtop (values needed below it)
+  f.vtop = jtop > 0 ? vbuf + vofs[jtop] : nullptr;
+  f.norm2 = norm2;
+  if (norm2) {
+    const cudaError_t e = cudaMemsetAsync(norm2, 0, 8, st);
+    if (e != cudaSuccess) return cuda_status(e, "full_active_all_fused norm");
+  }
+  int rc = spectrum_fused(x, dtype, n, Yout, f, st);
+  if (rc) return rc;
+  for (int j = jtop - 1; j >= 0; --j) {
     const int64_t b = int64_t(1) << (d0 + j);
     tree_level_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
         vbuf + vofs[j + 1], b, thr[j], vbuf + vofs[j], words + D.word_off[j]);

@@ -350,12 +350,17 @@ struct Dsfft {
     const char* e = std::getenv("AFFT_DSFFT_Y_L");
     return e ? std::max<int64_t>(1, std::atoll(e)) : 64;
   }();
-  bool alias_rows_ok(int64_t b) const {
+  // Larger L: one CTA per row (L <= 2^14), when asked for (AFFT_DSFFT_Y_L) or when the
+  // list is short enough (probe classifies) that its A L products cost less than the
+  // coset DFTs: ~83 ns per row at L = 2048 against ~23 us for the DFTs at config 4's
+  // depth 13 (launch lists), so up to A L = 2^19 once Y is resident.
+  static constexpr int64_t kShortRowsBudget = int64_t(1) << 19;
+  bool alias_rows_ok(int64_t b, int64_t count = -1) const {
     const int64_t L = n / b;
     if (L <= kAliasMaxL) return true;
     if (L <= kAliasRowsMaxL) return Y.p || L <= y_rows_l;
-    // larger L: one CTA per row (L <= 2^14), only when asked for (AFFT_DSFFT_Y_L)
-    return L <= (1 << 14) && L <= y_rows_l;
+    if (L > (1 << 14)) return false;
+    return L <= y_rows_l || (Y.p && count >= 0 && count * L <= kShortRowsBudget);
   }
 
   // ||Y||^2 for the noisy floor bound: from Y when resident, else by Parseval from x
@@ -530,17 +535,43 @@ struct Dsfft {
     deep_done = true;  // attempted: a failure below leaves the per-layer path
     const int nl = max_depth - depth + 1;
     if (nl < 1 || nl > 16 || (1LL << depth) < 32 || (n & (n - 1))) return AFFT_OK;
-    RC(spectrum());
     std::vector<double> thr((size_t)nl);
     for (int j = 0; j < nl; ++j) thr[j] = threshold(depth + j);
     DBuf counts, scratch;
     RC(deep_lists.alloc((size_t)nl * cap * 8, st, "dsfft layer lists"));
-    RC(counts.alloc((size_t)nl * 4, st, "dsfft layer counts"));
+    const size_t onorm = ((size_t)nl * 4 + 7) & ~size_t(7);  // counts | sum |Y|^2
+    RC(counts.alloc(onorm + 8, st, "dsfft layer counts"));
     const size_t sb = full_active_scratch(n, depth, nl);
     RC(scratch.alloc(sb, st, "dsfft layer scratch"));
-    RC(full_active_all(Y.as<double>(), n, depth, nl, thr.data(), deep_lists.as<int64_t>(), cap,
-                       counts.as<int32_t>(), scratch.p, sb, st));
-    RC(d2h(deep_counts, counts.p, (size_t)nl, st));
+    // the spectrum's last pass deciding the deepest nine layers in its epilogue
+    // (AFFT_DSFFT_FUSE=0: spectrum, then one pass over it)
+    const char* fe = std::getenv("AFFT_DSFFT_FUSE");
+    const bool fuse_env = !(fe && fe[0] == '0');
+    bool fused = false;
+    if (!Y.p && fuse_env) {
+      RC(Y.alloc((size_t)n * 16, st, "dsfft spectrum"));
+      double* norm2 = reinterpret_cast<double*>(counts.as<char>() + onorm);
+      const int rc = full_active_all_fused(x, dtype, n, Y.as<double>(), depth, nl, thr.data(),
+                                           deep_lists.as<int64_t>(), cap, counts.as<int32_t>(),
+                                           norm2, scratch.p, sb, st);
+      if (rc == AFFT_OK) {
+        fused = true;
+      } else if (rc == AFFT_EUNSUPPORTED) {
+        Y.reset();  // another plan: the unfused path below
+      } else {
+        return rc;
+      }
+    }
+    if (!fused) {
+      RC(spectrum());
+      RC(full_active_all(Y.as<double>(), n, depth, nl, thr.data(), deep_lists.as<int64_t>(), cap,
+                         counts.as<int32_t>(), scratch.p, sb, st));
+    }
+    std::vector<char> hb;
+    RC(d2h(hb, counts.p, onorm + (fused ? 8 : 0), st));
+    deep_counts.resize((size_t)nl);
+    std::memcpy(deep_counts.data(), hb.data(), (size_t)nl * 4);
+    if (fused && normY < 0) std::memcpy(&normY, hb.data() + onorm, 8);
     deep_d0 = depth;
     deep_nl = nl;
     deep_cap = cap;
@@ -579,7 +610,7 @@ struct Dsfft {
            DBuf& out, double* energy) {
     const int ns = (int)shifts.size();
     RC(out.alloc((size_t)std::max<int64_t>(count, 1) * ns * 16, st, "dsfft rows"));
-    if (alias_ok(b) || (!energy && alias_rows_ok(b))) {
+    if (alias_ok(b) || (!energy && alias_rows_ok(b, count))) {
       RC(spectrum());
       return afft_alias_rows(Y.as<double>(), n, b, shifts.data(), ns, count ? idx : nullptr, count,
                              out.as<double>(), energy, nullptr, st);

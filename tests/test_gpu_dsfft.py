@@ -129,3 +129,28 @@ def test_probe_classifies_change_nothing(golden_dsfft, monkeypatch, probe0):
         (pl, vl), (pf, vf) = _entries_lazy_and_full(case, monkeypatch, probe0)
         assert pl.tolist() == pf.tolist()
         assert np.array_equal(vl, vf)
+
+
+def test_fused_spectrum_layers_change_nothing(golden_dsfft, monkeypatch):
+    """The spectrum's last radix-256 pass decides the deepest nine full layers in its
+    epilogue (bucketize.cu deep_fuse_epilogue, n = 2^24 at config 4) instead of a
+    separate pass over Y; the sums run in the same order, so the layer traces and the
+    entries must be bit-identical to the unfused path (AFFT_DSFFT_FUSE=0)."""
+    from paper_2011_05749_b200 import DsfftConfig, _device
+    from paper_2011_05749_b200.dsfft import _dsfft_arrays
+
+    cases = [c for c in golden_dsfft["cases"] if c["mode"] != "exact"]
+    cases += [json.load(open(p)) for p in C4]
+    for case in cases:
+        xd = _device.as_device_signal(dsfft_signal(case))
+        cfg = DsfftConfig(mode=case["mode"], seed=case["seed"], noise_std=case["noise_std"])
+        got = {}
+        for fuse in ("1", "0"):
+            monkeypatch.setenv("AFFT_DSFFT_FUSE", fuse)
+            tr = []
+            got[fuse] = (_dsfft_arrays(xd, case["k"], cfg, trace=tr), tr)
+        (p1, v1), t1 = got["1"]
+        (p0, v0), t0 = got["0"]
+        assert t1 == t0
+        assert p1.tolist() == p0.tolist()
+        assert np.array_equal(v1, v0)
