@@ -139,6 +139,16 @@ int afft_truncate(const int64_t* pos, const double* val, const int32_t* count, i
                   int64_t batch, int32_t k, int64_t* out_pos, double* out_val,
                   int32_t* out_count, void* stream);
 
+/*
+ * truncate_spectrum (oneshot.py:260-263) of one HOST entry list (the native DSFFT loop's
+ * output): the min(k, count) largest |v| (hypot, as numpy's abs), ties to the smaller
+ * position, written in that order to out_pos/out_val (host).  Runs on the calling
+ * thread without touching the device (the Python drop-in calls it per signal with the
+ * GIL released, instead of a numpy lexsort under the GIL).
+ */
+int afft_truncate_host(const int64_t* pos, const double* val, int64_t count, int32_t k,
+                       int64_t* out_pos, double* out_val, int64_t* out_count);
+
 /* Resident ffast_fused_kernel CTAs per SM and its dynamic shared memory for a plan. */
 int afft_ffast_occupancy(int64_t n, const int64_t* factors /* host */, int32_t ncycles,
                          int32_t* blocks_per_sm /* host */, int32_t* smem_bytes /* host */);

@@ -48,6 +48,7 @@ SIGNATURES = {
     "afft_classify_exact": (_INT, [_P, _P, _I64, _I64, _I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]),
     "afft_subtract": (_INT, [_P, _P, _I32, _P, _P, _I64, _I64, _P]),
     "afft_truncate": (_INT, [_P, _P, _P, _I32, _I64, _I32, _P, _P, _P, _P]),
+    "afft_truncate_host": (_INT, [_P, _P, _I64, _I32, _P, _P, _P]),
     "afft_ffast_occupancy": (_INT, [_I64, _P, _I32, _P, _P]),
     "afft_ffast_workspace_size": (_SZ, [_I64, _INT, _I64, _P, _I32]),
     "afft_ffast": (

@@ -429,6 +429,68 @@ __global__ void __launch_bounds__(256) alias_rows_cta_kernel(
   }
 }
 
+// alias_rows_cta_kernel for rows of several signals (DSFFT batches, probe lists at the
+// shallow layers): row r is bucket idx[r] of signal sig[r] (spectrum Y + sig n, reduced
+// shifts tau_tab[sig][0..nshift)); the same arithmetic per row.
+__global__ void __launch_bounds__(256) alias_rows_cta_multi_kernel(
+    const cd* __restrict__ Y, int64_t n, int64_t b, int L, const int64_t* __restrict__ tau_tab,
+    int nshift, const int64_t* __restrict__ idx, const int32_t* __restrict__ sig, int64_t nrows,
+    cd* __restrict__ rows, bool tabled) {
+  extern __shared__ cd alias_smem[];
+  const int64_t r = blockIdx.x;
+  if (r >= nrows) return;
+  const int64_t i = idx[r];
+  const int s = sig[r];
+  const cd* Ys = Y + (int64_t)s * n;
+  cd* x = alias_smem;
+  cd* z = alias_smem + L;
+  cd* rt = tabled ? alias_smem + 2 * L : nullptr;  // w_L^j, j < L/2
+  for (int l = threadIdx.x; l < L; l += blockDim.x) x[l] = Ys[i + (int64_t)l * b];
+  if (rt)
+    for (int j = threadIdx.x; j < L / 2; j += blockDim.x) rt[j] = root_pi(j, L);
+  __syncthreads();
+  for (int Ls = 1; Ls < L; Ls <<= 1) {
+    for (int k = threadIdx.x; k < L / 2; k += blockDim.x) {
+      const int j = k & (Ls - 1), g = k / Ls;
+      const cd a = x[g * Ls + j];
+      const cd u = x[g * Ls + j + L / 2];
+      const int m = j * (L / (2 * Ls));
+      const cd t = j ? cmul(u, rt ? rt[m] : root_pi(m, L)) : u;
+      z[2 * g * Ls + j] = cadd(a, t);
+      z[2 * g * Ls + j + Ls] = csub(a, t);
+    }
+    __syncthreads();
+    cd* tmp = x;
+    x = z;
+    z = tmp;
+  }
+  const int64_t* taus = tau_tab + (int64_t)s * nshift;
+  for (int t = threadIdx.x; t < nshift; t += blockDim.x) {
+    const int64_t tau = taus[t];
+    rows[r * nshift + t] = cmul(x[(int)(tau & (L - 1))], root_pi(mulmod(i, tau, n), n));
+  }
+}
+
+int alias_rows_cta_multi(const double* Y, int64_t n, int64_t b, const int64_t* tau_tab,
+                         int nshift, const int64_t* idx, const int32_t* sig, int64_t nrows,
+                         double* rows, cudaStream_t st) {
+  const int64_t L = n / b;
+  if (nrows == 0 || nshift == 0) return AFFT_OK;
+  if (L > (1 << 14) || (L & (L - 1)) || b < 1 || n % b) {
+    set_error("alias_rows_cta_multi: n/b = %lld unsupported", (long long)L);
+    return AFFT_EUNSUPPORTED;
+  }
+  const bool tabled = L <= 4096;  // as afft_alias_rows
+  const size_t smem = (size_t)(tabled ? 2 * L + L / 2 : 2 * L) * sizeof(cd);
+  cudaError_t e = ensure_smem((const void*)alias_rows_cta_multi_kernel, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(alias_rows_cta_multi)");
+  alias_rows_cta_multi_kernel<<<(unsigned)nrows, 256, smem, st>>>(
+      reinterpret_cast<const cd*>(Y), n, b, (int)L, tau_tab, nshift, idx, sig, nrows,
+      reinterpret_cast<cd*>(rows), tabled);
+  AFFT_CHECK_LAUNCH("alias_rows_cta_multi_kernel");
+  return AFFT_OK;
+}
+
 struct AliasCosets {
   int32_t U;
   int32_t r[kAliasMaxL];     // distinct tau mod L

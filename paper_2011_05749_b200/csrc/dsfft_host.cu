@@ -715,7 +715,9 @@ struct Dsfft {
       *declined = true;
       return AFFT_OK;
     }
-    tr.add(5, depth, R, 1);  // ledger: the plan shifts
+    // ledger: the plan shifts, once per layer the reference classifies (a probe records
+    // them only when it decides the layer, i.e. finds a multi-ton; see finish_classify)
+    if (!is_probe) tr.add(5, depth, R, 1);
     DBuf energy;
     if (!skip) RC(energy.alloc((size_t)b * 8, st, "dsfft energies"));
     PMARK("classify setup");
@@ -787,7 +789,9 @@ struct Dsfft {
         }
       }
     }
-    tr.add(3, depth, is_probe ? -1 : (int64_t)E.f.size(), (int64_t)multi.size());
+    if (is_probe && !multi.empty()) tr.add(5, depth, P.c * P.m, 1);
+    if (!is_probe || !multi.empty())
+      tr.add(3, depth, is_probe ? -1 : (int64_t)E.f.size(), (int64_t)multi.size());
     return AFFT_OK;
   }
 
@@ -947,13 +951,14 @@ struct Dsfft {
 // them alone (afft_dsfft); every other signal's decisions are the single-signal ones.
 struct BatchSig {
   bool on = false, fallback = false;
+  bool lazy = false;  // probe classifies (full_classify = 0)
+  int mode = 0;       // next classify: 0 first probe, 1 children probe, 2 whole layer
   int depth = 0;
   int64_t m = 0;
   double normY = 0.0;
   std::vector<int64_t> shifts;  // raw plan shifts anchors[j] + 2^j t
   Entries E;
   std::vector<int64_t> multi;
-  int64_t nsingle = 0;
   std::vector<int32_t> trace;   // [kind, depth, a, b] records
   void add(int kind, int64_t a, int64_t b, int64_t c) {
     trace.push_back(kind);
@@ -963,40 +968,16 @@ struct BatchSig {
   }
 };
 
-// The concatenated active list of one step: member q's m[q] buckets from its cached
-// list at src[q], its signal id alongside (one launch for every member).
 constexpr int kBatchMax = 64;
-struct StepMembers {
-  int n;
-  int32_t sig[kBatchMax];
-  int64_t off[kBatchMax + 1];   // row offsets (off[n] = total)
-  const int64_t* src[kBatchMax];
-};
-__global__ void step_list_kernel(const __grid_constant__ StepMembers M, int64_t* __restrict__ idx,
-                                 int32_t* __restrict__ sig) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M.off[M.n]) return;
-  int q = 0;
-  while (i >= M.off[q + 1]) ++q;
-  idx[i] = M.src[q][i - M.off[q]];
-  sig[i] = M.sig[q];
-}
 
-// per member: singles and multitons of its rows (the trace and the loop control need
-// only the counts; entries are read back at a signal's last classify only)
-__global__ void step_count_kernel(const __grid_constant__ StepMembers M,
-                                  const int8_t* __restrict__ state, int32_t* __restrict__ cnt) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t tot = M.off[M.n];
-  int q = 0;
-  int single = 0, multi = 0;
-  if (i < tot) {
-    while (i >= M.off[q + 1]) ++q;
-    single = state[i] == AFFT_SINGLE_TON;
-    multi = state[i] == AFFT_MULTI_TON;
-  }
-  if (single) atomicAdd(cnt + 2 * q, 1);
-  if (multi) atomicAdd(cnt + 2 * q + 1, 1);
+// The active lists of every (signal, layer) packed end to end as int32 (bucket < 2^31)
+// for one read-back: segment g = s nl + j holds min(count, cap) entries from
+// lists + g cap, at packed offset off[g].
+__global__ void pack_lists_kernel(const int64_t* __restrict__ lists, int cap,
+                                  const int64_t* __restrict__ off, int32_t* __restrict__ out) {
+  const int64_t g = blockIdx.x;
+  const int64_t o = off[g], m = off[g + 1] - o;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) out[o + i] = (int32_t)lists[g * cap + i];
 }
 
 static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64_t ld, int k,
@@ -1009,6 +990,8 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
   d0 = std::min(d0, max_depth);
   const int nl = max_depth - d0 + 1;
   const int c = prm[0].c, mm = prm[0].m, R = c * mm;
+  const char* pe = std::getenv("AFFT_DSFFT_PROBE0");
+  const int64_t probe0 = pe ? std::max<int64_t>(0, std::atoll(pe)) : 256;
   sig.assign((size_t)S, BatchSig());
   for (int64_t s = 0; s < S; ++s) {
     const AfftDsfftParams& P = prm[s];
@@ -1016,6 +999,7 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
     g.on = P.mode != 0 && P.noise_std > 0.0 && P.c == c && P.m == mm && P.anchors &&
            P.weights;
     g.fallback = !g.on;
+    g.lazy = g.on && !P.full_classify && probe0 > 0;
     if (g.on)
       for (int j = 0; j < c; ++j)
         for (int t = 0; t < mm; ++t) g.shifts.push_back(P.anchors[j] + (int64_t(1) << j) * t);
@@ -1026,33 +1010,76 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
     return AFFT_OK;
   }
   const int cap = (int)std::min<int64_t>(16384, n);
-  // spectra of every signal and the |x|^2 partials (the floor bound), then every full
-  // layer's active list per signal, one read-back for all the counts and partials
-  DBuf Y, parts, lists, counts, scratch, taus;
+  const int64_t esz = dtype == AFFT_C64 ? 8 : 16;
+  // every signal's spectrum and full layers' active lists, as afft_dsfft makes them
+  // (the fused last pass when the plan allows: the same Y, bitmaps and sum |Y|^2), then
+  // one read-back of all counts and norms
+  DBuf Y, lists, blk, scratch, taus;
   RC(Y.alloc((size_t)S * n * 16, st, "dsfft batch spectra"));
-  const int64_t zero = 0;
-  RC(afft_bucketize(x, dtype, n, S, ld, n, &zero, 1, Y.as<double>(), n, n, 1, st));
-  const int nparts = afft_sumsq_parts(n, dtype);
-  RC(parts.alloc((size_t)S * nparts * 8, st, "dsfft batch partials"));
-  RC(afft_sumsq(x, dtype, n, S, ld, parts.as<double>(), st));
   RC(lists.alloc((size_t)S * nl * cap * 8, st, "dsfft batch lists"));
-  RC(counts.alloc((size_t)S * nl * 4, st, "dsfft batch counts"));
+  const int nparts = afft_sumsq_parts(n, dtype);
+  const size_t onorm = ((size_t)S * nl * 4 + 7) & ~size_t(7), opart = onorm + (size_t)S * 8;
+  RC(blk.alloc(opart + (size_t)S * nparts * 8, st, "dsfft batch counts"));
+  int32_t* counts = blk.as<int32_t>();
+  double* norms = reinterpret_cast<double*>(blk.as<char>() + onorm);
+  double* parts = reinterpret_cast<double*>(blk.as<char>() + opart);
   const size_t sb = full_active_scratch(n, d0, nl);
   RC(scratch.alloc(sb, st, "dsfft batch layer scratch"));
+  const char* fe = std::getenv("AFFT_DSFFT_FUSE");
+  bool fused = !(fe && fe[0] == '0');
+  std::vector<char> was_fused((size_t)S, 0);
   for (int64_t s = 0; s < S; ++s) {
     if (!sig[s].on) continue;
     std::vector<double> thr((size_t)nl);
     for (int j = 0; j < nl; ++j)
       thr[j] = std::max(prm[s].activity_floor,
                         3.0 * prm[s].noise_std / std::sqrt((double)(1LL << (d0 + j))));
-    RC(full_active_all(Y.as<double>() + 2 * s * n, n, d0, nl, thr.data(),
-                       lists.as<int64_t>() + s * nl * cap, cap, counts.as<int32_t>() + s * nl,
-                       scratch.p, sb, st));
+    const char* xs = reinterpret_cast<const char*>(x) + s * ld * esz;
+    double* Ys = Y.as<double>() + 2 * s * n;
+    int64_t* ls = lists.as<int64_t>() + s * nl * cap;
+    if (fused) {
+      const int rc = full_active_all_fused(xs, dtype, n, Ys, d0, nl, thr.data(), ls, cap,
+                                           counts + s * nl, norms + s, scratch.p, sb, st);
+      if (rc == AFFT_OK) {
+        was_fused[s] = 1;
+        continue;
+      }
+      if (rc != AFFT_EUNSUPPORTED) return rc;
+      fused = false;  // another plan (nothing launched): the unfused path from here on
+    }
+    const int64_t zero = 0;
+    RC(afft_bucketize(xs, dtype, n, 1, n, n, &zero, 1, Ys, n, n, 1, st));
+    RC(afft_sumsq(xs, dtype, n, 1, n, parts + s * nparts, st));
+    RC(full_active_all(Ys, n, d0, nl, thr.data(), ls, cap, counts + s * nl, scratch.p, sb, st));
   }
-  std::vector<int32_t> hc;
-  std::vector<double> hp;
-  RC(d2h(hc, counts.p, (size_t)S * nl, st));
-  RC(d2h(hp, parts.p, (size_t)S * nparts, st));
+  PMARK("b spectra enqueue");
+  std::vector<char> hb;
+  RC(d2h(hb, blk.p, opart + (size_t)S * nparts * 8, st));
+  PMARK("b counts read-back");
+  std::vector<int32_t> hc((size_t)S * nl);
+  std::memcpy(hc.data(), hb.data(), hc.size() * 4);
+  auto count_at = [&](int64_t s, int depth) { return (int64_t)hc[(size_t)s * nl + (depth - d0)]; };
+  // host copies of every list (probe lists and the full members' rows come from them)
+  std::vector<int64_t> hoff((size_t)S * nl + 1, 0);
+  for (int64_t g = 0; g < S * nl; ++g)
+    hoff[g + 1] = hoff[g] + (sig[g / nl].on ? std::min<int64_t>(hc[g], cap) : 0);
+  std::vector<int32_t> hl;
+  {
+    DBuf doff, packed;
+    RC(doff.alloc(hoff.size() * 8, st, "dsfft batch list offsets"));
+    CK(cudaMemcpyAsync(doff.p, hoff.data(), hoff.size() * 8, cudaMemcpyHostToDevice, st));
+    RC(packed.alloc((size_t)std::max<int64_t>(hoff.back(), 1) * 4, st, "dsfft batch packed lists"));
+    pack_lists_kernel<<<(unsigned)(S * nl), 256, 0, st>>>(lists.as<int64_t>(), cap,
+                                                          doff.as<int64_t>(), packed.as<int32_t>());
+    CK(cudaGetLastError());
+    RC(d2h(hl, packed.p, (size_t)hoff.back(), st));
+  }
+  PMARK("b lists read-back");
+  auto host_list = [&](int64_t s, int depth, int64_t* m) -> const int32_t* {
+    const int64_t g = s * nl + (depth - d0);
+    *m = hoff[g + 1] - hoff[g];
+    return hl.data() + hoff[g];
+  };
   // reduced shift tables for the alias rows and the fit
   {
     std::vector<int64_t> tt((size_t)S * R, 0);
@@ -1062,14 +1089,18 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
     RC(taus.alloc(tt.size() * 8, st, "dsfft batch shifts"));
     CK(cudaMemcpyAsync(taus.p, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, st));
   }
-  auto count_at = [&](int64_t s, int depth) { return (int64_t)hc[(size_t)s * nl + (depth - d0)]; };
   // initial layer and the first expansions, from the counts (dsfft.py:258-264)
   for (int64_t s = 0; s < S; ++s) {
     BatchSig& g = sig[s];
     if (!g.on) continue;
-    double sum = 0.0;
-    for (int q = 0; q < nparts; ++q) sum += hp[(size_t)s * nparts + q];
-    g.normY = sum / (double)n;
+    if (was_fused[s]) {
+      std::memcpy(&g.normY, hb.data() + onorm + (size_t)s * 8, 8);
+    } else {
+      double sum = 0.0;
+      for (int q = 0; q < nparts; ++q)
+        sum += reinterpret_cast<const double*>(hb.data() + opart)[(size_t)s * nparts + q];
+      g.normY = sum / (double)n;
+    }
     g.depth = d0;
     g.m = count_at(s, d0);
     if (g.m > cap) {
@@ -1087,8 +1118,11 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
       g.depth = next;
       g.add(2, next, g.m, -1);
     }
+    g.mode = 0;  // first classify at the stop layer
   }
-  // classify steps: all signals at the smallest pending depth together
+  // classify steps: all signals at the smallest pending depth together, each with its
+  // probe list (afft_dsfft's classify_layer: the active children of the multi-tons it
+  // found one layer up, or the stop layer's first probe0 buckets) or its whole layer
   DBuf idx, sidx, rows, ws, gates;
   for (;;) {
     int depth = INT32_MAX;
@@ -1096,9 +1130,13 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
       if (g.on) depth = std::min(depth, g.depth);
     if (depth == INT32_MAX) break;
     const int64_t b = 1LL << depth, L = n / b;
-    std::vector<int64_t> members, offs;
+    struct Mem {
+      int64_t s, off, cnt;
+      bool probe, alias;
+    };
+    std::vector<Mem> mem;
     std::vector<double> t0s((size_t)S, 0.0), t1s((size_t)S, 0.0);
-    int64_t A = 0;
+    std::vector<std::vector<int64_t>> cand_of((size_t)S);
     for (int64_t s = 0; s < S; ++s) {
       BatchSig& g = sig[s];
       if (!g.on || g.depth != depth) continue;
@@ -1110,75 +1148,110 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
       }
       t0s[s] = 1.5 * base;
       t1s[s] = 2.5 * base;
-      members.push_back(s);
-      offs.push_back(A);
-      A += g.m;
+      int64_t m = 0;
+      const int32_t* act = host_list(s, depth, &m);
+      std::vector<int64_t>& cand = cand_of[s];
+      bool probe = false;
+      if (g.lazy && depth < max_depth && g.mode != 2 && m > 0) {
+        if (g.mode == 0) {
+          cand.assign(act, act + std::min<int64_t>(m, probe0));
+        } else {
+          const int64_t half = 1LL << (depth - 1);
+          for (int pass = 0; pass < 2; ++pass)
+            for (int64_t i : g.multi) {
+              const int64_t cb = i + (pass ? half : 0);
+              if (std::binary_search(act, act + m, (int32_t)cb)) cand.push_back(cb);
+            }
+        }
+        probe = !cand.empty() && (int64_t)cand.size() < m;
+      }
+      if (!probe) cand.assign(act, act + m);
+      // the row source afft_dsfft's rows() picks for this list (alias_rows_ok)
+      const int64_t cnt = (int64_t)cand.size();
+      const bool alias = L <= 256 || (L <= (1 << 14) && cnt * L <= (int64_t(1) << 19));
+      mem.push_back({s, 0, cnt, probe, alias});
     }
-    if (members.empty()) continue;
-    StepMembers M;
-    memset(&M, 0, sizeof(M));
-    M.n = (int)members.size();
-    for (size_t q = 0; q < members.size(); ++q) {
-      M.sig[q] = (int32_t)members[q];
-      M.off[q] = offs[q];
-      M.src[q] = lists.as<int64_t>() + (members[q] * nl + (depth - d0)) * cap;
+    PMARK("b step lists");
+    if (mem.empty()) continue;
+    // members with alias rows first, so the coset-DFT members are one contiguous range
+    std::stable_sort(mem.begin(), mem.end(),
+                     [](const Mem& a, const Mem& b2) { return a.alias && !b2.alias; });
+    int64_t A = 0;
+    for (auto& q : mem) {
+      q.off = A;
+      A += q.cnt;
     }
-    M.off[members.size()] = A;
-    std::vector<int32_t> hcnt((size_t)2 * members.size(), 0);
-    DBuf pk_state, pk_f0, pk_val, dcnt;
+    std::vector<int64_t> h_idx((size_t)A);
+    std::vector<int32_t> h_sig((size_t)A);
+    int64_t A_alias = 0;
+    for (auto& q : mem) {
+      std::copy(cand_of[q.s].begin(), cand_of[q.s].end(), h_idx.begin() + q.off);
+      std::fill(h_sig.begin() + q.off, h_sig.begin() + q.off + q.cnt, (int32_t)q.s);
+      if (q.alias) A_alias = q.off + q.cnt;
+    }
+    DBuf pk;  // state [A] | f0 [A] | val [A]: one read-back per step
+    const size_t of0 = ((size_t)A + 7) & ~size_t(7), oval = of0 + (size_t)A * 8;
+    std::vector<char> hpk;
     if (A > 0) {
       RC(idx.alloc((size_t)A * 8, st, "dsfft batch rows index"));
       RC(sidx.alloc((size_t)A * 4, st, "dsfft batch rows signal"));
-      step_list_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(M, idx.as<int64_t>(),
-                                                                    sidx.as<int32_t>());
-      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(idx.p, h_idx.data(), (size_t)A * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(sidx.p, h_sig.data(), (size_t)A * 4, cudaMemcpyHostToDevice, st));
       RC(rows.alloc((size_t)A * R * 16, st, "dsfft batch rows"));
       if (L <= 256) {
         RC(alias_rows_multi(Y.as<double>(), n, b, taus.as<int64_t>(), R, idx.as<int64_t>(),
                             sidx.as<int32_t>(), A, rows.as<double>(), st));
       } else {
-        // shallow layers: every member's distinct-residue coset DFTs (tau mod L) over its
-        // own signal in one batched transform, then the rows picked and rotated
-        std::vector<std::vector<int64_t>> res(S);
-        std::vector<int32_t> coset((size_t)S * R, 0);
-        std::vector<int64_t> qrot((size_t)S * R, 0);
-        int U = 1;
-        for (int64_t s2 : members) {
-          std::map<int64_t, int> seen;
-          for (int t = 0; t < R; ++t) {
-            const int64_t tm = host_pymod(sig[s2].shifts[t], n), r = tm % L;
-            auto it = seen.find(r);
-            int u;
-            if (it == seen.end()) {
-              u = (int)res[s2].size();
-              seen[r] = u;
-              res[s2].push_back(r);
-            } else {
-              u = it->second;
+        if (A_alias > 0)  // short (probe) lists at shallow layers: one CTA per row
+          RC(alias_rows_cta_multi(Y.as<double>(), n, b, taus.as<int64_t>(), R, idx.as<int64_t>(),
+                                  sidx.as<int32_t>(), A_alias, rows.as<double>(), st));
+        if (A > A_alias) {
+          // whole shallow layers: each member's distinct-residue coset DFTs (tau mod L)
+          // over its own signal in one batched transform, then the rows picked and rotated
+          std::vector<std::vector<int64_t>> res(S);
+          std::vector<int32_t> coset((size_t)S * R, 0);
+          std::vector<int64_t> qrot((size_t)S * R, 0);
+          int U = 1;
+          for (auto& q : mem) {
+            if (q.alias) continue;
+            const int64_t s2 = q.s;
+            std::map<int64_t, int> seen;
+            for (int t = 0; t < R; ++t) {
+              const int64_t tm = host_pymod(sig[s2].shifts[t], n), r = tm % L;
+              auto it = seen.find(r);
+              int u;
+              if (it == seen.end()) {
+                u = (int)res[s2].size();
+                seen[r] = u;
+                res[s2].push_back(r);
+              } else {
+                u = it->second;
+              }
+              coset[(size_t)s2 * R + t] = u;
+              qrot[(size_t)s2 * R + t] = tm / L;
             }
-            coset[(size_t)s2 * R + t] = u;
-            qrot[(size_t)s2 * R + t] = tm / L;
+            U = std::max(U, (int)res[s2].size());
           }
-          U = std::max(U, (int)res[s2].size());
+          // every signal of the batch gets U residues (non-members / padding repeat one)
+          std::vector<int64_t> table((size_t)S * U, 0);
+          for (int64_t s2 = 0; s2 < S; ++s2)
+            for (int u = 0; u < U; ++u)
+              table[(size_t)s2 * U + u] =
+                  res[s2].empty() ? 0 : res[s2][std::min<size_t>((size_t)u, res[s2].size() - 1)];
+          DBuf dtab, dcos, dq, cosets;
+          RC(dtab.alloc(table.size() * 8, st, "dsfft batch residues"));
+          RC(dcos.alloc(coset.size() * 4, st, "dsfft batch coset map"));
+          RC(dq.alloc(qrot.size() * 8, st, "dsfft batch rotations"));
+          CK(cudaMemcpyAsync(dtab.p, table.data(), table.size() * 8, cudaMemcpyHostToDevice, st));
+          CK(cudaMemcpyAsync(dcos.p, coset.data(), coset.size() * 4, cudaMemcpyHostToDevice, st));
+          CK(cudaMemcpyAsync(dq.p, qrot.data(), qrot.size() * 8, cudaMemcpyHostToDevice, st));
+          RC(cosets.alloc((size_t)S * U * b * 16, st, "dsfft batch coset DFTs"));
+          RC(afft_bucketize_table(x, dtype, n, S, ld, b, dtab.as<int64_t>(), U,
+                                  cosets.as<double>(), (int64_t)U * b, b, 1, st));
+          RC(rows_gather_multi(cosets.as<double>(), b, U, R, dcos.as<int32_t>(), dq.as<int64_t>(),
+                               idx.as<int64_t>() + A_alias, sidx.as<int32_t>() + A_alias,
+                               A - A_alias, rows.as<double>() + 2 * A_alias * R, st));
         }
-        // every signal of the batch gets U residues (non-members / padding repeat one)
-        std::vector<int64_t> table((size_t)S * U, 0);
-        for (int64_t s2 = 0; s2 < S; ++s2)
-          for (int u = 0; u < U; ++u)
-            table[(size_t)s2 * U + u] =
-                res[s2].empty() ? 0 : res[s2][std::min<size_t>((size_t)u, res[s2].size() - 1)];
-        DBuf dtab, dcos, dq, cosets;
-        RC(dtab.alloc(table.size() * 8, st, "dsfft batch residues"));
-        RC(dcos.alloc(coset.size() * 4, st, "dsfft batch coset map"));
-        RC(dq.alloc(qrot.size() * 8, st, "dsfft batch rotations"));
-        CK(cudaMemcpyAsync(dtab.p, table.data(), table.size() * 8, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(dcos.p, coset.data(), coset.size() * 4, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(dq.p, qrot.data(), qrot.size() * 8, cudaMemcpyHostToDevice, st));
-        RC(cosets.alloc((size_t)S * U * b * 16, st, "dsfft batch coset DFTs"));
-        RC(afft_bucketize_table(x, dtype, n, S, ld, b, dtab.as<int64_t>(), U, cosets.as<double>(),
-                                (int64_t)U * b, b, 1, st));
-        RC(rows_gather_multi(cosets.as<double>(), b, U, R, dcos.as<int32_t>(), dq.as<int64_t>(),
-                             idx.as<int64_t>(), sidx.as<int32_t>(), A, rows.as<double>(), st));
       }
       std::vector<double> gt((size_t)2 * S);
       for (int64_t s2 = 0; s2 < S; ++s2) {
@@ -1187,69 +1260,75 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
       }
       RC(gates.alloc(gt.size() * 8, st, "dsfft batch gates"));
       CK(cudaMemcpyAsync(gates.p, gt.data(), gt.size() * 8, cudaMemcpyHostToDevice, st));
-      RC(pk_state.alloc((size_t)A, st, "dsfft batch states"));
-      RC(pk_f0.alloc((size_t)A * 8, st, "dsfft batch f0"));
-      RC(pk_val.alloc((size_t)A * 16, st, "dsfft batch values"));
+      RC(pk.alloc(oval + (size_t)A * 16, st, "dsfft batch results"));
       DBuf rn;
       RC(rn.alloc((size_t)A * 8, st, "dsfft batch resnorm"));
       const size_t need = afft_singleton_workspace_size(n, A, b, c, mm);
       RC(ws.alloc(need, st, "dsfft batch search workspace"));
       RC(classify_noisy_multi(rows.as<double>(), idx.as<int64_t>(), sidx.as<int32_t>(), A, b, n,
-                              taus.as<int64_t>(), c, mm, prm[members[0]].weights,
-                              gates.as<double>(), gates.as<double>() + S,
-                              pk_state.as<int8_t>(), pk_f0.as<int64_t>(), pk_val.as<double>(),
-                              rn.as<double>(), ws.p, need, st));
-      RC(dcnt.alloc((size_t)2 * members.size() * 4, st, "dsfft batch step counts"));
-      CK(cudaMemsetAsync(dcnt.p, 0, (size_t)2 * members.size() * 4, st));
-      step_count_kernel<<<(unsigned)((A + 255) / 256), 256, 0, st>>>(M, pk_state.as<int8_t>(),
-                                                                     dcnt.as<int32_t>());
-      CK(cudaGetLastError());
-      RC(d2h(hcnt, dcnt.p, (size_t)2 * members.size(), st));
+                              taus.as<int64_t>(), c, mm, prm[mem[0].s].weights,
+                              gates.as<double>(), gates.as<double>() + S, pk.as<int8_t>(),
+                              reinterpret_cast<int64_t*>(pk.as<char>() + of0),
+                              reinterpret_cast<double*>(pk.as<char>() + oval), rn.as<double>(),
+                              ws.p, need, st));
+      PMARK("b step enqueue");
+      RC(d2h(hpk, pk.p, oval + (size_t)A * 16, st));
+      PMARK("b step read-back");
     }
-    // trace and loop control from the counts; the entries of a signal's last classify
-    std::vector<size_t> last;
-    for (size_t q = 0; q < members.size(); ++q) {
-      BatchSig& g = sig[members[q]];
-      const int64_t ns = hcnt[2 * q], nm = hcnt[2 * q + 1];
-      g.add(5, depth, R, 1);
-      g.add(3, depth, ns, nm);
-      g.E.clear();
-      g.multi.clear();
-      g.nsingle = ns;
-      if (nm > 0 && g.depth < max_depth) {  // re-expand (dsfft.py:190-192)
+    const int8_t* hs = reinterpret_cast<const int8_t*>(hpk.data());
+    const int64_t* hf = reinterpret_cast<const int64_t*>(hpk.data() + of0);
+    const cd* hv = reinterpret_cast<const cd*>(hpk.data() + oval);
+    // trace and loop control per member, as afft_dsfft's classify_layer / run
+    for (auto& q : mem) {
+      BatchSig& g = sig[q.s];
+      int64_t ns = 0;
+      std::vector<int64_t> multis;
+      for (int64_t i = q.off; i < q.off + q.cnt; ++i) {
+        if (hs[i] == AFFT_SINGLE_TON) ++ns;
+        else if (hs[i] == AFFT_MULTI_TON) multis.push_back(h_idx[i]);
+      }
+      if (q.probe) {
+        if (multis.empty()) {  // no multi-ton among the probes: the whole layer next step
+          g.mode = 2;
+          continue;
+        }
+        g.add(5, depth, R, 1);
+        g.add(3, depth, -1, (int64_t)multis.size());
+      } else {
+        g.add(5, depth, R, 1);
+        g.add(3, depth, ns, (int64_t)multis.size());
+      }
+      g.multi.swap(multis);
+      if (!g.multi.empty() && g.depth < max_depth) {  // re-expand (dsfft.py:190-192)
         const int next = g.depth + 1;
-        if (2 * g.m <= next || count_at(members[q], next) > cap) {
+        if (2 * g.m <= next || count_at(q.s, next) > cap) {
           g.on = false, g.fallback = true;
           continue;
         }
-        g.m = count_at(members[q], next);
+        g.m = count_at(q.s, next);
         g.depth = next;
+        g.mode = 1;
         g.add(2, next, g.m, -1);
       } else {
         g.on = false;
-        if (nm > 0 && (int64_t)k - ns > 0) {
+        if (!g.multi.empty() && (int64_t)k - ns > 0) {
           g.fallback = true;  // leftover multitons: _resolve_aliased, alone
         } else {
-          last.push_back(q);
+          // the entries of the last classify, ascending bucket order (a full layer); the
+          // keys are distinct (f0 mod b is the bucket), so no dict look-ups are needed
+          g.E.f.clear();
+          g.E.v.clear();
+          g.E.f.reserve((size_t)ns);
+          g.E.v.reserve((size_t)ns);
+          for (int64_t i = q.off; i < q.off + q.cnt; ++i)
+            if (hs[i] == AFFT_SINGLE_TON) {
+              g.E.f.push_back(hf[i]);
+              g.E.v.push_back(hv[i]);
+            }
         }
       }
     }
-    if (!last.empty() && A > 0) {
-      std::vector<int8_t> hs;
-      std::vector<int64_t> hf;
-      std::vector<cd> hv;
-      RC(d2h(hs, pk_state.p, (size_t)A, st));
-      RC(d2h(hf, pk_f0.p, (size_t)A, st));
-      RC(d2h(hv, pk_val.p, (size_t)A, st));
-      for (size_t q : last) {
-        BatchSig& g = sig[members[q]];
-        g.E.reserve((size_t)g.nsingle);
-        // ascending bucket order within the member (its cached list is ascending); the
-        // singletons' f0 are distinct (f0 mod b is the bucket)
-        for (int64_t i = offs[q]; i < offs[q] + M.off[q + 1] - M.off[q]; ++i)
-          if (hs[i] == AFFT_SINGLE_TON) g.E.put(hf[i], hv[i]);
-      }
-    }
+    PMARK("b step results");
   }
   return AFFT_OK;
 }
@@ -1258,6 +1337,34 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
 }  // namespace afft
 
 using namespace afft;
+
+extern "C" int afft_truncate_host(const int64_t* pos, const double* val, int64_t count, int32_t k,
+                                  int64_t* out_pos, double* out_val, int64_t* out_count) {
+  if (count < 0 || k < 0 || !out_count || (count > 0 && (!pos || !val)) ||
+      (k > 0 && count > 0 && (!out_pos || !out_val))) {
+    set_error("afft_truncate_host: bad arguments");
+    return AFFT_EINVAL;
+  }
+  const int64_t m = std::min<int64_t>(count, k);
+  std::vector<double> mag((size_t)count);
+  for (int64_t i = 0; i < count; ++i) mag[i] = std::hypot(val[2 * i], val[2 * i + 1]);
+  std::vector<int64_t> ord((size_t)count);
+  for (int64_t i = 0; i < count; ++i) ord[i] = i;
+  // key (-|v|, f): larger magnitude first, then the smaller position (the positions
+  // are distinct, so the order is total and the result deterministic)
+  auto before = [&](int64_t a, int64_t b) {
+    return mag[a] != mag[b] ? mag[a] > mag[b] : pos[a] < pos[b];
+  };
+  if (m < count) std::nth_element(ord.begin(), ord.begin() + m, ord.end(), before);
+  std::sort(ord.begin(), ord.begin() + m, before);
+  for (int64_t i = 0; i < m; ++i) {
+    out_pos[i] = pos[ord[i]];
+    out_val[2 * i] = val[2 * ord[i]];
+    out_val[2 * i + 1] = val[2 * ord[i] + 1];
+  }
+  *out_count = m;
+  return AFFT_OK;
+}
 
 extern "C" int afft_dsfft(const void* x, int dtype, int64_t n, int32_t k,
                           const AfftDsfftParams* params, int64_t* out_pos, double* out_val,
@@ -1340,11 +1447,18 @@ extern "C" int afft_dsfft_batch(const void* x, int dtype, int64_t n, int64_t bat
   g_prof.wait_s = 0.0;
   g_prof.syncs = 0;
   const double t_start = g_prof.on ? now_s() : 0.0;
+  g_marks.acc.clear();
+  g_marks.last = t_start;
+  g_marks.last_wait = 0.0;
   const int rc = dsfft_batch_run(x, dtype, n, batch, ld, k, params, sig, (cudaStream_t)stream);
-  if (g_prof.on)
+  if (g_prof.on) {
     std::fprintf(stderr, "afft_dsfft_batch: %lld signals, %.3f ms total, %.3f ms waiting in %d "
                  "read-backs\n", (long long)batch, (now_s() - t_start) * 1e3, g_prof.wait_s * 1e3,
                  g_prof.syncs);
+    for (auto& a : g_marks.acc)
+      std::fprintf(stderr, "  %-22s x%-3d %.3f ms, host %.3f ms\n", a.what, a.n, a.total * 1e3,
+                   (a.total - a.wait) * 1e3);
+  }
   if (rc) {
     cudaStreamSynchronize((cudaStream_t)stream);
     return rc;

@@ -261,10 +261,7 @@ def dsfft(x, k: int, config: DsfftConfig | None = None,
     if k > 64:
         warnings.warn(f"binary-tree search degrades for large sparsity (k={k})", stacklevel=2)
     pos, val = _dsfft_arrays(_device.as_device_signal(x), k, config or DsfftConfig(), ledger)
-    # truncate_spectrum order (-|v|, f), first k (oneshot.py:260-263); the entry keys
-    # are distinct, so the lexicographic sort is total
-    order = np.lexsort((pos, -np.abs(val)))[:k]
-    return SparseSpectrum(n, dict(zip(pos[order].tolist(), val[order].tolist())))
+    return _top_k(n, k, pos, val)
 
 
 _POOL_LOCK = __import__("threading").Lock()
@@ -306,7 +303,8 @@ def _dsfft_batch_native(xd: torch.Tensor, k: int, cfgs, idx: list[int]):
             activity_floor=float(c.activity_floor), c=int(plan.c), m=int(plan.m),
             anchors=anchors.ctypes.data, weights=weights.ctypes.data,
             dt_shifts=table[0].ctypes.data if table[0].size else None,
-            dt_shift_off=table[1].ctypes.data, full_classify=1)
+            dt_shift_off=table[1].ctypes.data,
+            full_classify=int(os.environ.get("AFFT_DSFFT_LAZY") == "0"))
     sub = xd[idx] if idx != list(range(xd.shape[0])) else xd
     sub = sub.contiguous()
     lib = _lib.load()
@@ -333,14 +331,20 @@ def _dsfft_batch_native(xd: torch.Tensor, k: int, cfgs, idx: list[int]):
 
 def _top_k(n: int, k: int, pos, val) -> SparseSpectrum:
     """truncate_spectrum (oneshot.py:260-263): the k largest |v|, ties to the smaller
-    position, in that order (the keys are distinct, so the sort is total)."""
-    mag = np.abs(val)
-    if pos.size > k:  # only the candidates at or above the k-th magnitude need sorting
-        cut = np.partition(mag, pos.size - k)[pos.size - k]
-        sel = np.flatnonzero(mag >= cut)
-        pos, val, mag = pos[sel], val[sel], mag[sel]
-    order = np.lexsort((pos, -mag))[:k]
-    return SparseSpectrum(n, dict(zip(pos[order].tolist(), val[order].tolist())))
+    position, in that order (the keys are distinct, so the sort is total).  The sort runs
+    in afft_truncate_host with the GIL released (worker threads overlap it); only the
+    dict is built here."""
+    pos = np.ascontiguousarray(pos, dtype=np.int64)
+    val = np.ascontiguousarray(val, dtype=np.complex128)
+    m = min(int(pos.size), int(k))
+    op = np.empty(max(m, 1), dtype=np.int64)
+    ov = np.empty(max(m, 1), dtype=np.complex128)
+    cnt = ctypes.c_int64(0)
+    _lib.check(_lib.load().afft_truncate_host(pos.ctypes.data, val.ctypes.data, int(pos.size),
+                                              int(k), op.ctypes.data, ov.ctypes.data,
+                                              ctypes.byref(cnt)), "truncate")
+    m = int(cnt.value)
+    return SparseSpectrum._trusted(n, dict(zip(op[:m].tolist(), ov[:m].tolist())))
 
 
 def dsfft_batch(xs, k: int, configs, streams: int = 8, lockstep: bool = False,

@@ -67,3 +67,32 @@ def test_no_cpu_fallback():
         bucketize(np.zeros(8, dtype=complex), 4, 0)
     with pytest.raises(NoCudaDevice):
         ffast(np.zeros(20, dtype=complex), 2, plan=None)
+
+
+def test_truncate_host_matches_numpy_order():
+    """afft_truncate_host (host only, no device) keeps truncate_spectrum's order
+    (oneshot.py:260-263): the k largest |v| (numpy's abs), ties to the smaller position —
+    checked against a numpy lexsort, with exact magnitude ties forced in."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2011_05749_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    for count, k in ((0, 4), (1, 1), (50, 10), (1000, 1000), (4600, 4096), (300, 400)):
+        pos = rng.permutation(1 << 20)[:count].astype(np.int64)
+        val = rng.normal(size=count) + 1j * rng.normal(size=count)
+        if count > 8:  # exact ties: equal magnitudes at different positions
+            val[1::7] = val[0]
+            val[2::9] = val[0].conjugate()
+        op = np.empty(max(1, min(count, k)), dtype=np.int64)
+        ov = np.empty(max(1, min(count, k)), dtype=np.complex128)
+        cnt = ctypes.c_int64(-1)
+        rc = _lib.load().afft_truncate_host(pos.ctypes.data, val.ctypes.data, count, k,
+                                            op.ctypes.data, ov.ctypes.data, ctypes.byref(cnt))
+        assert rc == 0
+        order = np.lexsort((pos, -np.abs(val)))[:k]
+        assert cnt.value == len(order)
+        assert op[: cnt.value].tolist() == pos[order].tolist()
+        assert np.array_equal(ov[: cnt.value], val[order])

@@ -101,15 +101,20 @@ def test_dsfft_goldens_active_fallback(golden_dsfft, monkeypatch):
 def _entries_lazy_and_full(case, monkeypatch, probe0=None):
     """The native loop's entries dict with probe classifies (no trace requested) and with
     every layer classified in full (trace requested)."""
-    from paper_2011_05749_b200 import DsfftConfig, _device
+    from paper_2011_05749_b200 import DsfftConfig, SampleLedger, _device
     from paper_2011_05749_b200.dsfft import _dsfft_arrays
 
     if probe0 is not None:
         monkeypatch.setenv("AFFT_DSFFT_PROBE0", str(probe0))
     xd = _device.as_device_signal(dsfft_signal(case))
     cfg = DsfftConfig(mode=case["mode"], seed=case["seed"], noise_std=case["noise_std"])
-    lazy = _dsfft_arrays(xd, case["k"], cfg)
-    full = _dsfft_arrays(xd, case["k"], cfg, trace=[])
+    small = case["n"] <= 1 << 20  # the host ledger replay of a 2^24 decode is slow
+    led_lazy = SampleLedger(case["n"]) if small else None
+    led_full = SampleLedger(case["n"]) if small else None
+    lazy = _dsfft_arrays(xd, case["k"], cfg, led_lazy)
+    full = _dsfft_arrays(xd, case["k"], cfg, led_full, trace=[])
+    if small:  # the ledger models the reference's reads: one classify per layer either way
+        assert (led_lazy.count, led_lazy.unique_count) == (led_full.count, led_full.unique_count)
     return lazy, full
 
 
