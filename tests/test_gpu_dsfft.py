@@ -159,3 +159,29 @@ def test_fused_spectrum_layers_change_nothing(golden_dsfft, monkeypatch):
         assert t1 == t0
         assert p1.tolist() == p0.tolist()
         assert np.array_equal(v1, v0)
+
+
+@pytest.mark.parametrize("n,k", [(1 << 16, 64), (1 << 16, 512), (1 << 24, 1024)])
+def test_fused_layers_other_shapes(monkeypatch, n, k):
+    """The fused epilogue at the other plan shapes it serves: n = 2^16 (two radix-256
+    passes) with the stop layer below the fused depths (tree levels from the depth-8
+    values) and above them (k = 512: depth 9, no shallower layer), and n = 2^24 with a
+    stop layer at depth 10.  Layer traces and entries bit-identical to the unfused path."""
+    from paper_2011_05749_b200 import DsfftConfig, _device, generate_test_case
+    from paper_2011_05749_b200.dsfft import _dsfft_arrays
+
+    snr = 20.0
+    x = generate_test_case(n, k, snr, seed=77).signal.astype(np.complex64)
+    xd = _device.as_device_signal(x)
+    cfg = DsfftConfig(mode="noisy", seed=3, noise_std=float(np.sqrt(k * 10 ** (-snr / 10))))
+    got = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("AFFT_DSFFT_FUSE", fuse)
+        tr = []
+        got[fuse] = (_dsfft_arrays(xd, k, cfg, trace=tr), tr)
+    (p1, v1), t1 = got["1"]
+    (p0, v0), t0 = got["0"]
+    assert t1 == t0
+    assert p1.tolist() == p0.tolist()
+    assert np.array_equal(v1, v0)
+    assert len(p1) > k // 2
