@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "afft_common.cuh"
 #include "dt_warp.cuh"
 #include "oneshot_core.cuh"
@@ -408,15 +410,30 @@ __global__ void __launch_bounds__(32, W == 32 ? 24 : 16) dt_estimate_warp_kernel
 
 // ------------------------------------------------------------------ truncate
 
+// truncate_spectrum's order by two stable block radix sorts of up to 8192 entries: by
+// position, then by magnitude descending (key ~bits(|v|): non-negative doubles order like
+// their bits), so equal magnitudes stay in position order — the (-|v|, f) key.
+constexpr int kTruncSortItems = 8;
+constexpr int kTruncSortMax = 1024 * kTruncSortItems;
+using TruncSortF = cub::BlockRadixSort<uint32_t, 1024, kTruncSortItems, int32_t>;
+using TruncSortM = cub::BlockRadixSort<uint64_t, 1024, kTruncSortItems, int32_t>;
+union TruncSortTemp {
+  typename TruncSortF::TempStorage f;
+  typename TruncSortM::TempStorage m;
+};
+
 // Compact the per-bucket entries of each signal (bucket order, block scan over the
 // per-row counts) and keep the k largest by (-|v|, f) with a bitonic sort — in
-// shared memory when it fits, else in a global scratch.  One CTA per signal.
+// shared memory when the signal's own entry count fits (smem_bytes), else in a global
+// scratch (sized for the worst case, nrows a_m).  One CTA per signal.  (Deciding on the
+// worst case sent config 4's ~8k entries per signal, 16 k possible, to a global-memory
+// sort: 0.2 ms per call.)
 __global__ void __launch_bounds__(1024) dt_truncate_kernel(
     int64_t nrows, int a_m, int k, const int64_t* __restrict__ pos,
     const double* __restrict__ val, const int32_t* __restrict__ cnt, int cap,
     int64_t* __restrict__ all_pos, double* __restrict__ all_val, int32_t* __restrict__ all_count,
     int64_t* __restrict__ out_pos, double* __restrict__ out_val, int32_t* __restrict__ out_count,
-    unsigned char* gscratch, size_t scratch_bytes) {
+    unsigned char* gscratch, size_t scratch_bytes, size_t smem_bytes) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int warp_sum[32];
   const int64_t s = blockIdx.x;
@@ -457,9 +474,40 @@ __global__ void __launch_bounds__(1024) dt_truncate_kernel(
   }
   if (tid == 0) all_count[s] = m;
   __syncthreads();
+  if (m <= kTruncSortMax) {  // radix sorts (the bitonic network below took 0.18 ms per call)
+    TruncSortTemp& ts = *reinterpret_cast<TruncSortTemp*>(smem_raw);
+    uint32_t kf[kTruncSortItems];
+    int32_t ix[kTruncSortItems];
+#pragma unroll
+    for (int j = 0; j < kTruncSortItems; ++j) {
+      const int i = tid * kTruncSortItems + j;
+      kf[j] = i < m ? (uint32_t)ap[i] : 0xffffffffu;  // positions < n < 2^32
+      ix[j] = i < m ? i : -1;
+    }
+    TruncSortF(ts.f).Sort(kf, ix);
+    __syncthreads();
+    uint64_t km[kTruncSortItems];
+#pragma unroll
+    for (int j = 0; j < kTruncSortItems; ++j)  // padding sorts last (stable after |v| = 0)
+      km[j] = ix[j] >= 0 ? ~(uint64_t)__double_as_longlong(la::cabs(av[ix[j]])) : ~0ull;
+    TruncSortM(ts.m).Sort(km, ix);
+    la::c2* ov = reinterpret_cast<la::c2*>(out_val) + s * k;
+    const int kept = m < k ? m : k;
+#pragma unroll
+    for (int j = 0; j < kTruncSortItems; ++j) {
+      const int r = tid * kTruncSortItems + j;
+      if (r < kept) {
+        out_pos[s * k + r] = ap[ix[j]];
+        ov[r] = av[ix[j]];
+      }
+    }
+    if (tid == 0) out_count[s] = kept;
+    return;
+  }
   int pow2 = 1;
   while (pow2 < m) pow2 <<= 1;
-  unsigned char* mem = gscratch ? gscratch + s * scratch_bytes : smem_raw;
+  unsigned char* mem =
+      (size_t)pow2 * 20 <= smem_bytes || !gscratch ? smem_raw : gscratch + s * scratch_bytes;
   double* key = reinterpret_cast<double*>(mem);
   int64_t* kpos = reinterpret_cast<int64_t*>(key + pow2);
   int32_t* kidx = reinterpret_cast<int32_t*>(kpos + pow2);
@@ -673,20 +721,21 @@ extern "C" int afft_dt_truncate(const int64_t* pos, const double* val, const int
   int64_t pow2 = 1;
   while (pow2 < std::max<int64_t>(cap, 1)) pow2 <<= 1;
   const size_t need = ((size_t)pow2 * 20 + 255) / 256 * 256;
-  size_t smem = need;
+  const size_t kSmemMax = 200 * 1024;
+  // signals whose entries fit sort here; at least the radix sorts' temporary storage
+  const size_t smem = std::max(std::min(need, kSmemMax), sizeof(TruncSortTemp));
+  static_assert(sizeof(TruncSortTemp) <= 200 * 1024, "radix sort storage");
   unsigned char* scratch = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
-  if (smem > 200 * 1024) {  // many buckets: bitonic sort in global memory
+  if (need > kSmemMax) {  // the worst case does not fit: a global scratch for those
     cudaError_t e = scratch_alloc(reinterpret_cast<void**>(&scratch), (size_t)batch * need, st);
     if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(dt_truncate scratch)");
-    smem = 0;
-  } else {
-    cudaError_t e = ensure_smem((const void*)dt_truncate_kernel, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(dt_truncate)");
   }
+  cudaError_t e = ensure_smem((const void*)dt_truncate_kernel, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(dt_truncate)");
   dt_truncate_kernel<<<(unsigned)batch, 1024, smem, st>>>(
       nrows, a_m, k, pos, val, cnt, (int)cap, all_pos, all_val, all_count, out_pos, out_val,
-      out_count, scratch, need);
+      out_count, scratch, need, smem);
   if (scratch) scratch_free(scratch, st);
   AFFT_CHECK_LAUNCH("dt_truncate_kernel");
   return AFFT_OK;
