@@ -155,19 +155,19 @@ inline int64_t host_pymod(int64_t a, int64_t n) {
 
 // The tree layers a K2' final radix-256 pass can decide in its epilogue (bucketize.cu
 // gfft_flags_kernel): the last pass of the n-point spectrum holds, per tile, the alias
-// classes Y[j + q n/256] (q < 256) of 8 consecutive j, i.e. every bucket of the depths
-// dtop = log2(n) - 8 .. log2(n) that lies over those j (values in the tree order of
-// dsfft.cu tree_sum).  Depth dtop + t's bitmap at
-// words + word_off[t] (bytes written whole: a tile owns 8 consecutive bits), flagged for
-// t >= t_lo; the depth-dtop values to vtop (b = n/256 entries) when non-null; sum |Y|^2
-// added into *norm2 when non-null.
+// classes Y[j + q n/256] (q < 256) of 8 consecutive j, and one thread holds q = qb + 16 qa
+// (qa < 16), i.e. every alias of the buckets of depths dtop + 4 .. dtop + 8 over its j
+// (dtop = log2(n) - 8; values in the tree order of dsfft.cu tree_sum).  Depth dtop + t's
+// bitmap at words + word_off[t] (bytes written whole: a tile owns 8 consecutive bits),
+// flagged for t_lo <= t (t >= 4); the depth-(dtop + 4) values to vmid (16 n/256 entries)
+// when non-null, for the shallower layers' tree; sum |Y|^2 added into *norm2 when non-null.
 struct DeepFuse {
   uint32_t* words;
   int64_t word_off[9];
   double thr[9];
   double t2hi[9], t2lo[9];  // thr^2 (1 +- 1e-14): the |v|^2 guard band
   int t_lo;
-  cd* vtop;
+  cd* vmid;
   double* norm2;
 };
 // bucketize.cu: Y = fft(x)/n (x one signal, n a power of two planned as three radix-256
@@ -180,5 +180,6 @@ int spectrum_fused(const void* x, int dtype, int64_t n, double* Y, const DeepFus
 int full_active_all_fused(const void* x, int dtype, int64_t n, double* Y, int d0, int nl,
                           const double* thr, int64_t* out, int cap, int32_t* counts,
                           double* norm2, void* scratch, size_t scratch_bytes, cudaStream_t st);
+size_t full_active_fused_scratch(int64_t n, int d0, int nl);
 
 }  // namespace afft

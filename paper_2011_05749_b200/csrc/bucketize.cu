@@ -330,23 +330,25 @@ constexpr int kGfftThreads = 128;
 // tile, thread (jj = tid & 7, qb = tid >> 3) holding y[qa] = Y[j + (qb + 16 qa) N_s]).
 // Depth dtop + t (dtop = log2 n - 8) has 2^t buckets r over each j, with values in the
 // tree order of dsfft.cu tree_sum: v_8(r) = Y[j + r N_s], v_t(r) = v_{t+1}(r) +
-// v_{t+1}(r + 2^t).  t >= 4: r = qb + 16 m, and r + 2^t is the same thread's m + 2^(t-4)
-// (in registers, in place); t = 3: the partner is thread qb + 8 (one value through
-// shared memory); t < 3: within warp 0.  The same sums as deep_flags_kernel and
-// tree_level_kernel, so every decision is bit-identical to the unfused path.  A tile owns
-// 8 consecutive bits (j0 % 8 == 0) of every bitmap: whole bytes, no atomics; a warp's
+// v_{t+1}(r + 2^t).  For t >= 4, r = qb + 16 m and r + 2^t is the same thread's
+// m + 2^(t-4): every level from 8 down to 4 is computed in registers, in place, with no
+// shared memory and no barrier (the levels below, whose children sit in other threads,
+// come from the depth-(dtop + 4) values by tree_level_kernel, which adds in the same
+// order).  Every decision is bit-identical to deep_flags_kernel's.  A tile owns 8
+// consecutive bits (j0 % 8 == 0) of every bitmap: whole bytes, no atomics; a warp's
 // ballot holds 4 of them (lanes jj + 8 (qb & 3)).
-__device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], cd* V, int tid, int64_t j0,
-                                                   int dtop, const DeepFuse& f) {
+__device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], int tid, int64_t j0, int dtop,
+                                                   const DeepFuse& f) {
   const int jj = tid & 7, qb = tid >> 3, lane = tid & 31;
   uint8_t* wb = reinterpret_cast<uint8_t*>(f.words);
   const int64_t byte0 = j0 >> 3, rstride = int64_t(1) << (dtop - 3);
-  // |v| > thr_t: |v|^2 against the guard band, hypot only inside it (deep_flags_kernel)
-  auto put = [&](int t, int r, cd v, bool on) {
-    const double sq = v.re * v.re + v.im * v.im;
+  // |v| > thr_t: |v|^2 against the guard band, hypot only inside it (deep_flags_kernel;
+  // |v|^2 within an ulp either way, the band is 1e-14 wide)
+  auto put = [&](int t, int r, cd v) {
+    const double sq = __fma_rn(v.re, v.re, v.im * v.im);
     const bool flag = sq > f.t2hi[t] ? true : sq < f.t2lo[t] ? false : cabs_(v) > f.thr[t];
-    const unsigned bal = __ballot_sync(0xffffffffu, on && flag);
-    if (on && (lane & 7) == 0)
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if ((lane & 7) == 0)
       wb[f.word_off[t] * 4 + byte0 + (int64_t)r * rstride] = (uint8_t)(bal >> (lane & 24));
   };
   auto level = [&](auto tc) {  // compile-time M (a runtime bound left y[] in local memory)
@@ -357,7 +359,7 @@ __device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], cd* V, int tid, 
     }
     if (t >= f.t_lo) {  // warp-uniform: shallower layers may not be asked for
 #pragma unroll
-      for (int m = 0; m < M; ++m) put(t, qb + 16 * m, y[m], true);
+      for (int m = 0; m < M; ++m) put(t, qb + 16 * m, y[m]);
     }
   };
   level(std::integral_constant<int, 8>{});
@@ -365,36 +367,8 @@ __device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], cd* V, int tid, 
   level(std::integral_constant<int, 6>{});
   level(std::integral_constant<int, 5>{});
   level(std::integral_constant<int, 4>{});
-  // V: [0, 128) v_4 by (jj, qb); then v_3 [64], v_2 [32], v_1 [16], v_0 [8]
-  __syncthreads();  // the previous tile's reads of V are done
-  V[jj * 16 + qb] = y[0];
-  __syncthreads();
-  if (tid < 64) {  // t = 3: 64 buckets, whole warps 0 and 1
-    const int r = tid >> 3;
-    const cd v = cadd(V[jj * 16 + r], V[jj * 16 + r + 8]);
-    V[128 + jj * 8 + r] = v;
-    if (3 >= f.t_lo) put(3, r, v, true);
-  }
-  __syncthreads();
-  if (tid < 32) {
-    const cd* vin = V + 128;
-    cd* vout = V + 192;
-#pragma unroll
-    for (int t = 2; t >= 0; --t) {
-      const int items = 8 << t, r = tid >> 3;
-      const bool on = tid < items;
-      cd v = cd{0.0, 0.0};
-      if (on) {
-        v = cadd(vin[jj * (2 << t) + r], vin[jj * (2 << t) + r + (1 << t)]);
-        vout[jj * (1 << t) + r] = v;
-      }
-      __syncwarp();
-      if (t >= f.t_lo) put(t, r, v, on);
-      if (t == 0 && f.vtop && on) f.vtop[j0 + jj] = v;
-      vin = vout;
-      vout += items;
-    }
-  }
+  // depth dtop + 4, bucket i = j + qb N_s: 8 consecutive j per qb, 128-byte runs
+  if (f.vmid) f.vmid[j0 + jj + ((int64_t)qb << dtop)] = y[0];
 }
 
 template <int LA, int LB, bool FUSE>
@@ -551,8 +525,10 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
       }
       if constexpr (FUSE) {
         static_assert(A == 16 && B == 16 && IB == 1, "fused epilogue: the radix-256 last pass");
-        // dtop = log2(N_s): N_s = n / 256 on the last pass
-        deep_fuse_epilogue(a, U + kCnt * LD, tid, j0, 63 - __clzll((unsigned long long)p.Ns), f);
+        // dtop = log2(N_s): N_s = n / 256 on the last pass.  (Deferring it behind the next
+        // tile's loads, to keep them in flight through it, spilled at 3 CTAs per SM and
+        // ran at 2: 223 / 258 against 186 us.)
+        deep_fuse_epilogue(a, tid, j0, 63 - __clzll((unsigned long long)p.Ns), f);
       }
     }
   }
@@ -1025,7 +1001,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     if (fuse && s == P - 1) {  // last pass with the DeepFuse epilogue
       kfn = (const void*)gfft_flags_kernel;
       g.perm = 0;
-      smem = (size_t)(R + (int64_t)g.cnt * (R + 1) + 256) * 16;  // + V (248 values)
+      smem = (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
       threads = kGfftThreads;
     } else if (lgr >= 4 && !fft_smem_path() && contiguous && (tma_env || tmap_env())) {
       kfn = gfft_tma_fn(lgr);

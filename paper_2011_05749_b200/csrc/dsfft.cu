@@ -921,16 +921,35 @@ int full_active_all(const double* spectrum, int64_t n, int d0, int nl, const dou
 }
 
 // full_active_all with the spectrum computed here: the last K2' pass decides every layer
-// at depths >= dtop = log2(n) - 8 in its epilogue (bucketize.cu deep_fuse_epilogue, the
-// tree_sum order, so the bitmaps are bit-identical to deep_flags_kernel's and
-// tree_level_kernel's) and leaves the depth-dtop values for the shallower layers; sum |Y|^2
-// into *norm2 (device, zeroed here).  Saves the deep_flags pass over Y (n 16 bytes).
+// at depths dtop + 4 .. log2(n) (dtop = log2(n) - 8) in its epilogue (bucketize.cu
+// deep_fuse_epilogue, the tree_sum order, so the bitmaps are bit-identical to
+// deep_flags_kernel's) and leaves the depth-(dtop + 4) values; tree_level_kernel makes
+// the shallower layers from them; sum |Y|^2 into *norm2 (device, zeroed here).  Saves
+// the deep_flags pass over Y (n 16 bytes) and the |x|^2 pass.
+// Scratch: bitmaps | count chunks | values of depths dmid = dtop + 4, dmid - 1, ..., d0.
+static void fused_layout(int64_t n, int d0, int nl, DeepLayers* D, size_t* wb, size_t* cb,
+                         int* dmid, size_t* vb) {
+  int jd = 0, log2n = 0;
+  size_t vdummy = 0;
+  full_layers_layout(n, d0, nl, D, &jd, wb, cb, &vdummy);
+  while ((int64_t(1) << log2n) < n) ++log2n;
+  *dmid = log2n - 4;
+  *vb = 0;
+  if (d0 < *dmid)
+    for (int d = d0; d <= *dmid; ++d) *vb += (size_t)16 << d;
+}
+
+size_t full_active_fused_scratch(int64_t n, int d0, int nl) {
+  DeepLayers D;
+  size_t wb = 0, cb = 0, vb = 0;
+  int dmid = 0;
+  fused_layout(n, d0, nl, &D, &wb, &cb, &dmid, &vb);
+  return wb + cb + vb;
+}
+
 int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int d0, int nl,
                           const double* thr, int64_t* out, int cap, int32_t* counts,
                           double* norm2, void* scratch, size_t scratch_bytes, cudaStream_t st) {
-  DeepLayers D;
-  int jd = 0;
-  size_t wb = 0, cb = 0, vb = 0;
   int log2n = 0;
   while ((int64_t(1) << log2n) < n) ++log2n;
   const int dtop = log2n - 8;
@@ -940,7 +959,10 @@ int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int
               d0, nl);
     return AFFT_EUNSUPPORTED;
   }
-  full_layers_layout(n, d0, nl, &D, &jd, &wb, &cb, &vb);
+  DeepLayers D;
+  size_t wb = 0, cb = 0, vb = 0;
+  int dmid = 0;
+  fused_layout(n, d0, nl, &D, &wb, &cb, &dmid, &vb);
   for (int j = 0; j < nl; ++j) set_layer_threshold(&D, j, thr[j]);
   if (!scratch || scratch_bytes < wb + cb + vb) {
     set_error("full_active_all_fused: scratch of %zu bytes needed", wb + cb + vb);
@@ -948,14 +970,20 @@ int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int
   }
   uint32_t* words = reinterpret_cast<uint32_t*>(scratch);
   int32_t* chunk = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch) + wb);
-  cd* vbuf = jd > 0 ? reinterpret_cast<cd*>(reinterpret_cast<char*>(scratch) + wb + cb) : nullptr;
-  int64_t vofs[kDeepMaxLayers + 1] = {0};
-  for (int j = 0; j < jd; ++j) vofs[j + 1] = vofs[j] + (int64_t(1) << (d0 + j));
-  // layer j = depth d0 + j; fused depths dtop + t, t = 0..8
+  // values of depth d (d0 <= d <= dmid) at vals[d]
+  cd* vals[64] = {nullptr};
+  if (vb) {
+    char* v = reinterpret_cast<char*>(scratch) + wb + cb;
+    for (int d = dmid; d >= d0; --d) {
+      vals[d] = reinterpret_cast<cd*>(v);
+      v += (size_t)16 << d;
+    }
+  }
+  // layer j = depth d0 + j; fused depths dtop + t, t = 4..8
   DeepFuse f;
   memset(&f, 0, sizeof(f));
   f.words = words;
-  f.t_lo = std::max(0, d0 - dtop);
+  f.t_lo = std::max(4, d0 - dtop);
   for (int t = 0; t <= 8; ++t) {
     const int j = dtop + t - d0;
     f.word_off[t] = j >= 0 ? D.word_off[j] : 0;
@@ -963,8 +991,7 @@ int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int
     f.t2hi[t] = j >= 0 ? D.t2hi[j] : 0.0;
     f.t2lo[t] = j >= 0 ? D.t2lo[j] : 0.0;
   }
-  const int jtop = dtop - d0;  // layer index of depth dtop (values needed below it)
-  f.vtop = jtop > 0 ? vbuf + vofs[jtop] : nullptr;
+  f.vmid = d0 < dmid ? vals[dmid] : nullptr;
   f.norm2 = norm2;
   if (norm2) {
     const cudaError_t e = cudaMemsetAsync(norm2, 0, 8, st);
@@ -972,10 +999,10 @@ int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int
   }
   int rc = spectrum_fused(x, dtype, n, Yout, f, st);
   if (rc) return rc;
-  for (int j = jtop - 1; j >= 0; --j) {
-    const int64_t b = int64_t(1) << (d0 + j);
+  for (int d = dmid - 1; d >= d0; --d) {  // v_d[i] = v_{d+1}[i] + v_{d+1}[i + 2^d]
+    const int64_t b = int64_t(1) << d;
     tree_level_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
-        vbuf + vofs[j + 1], b, thr[j], vbuf + vofs[j], words + D.word_off[j]);
+        vals[d + 1], b, thr[d - d0], vals[d], words + D.word_off[d - d0]);
   }
   AFFT_CHECK_LAUNCH("tree_level_kernel");
   const unsigned chunks = (unsigned)D.chunk_off[nl];

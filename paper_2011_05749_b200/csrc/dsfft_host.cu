@@ -541,7 +541,8 @@ struct Dsfft {
     RC(deep_lists.alloc((size_t)nl * cap * 8, st, "dsfft layer lists"));
     const size_t onorm = ((size_t)nl * 4 + 7) & ~size_t(7);  // counts | sum |Y|^2
     RC(counts.alloc(onorm + 8, st, "dsfft layer counts"));
-    const size_t sb = full_active_scratch(n, depth, nl);
+    const size_t sb = std::max(full_active_scratch(n, depth, nl),
+                                 full_active_fused_scratch(n, depth, nl));
     RC(scratch.alloc(sb, st, "dsfft layer scratch"));
     // the spectrum's last pass deciding the deepest nine layers in its epilogue
     // (AFFT_DSFFT_FUSE=0: spectrum, then one pass over it)
@@ -1023,7 +1024,8 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
   int32_t* counts = blk.as<int32_t>();
   double* norms = reinterpret_cast<double*>(blk.as<char>() + onorm);
   double* parts = reinterpret_cast<double*>(blk.as<char>() + opart);
-  const size_t sb = full_active_scratch(n, d0, nl);
+  const size_t sb = std::max(full_active_scratch(n, d0, nl),
+                             full_active_fused_scratch(n, d0, nl));
   RC(scratch.alloc(sb, st, "dsfft batch layer scratch"));
   const char* fe = std::getenv("AFFT_DSFFT_FUSE");
   bool fused = !(fe && fe[0] == '0');
