@@ -342,24 +342,34 @@ __device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], int tid, int64_t
   const int jj = tid & 7, qb = tid >> 3, lane = tid & 31;
   uint8_t* wb = reinterpret_cast<uint8_t*>(f.words);
   const int64_t byte0 = j0 >> 3, rstride = int64_t(1) << (dtop - 3);
-  // |v| > thr_t: |v|^2 against the guard band, hypot only inside it (deep_flags_kernel;
-  // |v|^2 within an ulp either way, the band is 1e-14 wide)
-  auto put = [&](int t, int r, cd v) {
-    const double sq = __fma_rn(v.re, v.re, v.im * v.im);
-    const bool flag = sq > f.t2hi[t] ? true : sq < f.t2lo[t] ? false : cabs_(v) > f.thr[t];
-    const unsigned bal = __ballot_sync(0xffffffffu, flag);
-    if ((lane & 7) == 0)
-      wb[f.word_off[t] * 4 + byte0 + (int64_t)r * rstride] = (uint8_t)(bal >> (lane & 24));
-  };
   auto level = [&](auto tc) {  // compile-time M (a runtime bound left y[] in local memory)
     constexpr int t = decltype(tc)::value, M = 1 << (t - 4);
     if (t < 8) {
 #pragma unroll
       for (int m = 0; m < M; ++m) y[m] = cadd(y[m], y[m + M]);
     }
-    if (t >= f.t_lo) {  // warp-uniform: shallower layers may not be asked for
+    if (t < f.t_lo) return;  // warp-uniform: shallower layers may not be asked for
+    // |v| > thr_t: |v|^2 against the guard band (within an ulp either way; the band is
+    // 1e-14 wide), hypot only inside it (deep_flags_kernel) — those rare values after
+    // the cheap tests of the whole level, behind one warp-uniform branch
+    bool fl[M];
+    unsigned unsure = 0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) put(t, qb + 16 * m, y[m]);
+    for (int m = 0; m < M; ++m) {
+      const double sq = __fma_rn(y[m].re, y[m].re, y[m].im * y[m].im);
+      fl[m] = sq > f.t2hi[t];
+      if (!fl[m] && !(sq < f.t2lo[t])) unsure |= 1u << m;
+    }
+    if (__any_sync(0xffffffffu, unsure != 0)) {
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        if ((unsure >> m) & 1u) fl[m] = cabs_(y[m]) > f.thr[t];
+    }
+    uint8_t* row = wb + f.word_off[t] * 4 + byte0 + (int64_t)qb * rstride;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {  // bucket r = qb + 16 m
+      const unsigned bal = __ballot_sync(0xffffffffu, fl[m]);
+      if ((lane & 7) == 0) row[(int64_t)(16 * m) * rstride] = (uint8_t)(bal >> (lane & 24));
     }
   };
   level(std::integral_constant<int, 8>{});
