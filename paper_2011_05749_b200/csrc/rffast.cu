@@ -174,14 +174,37 @@ __device__ __forceinline__ double search_bound(int64_t n, int64_t b, int64_t L, 
                                                const double* s_est, int c, double inv) {
   using rt = typename std::conditional<k32, uint32_t, int64_t>::type;
   const double dn = (double)n;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  auto cand_of = [&](double f) {  // the residue-class candidate nearest frequency f
+    int64_t th = (int64_t)floor((f - (double)idx) / (double)b + 0.5);
+    th %= L;
+    if (th < 0) th += L;
+    return th;
+  };
   const double fe = (-s_est[0] * dn) / kTwoPi;
-  double dd = (fe - (double)idx) / (double)b;
-  int64_t th = (int64_t)floor(dd + 0.5);
-  th %= L;
-  if (th < 0) th += L;
-  double bound = cand_score<k32>((rt)(idx + b * th), (rt)n, s_est, c, dn, inv,
-                                 __longlong_as_double(0x7ff0000000000000LL));
-  if (!(bound == bound)) bound = __longlong_as_double(0x7ff0000000000000LL);  // NaN: no pruning
+  const int64_t th0 = cand_of(fe);
+  double bound = cand_score<k32>((rt)(idx + b * th0), (rt)n, s_est, c, dn, inv, inf);
+  if (!(bound == bound)) return inf;  // NaN: no pruning
+  // Successive refinement (any real candidate's score is a valid bound; a better one
+  // prunes more and narrows the stride-0 arc): stride 2^j's estimate fixes 2^j f / n
+  // modulo 1, so of the 2^j frequencies it allows keep the one nearest the running
+  // estimate, while 2^j < 8 L (finer than the candidate grid after that).
+  double f = fe - floor(fe / dn) * dn;
+  for (int j = 1; j < c && (int64_t(1) << j) < 8 * L; ++j) {
+    const double sc = ldexp(1.0, j);
+    const double x = f * sc / dn;
+    double g = -s_est[j] * (1.0 / kTwoPi);
+    g -= floor(g);
+    double d = g - (x - floor(x));
+    d -= floor(d + 0.5);  // wrap into [-1/2, 1/2)
+    f += d * dn / sc;
+    f -= floor(f / dn) * dn;
+  }
+  const int64_t th = cand_of(f);
+  if (th != th0) {
+    const double s1 = cand_score<k32>((rt)(idx + b * th), (rt)n, s_est, c, dn, inv, bound);
+    if (s1 < bound) bound = s1;
+  }
   return bound;
 }
 
@@ -282,12 +305,54 @@ __device__ __forceinline__ bool approx_pruned(uint64_t G, const uint32_t* E, int
   return sum > lim;
 }
 
+// The candidates t of [t0, t1) that can still score <= B: the stride-0 term alone is
+// d0(t) = wrap(est_0 + 2 pi (idx + b t) / n), linear in t with slope 2 pi / L (idx + b t
+// < n), so score(t) <= B needs |d0(t)| <= sqrt(B): a circular arc of half-width
+// sqrt(B) L / (2 pi) around the seed's candidate.  Candidates outside it (with two
+// candidates and 1e-9 relative of margin, far above the rounding of est_0 / (2 pi),
+// idx / n and the device's d0) score > B, so skipping them changes neither the minimum
+// nor its smallest t.  Up to two ranges [r[0], r[1]) and [r[2], r[3]) (the arc may wrap);
+// the whole chunk when B gives no restriction.
+struct CandRanges {
+  int64_t r[4];
+  __device__ int64_t len() const { return (r[1] - r[0]) + (r[3] - r[2]); }
+  __device__ int64_t at(int64_t v) const { return v < r[1] - r[0] ? r[0] + v : r[2] + (v - (r[1] - r[0])); }
+};
+__device__ __forceinline__ CandRanges stride0_ranges(double est0, int64_t idx, int64_t n,
+                                                     int64_t L, double B, int64_t t0,
+                                                     int64_t t1) {
+  CandRanges c{{t0, t1, 0, 0}};
+  if (!(B < 9.0) || !(est0 == est0) || isinf(est0)) return c;  // NaN / no restriction
+  const double w = sqrt(B) * (1.0 / kTwoPi) * (1.0 + 1e-9) + 1e-12;  // turns
+  double u = -(est0 * (1.0 / kTwoPi) + (double)idx / (double)n);
+  u -= floor(u);
+  const double ct = u * (double)L, hw = w * (double)L + 2.0;
+  if (!(2.0 * hw + 2.0 < (double)L)) return c;
+  const int64_t lo = (int64_t)floor(ct - hw), hi = (int64_t)ceil(ct + hw) + 1;  // [lo, hi)
+  // the arc as up to two pieces of [0, L), each intersected with [t0, t1)
+  int64_t p[4];
+  if (lo < 0) {
+    p[0] = lo + L; p[1] = L; p[2] = 0; p[3] = hi;
+  } else if (hi > L) {
+    p[0] = lo; p[1] = L; p[2] = 0; p[3] = hi - L;
+  } else {
+    p[0] = lo; p[1] = hi; p[2] = 0; p[3] = 0;
+  }
+  for (int q = 0; q < 4; q += 2) {
+    const int64_t a = max(p[q], t0), e = min(p[q + 1], t1);
+    c.r[q] = a;
+    c.r[q + 1] = e > a ? e : a;
+  }
+  return c;
+}
+
 // Shared state of one CTA's chunk scan.
 struct ScanSmem {
   double est[kMaxStrides];
   uint32_t e32[kMaxStrides];
   int nan;
   unsigned long long bound;
+  CandRanges rng;  // the chunk's candidates left by the stride-0 arc (one copy per CTA)
   double w_score[kSearchThreads / 32];
   int32_t w_t[kSearchThreads / 32];
 };
@@ -319,6 +384,11 @@ __device__ __forceinline__ void scan_chunk(ScanSmem& sm, int64_t n, int c, int a
     u -= floor(u);
     sm.e32[threadIdx.x] = (uint32_t)(uint64_t)(u * 4294967296.0);
     if (!(e == e) || isinf(e)) sm.nan = 1;
+    // one CTA-wide copy of the candidate ranges, from the bound as loaded above (threads
+    // that computed their own could see different bounds and leave gaps between them)
+    if (threadIdx.x == 0)
+      sm.rng = stride0_ranges(e, act_index[a], n, L, bound_of_bits(sm.bound), t0,
+                              min(L, t0 + (int64_t)kChunk));
   }
   __syncthreads();
   const int64_t idx = act_index[a];
@@ -331,7 +401,6 @@ __device__ __forceinline__ void scan_chunk(ScanSmem& sm, int64_t n, int c, int a
   if (t0 < L) {
     unsigned long long* gb = node_bound + a;
     double bound = bound_of_bits(sm.bound);  // seeded by noisy_seed_kernel
-    const int64_t t1 = min(L, t0 + (int64_t)kChunk);
     // Two levels: the CTA's own bound in shared memory, read before every candidate,
     // and the node's global bound, folded into it every 4 candidates from a load
     // issued 4 candidates earlier (a global load waited on before every candidate was
@@ -340,7 +409,10 @@ __device__ __forceinline__ void scan_chunk(ScanSmem& sm, int64_t n, int c, int a
     volatile unsigned long long* vs_bound = &sm.bound;
     unsigned long long pending = load_bound_bits(gb);
     int k = 0;
-    for (int64_t t = t0 + threadIdx.x; t < t1; t += kSearchThreads, ++k) {
+    // only the candidates the stride-0 term leaves possible under the chunk's bound
+    const int64_t nv = sm.rng.len();
+    for (int64_t v = threadIdx.x; v < nv; v += kSearchThreads, ++k) {
+      const int64_t t = sm.rng.at(v);
       if ((k & 3) == 3) {
         atomicMin(&sm.bound, pending);
         pending = load_bound_bits(gb);
@@ -503,12 +575,16 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
   int32_t bt = INT32_MAX;
   double bound = single ? __longlong_as_double(0x7ff0000000000000LL)
                         : search_bound<k32>(n, b, L, idx, s_est, c, inv);
+  // only the candidates the stride-0 term leaves possible under the seed bound
+  const CandRanges cr = stride0_ranges(s_est[0], idx, n, L, bound, 0, L);
+  const int64_t nv = cr.len();
   // the warp shares its pruning bound after every 32 candidates (see shared_bound)
-  for (int64_t tb = 0; tb < L; tb += 32) {
-    const int64_t t = tb + lane;
+  for (int64_t vb = 0; vb < nv; vb += 32) {
+    const bool in = vb + lane < nv;
+    const int64_t t = in ? cr.at(vb + lane) : L;
     uint32_t lim = 0;
     if (ap.on) lim = approx_limit(bound, ap.margin);
-    if (t < L && !(lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, s_e32, c, lim))) {
+    if (in && !(lim && approx_pruned(ap.A0 + (uint64_t)t * ap.S, s_e32, c, lim))) {
       const double sc = cand_score<k32>((rt)(idx + b * t), (rt)n, s_est, c, dn, inv, bound);
       if (sc <= bound) {
         if (sc < best) {
