@@ -835,12 +835,17 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
     const double* __restrict__ node_val, int32_t* __restrict__ done, int64_t* __restrict__ rec_pos,
     double* __restrict__ rec_val, int rec_cap, int32_t* __restrict__ rec_count,
     int32_t* __restrict__ rounds, int32_t* __restrict__ total_found, char* gscratch,
-    size_t scratch_bytes) {
+    size_t scratch_bytes, int32_t* __restrict__ nf_round = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int warp_tmp[32];
   __shared__ int carry;
   const int64_t s = blockIdx.x;
-  if (done[s]) return;
+  // nf_round (global harvest state only): the subtraction is left to
+  // noisy_subtract_kernel, which reads this round's tone count per signal
+  if (done[s]) {
+    if (nf_round && threadIdx.x == 0) nf_round[s] = 0;
+    return;
+  }
   const int N = P.nodes;
   const int tid = threadIdx.x, nt = blockDim.x;
   unsigned char* mem = gscratch ? reinterpret_cast<unsigned char*>(gscratch) + s * scratch_bytes
@@ -881,6 +886,7 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
   }
   __syncthreads();
   const int nf = block_exclusive_scan(flag, N, warp_tmp, &carry);
+  if (tid == 0 && nf_round) nf_round[s] = nf;
   if (nf == 0) {
     if (tid == 0) done[s] = 1;
     return;
@@ -911,8 +917,11 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
   }
   __syncthreads();
   // subtract: one warp per hit node, lanes over the R measurements, tones in found order
+  // (here for graphs whose harvest state fits in shared memory; else one warp per node
+  // across the whole grid in noisy_subtract_kernel — one CTA per signal left C3′'s
+  // 23.5 k-node subtraction on 16 SMs)
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  for (int g = wid; g < N; g += nw) {
+  for (int g = wid; g < N && !nf_round; g += nw) {
     const int lo = g ? flag[g - 1] : 0, hi = flag[g];
     if (lo == hi) continue;
     if (lane == 0) {  // insertion sort of the (short) segment restores found order
@@ -948,6 +957,55 @@ __global__ void __launch_bounds__(1024) noisy_harvest_kernel(
     rec_count[s] = rc + nf;
     atomicAdd(total_found, nf);
   }
+}
+
+// noisy_harvest_kernel's subtraction for global harvest state: grid (node blocks, signal),
+// one warp per node, the same per-node tone lists (flag = segment ends after the
+// scatter, found_res, found_g in the signal's scratch block) and the same arithmetic in
+// the same order.
+__global__ void __launch_bounds__(256) noisy_subtract_kernel(
+    const __grid_constant__ NoisyPlan P, double* __restrict__ residual,
+    int8_t* __restrict__ dirty, const int64_t* __restrict__ node_f0,
+    const double* __restrict__ node_val, const int32_t* __restrict__ nf_round, char* gscratch,
+    size_t scratch_bytes) {
+  const int64_t s = blockIdx.y;
+  if (nf_round[s] == 0) return;
+  const int N = P.nodes;
+  const int lane = threadIdx.x & 31;
+  const int g = (int)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (g >= N) return;
+  unsigned char* mem = reinterpret_cast<unsigned char*>(gscratch) + s * scratch_bytes;
+  unsigned* hash = reinterpret_cast<unsigned*>(mem);
+  const int* flag = reinterpret_cast<const int*>(hash + P.hmask + 1);
+  const int32_t* found_g = flag + N;
+  int32_t* found_res = const_cast<int32_t*>(found_g) + N;
+  const int lo = g ? flag[g - 1] : 0, hi = flag[g];
+  if (lo == hi) return;
+  const int64_t so = s * N;
+  if (lane == 0) {  // insertion sort of the (short) segment restores found order
+    for (int a2 = lo + 1; a2 < hi; ++a2) {
+      const int v = found_res[a2];
+      int b2 = a2 - 1;
+      while (b2 >= lo && found_res[b2] > v) {
+        found_res[b2 + 1] = found_res[b2];
+        --b2;
+      }
+      found_res[b2 + 1] = v;
+    }
+  }
+  __syncwarp();
+  cd* y = reinterpret_cast<cd*>(residual) + (so + g) * P.R;
+  for (int r = lane; r < P.R; r += 32) {
+    cd acc = y[r];
+    for (int a2 = lo; a2 < hi; ++a2) {
+      const int i = found_res[a2];
+      const int64_t f = node_f0[so + found_g[i]];
+      const cd v = reinterpret_cast<const cd*>(node_val)[so + found_g[i]];
+      acc = csub(acc, cmul(v, unit_root(plan_mulmod(P, plan_tau(P, s, r), f), P.n)));
+    }
+    y[r] = acc;
+  }
+  if (lane == 0) dirty[so + g] = 1;
 }
 
 __global__ void count_multi_kernel(int64_t batch, int N, const int8_t* __restrict__ state,
@@ -1387,6 +1445,23 @@ static int device_sms() {
   return v;
 }
 
+// Harvest, then (global harvest state) the grid-wide subtraction; nf_round sits right
+// after the batch's harvest blocks.
+static void launch_harvest(const NoisyPlan& P, int64_t batch, double* residual, int8_t* state,
+                           int8_t* dirty, int64_t* node_f0, double* node_val, int32_t* done,
+                           int64_t* rec_pos, double* rec_val, int32_t rec_cap, int32_t* rec_count,
+                           int32_t* rounds, int32_t* found, char* hscratch, size_t hbytes,
+                           size_t hsmem, cudaStream_t st) {
+  int32_t* nf_round =
+      hscratch ? reinterpret_cast<int32_t*>(hscratch + (size_t)batch * hbytes) : nullptr;
+  noisy_harvest_kernel<<<(unsigned)batch, 1024, hsmem, st>>>(
+      P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap, rec_count,
+      rounds, found, hscratch, hbytes, nf_round);
+  if (nf_round)
+    noisy_subtract_kernel<<<dim3((unsigned)((P.nodes + 7) / 8), (unsigned)batch), 256, 0, st>>>(
+        P, residual, dirty, node_f0, node_val, nf_round, hscratch, hbytes);
+}
+
 // Enqueue one round's kernels on the capturing stream `cs`.
 static int enqueue_round(const NoisyPlan& P, const NoisyWs& w, char* ws, int64_t batch,
                          double* residual, int8_t* state, int8_t* dirty, int32_t* done,
@@ -1436,9 +1511,8 @@ static int enqueue_round(const NoisyPlan& P, const NoisyWs& w, char* ws, int64_t
   noisy_apply_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, cs>>>(
       0, P, act_row, f0s, vals, res, t1, state, dirty, node_f0, node_val, A_dev);
   AFFT_CHECK_LAUNCH("noisy_apply_kernel");
-  noisy_harvest_kernel<<<(unsigned)batch, 1024, hsmem, cs>>>(
-      P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap, rec_count,
-      rounds, counters + 1, hscratch, hbytes);
+  launch_harvest(P, batch, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val,
+                 rec_cap, rec_count, rounds, counters + 1, hscratch, hbytes, hsmem, cs);
   AFFT_CHECK_LAUNCH("noisy_harvest_kernel");
   noisy_round_control_kernel<<<1, 1, 0, cs>>>(handle, counters, max_rounds);
   AFFT_CHECK_LAUNCH("noisy_round_control_kernel");
@@ -1741,8 +1815,8 @@ static int peel_noisy_core(NoisyPlan* P, int64_t batch, double* residual, int8_t
       ((size_t)hcap * 4 + (size_t)N * 4 * 2 + (size_t)N * P->ncycles * 4 + N + 64 + 15) & ~size_t(15);
   size_t hsmem = hbytes;
   char* hscratch = nullptr;
-  if (hbytes > 200 * 1024) {  // large graphs: harvest state in global memory
-    e = scratch_alloc(reinterpret_cast<void**>(&hscratch), (size_t)batch * hbytes, st);
+  if (hbytes > 200 * 1024) {  // large graphs: harvest state in global memory (+ nf_round)
+    e = scratch_alloc(reinterpret_cast<void**>(&hscratch), (size_t)batch * (hbytes + 4), st);
     if (e != cudaSuccess) {
       return cuda_status(e, "scratch_alloc(noisy harvest scratch)");
     }
@@ -1793,9 +1867,9 @@ static int peel_noisy_core(NoisyPlan* P, int64_t batch, double* residual, int8_t
           reinterpret_cast<const double*>(ws + w.res), t1, state, dirty, node_f0, node_val);
       AFFT_CHECK_LAUNCH("noisy_apply_kernel");
     }
-    noisy_harvest_kernel<<<(unsigned)batch, 1024, hsmem, st>>>(
-        *P, residual, state, dirty, node_f0, node_val, done, rec_pos, rec_val, rec_cap,
-        rec_count, rounds, counters + 1, hscratch, hbytes);
+    launch_harvest(*P, batch, residual, state, dirty, node_f0, node_val, done, rec_pos,
+                   rec_val, rec_cap, rec_count, rounds, counters + 1, hscratch, hbytes, hsmem,
+                   st);
     AFFT_CHECK_LAUNCH("noisy_harvest_kernel");
     cudaMemcpyAsync(host + 1, counters + 1, 4, cudaMemcpyDeviceToHost, st);
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
