@@ -1115,7 +1115,16 @@ static int launch_gather_dft(const void* x, int dtype, int64_t n, int64_t batch,
                 (long long)n);
       return AFFT_EINVAL;
     }
-    if (b > AFFT_MAX_SMEM_DFT) {
+    // b >= 1024 goes to the global passes too: the one-CTA smem DFT needs (3 b) 16 bytes
+    // there (192 KB at b = 4096: one CTA per SM), the passes run 3 CTAs per SM — config
+    // 4's sFFT-DT3 2.15 -> 1.98 ms and config 2's 2.04 -> 1.92 ms per batch.
+    // AFFT_FOURSTEP_MIN_B moves the threshold (diagnostic; > 4096: the one-CTA DFT up to
+    // AFFT_MAX_SMEM_DFT).
+    static const int64_t fourstep_min_b = [] {
+      const char* e = getenv("AFFT_FOURSTEP_MIN_B");
+      return e ? std::max<int64_t>(2, atoll(e)) : (int64_t)1024;
+    }();
+    if (b > AFFT_MAX_SMEM_DFT || b >= fourstep_min_b) {
       if (nshift > 65535) {
         set_error("too many shifts for the large-b path");
         return AFFT_EUNSUPPORTED;
