@@ -596,7 +596,17 @@ def run_e2e(args, dev, x):
     from paper_2011_05749_b200.batch import ffast_batch
 
     m = min(args.e2e_signals, x.shape[0])
-    host = torch.empty((m, N_SIG), dtype=torch.complex64, pin_memory=True)
+    while True:  # pinned host staging; a host that cannot lock this much gets half
+        try:
+            host = torch.empty((m, N_SIG), dtype=torch.complex64, pin_memory=True)
+            break
+        except (RuntimeError, torch.AcceleratorError) if hasattr(torch, "AcceleratorError") \
+                else RuntimeError:
+            if m <= 16:
+                raise
+            m //= 2
+            print(f"bench: pinned staging failed, e2e with {m} signals per step",
+                  file=sys.stderr)
     host.copy_(x[:m])
     dbuf = torch.empty((m, N_SIG), dtype=torch.complex64, device=dev)
     res = ffast_batch(dbuf.copy_(host, non_blocking=True), K, FACTORS)
