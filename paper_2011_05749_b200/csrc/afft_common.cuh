@@ -57,7 +57,9 @@ int classify_noisy_multi(const double* residual, const int64_t* index, const int
 int rows_gather_multi(const double* Y, int64_t b, int U, int nshift, const int32_t* coset,
                       const int64_t* q, const int64_t* idx, const int32_t* sig, int64_t nrows,
                       double* rows, cudaStream_t st);
-// dsfft.cu: alias_rows_multi for n/b > 256 (one CTA per row, n/b <= 2^14)
+// The one-CTA-per-row alias rows keep 2.5 L values in shared memory: L <= 4096.
+constexpr int64_t kAliasCtaMaxL = 4096;
+// dsfft.cu: alias_rows_multi for 256 < n/b <= kAliasCtaMaxL (one CTA per row)
 int alias_rows_cta_multi(const double* Y, int64_t n, int64_t b, const int64_t* tau_tab,
                          int nshift, const int64_t* idx, const int32_t* sig, int64_t nrows,
                          double* rows, cudaStream_t st);

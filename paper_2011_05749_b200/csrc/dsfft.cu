@@ -476,11 +476,11 @@ int alias_rows_cta_multi(const double* Y, int64_t n, int64_t b, const int64_t* t
                          double* rows, cudaStream_t st) {
   const int64_t L = n / b;
   if (nrows == 0 || nshift == 0) return AFFT_OK;
-  if (L > (1 << 14) || (L & (L - 1)) || b < 1 || n % b) {
+  if (L > kAliasCtaMaxL || (L & (L - 1)) || b < 1 || n % b) {
     set_error("alias_rows_cta_multi: n/b = %lld unsupported", (long long)L);
     return AFFT_EUNSUPPORTED;
   }
-  const bool tabled = L <= 4096;  // as afft_alias_rows
+  const bool tabled = true;  // L <= kAliasCtaMaxL, as afft_alias_rows
   const size_t smem = (size_t)(tabled ? 2 * L + L / 2 : 2 * L) * sizeof(cd);
   cudaError_t e = ensure_smem((const void*)alias_rows_cta_multi_kernel, smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(alias_rows_cta_multi)");
@@ -1150,7 +1150,7 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
   }
   const int64_t L = n / b;
   const bool pow2L = (L & (L - 1)) == 0;
-  if ((L > kAliasRowsMaxL && !(pow2L && !energy && !values0 && L <= (1 << 14))) ||
+  if ((L > kAliasRowsMaxL && !(pow2L && !energy && !values0 && L <= kAliasCtaMaxL)) ||
       ((energy || values0) && L > kAliasMaxL)) {
     set_error("afft_alias_rows: n/b = %lld above %d (rows) / %d (energies, values)",
               (long long)L, kAliasRowsMaxL, kAliasMaxL);
@@ -1162,8 +1162,8 @@ extern "C" int afft_alias_rows(const double* spectrum, int64_t n, int64_t b,
     AliasShifts sh;
     sh.nshift = nshift;
     for (int t = 0; t < nshift; ++t) sh.tau[t] = host_pymod(shifts[t], n);
-    if (L > kAliasRowsMaxL) {  // one CTA per row, 2 L entries of shared memory
-      const bool tabled = L <= 4096;  // the root table fits beside the two buffers
+    if (L > kAliasRowsMaxL) {  // one CTA per row, 2.5 L entries of shared memory
+      const bool tabled = true;  // L <= kAliasCtaMaxL: the root table fits beside the buffers
       const size_t smem = (size_t)(tabled ? 2 * L + L / 2 : 2 * L) * sizeof(cd);
       cudaError_t e = ensure_smem((const void*)alias_rows_cta_kernel, smem);
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(alias_rows_cta)");

@@ -350,7 +350,7 @@ struct Dsfft {
     const char* e = std::getenv("AFFT_DSFFT_Y_L");
     return e ? std::max<int64_t>(1, std::atoll(e)) : 64;
   }();
-  // Larger L: one CTA per row (L <= 2^14), when asked for (AFFT_DSFFT_Y_L) or when the
+  // Larger L: one CTA per row (L <= kAliasCtaMaxL), when asked for (AFFT_DSFFT_Y_L) or when the
   // list is short enough (probe classifies) that its A L products cost less than the
   // coset DFTs: ~83 ns per row at L = 2048 against ~23 us for the DFTs at config 4's
   // depth 13 (launch lists), so up to A L = 2^19 once Y is resident.
@@ -359,7 +359,7 @@ struct Dsfft {
     const int64_t L = n / b;
     if (L <= kAliasMaxL) return true;
     if (L <= kAliasRowsMaxL) return Y.p || L <= y_rows_l;
-    if (L > (1 << 14)) return false;
+    if (L > kAliasCtaMaxL) return false;
     return L <= y_rows_l || (Y.p && count >= 0 && count * L <= kShortRowsBudget);
   }
 
@@ -1170,7 +1170,7 @@ static int dsfft_batch_run(const void* x, int dtype, int64_t n, int64_t S, int64
       if (!probe) cand.assign(act, act + m);
       // the row source afft_dsfft's rows() picks for this list (alias_rows_ok)
       const int64_t cnt = (int64_t)cand.size();
-      const bool alias = L <= 256 || (L <= (1 << 14) && cnt * L <= (int64_t(1) << 19));
+      const bool alias = L <= 256 || (L <= kAliasCtaMaxL && cnt * L <= (int64_t(1) << 19));
       mem.push_back({s, 0, cnt, probe, alias});
     }
     PMARK("b step lists");

@@ -161,7 +161,8 @@ def test_fused_spectrum_layers_change_nothing(golden_dsfft, monkeypatch):
         assert np.array_equal(v1, v0)
 
 
-@pytest.mark.parametrize("n,k", [(1 << 16, 64), (1 << 16, 512), (1 << 24, 1024)])
+@pytest.mark.parametrize("n,k", [(1 << 16, 64), (1 << 16, 512), (1 << 24, 1024),
+                                 (1 << 24, 256)])
 def test_fused_layers_other_shapes(monkeypatch, n, k):
     """The fused epilogue at the other plan shapes it serves: n = 2^16 (two radix-256
     passes) with the stop layer below the fused depths (tree levels from the depth-8
