@@ -178,7 +178,17 @@ int d2h(std::vector<T>& h, const void* d, size_t count, cudaStream_t st) {
     }();
     if (blocking) {
       thread_local cudaEvent_t ev = nullptr;
-      if (!ev) e = cudaEventCreateWithFlags(&ev, cudaEventBlockingSync | cudaEventDisableTiming);
+      thread_local int ev_dev = -1;
+      int dev = 0;
+      e = cudaGetDevice(&dev);
+      if (e == cudaSuccess && ev && ev_dev != dev) {  // events belong to a device
+        cudaEventDestroy(ev);
+        ev = nullptr;
+      }
+      if (e == cudaSuccess && !ev) {
+        e = cudaEventCreateWithFlags(&ev, cudaEventBlockingSync | cudaEventDisableTiming);
+        ev_dev = dev;
+      }
       if (e == cudaSuccess) e = cudaEventRecord(ev, st);
       if (e == cudaSuccess) e = cudaEventSynchronize(ev);
     } else {

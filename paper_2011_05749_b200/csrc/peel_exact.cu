@@ -648,15 +648,14 @@ static bool fused_smem(const PeelGraph& G, bool rec_in_smem, size_t* total, size
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static int num_sms() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0, v = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
+static int num_sms() {  // of the current device (the attribute query is a cheap lookup)
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
   }
-  return cached;
+  return v > 0 ? v : 148;
 }
 
 // Auxiliary stream and events for the pipelined FFAST path, one set per device.
