@@ -652,8 +652,11 @@ struct Dsfft {
     RC(pk.buf.alloc(pk.bytes, st, "dsfft result pack"));
     char* p = pk.buf.as<char>();
     CK(cudaMemcpyAsync(p + pk.oa, idx, (size_t)A * 8, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(p + pk.of, 0xff, (size_t)A * 8, st));  // f0 = -1
-    CK(cudaMemsetAsync(p + pk.ov, 0, (size_t)A * 16, st));
+    if (P.mode == 0) {  // classify_exact writes f0 / value for single-tons only; the noisy
+                        // finalize writes every row's
+      CK(cudaMemsetAsync(p + pk.of, 0xff, (size_t)A * 8, st));  // f0 = -1
+      CK(cudaMemsetAsync(p + pk.ov, 0, (size_t)A * 16, st));
+    }
     return AFFT_OK;
   }
 

@@ -535,34 +535,15 @@ static int64_t warp_search_maxl() {
   return v;
 }
 constexpr int kWarpSearchWarps = 8;
+// One node's exact argmin over its L candidates by one warp (lanes over candidates;
+// s_est / s_e32 hold the node's stride estimates, `bad` any NaN / infinite one): the
+// (min score, smallest t) of the CTA kernel's single chunk.
 template <bool k32>
-__global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kernel(
-    int64_t n, int c, int A, const int64_t* __restrict__ act_index,
-    const int64_t* __restrict__ act_b, const double* __restrict__ est,
-    double* __restrict__ part_score, int32_t* __restrict__ part_t,
-    const int32_t* __restrict__ A_dev = nullptr) {
-  if (A_dev) A = *A_dev;
-  __shared__ double s_est_all[kWarpSearchWarps][kMaxStrides];
-  __shared__ uint32_t s_e32_all[kWarpSearchWarps][kMaxStrides];
-  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int a = blockIdx.x * kWarpSearchWarps + wl;
-  if (a >= A) return;  // whole warps only
-  double* s_est = s_est_all[wl];
-  uint32_t* s_e32 = s_e32_all[wl];
-  bool bad = false;
-  for (int j = lane; j < c; j += 32) {
-    const double e = est[(int64_t)a * c + j];
-    s_est[j] = e;
-    double u = e * 0.15915494309189535;
-    u -= floor(u);
-    s_e32[j] = (uint32_t)(uint64_t)(u * 4294967296.0);
-    bad |= !(e == e) || isinf(e);
-  }
-  bad = __any_sync(0xffffffffu, bad);
-  __syncwarp();
-  const int64_t b = act_b[a];
+__device__ __forceinline__ void warp_search_node(int64_t n, int c, int64_t idx, int64_t b,
+                                                 const double* s_est, const uint32_t* s_e32,
+                                                 bool bad, int lane, double* best_out,
+                                                 int32_t* bt_out) {
   const int64_t L = n / b;
-  const int64_t idx = act_index[a];
   // one candidate per lane (L <= 32, DSFFT's deep layers): no pruning bound to seed
   // and no pre-filter to set up — both cost a candidate's worth of dependent work and
   // could only save part of one score; every candidate is scored in full instead
@@ -606,6 +587,45 @@ __global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kerne
       bt = ot;
     }
   }
+  *best_out = best;
+  *bt_out = bt;
+}
+
+// a node's stride estimates into the warp's shared copies (lanes over strides);
+// returns whether any is NaN / infinite
+__device__ __forceinline__ bool stage_estimates(const double* e_src, int c, int lane,
+                                                double* s_est, uint32_t* s_e32) {
+  bool bad = false;
+  for (int j = lane; j < c; j += 32) {
+    const double e = e_src[j];
+    s_est[j] = e;
+    double u = e * 0.15915494309189535;
+    u -= floor(u);
+    s_e32[j] = (uint32_t)(uint64_t)(u * 4294967296.0);
+    bad |= !(e == e) || isinf(e);
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  __syncwarp();
+  return bad;
+}
+
+template <bool k32>
+__global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_search_warp_kernel(
+    int64_t n, int c, int A, const int64_t* __restrict__ act_index,
+    const int64_t* __restrict__ act_b, const double* __restrict__ est,
+    double* __restrict__ part_score, int32_t* __restrict__ part_t,
+    const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
+  __shared__ double s_est_all[kWarpSearchWarps][kMaxStrides];
+  __shared__ uint32_t s_e32_all[kWarpSearchWarps][kMaxStrides];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = blockIdx.x * kWarpSearchWarps + wl;
+  if (a >= A) return;  // whole warps only
+  const bool bad = stage_estimates(est + (int64_t)a * c, c, lane, s_est_all[wl], s_e32_all[wl]);
+  double best;
+  int32_t bt;
+  warp_search_node<k32>(n, c, act_index[a], act_b[a], s_est_all[wl], s_e32_all[wl], bad, lane,
+                        &best, &bt);
   if (lane == 0) {
     part_score[a] = best;
     part_t[a] = bt;
@@ -659,44 +679,20 @@ struct NoisyDecide {
   const double* t1s;
 };
 
-__global__ void noisy_finalize_kernel(int A, int chunks, const double* __restrict__ part_score,
-                                      const int32_t* __restrict__ part_t,
-                                      const int64_t* __restrict__ act_row,
-                                      const int64_t* __restrict__ act_index,
-                                      const int64_t* __restrict__ act_b,
-                                      const double* __restrict__ residual,
-                                      const __grid_constant__ NoisyPlan P,
-                                      int64_t* __restrict__ out_f0, double* __restrict__ out_val,
-                                      double* __restrict__ out_res, NoisyDecide decide,
-                                      const int32_t* __restrict__ A_dev = nullptr) {
-  if (A_dev) A = *A_dev;
-  // classify's zero-ton gate needs ||y||: the squares land in shared memory while the
-  // rows are loaded, and lane 0 sums them in node_norm's order (not 2 x R dependent
-  // global loads on one lane — 30% of this kernel's instructions and its latency chain)
+// The fit (peeling.py:247-250) and classify_noisy's decision (257-267) for node a of
+// the active list, one warp (lane, wl = its warp within a 256-thread CTA's nsq rows),
+// from the search's winner t = bt.
+__device__ __forceinline__ void finalize_node(int a, int lane, int wl, int32_t bt,
+                                              const int64_t* __restrict__ act_row,
+                                              const int64_t* __restrict__ act_index,
+                                              const int64_t* __restrict__ act_b,
+                                              const double* __restrict__ residual,
+                                              const NoisyPlan& P, int64_t* __restrict__ out_f0,
+                                              double* __restrict__ out_val,
+                                              double* __restrict__ out_res,
+                                              const NoisyDecide& decide,
+                                              double (*nsq)[2][128]) {
   constexpr int kNormRows = 128;
-  __shared__ double nsq[8][2][kNormRows];  // blockDim 256
-  const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31, wl = (threadIdx.x >> 5) & 7;
-  if (a >= A) return;
-  double best = __longlong_as_double(0x7ff0000000000000LL);
-  int32_t bt = INT32_MAX;
-  for (int ch = lane; ch < chunks; ch += 32) {
-    const double sc = part_score[(int64_t)a * chunks + ch];
-    const int32_t t = part_t[(int64_t)a * chunks + ch];
-    if (sc < best || (sc == best && t < bt)) {
-      best = sc;
-      bt = t;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
-    if (ob < best || (ob == best && ot < bt)) {
-      best = ob;
-      bt = ot;
-    }
-  }
   if (bt == INT32_MAX) bt = 0;  // all-NaN scores: numpy argmin would return the first NaN
   const int64_t n = P.n;
   // index < b and t < n / b, so the candidate is already reduced (no '% n')
@@ -766,6 +762,99 @@ __global__ void noisy_finalize_kernel(int A, int chunks, const double* __restric
                             ? AFFT_SINGLE_TON
                                                   : AFFT_MULTI_TON;
   }
+}
+
+__global__ void noisy_finalize_kernel(int A, int chunks, const double* __restrict__ part_score,
+                                      const int32_t* __restrict__ part_t,
+                                      const int64_t* __restrict__ act_row,
+                                      const int64_t* __restrict__ act_index,
+                                      const int64_t* __restrict__ act_b,
+                                      const double* __restrict__ residual,
+                                      const __grid_constant__ NoisyPlan P,
+                                      int64_t* __restrict__ out_f0, double* __restrict__ out_val,
+                                      double* __restrict__ out_res, NoisyDecide decide,
+                                      const int32_t* __restrict__ A_dev = nullptr) {
+  if (A_dev) A = *A_dev;
+  // classify's zero-ton gate needs ||y||: the squares land in shared memory while the
+  // rows are loaded, and lane 0 sums them in node_norm's order (not 2 x R dependent
+  // global loads on one lane — 30% of this kernel's instructions and its latency chain)
+  __shared__ double nsq[8][2][128];  // blockDim 256: per warp, finalize_node's squares
+  const int a = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31, wl = (threadIdx.x >> 5) & 7;
+  if (a >= A) return;
+  double best = __longlong_as_double(0x7ff0000000000000LL);
+  int32_t bt = INT32_MAX;
+  for (int ch = lane; ch < chunks; ch += 32) {
+    const double sc = part_score[(int64_t)a * chunks + ch];
+    const int32_t t = part_t[(int64_t)a * chunks + ch];
+    if (sc < best || (sc == best && t < bt)) {
+      best = sc;
+      bt = t;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (ob < best || (ob == best && ot < bt)) {
+      best = ob;
+      bt = ot;
+    }
+  }
+  finalize_node(a, lane, wl, bt, act_row, act_index, act_b, residual, P, out_f0, out_val, out_res,
+                decide, nsq);
+}
+
+// classify_noisy for short candidate lists in one launch (DSFFT's layers, n/b <= 2048):
+// one warp per node does the stride estimates (lanes over strides, stride_estimate as
+// noisy_est_kernel), the candidate scan (warp_search_node) and the fit + decision
+// (finalize_node) — the est -> warp search -> finalize sequence without its two extra
+// launches and the partials' round trip through memory; the same arithmetic, so the same
+// results.
+template <bool k32>
+__global__ void __launch_bounds__(kWarpSearchWarps * 32) noisy_classify_warp_kernel(
+    const __grid_constant__ NoisyPlan P, int A, const int64_t* __restrict__ act_row,
+    const int64_t* __restrict__ act_index, const int64_t* __restrict__ act_b,
+    const double* __restrict__ residual, EstFill fill, int64_t* __restrict__ out_f0,
+    double* __restrict__ out_val, double* __restrict__ out_res, NoisyDecide decide) {
+  static_assert(kWarpSearchWarps == 8, "finalize_node's squares: 8 warps per CTA");
+  __shared__ double s_est_all[kWarpSearchWarps][kMaxStrides];
+  __shared__ uint32_t s_e32_all[kWarpSearchWarps][kMaxStrides];
+  __shared__ double nsq[8][2][128];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = blockIdx.x * kWarpSearchWarps + wl;
+  if (a >= A) return;  // whole warps only
+  if (fill.index) {
+    if (lane == 0) {
+      fill.act_row[a] = a;
+      fill.act_index[a] = fill.index[a];
+      fill.act_b[a] = fill.b;
+    }
+    __syncwarp();  // finalize_node reads the lists back
+  }
+  const int64_t row = fill.index ? a : act_row[a];
+  const cd* y = reinterpret_cast<const cd*>(residual) + row * P.R;
+  double* s_est = s_est_all[wl];
+  uint32_t* s_e32 = s_e32_all[wl];
+  bool bad = false;
+  for (int j = lane; j < P.c; j += 32) {
+    const double e = stride_estimate(y + (int64_t)j * P.m, P.m, P.w);
+    s_est[j] = e;
+    double u = e * 0.15915494309189535;
+    u -= floor(u);
+    s_e32[j] = (uint32_t)(uint64_t)(u * 4294967296.0);
+    bad |= !(e == e) || isinf(e);
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  __syncwarp();
+  const int64_t idx = fill.index ? fill.index[a] : act_index[a];
+  const int64_t b = fill.index ? fill.b : act_b[a];
+  double best;
+  int32_t bt;
+  warp_search_node<k32>(P.n, P.c, idx, b, s_est, s_e32, bad, lane, &best, &bt);
+  finalize_node(a, lane, wl, bt, fill.index ? fill.act_row : act_row,
+                fill.index ? fill.act_index : act_index, fill.index ? fill.act_b : act_b,
+                residual, P, out_f0, out_val, out_res, decide, nsq);
 }
 
 // -------------------------------------------------------------- decoder rounds
@@ -1339,6 +1428,12 @@ struct SearchOut {  // null members: the workspace slots
   NoisyDecide decide = {nullptr, 0.0, 0.0};
 };
 
+// AFFT_FUSED_CLASSIFY=0: estimates, warp scan and fit as three launches (diagnostic)
+static bool fused_classify_on() {
+  const char* e = getenv("AFFT_FUSED_CLASSIFY");
+  return !(e && e[0] == '0');
+}
+
 static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
                       const double* residual, cudaStream_t st,
                       const AfftSearchShard* shard = nullptr, int64_t rows_total = 0,
@@ -1360,6 +1455,18 @@ static int run_search(const NoisyPlan& P, const NoisyWs& w, char* ws, int A,
   EstFill fill{fill_index, fill_b, const_cast<int64_t*>(act_row),
                const_cast<int64_t*>(act_index), const_cast<int64_t*>(act_b)};
   if (!fill_index) fill = EstFill{nullptr, 0, nullptr, nullptr, nullptr};
+  if (world == 1 && w.Lmax <= warp_search_maxl() && fused_classify_on()) {
+    // one warp per node does estimates, scan and fit in one launch
+    auto kfn = P.n < (int64_t(1) << 31) ? noisy_classify_warp_kernel<true>
+                                        : noisy_classify_warp_kernel<false>;
+    kfn<<<(unsigned)((A + kWarpSearchWarps - 1) / kWarpSearchWarps), kWarpSearchWarps * 32, 0,
+          st>>>(P, A, act_row, act_index, act_b, residual, fill,
+                out.f0 ? out.f0 : reinterpret_cast<int64_t*>(ws + w.f0),
+                out.val ? out.val : reinterpret_cast<double*>(ws + w.val),
+                out.res ? out.res : reinterpret_cast<double*>(ws + w.res), out.decide);
+    AFFT_CHECK_LAUNCH("noisy_classify_warp_kernel");
+    return AFFT_OK;
+  }
   noisy_est_kernel<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(A, P.c, P.m, act_row, residual,
                                                                 P.R, P, est, node_bound, nullptr,
                                                                 fill);
