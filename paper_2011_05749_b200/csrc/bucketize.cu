@@ -381,7 +381,11 @@ __device__ __forceinline__ void deep_fuse_epilogue(cd (&y)[16], int tid, int64_t
   if (f.vmid) f.vmid[j0 + jj + ((int64_t)qb << dtop)] = y[0];
 }
 
-template <int LA, int LB, bool FUSE>
+// PARTIAL: nb = b / R need not be a multiple of kCnt; the last chunk of a sequence loads
+// zeros for its missing columns and stores nothing for them (a separate instantiation:
+// predicating the full-chunk form's loads cost it its batched issue, 2^24 c64 0.38 ->
+// 0.53 ms).
+template <int LA, int LB, bool FUSE, bool PARTIAL = false>
 __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepFuse& f) {
   constexpr int A = 1 << LA, B = 1 << LB, LGR = LA + LB, R = A * B;
   constexpr int kCnt = kGStockPoints / R, kLgCnt = 11 - LGR;
@@ -396,7 +400,7 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
   const int tid = threadIdx.x;
   build_twiddles(twR, R, tid, kGfftThreads);
   const int64_t nb = p.b / R;
-  const int64_t nchunks = nb >> kLgCnt;
+  const int64_t nchunks = PARTIAL ? (nb + kCnt - 1) >> kLgCnt : nb >> kLgCnt;
   const int64_t ntiles = p.batch * p.nshift * nchunks;
   const int64_t tstep = p.b / (p.Ns * R);
   const bool pow2ns = (p.Ns & (p.Ns - 1)) == 0;  // N_s = product of earlier radices
@@ -415,6 +419,7 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
     const int t = (int)(st_ % p.nshift);
     const int64_t s = st_ / p.nshift;
     const int64_t j0 = chunk << kLgCnt;
+    const int valid = PARTIAL ? (int)(nb - j0 < kCnt ? nb - j0 : kCnt) : kCnt;
     const int64_t k0 = pow2ns ? (j0 & (p.Ns - 1)) : j0 % p.Ns;
     // k = (j0 + jj) mod N_s
     auto kmod = [&](int jj) -> int64_t {
@@ -442,7 +447,9 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
         for (int n2 = 0; n2 < B; ++n2) {
           int64_t idx = (j0 + jj + (int64_t)(n1 + A * n2) * nb) * p.L - tau;
           if (idx < 0) idx += p.n;
-          raw[i][n2] = __ldg(reinterpret_cast<const float2*>(xs) + idx);
+          raw[i][n2] = !PARTIAL || jj < valid
+                           ? __ldg(reinterpret_cast<const float2*>(xs) + idx)
+                           : make_float2(0.f, 0.f);
         }
       }
 #pragma unroll
@@ -463,7 +470,7 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
         for (int n2 = 0; n2 < B; ++n2) {
           int64_t idx = (j0 + jj + (int64_t)(n1 + A * n2) * nb) * L - off;
           if (idx < 0) idx += p.n;
-          raw[i][n2] = __ldcs(base + idx);
+          raw[i][n2] = !PARTIAL || jj < valid ? __ldcs(base + idx) : make_double2(0.0, 0.0);
         }
       }
 #pragma unroll
@@ -519,6 +526,7 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
       const int64_t j = j0 + jj;
       const int64_t k = kmod(jj);
       const int64_t base = (j - k) * R + k;
+      if (PARTIAL && jj >= valid) continue;  // a partial chunk's missing column
 #pragma unroll
       for (int qa = 0; qa < A; ++qa) {
         const int64_t dst = base + (int64_t)(qb + B * qa) * p.Ns;
@@ -553,10 +561,10 @@ __device__ __forceinline__ void gfft_reg_body(const GStockParams& p, const DeepF
   }
 }
 
-template <int LA, int LB>
+template <int LA, int LB, bool PARTIAL = false>
 __global__ void __launch_bounds__(kGfftThreads) gfft_reg_kernel(
     const __grid_constant__ GStockParams p) {
-  gfft_reg_body<LA, LB, false>(p, DeepFuse{});
+  gfft_reg_body<LA, LB, false, PARTIAL>(p, DeepFuse{});
 }
 
 // The last radix-256 pass of a DSFFT spectrum with the tree layers decided in its
@@ -793,6 +801,17 @@ static const void* gfft_tma_fn(int lgr) {
   }
 }
 
+static const void* gfft_reg_partial_fn(int lgr) {
+  switch (lgr) {
+    case 4: return (const void*)gfft_reg_kernel<2, 2, true>;
+    case 5: return (const void*)gfft_reg_kernel<3, 2, true>;
+    case 6: return (const void*)gfft_reg_kernel<3, 3, true>;
+    case 7: return (const void*)gfft_reg_kernel<4, 3, true>;
+    case 8: return (const void*)gfft_reg_kernel<4, 4, true>;
+    default: return nullptr;
+  }
+}
+
 static const void* gfft_reg_fn(int lgr) {
   switch (lgr) {
     case 2: return (const void*)gfft_reg_kernel<1, 1>;
@@ -991,6 +1010,13 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
       while ((1 << lgr) < R) ++lgr;
       g.cnt = kGStockPoints / R;
     }
+    // power-of-two radices >= 16 over partial chunks (b not a multiple of 2048, e.g. the
+    // radix-64 pass of 9728 = 152 x 64): the register pass's partial instantiation
+    int lgr_partial = -1;
+    if (lgr < 0 && (R & (R - 1)) == 0 && R >= 16 && R <= 256 && !fft_smem_path()) {
+      lgr_partial = 0;
+      while ((1 << lgr_partial) < R) ++lgr_partial;
+    }
     const void* kfn = lgr < 0 ? (const void*)gstockham_kernel<-1> : gstockham_fixed_table()[lgr];
     size_t smem = (size_t)(R + 2 * (int64_t)g.cnt * ldR) * 16;
     int threads = kGStockThreads;
@@ -1024,6 +1050,12 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
         const int64_t sstride = s == 0 ? ld * (dtype == AFFT_C64 ? 8 : 16) : b * 16;
         use_tmap = encode_pass_map(&tmap, base, f32, b / R, R, g.cnt, (int64_t)seqs, sstride) ? 1 : 0;
       }
+    } else if (lgr_partial >= 4 && !(fuse && s == P - 1)) {  // register pass, partial chunks
+      kfn = gfft_reg_partial_fn(lgr_partial);
+      g.cnt = kGStockPoints / R;
+      g.perm = 0;
+      smem = (size_t)(R + (int64_t)g.cnt * (R + 1)) * 16;
+      threads = kGfftThreads;
     } else if (lgr >= 2 && !fft_smem_path()) {  // register-resident pass
       kfn = gfft_reg_fn(lgr);
       const int64_t nch = (b / R) / g.cnt;
