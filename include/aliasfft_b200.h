@@ -114,6 +114,22 @@ int afft_peel_exact(int64_t n, int64_t batch, const int64_t* factors /* host */,
                     int32_t* rec_count, int32_t* rounds, int32_t* unresolved, void* stream);
 
 /*
+ * The paper's Fig. 5 tree-walk ("sparse-graph decoder by packet erasure channel
+ * method"; a non-goal of the reference) for exact mode:
+ * every live node identified once, then paths extended from single-ton nodes through a
+ * FIFO queue — each decoded tone is subtracted from its d check nodes and only those
+ * are re-identified.  Same arguments and outputs as afft_peel_exact (recovered set equal
+ * to the round decoder's; order the walk's); rounds[s] = the walk's generations,
+ * identifications[s] (may be NULL) = check-node identifications performed.
+ */
+int afft_peel_tree_exact(int64_t n, int64_t batch, const int64_t* factors /* host */,
+                         int32_t ncycles, double* residual, int8_t* state, int64_t* node_f0,
+                         double* node_val, const double* eps_zero, const double* eps_ratio,
+                         int64_t* rec_pos, double* rec_val, int32_t rec_cap,
+                         int32_t* rec_count, int32_t* rounds, int32_t* unresolved,
+                         int32_t* identifications, void* stream);
+
+/*
  * classify_exact (peeling.py:193-215) for `count` independent nodes of one cycle
  * size b: residual [count][3] complex128, index [count] bucket indices.  Writes
  * state, and f0/val where the node is a SINGLE_TON (f0/val are in/out so a

@@ -45,6 +45,10 @@ SIGNATURES = {
         _INT,
         [_I64, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P],
     ),
+    "afft_peel_tree_exact": (
+        _INT,
+        [_I64, _I64, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
+    ),
     "afft_classify_exact": (_INT, [_P, _P, _I64, _I64, _I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P]),
     "afft_subtract": (_INT, [_P, _P, _I32, _P, _P, _I64, _I64, _P]),
     "afft_truncate": (_INT, [_P, _P, _P, _I32, _I64, _I32, _P, _P, _P, _P]),

@@ -98,6 +98,144 @@ __global__ void __launch_bounds__(256) peel_exact_kernel(const __grid_constant__
   }
 }
 
+// ------------------------------------------------------------------ tree walk
+//
+// The paper's Fig. 5 "sparse-graph decoder by packet erasure channel method"
+// (a non-goal of the reference, "identical output to
+// Fig. 4 with fewer identifications"): instead of re-identifying every live check node
+// each round (peeling.py:288-295), paths are extended from single-ton check nodes —
+// identify the left node (the tone), subtract it from its d right neighbours, and
+// re-identify only those; a neighbour that becomes a single-ton extends the path.
+// A FIFO queue of single-ton nodes per signal (one CTA per signal; the initial
+// identification of every node is parallel, the walk itself sequential on one thread,
+// which is what the method is).  Exact mode, shifts (0, 1, 2).  The recovered set
+// equals the round decoder's (tests/test_gpu_ffast.py); the order is the walk's, and
+// the values differ from the rounds' by the rounding of the subtraction order.
+// rounds[s] = the longest path (queue generations), ident[s] = identifications.
+__global__ void __launch_bounds__(256) peel_tree_kernel(const __grid_constant__ PeelParams p,
+                                                        int32_t* __restrict__ ident) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tmp[32];
+  __shared__ int carry, red, nq0, nident;
+  const int64_t s = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const PeelGraph& G = p.G;
+  const int N = G.nodes, F = G.ncycles;
+  const int64_t n = G.n;
+  unsigned char* mem =
+      p.gscratch ? reinterpret_cast<unsigned char*>(p.gscratch) + (size_t)s * p.scratch_bytes
+                 : smem_raw;
+  const PeelLayout L = peel_layout(N, G.ncycles, G.hmask + 1, false);
+  const PeelMem M = peel_carve(mem, L);
+  const cd* gres = reinterpret_cast<const cd*>(p.residual) + s * (int64_t)N * 3;
+  for (int e = tid; e < N * 3; e += nt) M.res[e] = gres[e];
+  for (int g = tid; g < N; g += nt) {
+    M.st[g] = p.state[s * N + g];
+    M.hv[g] = 0;  // in the queue
+    M.f0[g] = p.node_f0 ? p.node_f0[s * N + g] : -1;
+    M.val[g] = p.node_val ? reinterpret_cast<const cd*>(p.node_val)[s * N + g] : cd{0.0, 0.0};
+  }
+  for (int h = tid; h <= G.hmask; h += nt) M.hash[h] = kEmpty;
+  peel_fill_cycles(G, M);
+  if (tid == 0) nident = 0;
+  __syncthreads();
+  int rc = p.rec_count[s];
+  int64_t* rpos = p.rec_pos + s * (int64_t)p.rec_cap;
+  cd* rval = reinterpret_cast<cd*>(p.rec_val) + s * (int64_t)p.rec_cap;
+  for (int i = tid; i < rc; i += nt) hash_insert(M.hash, G.hmask, rpos[i]);
+  const double eps0 = p.eps_zero[s], epsr = p.eps_ratio[s];
+  const double cfac = (double)(-n) / 6.283185307179586;  // -n / (2.0 * np.pi)
+  // step 1: identify every live node once (parallel); single-tons start the paths
+  int mine = 0;
+  for (int g = tid; g < N; g += nt) {
+    int start = 0;
+    const int8_t s0 = M.st[g];
+    if (s0 != AFFT_RESOLVED && s0 != AFFT_ZERO_TON) {
+      const int c = M.cyc[g];
+      M.st[g] = classify_exact_dev(M.res[3 * g], M.res[3 * g + 1], M.res[3 * g + 2],
+                                   g - G.base[c], G.b[c], n, eps0, epsr, cfac, &M.f0[g],
+                                   &M.val[g]);
+      ++mine;
+      start = M.st[g] == AFFT_SINGLE_TON;
+    }
+    M.flag[g] = start;
+  }
+  if (mine) atomicAdd(&nident, mine);
+  __syncthreads();
+  const int q0 = block_exclusive_scan(M.flag, N, warp_tmp, &carry);
+  // the queue lives in found_res (N * ncycles entries: a node re-enters only after it
+  // was popped, so at most N entries are ever live; indices wrap)
+  int* Q = M.found_res;
+  const int qcap = N * F;
+  for (int g = tid; g < N; g += nt) {
+    const int start = (g + 1 < N ? M.flag[g + 1] : q0) - M.flag[g];
+    if (start) {
+      Q[M.flag[g]] = g;
+      M.hv[g] = 1;
+    }
+  }
+  if (tid == 0) nq0 = q0;
+  __syncthreads();
+  // steps 2..p: the walk (one thread: the method is a sequential path extension)
+  if (tid == 0) {
+    int head = 0, tail = nq0, gen_end = nq0, gens = nq0 ? 1 : 0, extra = 0;
+    while (head != tail) {
+      if (head == gen_end) {  // the previous generation is exhausted
+        gen_end = tail;
+        ++gens;
+      }
+      const int g = Q[head];
+      head = head + 1 == qcap ? 0 : head + 1;
+      M.hv[g] = 0;
+      if (M.st[g] != AFFT_SINGLE_TON) continue;
+      const int64_t f = M.f0[g];
+      if (hash_contains(M.hash, G.hmask, f)) continue;  // peeling.py:296-299
+      const cd v = M.res[3 * g];  // a single-ton's value is r0 of its residual
+      hash_insert(M.hash, G.hmask, f);
+      rpos[rc] = f;
+      rval[rc] = v;
+      ++rc;
+      M.st[g] = AFFT_RESOLVED;
+      const cd v1 = cmul(v, unit_root(mulmod(G.tau[1], f, n), n));
+      const cd v2 = cmul(v, unit_root(mulmod(G.tau[2], f, n), n));
+      for (int c = 0; c < F; ++c) {  // the left node's d right neighbours
+        const int g2 = G.base[c] + (int)(f % G.b[c]);
+        M.res[3 * g2] = csub(M.res[3 * g2], v);
+        M.res[3 * g2 + 1] = csub(M.res[3 * g2 + 1], v1);
+        M.res[3 * g2 + 2] = csub(M.res[3 * g2 + 2], v2);
+        const int8_t s2 = M.st[g2];
+        if (g2 == g || s2 == AFFT_RESOLVED || s2 == AFFT_ZERO_TON) continue;
+        const int c2 = M.cyc[g2];
+        M.st[g2] = classify_exact_dev(M.res[3 * g2], M.res[3 * g2 + 1], M.res[3 * g2 + 2],
+                                      g2 - G.base[c2], G.b[c2], n, eps0, epsr, cfac,
+                                      &M.f0[g2], &M.val[g2]);
+        ++extra;
+        if (M.st[g2] == AFFT_SINGLE_TON && !M.hv[g2]) {
+          Q[tail] = g2;
+          tail = tail + 1 == qcap ? 0 : tail + 1;
+          M.hv[g2] = 1;
+        }
+      }
+    }
+    nident += extra;
+    if (p.rounds) p.rounds[s] = gens;
+    p.rec_count[s] = rc;
+    if (ident) ident[s] = nident;
+  }
+  __syncthreads();
+  const int unres = count_multitons(G, M, &red);
+  if (tid == 0 && p.unresolved) p.unresolved[s] = unres;
+  if (p.writeback) {
+    cd* gw = reinterpret_cast<cd*>(p.residual) + s * (int64_t)N * 3;
+    for (int e = tid; e < N * 3; e += nt) gw[e] = M.res[e];
+    for (int g = tid; g < N; g += nt) {
+      p.state[s * N + g] = M.st[g];
+      if (p.node_f0) p.node_f0[s * N + g] = M.f0[g];
+      if (p.node_val) reinterpret_cast<cd*>(p.node_val)[s * N + g] = M.val[g];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ fused FFAST
 
 struct FusedParams {
@@ -605,6 +743,28 @@ static int launch_peel(PeelParams& p, int64_t batch, void* scratch, cudaStream_t
   return AFFT_OK;
 }
 
+static int launch_peel_tree(PeelParams& p, int64_t batch, void* scratch, int32_t* ident,
+                            cudaStream_t stream) {
+  const size_t bytes = peel_layout(p.G.nodes, p.G.ncycles, p.G.hmask + 1, false).total;
+  size_t dyn = 0;
+  if (bytes <= kSmemLimit) {
+    p.gscratch = nullptr;
+    dyn = bytes;
+    cudaError_t e = ensure_smem((const void*)peel_tree_kernel, (int)dyn);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(peel_tree)");
+  } else {
+    if (!scratch) {
+      set_error("peeling graph does not fit in shared memory and no scratch was given");
+      return AFFT_ENOMEM;
+    }
+    p.gscratch = reinterpret_cast<char*>(scratch);
+    p.scratch_bytes = bytes;
+  }
+  peel_tree_kernel<<<(unsigned)batch, 256, dyn, stream>>>(p, ident);
+  AFFT_CHECK_LAUNCH("peel_tree_kernel");
+  return AFFT_OK;
+}
+
 static int launch_truncate(const int64_t* pos, const double* val, const int32_t* count, int cap,
                            int64_t batch, int k, int64_t* out_pos, double* out_val,
                            int32_t* out_count, cudaStream_t stream) {
@@ -764,6 +924,52 @@ extern "C" int afft_peel_exact(int64_t n, int64_t batch, const int64_t* factors,
     if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(peel scratch)");
   }
   rc = launch_peel(p, batch, scratch, st);
+  if (scratch) scratch_free(scratch, st);
+  return rc;
+}
+
+extern "C" int afft_peel_tree_exact(int64_t n, int64_t batch, const int64_t* factors,
+                                    int32_t ncycles, double* residual, int8_t* state,
+                                    int64_t* node_f0, double* node_val, const double* eps_zero,
+                                    const double* eps_ratio, int64_t* rec_pos, double* rec_val,
+                                    int32_t rec_cap, int32_t* rec_count, int32_t* rounds,
+                                    int32_t* unresolved, int32_t* identifications,
+                                    void* stream) {
+  if (batch == 0) return AFFT_OK;
+  if (!residual || !state || !eps_zero || !eps_ratio || !rec_pos || !rec_val || !rec_count ||
+      batch < 0) {
+    set_error("afft_peel_tree_exact: bad arguments");
+    return AFFT_EINVAL;
+  }
+  PeelParams p;
+  memset(&p, 0, sizeof(p));
+  int rc = setup_graph(&p.G, n, factors, ncycles, rec_cap);
+  if (rc) return rc;
+  if (rec_cap < p.G.nodes) {
+    set_error("rec_cap %d must cover the node count %d plus prior entries", rec_cap, p.G.nodes);
+    return AFFT_EINVAL;
+  }
+  p.residual = residual;
+  p.state = state;
+  p.node_f0 = node_f0;
+  p.node_val = node_val;
+  p.eps_zero = eps_zero;
+  p.eps_ratio = eps_ratio;
+  p.rec_pos = rec_pos;
+  p.rec_val = rec_val;
+  p.rec_cap = rec_cap;
+  p.rec_count = rec_count;
+  p.rounds = rounds;
+  p.unresolved = unresolved;
+  p.writeback = 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  void* scratch = nullptr;
+  const size_t bytes = peel_layout(p.G.nodes, ncycles, p.G.hmask + 1, false).total;
+  if (bytes > kSmemLimit) {
+    cudaError_t e = scratch_alloc(&scratch, (size_t)batch * bytes, st);
+    if (e != cudaSuccess) return cuda_status(e, "scratch_alloc(peel tree scratch)");
+  }
+  rc = launch_peel_tree(p, batch, scratch, identifications, st);
   if (scratch) scratch_free(scratch, st);
   return rc;
 }

@@ -111,6 +111,8 @@ class DecodeResult:
     spectrum: SparseSpectrum
     unresolved_multitons: int
     rounds: int
+    # extension: check-node identifications of peel_decode(..., decoder="tree")
+    identifications: int | None = None
 
 
 # ------------------------------------------------------------------ planning (host)
@@ -325,11 +327,22 @@ def _graph_from_device(nodes, res, st, f0, val) -> None:
 
 def peel_decode(graph: PeelingGraph, mode: str = "exact", eps_zero: float = 0.0,
                 eps_ratio: float = 0.0, search_plan: SearchPlan | None = None,
-                max_rounds: int | None = None) -> DecodeResult:
-    """Synchronous peeling (peeling.py:270-313), whole round loop on the device."""
+                max_rounds: int | None = None, *, decoder: str = "rounds") -> DecodeResult:
+    """Synchronous peeling (peeling.py:270-313), whole round loop on the device.
+
+    ``decoder="tree"`` (keyword-only, an extension; exact mode) runs the paper's Fig. 5
+    tree-walk decoder instead (a non-goal of the reference,
+    SPEC.md:460): paths extended from single-ton check nodes, only the d check nodes of
+    each decoded tone re-identified (afft_peel_tree_exact).  The recovered set is the
+    round decoder's; the insertion order is the walk's; ``rounds`` counts the walk's
+    generations and ``identifications`` the check-node identifications."""
+    if decoder not in ("rounds", "tree"):
+        raise ValueError(f"unknown decoder {decoder!r}")
     if max_rounds is None:
         max_rounds = len(graph.recovered) + 8
     if mode != "exact":
+        if decoder == "tree":
+            raise ValueError("the tree-walk decoder is exact-mode only")
         return peel_decode_noisy(graph, search_plan, max_rounds)
     live = any(
         node.state not in (NodeState.RESOLVED, NodeState.ZERO_TON)
@@ -352,17 +365,29 @@ def peel_decode(graph: PeelingGraph, mode: str = "exact", eps_zero: float = 0.0,
     epsr = torch.tensor([float(eps_ratio)], dtype=torch.float64, device=dev)
     rounds = torch.zeros(1, dtype=torch.int32, device=dev)
     unresolved = torch.zeros(1, dtype=torch.int32, device=dev)
+    ident = torch.zeros(1, dtype=torch.int32, device=dev)
     if nodes:
         fb, nc = _lib.host_i64(graph.factors)
-        _lib.check(
-            _lib.load().afft_peel_exact(
-                graph.n, 1, fb, nc, res.data_ptr(), st.data_ptr(), f0.data_ptr(), val.data_ptr(),
-                eps0.data_ptr(), epsr.data_ptr(), int(max_rounds), rec_pos.data_ptr(),
-                rec_val.data_ptr(), cap, rec_count.data_ptr(), rounds.data_ptr(),
-                unresolved.data_ptr(), _device.stream_ptr(),
-            ),
-            "peel_decode",
-        )
+        if decoder == "tree":
+            _lib.check(
+                _lib.load().afft_peel_tree_exact(
+                    graph.n, 1, fb, nc, res.data_ptr(), st.data_ptr(), f0.data_ptr(),
+                    val.data_ptr(), eps0.data_ptr(), epsr.data_ptr(), rec_pos.data_ptr(),
+                    rec_val.data_ptr(), cap, rec_count.data_ptr(), rounds.data_ptr(),
+                    unresolved.data_ptr(), ident.data_ptr(), _device.stream_ptr(),
+                ),
+                "peel_decode",
+            )
+        else:
+            _lib.check(
+                _lib.load().afft_peel_exact(
+                    graph.n, 1, fb, nc, res.data_ptr(), st.data_ptr(), f0.data_ptr(),
+                    val.data_ptr(), eps0.data_ptr(), epsr.data_ptr(), int(max_rounds),
+                    rec_pos.data_ptr(), rec_val.data_ptr(), cap, rec_count.data_ptr(),
+                    rounds.data_ptr(), unresolved.data_ptr(), _device.stream_ptr(),
+                ),
+                "peel_decode",
+            )
         _graph_from_device(nodes, res, st, f0, val)
     count = int(rec_count.item())
     pos = rec_pos[:count].cpu().numpy()
@@ -372,7 +397,8 @@ def peel_decode(graph: PeelingGraph, mode: str = "exact", eps_zero: float = 0.0,
     n_rounds = int(rounds.item()) if nodes else max(0, min(1, int(max_rounds)))
     spectrum = SparseSpectrum(graph.n, dict(graph.recovered))
     return DecodeResult(spectrum=spectrum, unresolved_multitons=int(unresolved.item()),
-                        rounds=n_rounds)
+                        rounds=n_rounds,
+                        identifications=int(ident.item()) if decoder == "tree" else None)
 
 
 def ffast(x, k: int, ledger: SampleLedger | None = None, max_rounds: int | None = None, *,
