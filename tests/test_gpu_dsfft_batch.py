@@ -53,3 +53,27 @@ def test_lockstep_equals_per_signal_path():
     for i in range(len(xs)):
         assert list(a[i].entries) == list(b[i].entries), i
         assert max(abs(a[i].entries[f] - v) for f, v in b[i].entries.items()) == 0.0
+
+
+def test_lockstep_equals_per_signal_path_c128_mixed():
+    """complex128 input, mixed noise levels and seeds, plus an exact-mode signal (which
+    leaves the lockstep path and is decoded alone): lockstep and per-signal decodes agree
+    entry for entry."""
+    from paper_2011_05749_b200 import DsfftConfig, dsfft_batch, generate_test_case
+
+    n, k = 1 << 20, 256
+    xs, cfgs = [], []
+    for i, snr in enumerate((10.0, 30.0, "exact", 20.0)):
+        seed = 2000 + i
+        xs.append(generate_test_case(n, k, snr, seed).signal)
+        if snr == "exact":
+            cfgs.append(DsfftConfig(mode="exact", seed=seed))
+        else:
+            cfgs.append(DsfftConfig(mode="noisy", seed=seed,
+                                    noise_std=float(np.sqrt(k * 10 ** (-snr / 10)))))
+    xd = torch.from_numpy(np.stack(xs)).cuda()
+    a = dsfft_batch(xd, k, cfgs, lockstep=True, chunk=3)
+    b = dsfft_batch(xd, k, cfgs, lockstep=False)
+    for i in range(len(xs)):
+        assert list(a[i].entries) == list(b[i].entries), i
+        assert max(abs(a[i].entries[f] - v) for f, v in b[i].entries.items()) == 0.0
