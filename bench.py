@@ -587,6 +587,12 @@ def config_dict(world, total=TOTAL_SIGNALS):
     }
 
 
+def dist_ready() -> bool:
+    import torch.distributed as dist
+
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+
+
 def run_e2e(args, dev, x):
     """Same metric through the public API with HOST (pinned) buffers: H2D of every
     step's signals + the decode + D2H of the result slots, all timed.  Per rank; the
@@ -607,6 +613,11 @@ def run_e2e(args, dev, x):
             m //= 2
             print(f"bench: pinned staging failed, e2e with {m} signals per step",
                   file=sys.stderr)
+    if dist_ready():  # every rank stages the same count (the line reports world x m)
+        mt = torch.tensor([m], dtype=torch.int64, device=dev)
+        torch.distributed.all_reduce(mt, op=torch.distributed.ReduceOp.MIN)
+        m = int(mt.item())
+        host = host[:m]  # a view of the pinned block
     host.copy_(x[:m])
     dbuf = torch.empty((m, N_SIG), dtype=torch.complex64, device=dev)
     res = ffast_batch(dbuf.copy_(host, non_blocking=True), K, FACTORS)
