@@ -170,6 +170,8 @@ def _dt3_shift_table_cached(n: int, a_m: int, seed: int):
 
 def _replay(trace_rec, n, config, plan, dt_table, ledger, trace):
     """Ledger records and the Python trace from the native trace records."""
+    if ledger is None and trace is None:
+        return  # nothing to replay (the common batch case: no per-record Python work)
     flat, offs = dt_table
     for kind, depth, a, c in trace_rec:
         b = 1 << depth
