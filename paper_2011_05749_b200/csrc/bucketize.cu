@@ -574,6 +574,191 @@ __global__ void __launch_bounds__(kGfftThreads, 3) gfft_flags_kernel(
   gfft_reg_body<4, 4, true>(p, f);
 }
 
+// ---- Radix-4096 register pass (opt-in, AFFT_FFT_4K=1; slower, see launch_fourstep):
+// a 2^24-point transform in TWO passes (4096 x 4096) instead of three radix-256 ones —
+// 0.9 instead of 1.4 GB of HBM traffic per c64 signal.  One column j per tile (kCnt = 1; the 8-16 B row pieces of neighbouring
+// columns are fetched by the CTAs resident beside it and combine in L2), 256 threads x
+// 16 points, the 4096-point DFT as 16 x 16 x 16 in registers with two shared-memory
+// exchanges:
+//   r = r0 + 16 r1 + 256 r2,  q = q0 + 16 q1 + 256 q2,
+//   stage 1, thread (r0, r1): DFT_16 over r2 -> q0, times w_256^(r1 q0);
+//   stage 2, thread (r0, q0): DFT_16 over r1 -> q1, times w_4096^(r0 (q0 + 16 q1));
+//   stage 3, thread (q0, q1): DFT_16 over r0 -> q2; V[q] to (j - k) 4096 + k + q N_s.
+// Shared layouts (16-B elements): stage 1 -> 2 at r0 + 16 r1 + 256 q0, stage 2 -> 3 at
+// q0 + 17 r0 + 272 q1 (a quarter warp's lanes always hit 8 distinct 16-B bank groups).
+// Internal twiddles w_4096^e = thi[e] (the b = 2^24 table's w_b^(4096 e), exact
+// sincospi values).  With FUSE (the spectrum's last pass, N_s = 4096) thread (q0, q1)
+// holds y[q2] = Y[J + (q1 + 16 q2) n/256], J = j + 4096 q0 < n/256: the alias classes
+// deep_fuse_epilogue expects, bits set by atomicOr into zeroed bitmaps (consecutive J
+// belong to different tiles).
+constexpr int kG4Threads = 256;
+constexpr int kG4Smem = 4352 * 16;
+
+__device__ __forceinline__ void deep_fuse_epilogue_atomic(cd (&y)[16], int64_t J, int qb,
+                                                          int dtop, const DeepFuse& f) {
+  auto level = [&](auto tc) {
+    constexpr int t = decltype(tc)::value, M = 1 << (t - 4);
+    if (t < 8) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) y[m] = cadd(y[m], y[m + M]);
+    }
+    if (t < f.t_lo) return;
+    bool fl[M];
+    unsigned unsure = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const double sq = __fma_rn(y[m].re, y[m].re, y[m].im * y[m].im);
+      fl[m] = sq > f.t2hi[t];
+      if (!fl[m] && !(sq < f.t2lo[t])) unsure |= 1u << m;
+    }
+    if (unsure) {
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        if ((unsure >> m) & 1u) fl[m] = cabs_(y[m]) > f.thr[t];
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {  // bucket r = qb + 16 m: bit J + r 2^dtop
+      if (fl[m]) {
+        const int64_t bit = J + ((int64_t)(qb + 16 * m) << dtop);
+        atomicOr(f.words + f.word_off[t] + (bit >> 5), 1u << (bit & 31));
+      }
+    }
+  };
+  level(std::integral_constant<int, 8>{});
+  level(std::integral_constant<int, 7>{});
+  level(std::integral_constant<int, 6>{});
+  level(std::integral_constant<int, 5>{});
+  level(std::integral_constant<int, 4>{});
+  if (f.vmid) f.vmid[J + ((int64_t)qb << dtop)] = y[0];
+}
+
+template <bool FUSE>
+__device__ __forceinline__ void gfft4k_body(const GStockParams& p, const DeepFuse& f) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cd* S = reinterpret_cast<cd*>(smem_raw);
+  const int tid = threadIdx.x, lo = tid & 15, hi = tid >> 4;
+  const int64_t nb = p.b >> 12;
+  const int64_t ntiles = p.batch * p.nshift * nb;
+  const int64_t tstep = p.b / (p.Ns << 12);
+  const bool first = p.in == nullptr;
+  const bool c64 = first && p.dtype == AFFT_C64;
+  const int64_t esz = p.dtype == AFFT_C64 ? 8 : 16;
+  const double inv_b = 1.0 / (double)p.b;
+  const cd* __restrict__ w4k = p.thi;  // w_4096^e, e < 4096
+  double fsq = 0.0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t j = tile % nb, st_ = tile / nb;
+    const int t = (int)(st_ % p.nshift);
+    const int64_t s = st_ / p.nshift;
+    const int64_t k = j % p.Ns;
+    const int64_t seq = s * p.nshift + t;
+    // ---- stage 1: rows r = lo + 16 hi + 256 m (all 16 loads issued first)
+    cd v[16];
+    if (first) {
+      const char* xs = reinterpret_cast<const char*>(p.x) + s * p.ld * esz;
+      const int64_t tau = p.shift_table ? pymod(p.shift_table[s * p.nshift + t], p.n) : p.tau[t];
+      if (c64) {
+        float2 raw[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          int64_t idx = (j + (int64_t)(lo + 16 * hi + 256 * m) * nb) * p.L - tau;
+          if (idx < 0) idx += p.n;
+          raw[m] = __ldg(reinterpret_cast<const float2*>(xs) + idx);
+        }
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v[m] = cd{(double)raw[m].x, (double)raw[m].y};
+      } else {
+        double2 raw[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          int64_t idx = (j + (int64_t)(lo + 16 * hi + 256 * m) * nb) * p.L - tau;
+          if (idx < 0) idx += p.n;
+          raw[m] = __ldcs(reinterpret_cast<const double2*>(xs) + idx);
+        }
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v[m] = cd{raw[m].x, raw[m].y};
+      }
+    } else {
+      const double2* base = reinterpret_cast<const double2*>(p.in + seq * p.b);
+      double2 raw[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) raw[m] = __ldcs(base + j + (int64_t)(lo + 16 * hi + 256 * m) * nb);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) v[m] = cd{raw[m].x, raw[m].y};
+    }
+    if (p.Ns > 1) {  // w_b^(k r tstep), r = lo + 16 hi + 256 m
+      const int64_t kt = k * tstep;
+      if (kt) {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const int64_t r = lo + 16 * hi + 256 * m;
+          if (r) v[m] = cmul(v[m], tw_b(p.tlo, p.thi, kt * r));
+        }
+      }
+    }
+    dft_reg<16>(v);
+    __syncthreads();  // the previous tile's stage 3 has finished reading S
+#pragma unroll
+    for (int q0 = 0; q0 < 16; ++q0)
+      S[lo + 16 * hi + 256 * q0] = (hi && q0) ? cmul(v[q0], w4k[16 * hi * q0]) : v[q0];
+    __syncthreads();
+    // ---- stage 2: thread (r0 = lo, q0 = hi)
+#pragma unroll
+    for (int r1 = 0; r1 < 16; ++r1) v[r1] = S[lo + 16 * r1 + 256 * hi];
+    __syncthreads();  // S is rewritten below
+    dft_reg<16>(v);
+#pragma unroll
+    for (int q1 = 0; q1 < 16; ++q1) {
+      const int e = lo * (hi + 16 * q1);
+      S[hi + 17 * lo + 272 * q1] = e ? cmul(v[q1], w4k[e]) : v[q1];
+    }
+    __syncthreads();
+    // ---- stage 3: thread (q0 = lo, q1 = hi)
+#pragma unroll
+    for (int r0 = 0; r0 < 16; ++r0) v[r0] = S[lo + 17 * r0 + 272 * hi];
+    dft_reg<16>(v);
+    double* out = p.out ? p.out + 2 * (s * p.out_signal_stride + p.out_offset +
+                                       t * p.out_shift_stride)
+                        : nullptr;
+    cd* tmp = p.tmp ? p.tmp + seq * p.b : nullptr;
+    const int64_t base = (j - k) * 4096 + k;
+#pragma unroll
+    for (int q2 = 0; q2 < 16; ++q2) {
+      const int64_t dst = base + (int64_t)(lo + 16 * hi + 256 * q2) * p.Ns;
+      if (tmp) {
+        __stcs(reinterpret_cast<double2*>(tmp + dst), make_double2(v[q2].re, v[q2].im));
+      } else {
+        const cd wv = cscale(v[q2], inv_b);
+        *reinterpret_cast<double2*>(out + 2 * dst * p.out_bin_stride) = make_double2(wv.re, wv.im);
+        if constexpr (FUSE) {
+          v[q2] = wv;
+          fsq += wv.re * wv.re + wv.im * wv.im;
+        }
+      }
+    }
+    if constexpr (FUSE) {
+      // N_s = 4096 = n / 4096: Y[j + 4096 (q0 + 16 q1) + 2^20 q2], dtop = log2 n - 8
+      const int dtop = 63 - __clzll((unsigned long long)p.b) - 8;
+      deep_fuse_epilogue_atomic(v, j + ((int64_t)lo << 12), hi, dtop, f);
+    }
+  }
+  if constexpr (FUSE) {
+    if (f.norm2) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) fsq += __shfl_xor_sync(0xffffffffu, fsq, o);
+      if ((tid & 31) == 0) atomicAdd(f.norm2, fsq);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kG4Threads, 2) gfft4k_kernel(const __grid_constant__ GStockParams p) {
+  gfft4k_body<false>(p, DeepFuse{});
+}
+__global__ void __launch_bounds__(kG4Threads, 2) gfft4k_flags_kernel(
+    const __grid_constant__ GStockParams p, const __grid_constant__ DeepFuse f) {
+  gfft4k_body<true>(p, f);
+}
+
 // ---- the same pass with its row loads on the TMA engine (bulk async copies into a
 // double-buffered shared-memory stage, completion on an mbarrier): a persistent CTA
 // issues tile k+1's R row segments before computing tile k, so loads overlap the
@@ -927,8 +1112,21 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     set_error("bucket count %lld has a prime factor above %d", (long long)b, AFFT_MAX_SMEM_DFT);
     return AFFT_EUNSUPPORTED;
   }
-  // the fused epilogue needs a register-resident radix-256 last pass over full tiles
-  if (fuse && (radices.size() < 2 || radices.back() != 256 || (b / 256) % (kGStockPoints / 256) ||
+  // 2^24 points: two radix-4096 passes (gfft4k_kernel) with AFFT_FFT_4K=1 (opt-in:
+  // measured 0.79 / 0.84 ms against 0.34 ms for the three radix-256 passes on a c64 /
+  // c128 2^24 transform, tools/k4_check.py — one-column tiles make 8-16 B row pieces,
+  // and a copy of that shape alone runs at 1.6-3.3 TB/s, tools/col_bw.cu; two columns
+  // would need 139 KB of shared memory per tile)
+  static const bool fft4k_env = [] {
+    const char* v = getenv("AFFT_FFT_4K");
+    return v && v[0] == '1';
+  }();
+  const bool use4k = b == (int64_t(1) << 24) && fft4k_env && !fft_smem_path();
+  if (use4k) radices.assign({4096, 4096});
+  // the fused epilogue needs a register-resident radix-256 (or radix-4096) last pass over
+  // full tiles
+  if (fuse && ((!use4k && (radices.size() < 2 || radices.back() != 256 ||
+                           (b / 256) % (kGStockPoints / 256))) ||
                fft_smem_path() || batch != 1 || nshift != 1 || obin != 1)) {
     set_error("spectrum_fused: plan without a radix-256 register last pass");
     return AFFT_EUNSUPPORTED;
@@ -994,6 +1192,38 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     g.R = R;
     g.Ns = Ns;
     g.cnt = std::max(1, kGStockPoints / R);
+    g.in = s == 0 ? nullptr : bufs[(s - 1) & 1];
+    g.tmp = s == P - 1 ? nullptr : bufs[s & 1];
+    g.out = s == P - 1 ? out : nullptr;
+    if (use4k) {
+      const bool fz = fuse && s == P - 1;
+      const void* k4 = fz ? (const void*)gfft4k_flags_kernel : (const void*)gfft4k_kernel;
+      if (fz) {  // the radix-4096 epilogue ORs its bits in: zero the fused depths' bitmaps
+        const int dtop = 63 - __builtin_clzll((unsigned long long)b) - 8;
+        for (int t = fuse->t_lo; t <= 8 && e == cudaSuccess; ++t)
+          e = cudaMemsetAsync(fuse->words + fuse->word_off[t], 0, (size_t)1 << (dtop + t - 3),
+                              stream);
+      }
+      if (e == cudaSuccess) e = ensure_smem(k4, kG4Smem);
+      int occ = 0;
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4, kG4Threads, kG4Smem);
+      if (e != cudaSuccess || occ < 1) {
+        rc = cuda_status(e != cudaSuccess ? e : cudaErrorInvalidConfiguration, "radix-4096 pass");
+        break;
+      }
+      const int64_t tiles = (int64_t)seqs * (b >> 12);
+      const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * occ);
+      DeepFuse fz_arg = fz ? *fuse : DeepFuse{};
+      void* args4[] = {&g, &fz_arg};
+      e = cudaLaunchKernel(k4, dim3(grid), dim3(kG4Threads), args4, kG4Smem, stream);
+      if (e != cudaSuccess) {
+        rc = cuda_status(e, "radix-4096 launch");
+        break;
+      }
+      Ns *= R;
+      continue;
+    }
     if (!make_dft_plan(R, &g.plan)) {
       rc = AFFT_EUNSUPPORTED;
       set_error("cannot plan a DFT of size %d", R);

@@ -198,7 +198,7 @@ def dsfft_device(xd: torch.Tensor, k: int, config: DsfftConfig,
     """dsfft body (dsfft.py:250-266) for one device signal; returns the entries dict
     in the reference's insertion order (see _dsfft_arrays)."""
     pos, val = _dsfft_arrays(xd, k, config, ledger, trace)
-    return dict(zip(pos.tolist(), val.tolist()))
+    return _lib.entries_dict(pos, val)
 
 
 def _dsfft_arrays(xd: torch.Tensor, k: int, config: DsfftConfig,
@@ -346,7 +346,7 @@ def _top_k(n: int, k: int, pos, val) -> SparseSpectrum:
                                               int(k), op.ctypes.data, ov.ctypes.data,
                                               ctypes.byref(cnt)), "truncate")
     m = int(cnt.value)
-    return SparseSpectrum._trusted(n, dict(zip(op[:m].tolist(), ov[:m].tolist())))
+    return SparseSpectrum._trusted(n, _lib.entries_dict(op[:m], ov[:m]))
 
 
 def dsfft_batch(xs, k: int, configs, streams: int = 8, lockstep: bool = False,
