@@ -181,6 +181,25 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
 }
 
+// Sequence stride of the staged tiles: R odd -> R, even -> R + 1 (column-wise transposes
+// hit distinct banks), except when R has an odd prime factor p >= 11 with fewer than 8
+// butterflies per sequence in that stage (nbp = R / p): then ld = nbp (mod 8), so the
+// symmetric stage's lanes (consecutive butterflies (seq, j), address seq ld + j + r nbp)
+// read 8 distinct 16-byte bank groups per quarter warp.
+__host__ __device__ inline int gstock_ld(int R) {
+  int m = R, big = 1;
+  for (int q = 2; q * q <= m; ++q)
+    while (m % q == 0) {
+      if (q > big) big = q;
+      m /= q;
+    }
+  if (m > big) big = m;
+  const int nbp = R / big;
+  if (big >= 11 && (big & 1) && nbp < 8) return R + (((nbp - R) % 8) + 8) % 8;
+  return (R & 1) ? R : R + 1;
+}
+
+
 // One pass.  The tile's rows arrive by cp.async into a staging copy (every request
 // in flight at once, no registers held), a second smem pass applies the inter-pass
 // twiddles while transposing into sequences of stride ld = R + 1 (bank-conflict
@@ -199,7 +218,7 @@ __global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
   constexpr int kCnt = kFixed ? kGStockPoints / kR : 1;
   constexpr int kLgCnt = kFixed ? 11 - LGR : 0;  // kGStockPoints = 2^11
   const int R = kFixed ? kR : p.R, cnt = kFixed ? kCnt : p.cnt;
-  const int ld = (R & 1) ? R : R + 1;
+  const int ld = kFixed ? ((R & 1) ? R : R + 1) : gstock_ld(R);
   const int tid = threadIdx.x, nt = blockDim.x;
   cd* tw = reinterpret_cast<cd*>(smem_raw);
   cd* bufA = tw + R;
@@ -1232,7 +1251,7 @@ static int launch_fourstep(const void* x, int dtype, int64_t n, int64_t batch, i
     g.in = s == 0 ? nullptr : bufs[(s - 1) & 1];
     g.tmp = s == P - 1 ? nullptr : bufs[s & 1];
     g.out = s == P - 1 ? out : nullptr;
-    const int ldR = (R & 1) ? R : R + 1;
+    const int ldR = std::max((R & 1) ? R : R + 1, gstock_ld(R));
     // compile-time shape for power-of-two radices whose tiles are always full
     int lgr = -1;
     if ((R & (R - 1)) == 0 && R >= 2 && R <= 256 && (b / R) % (kGStockPoints / R) == 0) {

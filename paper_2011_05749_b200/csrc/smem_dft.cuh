@@ -404,9 +404,15 @@ __device__ inline cd* smem_dft(cd* a, cd* b, int count, const DftPlan& p, const 
           __syncthreads();
           const int hq = ((R - 1) >> 1) / kSymQ + 1;  // groups of kSymQ q's over 0..h
           const int outs = total * hq;
+          // butterflies along the lanes, q group per warp: the twiddle reads tw[e wstep]
+          // (e = q r mod R, the same for every lane) broadcast and the s_r / d_r reads
+          // walk consecutive butterflies.  (Groups along the lanes made the twiddle reads
+          // a gather with up to 8-way bank conflicts: 58% of the shared-memory wavefronts
+          // of the radix-254 pass of N = 2,097,024, profiles/r02_gstockham_ncu.md.)
+          // Each output's arithmetic is unchanged (same sym_out), so results are too.
           for (int w = tid; w < outs; w += nthreads) {
-            const int bw = w / hq;
-            const int g = w - bw * hq;
+            const int g = w / total;
+            const int bw = w - g * total;
             const int seq = bw / nb, j = bw - seq * nb;
             sym_out(a + (size_t)seq * ld, b + (size_t)seq * ld, tw, n, R, nb, Ns, j, g * kSymQ);
           }
