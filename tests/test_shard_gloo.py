@@ -106,3 +106,56 @@ def test_search_shard_exchange_world2():
         assert (r2, w2) == (rank, 2)
         assert scores == [0.5 * i + 0.25 for i in range(7)]
         assert cands == [100 + i for i in range(7)]
+
+
+def _sharded_worker(rank, world, port, q):
+    from paper_2011_05749_b200.shard import sharded_batch, spectra_to_slots
+    from paper_2011_05749_b200 import SparseSpectrum
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    for total in (5, 6, 1):  # ragged slices, equal slices, fewer signals than ranks
+        calls = []
+
+        def decode(a, b, k=3):
+            calls.append((a, b))
+            # the stand-in decoder: signal i "recovers" i % 3 + 1 tones at 10 i + j
+            sp = [SparseSpectrum(1000, {10 * i + j: complex(i, -j) for j in range(i % 3 + 1)})
+                  for i in range(a, b)]
+            return spectra_to_slots(sp, k)
+
+        gp, gv, gc = sharded_batch(decode, total)
+        out[total] = (calls, gp.tolist(), gv.real.tolist(), gv.imag.tolist(), gc.tolist())
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_sharded_batch_world2():
+    """The C2/C3/C4 signal-sharded harness: every rank decodes only its slice and ends
+    with all signals' slots in signal order, ragged slices included."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out in res:
+        for total, (calls, gp, gre, gim, gc) in out.items():
+            assert calls == [shard_range(total, rank, 2)]
+            assert gc == [i % 3 + 1 for i in range(total)]
+            for i in range(total):
+                m = gc[i]
+                assert gp[i][:m] == [10 * i + j for j in range(m)]
+                assert gre[i][:m] == [float(i)] * m
+                assert gim[i][:m] == [-float(j) for j in range(m)]
+
+
+def test_sharded_batch_without_a_group():
+    from paper_2011_05749_b200.shard import sharded_batch
+
+    assert sharded_batch(lambda a, b: (a, b, None), 7) == (0, 7, None)
