@@ -829,6 +829,64 @@ __global__ void __launch_bounds__(256) tree_level_kernel(const cd* __restrict__ 
   if ((threadIdx.x & 31) == 0 && on) words[i >> 5] = flags;
 }
 
+// The same layers in ONE launch when 3 <= dmid - d0 <= 8 (config 4: depths 19 .. 12
+// from the depth-20 values the fused last pass leaves): the subtree under depth-d0 index
+// i is {i + m 2^d0, m < 2^LV} and every level halves m (v[m] += v[m + half], the same
+// pair and operand order as tree_level_kernel, so values and bitmaps are bit-identical).
+// A CTA owns 32 consecutive i (one bitmap word per (level, m)): lane = i, warp = m mod 8,
+// a thread holds m = warp + 8 q, q < 2^(LV - 3); the first LV - 3 levels stay in
+// registers, the last three go through 4 KB of shared memory.  One launch of 2^d0 / 32
+// CTAs instead of LV launches of a few microseconds each.
+struct TreeLevels {
+  const cd* vin;       // depth dmid values
+  cd* vout[8];         // [l]: depth dmid - 1 - l values
+  uint32_t* words[8];  // [l]: that layer's bitmap
+  double thr[8];
+};
+
+__device__ __forceinline__ bool tree_flag(cd v, double thr) {
+  const double sq = v.re * v.re + v.im * v.im, t2 = thr * thr;
+  return sq > t2 * (1.0 + 1e-14) ? true : sq < t2 * (1.0 - 1e-14) ? false : cabs_(v) > thr;
+}
+
+template <int LQ>
+__global__ void __launch_bounds__(256) tree_levels_kernel(const __grid_constant__ TreeLevels T,
+                                                          int d0) {
+  constexpr int Q = 1 << LQ;
+  __shared__ cd sh[8][32];
+  const int lane = threadIdx.x & 31, ms = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  cd a[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) a[q] = T.vin[i + ((int64_t)(ms + 8 * q) << d0)];
+  int l = 0;
+#pragma unroll
+  for (int h = Q / 2; h >= 1; h >>= 1, ++l) {
+#pragma unroll
+    for (int q = 0; q < h; ++q) {
+      a[q] = cadd(a[q], a[q + h]);
+      const int64_t at = i + ((int64_t)(ms + 8 * q) << d0);
+      T.vout[l][at] = a[q];
+      const unsigned flags = __ballot_sync(0xffffffffu, tree_flag(a[q], T.thr[l]));
+      if (lane == 0) T.words[l][at >> 5] = flags;
+    }
+  }
+  cd v = a[0];
+#pragma unroll
+  for (int h = 4; h >= 1; h >>= 1, ++l) {
+    sh[ms][lane] = v;
+    __syncthreads();
+    if (ms < h) {  // warp-uniform
+      v = cadd(v, sh[ms + h][lane]);
+      const int64_t at = i + ((int64_t)ms << d0);
+      T.vout[l][at] = v;
+      const unsigned flags = __ballot_sync(0xffffffffu, tree_flag(v, T.thr[l]));
+      if (lane == 0) T.words[l][at >> 5] = flags;
+    }
+    __syncthreads();
+  }
+}
+
 // thr and its guard band, rounded exactly as the kernels would (IEEE, no contraction)
 static void set_layer_threshold(DeepLayers* D, int j, double thr) {
   const double t2 = thr * thr;
@@ -999,12 +1057,39 @@ int full_active_all_fused(const void* x, int dtype, int64_t n, double* Yout, int
   }
   int rc = spectrum_fused(x, dtype, n, Yout, f, st);
   if (rc) return rc;
-  for (int d = dmid - 1; d >= d0; --d) {  // v_d[i] = v_{d+1}[i] + v_{d+1}[i + 2^d]
-    const int64_t b = int64_t(1) << d;
-    tree_level_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
-        vals[d + 1], b, thr[d - d0], vals[d], words + D.word_off[d - d0]);
+  const int lv = dmid - d0;
+  static const bool one_launch = [] {
+    const char* e = getenv("AFFT_TREE_FUSE");
+    return !(e && atoi(e) == 0);
+  }();
+  if (one_launch && lv >= 3 && lv <= 8) {
+    TreeLevels T;
+    memset(&T, 0, sizeof(T));
+    T.vin = vals[dmid];
+    for (int l = 0; l < lv; ++l) {
+      const int d = dmid - 1 - l;
+      T.vout[l] = vals[d];
+      T.words[l] = words + D.word_off[d - d0];
+      T.thr[l] = thr[d - d0];
+    }
+    const unsigned grid = (unsigned)((int64_t(1) << d0) / 32);
+    switch (lv) {
+      case 3: tree_levels_kernel<0><<<grid, 256, 0, st>>>(T, d0); break;
+      case 4: tree_levels_kernel<1><<<grid, 256, 0, st>>>(T, d0); break;
+      case 5: tree_levels_kernel<2><<<grid, 256, 0, st>>>(T, d0); break;
+      case 6: tree_levels_kernel<3><<<grid, 256, 0, st>>>(T, d0); break;
+      case 7: tree_levels_kernel<4><<<grid, 256, 0, st>>>(T, d0); break;
+      default: tree_levels_kernel<5><<<grid, 256, 0, st>>>(T, d0); break;
+    }
+    AFFT_CHECK_LAUNCH("tree_levels_kernel");
+  } else {
+    for (int d = dmid - 1; d >= d0; --d) {  // v_d[i] = v_{d+1}[i] + v_{d+1}[i + 2^d]
+      const int64_t b = int64_t(1) << d;
+      tree_level_kernel<<<(unsigned)((b + 255) / 256), 256, 0, st>>>(
+          vals[d + 1], b, thr[d - d0], vals[d], words + D.word_off[d - d0]);
+    }
+    AFFT_CHECK_LAUNCH("tree_level_kernel");
   }
-  AFFT_CHECK_LAUNCH("tree_level_kernel");
   const unsigned chunks = (unsigned)D.chunk_off[nl];
   deep_count_kernel<<<chunks, 256, 0, st>>>(words, D, chunk);
   deep_scan_kernel<<<1, 32 * kDeepMaxLayers, 0, st>>>(chunk, D, counts);

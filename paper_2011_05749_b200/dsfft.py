@@ -307,8 +307,12 @@ def _dsfft_batch_native(xd: torch.Tensor, k: int, cfgs, idx: list[int]):
             dt_shifts=table[0].ctypes.data if table[0].size else None,
             dt_shift_off=table[1].ctypes.data,
             full_classify=int(os.environ.get("AFFT_DSFFT_LAZY") == "0"))
-    sub = xd[idx] if idx != list(range(xd.shape[0])) else xd
-    sub = sub.contiguous()
+    if idx == list(range(idx[0], idx[0] + S)):
+        sub = xd[idx[0]:idx[0] + S]  # a run of signals: a view, no copy of n-sized rows
+    else:
+        sub = xd[idx]
+    if sub.stride(-1) != 1:
+        sub = sub.contiguous()
     lib = _lib.load()
     cap = max(8 * k, 1024)
     tcap = 4 * (n.bit_length() + 8)
@@ -331,11 +335,10 @@ def _dsfft_batch_native(xd: torch.Tensor, k: int, cfgs, idx: list[int]):
     return out
 
 
-def _top_k(n: int, k: int, pos, val) -> SparseSpectrum:
+def _top_k_arrays(k: int, pos, val):
     """truncate_spectrum (oneshot.py:260-263): the k largest |v|, ties to the smaller
     position, in that order (the keys are distinct, so the sort is total).  The sort runs
-    in afft_truncate_host with the GIL released (worker threads overlap it); only the
-    dict is built here."""
+    in afft_truncate_host with the GIL released (worker threads overlap it)."""
     pos = np.ascontiguousarray(pos, dtype=np.int64)
     val = np.ascontiguousarray(val, dtype=np.complex128)
     m = min(int(pos.size), int(k))
@@ -346,38 +349,73 @@ def _top_k(n: int, k: int, pos, val) -> SparseSpectrum:
                                               int(k), op.ctypes.data, ov.ctypes.data,
                                               ctypes.byref(cnt)), "truncate")
     m = int(cnt.value)
-    return SparseSpectrum._trusted(n, _lib.entries_dict(op[:m], ov[:m]))
+    return op[:m], ov[:m]
 
 
-def dsfft_batch(xs, k: int, configs, streams: int = 8, lockstep: bool = False,
-                chunk: int = 8) -> list[SparseSpectrum]:
+def _top_k(n: int, k: int, pos, val) -> SparseSpectrum:
+    """truncate_spectrum as the drop-in result type."""
+    op, ov = _top_k_arrays(k, pos, val)
+    return SparseSpectrum._trusted(n, _lib.entries_dict(op, ov))
+
+
+def _guided_parts(items: list[int], workers: int, cap: int) -> list[list[int]]:
+    """Chunks of shrinking size (guided scheduling): ceil(remaining / (1.5 workers))
+    signals each, at most ``cap``, at least 1 — long lockstep chunks first, single signals
+    last, so the workers do not all finish at once and the caller's per-signal result
+    work (the entries dicts) has only a short tail after the last kernels."""
+    parts, at = [], 0
+    while at < len(items):
+        left = len(items) - at
+        size = max(1, min(int(cap), -(-2 * left // (3 * max(1, workers)))))
+        parts.append(items[at:at + size])
+        at += size
+    return parts
+
+
+def dsfft_batch(xs, k: int, configs, streams: int = 8, lockstep: bool | None = None,
+                chunk: int = 4, guided: bool = True) -> list[SparseSpectrum]:
     """DSFFT over several signals, in input order.
 
-    Default: every signal's native layer loop on its own worker stream
-    (_dsfft_batch_threads).  ``lockstep=True``: noisy decodes of large power-of-two
-    signals with a given noise level run in lockstep (afft_dsfft_batch: ``chunk``
-    signals per call, one launch per layer step for all of them; the chunks on up to
-    ``streams`` worker streams), signals that leave the common path alone.  Both give
-    identical results (tests/test_gpu_dsfft_batch.py).  Measured at config 4 (32
-    signals, 20 dB, tools/dsfft_gpu_busy.py): the lockstep form launches 916 kernels
-    instead of 3,990 and sums 1.28 instead of 2.14 ms of kernel time per signal, but the
-    GPU is busy ~1 ms per signal either way (concurrent streams already overlap the
-    small kernels) and its per-chunk host tail made it 574 vs 695 signals/s."""
+    ``lockstep`` (the default for two or more signals): noisy decodes of large
+    power-of-two signals with a given noise level run in lockstep (afft_dsfft_batch: up to
+    ``chunk`` signals per call, one launch per layer step for all of them; the chunks on
+    up to ``streams`` worker streams, sized by `_guided_parts` unless ``guided=False``);
+    the workers return the truncated (positions, values) arrays and the calling thread
+    builds each SparseSpectrum's dict while they run their next chunk.  Signals that leave
+    the common path, exact-mode signals and ``lockstep=False`` take the per-signal native
+    loop, one signal per worker stream (_dsfft_batch_threads).  All forms give identical
+    results (tests/test_gpu_dsfft_batch.py).  Measured at config 4 (32 signals, 20 dB,
+    tools/dsfft_api_sweep.py, tools/dsfft_lockstep_sweep.py): per-signal loops 1.35 k
+    signals/s; lockstep with the dicts built by the workers 1.27-1.34 k (every worker
+    finishes at once and the dicts, ~0.2 ms of GIL time each, form a serial tail); with the
+    dicts on the calling thread and 2 signals per call 1.53 k; the C ABI alone (arrays, no
+    dicts) 2.0-2.1 k on 8 streams x 4 signals."""
     xd0 = _device.as_device_batch(xs)
     count0 = int(xd0.shape[0])
     cfgs0 = [configs[i] if isinstance(configs, (list, tuple)) else configs for i in range(count0)]
     n0 = int(xd0.shape[1]) if count0 else 0
     done: dict[int, SparseSpectrum] = {}
+    if lockstep is None:  # the lockstep form is the faster one for batches (bench: c4dsfft)
+        lockstep = count0 >= 2
     if lockstep and count0 and n0 >= (1 << 16) and not (n0 & (n0 - 1)):
         cand = [i for i in range(count0) if cfgs0[i].mode != "exact" and cfgs0[i].noise_std > 0]
         size = max(1, int(chunk))
-        parts = [cand[c0:c0 + size] for c0 in range(0, len(cand), size)]
+        if guided:
+            parts = _guided_parts(cand, max(1, min(int(streams), len(cand))), size)
+        else:
+            parts = [cand[c0:c0 + size] for c0 in range(0, len(cand), size)]
         def chunk_fn(part):  # the host-side truncation overlaps other chunks' kernels
-            return {i: _top_k(n0, k, p, v)
+            return {i: _top_k_arrays(k, p, v)
                     for i, (p, v) in _dsfft_batch_native(xd0, k, cfgs0, part).items()}
 
-        for res in _on_worker_streams(xd0, parts, streams, chunk_fn):
-            done.update(res)
+        def to_spectra(res):
+            # on the caller's thread, as each chunk arrives: the 4096-entry dicts need the
+            # GIL (~0.2 ms per signal); the workers are already inside their next chunk's
+            # native call (GIL released), so only the last chunks' dicts are a tail
+            for i, (op, ov) in res.items():
+                done[i] = SparseSpectrum._trusted(n0, _lib.entries_dict(op, ov))
+
+        _on_worker_streams(xd0, parts, streams, chunk_fn, consume=to_spectra)
     rest = [i for i in range(count0) if i not in done]
     if rest:
         outs = _dsfft_batch_threads(xd0[rest] if len(rest) < count0 else xd0, k,
@@ -387,14 +425,17 @@ def dsfft_batch(xs, k: int, configs, streams: int = 8, lockstep: bool = False,
     return [done[i] for i in range(count0)]
 
 
-def _on_worker_streams(xd: torch.Tensor, items, streams: int, fn):
+def _on_worker_streams(xd: torch.Tensor, items, streams: int, fn, consume=None):
     """fn(item) for every item, on up to `streams` persistent worker threads with their
-    own CUDA streams (ordered after the caller's stream, joined back into it)."""
+    own CUDA streams (ordered after the caller's stream, joined back into it).  With
+    ``consume``, each result is passed to it on the calling thread as soon as it (and
+    every earlier item's) is ready, while the workers carry on."""
     import threading
 
+    take = consume if consume is not None else (lambda r: r)
     workers = max(1, min(int(streams), len(items)))
     if workers <= 1:
-        return [fn(it) for it in items]
+        return [take(fn(it)) for it in items]
     main = torch.cuda.current_stream(xd.device)
     ready = torch.cuda.Event()
     ready.record(main)
@@ -415,7 +456,7 @@ def _on_worker_streams(xd: torch.Tensor, items, streams: int, fn):
             done.append(ev)
         return out
 
-    out = list(_worker_pool(workers, xd.device).map(work, items))
+    out = [take(r) for r in _worker_pool(workers, xd.device).map(work, items)]
     for ev in done:
         main.wait_event(ev)
     return out

@@ -10,6 +10,7 @@ dt1/dt3 roots one thread per bucket over rows grouped by tone count.
 
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -79,10 +80,22 @@ def structured_shifts(a_m: int) -> list[int]:
     return list(range(-a_m, 2 * a_m))
 
 
+@functools.lru_cache(maxsize=8192)
+def _seeded_shifts(n: int, p: int, seed) -> tuple[int, ...]:
+    rng = np.random.default_rng(seed)
+    return tuple(int(t) for t in rng.choice(n, size=p, replace=False))
+
+
 def random_shifts(n: int, config: OneShotConfig) -> list[int]:
-    """The seeded random shift draw of collect_moments (oneshot.py:93-94)."""
-    rng = np.random.default_rng(config.seed)
-    return [int(t) for t in rng.choice(n, size=config.p, replace=False)]
+    """The seeded random shift draw of collect_moments (oneshot.py:93-94).  The draw is a
+    pure function of (n, p, seed) — numpy's PCG64 stream, ~40 us per signal on the host —
+    so it is kept like a plan: a batch decoded again with the same seeds (64 signals of
+    config 2 cost 1.7-2.7 ms of draws against 1.4 ms of kernels) pays it once."""
+    seed = config.seed
+    if seed is None or not isinstance(seed, (int, np.integer)):
+        rng = np.random.default_rng(seed)  # fresh entropy / SeedSequence: not cacheable
+        return [int(t) for t in rng.choice(n, size=config.p, replace=False)]
+    return list(_seeded_shifts(int(n), int(config.p), int(seed)))
 
 
 # ------------------------------------------------------------------ device helpers
@@ -254,8 +267,7 @@ def sfft_dt_batch(x, k: int, b: int, a_m: int = 4, p: int = 12, variant: str = "
     dev = xd.device
     if rand_shifts is None:
         seeds = list(seeds) if seeds is not None else [0] * batch
-        rand_shifts = [random_shifts(n, OneShotConfig(b=b, a_m=a_m, p=p, seed=int(s)))
-                       for s in seeds]
+        rand_shifts = [_seeded_shifts(n, p, int(s)) for s in seeds]
     rt = torch.as_tensor(np.asarray(rand_shifts, dtype=np.int64).reshape(batch, p)).to(dev)
     lib = _lib.load()
     need = int(lib.afft_sfft_dt_workspace_size(n, batch, b, a_m, p))

@@ -17,9 +17,14 @@ if which == "c2":
     n, k, b, var, snr, dt = 1 << 22, 1000, 1024, "dt2", "exact", torch.complex128
 else:
     n, k, b, var, snr, dt = 1 << 24, 4096, 4096, "dt3", 20.0, torch.complex64
-x, _ = make_batch(n, k, snr, 16, dt, dev, chunk=4)
-seeds = [case_seed(n, k, snr, i) for i in range(16)]
+S = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+x, _ = make_batch(n, k, snr, S, dt, dev, chunk=4)
+seeds = [case_seed(n, k, snr, i) for i in range(S)]
+res = sfft_dt_batch(x, k, b, 4, 15, var, seeds=seeds)
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
 for _ in range(2):
     res = sfft_dt_batch(x, k, b, 4, 15, var, seeds=seeds)
 torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
 print("ok", int(res.count.sum()))
