@@ -77,3 +77,31 @@ def test_sparse_spectrum_and_evaluate():
     m = evaluate(a, b)
     assert m.l0 == 1 and abs(m.l1 - 1.05) < 1e-12
     assert np.array_equal(a.to_dense()[[1, 3]], [1.0, 1j])
+
+
+def test_seeded_shift_draws_are_the_reference_stream():
+    """collect_moments' random shifts (oneshot.py:93-94) are kept per (n, p, seed): the
+    kept value is numpy's own draw, a repeat is the same list, and the caller's copy is
+    not the cached object."""
+    from paper_2011_05749_b200.oneshot import OneShotConfig, random_shifts
+
+    for n, p, seed in ((1 << 22, 15, 7), (4096, 12, 0), (1 << 24, 15, 123456789)):
+        cfg = OneShotConfig(b=64, a_m=4, p=p, variant="dt3", seed=seed)
+        want = [int(t) for t in np.random.default_rng(seed).choice(n, size=p, replace=False)]
+        got = random_shifts(n, cfg)
+        assert got == want
+        got.append(-1)  # the caller may edit its list
+        assert random_shifts(n, cfg) == want
+
+
+def test_guided_parts_cover_the_batch_in_order():
+    from paper_2011_05749_b200.dsfft import _guided_parts
+
+    for count in (0, 1, 5, 32, 96, 97):
+        for workers in (1, 3, 8):
+            for cap in (1, 4, 8):
+                parts = _guided_parts(list(range(count)), workers, cap)
+                assert sum(parts, []) == list(range(count))
+                sizes = [len(p) for p in parts]
+                assert all(1 <= s <= cap for s in sizes)
+                assert sizes == sorted(sizes, reverse=True)  # long chunks first
