@@ -911,20 +911,20 @@ def run_configs(dev, args):
         cfgs = [DsfftConfig(mode="noisy", seed=s, noise_std=float(np.sqrt(k * 10 ** (-snr / 10))))
                 for s in seeds]
         outs = dsfft_batch(x, k, cfgs)
-        ds_ms[snr] = _timed(lambda: dsfft_batch(x, k, cfgs), max(1, reps // 2))
+        ds_ms[snr] = _timed(lambda: dsfft_batch(x, k, cfgs), reps)
         ds_rec[snr] = _recall([np.array(list(o.entries)) for o in outs], tr)
         # the C ABI in lockstep (afft_dsfft_batch: entries as arrays, no Python dicts)
         nat = _dsfft_batch_native(x, k, cfgs, list(range(S)))
         ds_nat_fb[snr] = S - len(nat)
         ds_nat_ms[snr] = _timed(lambda: _dsfft_batch_native(x, k, cfgs, list(range(S))),
-                                max(1, reps // 2))
+                                reps)
         # the same C ABI call on 8 worker streams x 4 signals (one group's read-backs and
         # small kernels overlap another's spectrum passes; tools/dsfft_lockstep_sweep.py)
         parts = [list(range(c0, min(S, c0 + 4))) for c0 in range(0, S, 4)]
         ds_nat4_ms[snr] = _timed(
             lambda: _on_worker_streams(x, parts, 8,
                                        lambda part: _dsfft_batch_native(x, k, cfgs, part)),
-            max(1, reps // 2))
+            reps)
         del x, res
         torch.cuda.empty_cache()
     tot_dt = sum(dt_ms.values())
