@@ -209,8 +209,11 @@ __host__ __device__ inline int gstock_ld(int R) {
 // full), so index splits are shifts, loops have constant trip counts and the DFT
 // stages are dft_fixed — the runtime-shaped variant (LGR = -1) spent ~80% of its
 // instructions on integer index math and control flow (ncu SASS mix).
+#ifndef AFFT_GSTOCK_RT_CTAS
+#define AFFT_GSTOCK_RT_CTAS 3
+#endif
 template <int LGR>
-__global__ void __launch_bounds__(kGStockThreads, 3) gstockham_kernel(
+__global__ void __launch_bounds__(kGStockThreads, LGR < 0 ? AFFT_GSTOCK_RT_CTAS : 3) gstockham_kernel(
     const __grid_constant__ GStockParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr bool kFixed = LGR >= 0;

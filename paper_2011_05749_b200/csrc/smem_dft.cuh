@@ -170,7 +170,10 @@ __device__ __forceinline__ void sym_prep(cd* src, const cd* tw, int n, int R, in
 // X[0] alone), sharing each loaded s_r, d_r across the kSymQ pairs (the one-pair
 // version spent most of its time on shared-memory loads).  Per output the arithmetic
 // is the same FMA chain over ascending r as one pair alone.
-constexpr int kSymQ = 2;
+#ifndef AFFT_SYMQ
+#define AFFT_SYMQ 2
+#endif
+constexpr int kSymQ = AFFT_SYMQ;
 __device__ __forceinline__ void sym_out(const cd* src, cd* dst, const cd* tw, int n, int R,
                                         int nb, int Ns, int j, int q0) {
   const int jm = j % Ns;
