@@ -1,3 +1,6 @@
+"""dsfft_batch (the drop-in API, SparseSpectrum dicts included) at config 4, 20 dB:
+per-signal loops against lockstep chunks of several sizes / stream counts.
+python tools/dsfft_api_sweep.py"""
 import os, sys
 import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
